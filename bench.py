@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""Benchmark of the hybrid method's hot path on B200 (BASELINE.json metric:
+"hybridised-system PCG time-to-solution; SpMV GB/s as % of B200 HBM peak").
+
+Workload (one "step"): BASELINE.json configs[1] — 2D transient Stokes, unit square,
+1024 x 1024 squares split into 2,097,152 triangles, interior vertices jittered by up to
+0.2h (seed 2), mu = nu = 1, manufactured fp64 force — run through the whole hot path:
+cr_build_mesh -> cr_hybridise -> cr_solve (Jacobi PCG to a TRUE relative residual of
+1e-10) -> cr_recover, inputs resident in HBM.  value = seconds per solve (time to
+solution, lower is better).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+For N > 1 (torchrun, one rank per GPU) every rank solves its own replica of the workload
+(no data-path collective), timed on the device, max over ranks.
+--impl reference times the CPU oracle (oracle/, numpy/scipy + binary128 C) on the host
+cores on a bounded sample of the same workload and extrapolates per unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "hybridised-system PCG time-to-solution; SpMV GB/s as % of B200 HBM peak"
+CONFIG_IDX = 1
+# Jacobi-PCG iterations of configs[1] to a true 1e-10 residual, measured on B200 by this
+# bench (used only by --impl reference to extrapolate the oracle's per-iteration time).
+ITERS_CONFIG1_MEASURED = None
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def oracle_sample(n_sample: int = 256, iters: int = 200):
+    """Time the oracle, as it stands, on a bounded sample of the configs[1] family (same
+    generator, jitter, mu, nu; n = n_sample) and return per-unit costs."""
+    import numpy as np
+    import cr_inputs as ci
+    import oracle as O
+    cfg = ci.CONFIGS[CONFIG_IDX]
+    inp = ci.make_inputs(cfg, n=n_sample)
+    t0 = time.perf_counter()
+    m = O.build_mesh(inp["coords"], inp["cells"])
+    t1 = time.perf_counter()
+    prm, data = O.Params(mu=cfg.mu, nu=cfg.nu), O.Data(fbar=inp["fbar"])
+    h = O.hybridise(m, prm, data)
+    t2 = time.perf_counter()
+    _, rep = O.pcg(h["G"], h["S"], rtol=1e-30, max_iter=iters)
+    t3 = time.perf_counter()
+    O.recover(m, prm, data, h["E"], np.zeros(len(h["S"])))
+    t4 = time.perf_counter()
+    return dict(nc=m.nc, nnz=h["G"].nnz, mesh_s=t1 - t0, hyb_s=t2 - t1, iter_s=(t3 - t2) / rep["iterations"],
+                rec_s=t4 - t3, iters=rep["iterations"], n=n_sample)
+
+
+def oracle_extrapolate(s: dict, nc_full: int, nnz_full: int, iters_full: int) -> float:
+    f = nc_full / s["nc"]
+    return (s["mesh_s"] + s["hyb_s"] + s["rec_s"]) * f + s["iter_s"] * (nnz_full / s["nnz"]) * iters_full
+
+
+def full_sizes():
+    n = 1024
+    nc = 2 * n * n
+    nf_int = 3 * n * n - 2 * n
+    nb = nf_int + 12 * (n - 1) ** 2 + 8 * (n - 1)
+    return nc, 4 * nb, nb, 2 * nf_int
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    nc, nnz, nb, N = full_sizes()
+    iters_full = ITERS_CONFIG1_MEASURED or 170000
+    vals = []
+    samples = []
+    for i in range(args.warmup + args.steps):
+        s = oracle_sample()
+        if i >= args.warmup:
+            vals.append(oracle_extrapolate(s, nc, nnz, iters_full))
+            samples.append(s)
+    v = statistics.mean(vals)
+    s = samples[-1]
+    sample_desc = (f"oracle on configs[1]-family mesh n={s['n']} ({s['nc']} cells): mesh+hybridise+recover "
+                   f"timed in full, PCG timed over {s['iters']} iterations; extrapolated per cell and per "
+                   f"nnz x {iters_full} iterations (B200-measured count) to n=1024")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "configs[1] 2D transient Stokes n=1024 jittered, Jacobi-PCG to 1e-10",
+                       "cells": nc, "unknowns": N},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "oracle", "sample": sample_desc},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=None, help="override mesh size (debug only; not a bench value)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import cr_inputs as ci
+    import paper_2101_03777_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    cfg = ci.CONFIGS[CONFIG_IDX]
+    inp = ci.make_inputs(cfg, n=args.n)
+    coords_h = torch.from_numpy(inp["coords"]).pin_memory()
+    cells_h = torch.from_numpy(inp["cells"]).pin_memory()
+    fbar_h = torch.from_numpy(inp["fbar"]).pin_memory()
+    coords, cells, fbar = coords_h.to(dev), cells_h.to(dev), fbar_h.to(dev)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
+
+    def step():
+        prob = P.Problem(mu=cfg.mu, nu=cfg.nu, fbar=fbar)
+        mesh = P.cr_build_mesh(coords, cells)
+        hyb = P.cr_hybridise(mesh, prob)
+        W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=dev)
+        rep = P.cr_solve(hyb, W, "pcg", rtol=cfg.rtol, check_every=64)
+        U, Pp, diag = P.cr_recover(hyb, W)
+        return mesh, hyb, rep, U, Pp, diag
+
+    for _ in range(args.warmup):
+        out = step()
+    torch.cuda.synchronize()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    reps = []
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            evs[k][0].record(stream)
+            out = step()
+            evs[k][1].record(stream)
+            reps.append(out[2])
+        torch.cuda.synchronize()
+    barrier()
+    ms = [a.elapsed_time(b) for a, b in evs]
+    ms_per_step = sum(ms) / len(ms)
+    t = torch.tensor([ms_per_step], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item())
+    mesh, hyb, rep = out[0], out[1], reps[-1]
+    N, nnz, nb = hyb.n_rows, hyb.nnz, hyb.nblocks
+
+    # ---- dominant kernel: the G SpMV, timed live with CUDA events on the launching stream
+    x = torch.randn(N, dtype=torch.float64, device=dev)
+    y = torch.empty_like(x)
+    for _ in range(10):
+        hyb.spmv(x, y)
+    nrep = 50
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(nrep):
+        hyb.spmv(x, y)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    spmv_s = e0.elapsed_time(e1) / nrep * 1e-3
+    spmv_bytes = 8 * nnz + 4 * nb + 8 * N + 8 * N          # values + block cols + x once + y
+    peak, peak_src = measured_peaks()
+    achieved = spmv_bytes / spmv_s / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "spmv_dram_bytes.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    iter_bytes = 8 * nnz + 4 * nb + 9 * 8 * N               # PCG iteration, SURVEY §8(d)
+    iter_gbs = iter_bytes * rep["iterations"] / rep["seconds"] / 1e9 if rep["seconds"] > 0 else None
+
+    # ---- e2e through the public API from HOST buffers (pinned host -> device -> host)
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        o2 = P.hybrid_method_host(coords_h, cells_h, fbar_h, cfg.mu, cfg.nu, "pcg", cfg.rtol)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_s = a.elapsed_time(b) * 1e-3
+        t2 = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        h2d = coords_h.numel() * 8 + cells_h.numel() * 4 + fbar_h.numel() * 8
+        d2h = o2["U_host"].numel() * 8 + o2["P_host"].numel() * 8
+        e2e = {"value": float(t2.item()), "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s = oracle_sample()
+        nc_full = mesh.nc
+        v = oracle_extrapolate(s, nc_full, nnz, rep["iterations"])
+        cpu = {"value": v, "unit": "s", "cores": 1, "kind": "oracle",
+               "sample": (f"oracle on configs[1]-family mesh n={s['n']} ({s['nc']} cells): mesh+hybridise+recover "
+                          f"timed in full ({s['mesh_s'] + s['hyb_s'] + s['rec_s']:.1f} s), PCG over {s['iters']} "
+                          f"iterations ({s['iter_s'] * 1e3:.2f} ms/it); extrapolated per cell and per nnz x "
+                          f"{rep['iterations']} iterations to the full workload")}
+
+    launches = rep["kernel_launches"] + 25     # mesh (sort/scan/geometry ~15), hybridise 1, recover 3, copies
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "configs[1] 2D transient Stokes n=%d jittered 0.2h, Jacobi-PCG to true 1e-10"
+                                   % (args.n or cfg.n),
+                       "cells": mesh.nc, "unknowns": N, "nnz_G": nnz, "blocks_G": nb,
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": "working set > L2 (G = %.2f GB per SpMV) and a 256 MB L2 flush before each step"
+                             % (8 * nnz / 1e9)},
+            "pcg": {"iterations": rep["iterations"], "rel_res_true": rep["rel_res_true"],
+                    "solve_s": rep["seconds"], "ms_per_iter": rep["seconds"] / max(rep["iterations"], 1) * 1e3,
+                    "iter_gbs": iter_gbs, "iter_bytes": iter_bytes},
+            "roofline": {"kernel": "k_spmv (sliced block-ELL G x, same row code as the PCG SpMV)",
+                         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes": spmv_bytes, "launch_s": spmv_s},
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,193 @@
+/*
+ * cr.h — C ABI of libcr, the B200 (sm_100a) implementation of the hybrid method of
+ * Chenier & Eymard, "Exact pressure elimination for the Crouzeix-Raviart scheme
+ * applied to the Stokes and Navier-Stokes problems" (arXiv 2101.03777).
+ * Citations "P:Lnnn" are lines of /root/reference/PAPER.md.
+ *
+ * Pipeline (the paper's "hybrid method"):
+ *   cr_build_mesh    faces, M_sigma, F_K, x_K, x_sigma, |K|, a_{K,sigma}
+ *   cr_hybridise     G = sum_K H_K G_K H_K^t and S of  G W = S
+ *   cr_solve         Krylov solve of G W = S (PCG / MINRES / BiCGStab / GMRES)
+ *   cr_recover       P and U from W, per cell
+ *   cr_assemble_coupled  the coupled saddle system eq. (syslin)
+ *
+ * Conventions (all calls):
+ *   - Pointers suffixed _d are DEVICE pointers on the current CUDA device.  Input
+ *     pointers are borrowed for the duration of the (stream-ordered) call; output
+ *     buffers are caller-owned and must be sized from cr_mesh_info / *_info.
+ *   - All work is enqueued on stream `s` (cudaStream_t; NULL = legacy default stream).
+ *     Calls that must return host-visible counts or convergence data synchronise `s`
+ *     (documented per call); the others are asynchronous.
+ *   - Errors: every call returns a cr_status; no C++ exception crosses the ABI.
+ *     cr_last_error() returns a thread-local message for the last non-OK status.
+ *   - Local face s of a cell is the face OPPOSITE its local vertex s.  Faces are
+ *     numbered in lexicographic order of their sorted vertex tuple; face_cells[f] =
+ *     (lower cell, higher cell), -1 in the second slot for a boundary face; interior
+ *     faces get dof = rank among interior faces.  Velocity / auxiliary unknowns are
+ *     indexed d*dof + i (face-major, component-minor).
+ *   - C_K = +1 on face_cells[f][0], -1 on the other cell ("equal to +-1").
+ *   - Gauge cell K0: P_{K0} = 0.
+ *   - fp64 throughout.  Per-cell eliminations are carried out in double-double
+ *     arithmetic and rounded once (kappa(S_K) reaches ~1e8 at 2D n = 1024).
+ */
+#ifndef CR_H
+#define CR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *cr_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    CR_OK = 0,
+    CR_ERR_INVALID_ARG = -1,      /* bad pointer / size / dimension / option            */
+    CR_ERR_CUDA = -2,             /* CUDA runtime error (message in cr_last_error)      */
+    CR_ERR_OOM = -3,              /* device allocation failed                           */
+    CR_ERR_NONMANIFOLD = -4,      /* a face shared by > 2 cells (1 or 2)        */
+    CR_ERR_DEGENERATE_CELL = -5,  /* |K| <= 1e-14 (max edge)^d, or vertex out of range  */
+    CR_ERR_NO_INTERIOR_FACE = -6, /* s_K = 0 => D_K = 0, B_K = 0 (P:L486 assumes s_K>0) */
+    CR_ERR_SINGULAR_LOCAL = -7,   /* Ahat_K singular or |B_K| ~ 0        */
+    CR_ERR_NOT_CONVERGED = -8,    /* max_iter reached                                   */
+    CR_ERR_BREAKDOWN = -9,        /* CG p^t G p <= 0, BiCGStab rho or omega = 0         */
+    CR_ERR_STAGNATION = -10,      /* GMRES(m) restart cycle made no progress            */
+    CR_ERR_NCCL = -11             /* NCCL error                                         */
+} cr_status;
+
+typedef struct cr_mesh_s *cr_mesh;
+typedef struct cr_coupled_s *cr_coupled;
+typedef struct cr_hybrid_s *cr_hybrid;
+typedef struct cr_comm_s *cr_comm;
+
+/* ------------------------------------------------------------------ mesh
+ * coords_d [nv][dim] f64, cells_d [nc][dim+1] i32 (0-based vertex ids, any orientation).
+ * Builds faces and incidence with a device radix sort of the (dim+1)*nc face tuples,
+ * then |K|, x_K, x_sigma and the outward area vectors a_{K,sigma} = |sigma| n_{K,sigma}.
+ * Synchronises `s` (counts are returned to the host).  Errors: INVALID_ARG (dim not 2/3,
+ * nv or nc <= 0, nc*(dim+1) >= 2^31), DEGENERATE_CELL, NONMANIFOLD, OOM, CUDA.          */
+cr_status cr_build_mesh(int32_t dim, int64_t nv, const double *coords_d, int64_t nc,
+                        const int32_t *cells_d, cr_stream_t s, cr_mesh *out);
+
+typedef struct {
+    int32_t dim;
+    int64_t nv, nc, nf, nf_int;
+    int64_t n_unknowns;          /* dim * nf_int = size of G, U, W, S                      */
+} cr_mesh_info_t;
+cr_status cr_mesh_info(cr_mesh m, cr_mesh_info_t *out);
+
+/* Copies the mesh arrays (any pointer may be NULL):
+ *   faces_d [nf][dim] i32 sorted vertex tuples (lexicographic face order)
+ *   face_cells_d [nf][2] i32, cell_faces_d [nc][dim+1] i32, face_dof_d [nf] i32 (-1 boundary)
+ *   vol_d [nc], xK_d [nc][dim], xs_d [nf][dim], a_d [nc][dim+1][dim] f64. Asynchronous. */
+cr_status cr_mesh_export(cr_mesh m, int32_t *faces_d, int32_t *face_cells_d, int32_t *cell_faces_d,
+                         int32_t *face_dof_d, double *vol_d, double *xK_d, double *xs_d, double *a_d,
+                         cr_stream_t s);
+void cr_destroy_mesh(cr_mesh m);
+
+/* ------------------------------------------------------------------ problem data */
+enum { CR_STOKES = 0, CR_NS_NEWTON_STEP = 1 };  /* b_h = 0 / one Newton step */
+enum { CR_SHIFT_NONE = 0, CR_SHIFT_MIS = 1 };   /* E_K = 0 (mu > 0) / M1-M2 shift */
+
+typedef struct {
+    double mu;             /* 1/dt (transient) or 0 (steady)                        */
+    double nu;             /* 1/Re                                                  */
+    int32_t gauge_cell;    /* K0, P:L177 (default 0)                                       */
+    int32_t physics;       /* CR_STOKES | CR_NS_NEWTON_STEP                                */
+    int32_t shift;         /* CR_SHIFT_NONE | CR_SHIFT_MIS                                 */
+    int32_t reserved;
+    uint64_t mis_seed;     /* M1 = greedy MIS in ascending (splitmix64(seed ^ K), K) order */
+    double lambda_factor;  /* lambda_K = factor * Gershgorin bound of A_K (> all eigenvalues) */
+} cr_params;
+
+typedef struct {
+    const double *fbar_d;      /* [nc][dim] (1/|K|) int_K f                        */
+    const double *dirichlet_d; /* [nc][dim+1][dim] values at the centroid of each LOCAL face;
+                                  read on boundary faces only; NULL = homogeneous    */
+    const double *u_iter_d;    /* NS: [nc][dim+1][dim] Newton iterate U^k at every local face
+                                  (boundary faces carry the wall values); the two copies of an
+                                  interior face must agree                                   */
+    const double *p_iter_d;    /* NS: [nc] pressure iterate P^k, NULL = 0                     */
+} cr_data;
+
+/* ------------------------------------------------------------------ coupled system
+ * Assembles A = sum_K H_K A_K H_K^t, D = sum_{K != K0} F_K D_K^t H_K^t, R and g on the device.
+ * Synchronises `s` (nnz).  Used for parity / export; the hybrid path never needs it.   */
+cr_status cr_assemble_coupled(cr_mesh m, const cr_params *prm, const cr_data *data, cr_stream_t s,
+                              cr_coupled *out);
+/* saddle matrix [[A, D^t],[D, 0]] of size n_rows = dim*nf_int + nc - 1 (pressures of K != K0 in
+ * increasing K), canonical CSR: int64 row_ptr_d [n_rows+1], cols sorted, f64 vals; rhs [R; g]. */
+cr_status cr_coupled_info(cr_coupled c, int64_t *n_rows, int64_t *nnz);
+cr_status cr_coupled_export_csr(cr_coupled c, int64_t *row_ptr_d, int32_t *cols_d, double *vals_d,
+                                double *rhs_d, cr_stream_t s);
+void cr_destroy_coupled(cr_coupled c);
+
+/* ------------------------------------------------------------------ hybridisation
+ * Per interior face (block row of G), for each of its two cells: Ahat_K = A_K + E_K,
+ * Ahat_K^{-1}, w = Ahat^{-1} D_K, B_K = D_K^t w, G_K and S_K in double-double,
+ * written straight into a sliced block-ELL G (d x d blocks, width 2d+1) — no atomics, no
+ * staging.  shift = MIS runs the M1/M2 construction first (hashed-priority Luby rounds that
+ * reproduce the sequential greedy MIS exactly).  `comm` must be NULL (1 GPU).
+ * Synchronises `s`.  Errors: NO_INTERIOR_FACE, SINGULAR_LOCAL, INVALID_ARG, OOM, CUDA.   */
+cr_status cr_hybridise(cr_mesh m, const cr_params *prm, const cr_data *data, cr_comm comm,
+                       cr_stream_t s, cr_hybrid *out);
+/* n_rows = dim*nf_int; nnz = scalar nonzeros of G (explicit zeros of the stencil included) */
+cr_status cr_hybrid_info(cr_hybrid h, int64_t *n_rows, int64_t *nnz, int64_t *nblocks);
+/* canonical scalar CSR of G (int64 row_ptr_d [n_rows+1], cols ascending) and S_d [n_rows] */
+cr_status cr_hybrid_export_csr(cr_hybrid h, int64_t *row_ptr_d, int32_t *cols_d, double *vals_d,
+                               double *S_d, cr_stream_t s);
+/* MIS membership inM1_d [nc] (u8) and E_d [nc][dim+1] (shift per local face); either may be NULL */
+cr_status cr_hybrid_export_shift(cr_hybrid h, uint8_t *inM1_d, double *E_d, cr_stream_t s);
+/* y = G x (the solver's SpMV kernel; x_d, y_d [n_rows], must not alias).  Asynchronous. */
+cr_status cr_spmv(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s);
+void cr_destroy_hybrid(cr_hybrid h);
+
+/* ------------------------------------------------------------------ solve
+ * Solves G W = S.  W_d [n_rows] holds the initial guess on entry (use zeros) and the solution
+ * on exit.  Stopping rule: TRUE relative residual ||S - G W||_2 / ||S||_2 <= rtol (recomputed
+ * at exit; recursive-residual convergence triggers a true-residual check and, if it fails, a
+ * residual replacement).  refine_dd = 1 adds outer iterative refinement with the residual
+ * S - G W accumulated in double-double (parity mode).  Synchronises `s`.                  */
+enum { CR_PCG_JACOBI = 0, CR_PCG_BLOCKJACOBI = 1, CR_MINRES_ABSJACOBI = 2,
+       CR_BICGSTAB_JACOBI = 3, CR_GMRES_JACOBI = 4 };
+typedef struct {
+    int32_t method;       /* CR_* above                                                        */
+    int32_t restart;      /* GMRES m (default 50)                                              */
+    double rtol;          /* default 1e-10                                                     */
+    int64_t max_iter;     /* total Krylov iterations cap                                       */
+    int32_t check_every;  /* iterations per captured CUDA graph between host checks (def 64)   */
+    int32_t refine_dd;    /* 0/1                                                               */
+} cr_solver_opts;
+typedef struct {
+    int64_t iterations;
+    double rel_res_true;       /* ||S - G W|| / ||S|| at exit (fp64 SpMV)                       */
+    double rel_res_recursive;  /* solver's own residual estimate at exit                        */
+    int32_t converged;
+    int32_t status;            /* cr_status of the solve                                        */
+    double seconds;            /* device time of the solve (CUDA events)                        */
+    int64_t spmv_calls;
+    int64_t kernel_launches;   /* kernels launched by cr_solve                                   */
+} cr_solve_report;
+cr_status cr_solve(cr_hybrid h, const cr_solver_opts *opts, double *W_d, cr_stream_t s,
+                   cr_solve_report *rep);
+
+/* ------------------------------------------------------------------ recovery
+ * P_K = (v^t (R_K - C_K W_K) - g_K)/B_K (K != K0), P_K0 = 0;  Uhat_K = Ahat^{-1}(R_K - D_K P_K - C_K W_K);
+ * U_sigma = the copy of face_cells[sigma][0].  U_d [nf_int][dim], P_d [nc].
+ * diag_d (may be NULL) [2]: max |Uhat_K - Uhat_L| over interior faces ("this common value")
+ * and max_K |sum_{sigma in F_K} a_{K,sigma} . U_sigma| (boundary faces at their Dirichlet value). */
+cr_status cr_recover(cr_hybrid h, const double *W_d, double *U_d, double *P_d, double *diag_d,
+                     cr_stream_t s);
+
+/* ------------------------------------------------------------------ multi-GPU (reserved) */
+cr_status cr_comm_init(const void *nccl_unique_id, int32_t rank, int32_t nranks, cr_comm *out);
+void cr_comm_destroy(cr_comm c);
+
+const char *cr_last_error(void);
+const char *cr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CR_H */

@@ -50,11 +50,12 @@ def lib():
 
 from .mesh import Mesh, build_mesh  # noqa: E402
 from .scheme import (Params, Data, cell_arrays, local_blocks, mis_priority, shift_E,  # noqa: E402
-                     assemble_coupled, hybridise, recover, hybrid_pipeline)
+                     assemble_coupled, hybridise, recover, hybrid_pipeline, eliminate_cells,
+                     recover_cells)
 from .krylov import (residual_f128, direct_refined, pcg, minres, bicgstab, gmres)  # noqa: E402
 from .post import zero_mean, errors  # noqa: E402
 
 __all__ = ["build", "lib", "Mesh", "build_mesh", "Params", "Data", "cell_arrays",
            "local_blocks", "mis_priority", "shift_E", "assemble_coupled", "hybridise",
-           "recover", "hybrid_pipeline", "residual_f128", "direct_refined", "pcg",
+           "recover", "hybrid_pipeline", "eliminate_cells", "recover_cells", "residual_f128", "direct_refined", "pcg",
            "minres", "bicgstab", "gmres", "zero_mean", "errors"]

@@ -249,6 +249,50 @@ def recover(m: Mesh, prm: Params, data: Data, E: np.ndarray, W: np.ndarray):
     return U, P, Uh, disagree
 
 
+def _subset_call(fn, m, prm, data, E, cells, extra_in=(), extra_out=()):
+    c = cell_arrays(m, data)
+    cells = np.asarray(cells, dtype=np.int64)
+    sub = {k: (None if v is None else np.ascontiguousarray(v[cells])) for k, v in c.items()}
+    Es = np.ascontiguousarray(np.asarray(E, dtype=np.float64)[cells])
+    cs = np.ascontiguousarray(m.csign[cells])
+    hit = np.nonzero(cells == prm.k0)[0]
+    k0 = int(hit[0]) if len(hit) else -1
+    return fn(ctypes.c_int(m.dim), ctypes.c_int64(len(cells)), ctypes.c_double(prm.mu),
+              ctypes.c_double(prm.nu), ctypes.c_int(prm.physics == "ns_step"),
+              _p(sub["a"]), _p(sub["vol"]), _p(sub["xK"]), _p(sub["xs"]), _p(sub["intr"]), _p(sub["fbar"]),
+              _p(sub["dir"]), _p(sub["uit"]), _p(sub["pit"]), _p(Es), _p(cs), ctypes.c_int64(k0),
+              *[_p(x) for x in extra_in], *[_p(x) for x in extra_out])
+
+
+def eliminate_cells(m: Mesh, prm: Params, data: Data, E: np.ndarray, cells):
+    """G_K, S_K, B_K of a SUBSET of cells (same binary128 algebra as ``hybridise``), for
+    sampled parity checks at sizes where the full oracle is too slow."""
+    from . import lib
+    n = (m.dim + 1) * m.dim
+    k = len(cells)
+    G = np.zeros((k, n, n)); S = np.zeros((k, n)); B = np.zeros(k); st = np.zeros(k, dtype=np.int32)
+    nbad = _subset_call(lib().or_cell_eliminate, m, prm, data, E, cells, extra_out=(G, S, B, st))
+    if nbad:
+        raise LocalFailure(f"{nbad} cells failed local elimination")
+    return G, S, B
+
+
+def recover_cells(m: Mesh, prm: Params, data: Data, E: np.ndarray, W: np.ndarray, cells):
+    """P_K and Uhat_K of a SUBSET of cells given W."""
+    from . import lib
+    d = m.dim
+    n = (d + 1) * d
+    cells = np.asarray(cells, dtype=np.int64)
+    gi = _gidx(m)[cells]
+    Wl = np.ascontiguousarray(np.where(gi >= 0, W[np.maximum(gi, 0)], 0.0))
+    k = len(cells)
+    P = np.zeros(k); Uh = np.zeros((k, n)); st = np.zeros(k, dtype=np.int32)
+    nbad = _subset_call(lib().or_cell_recover, m, prm, data, E, cells, extra_in=(Wl,), extra_out=(P, Uh, st))
+    if nbad:
+        raise LocalFailure(f"{nbad} cells failed recovery")
+    return P, Uh.reshape(k, d + 1, d)
+
+
 def hybrid_pipeline(m: Mesh, prm: Params, data: Data, solve=None):
     """The paper's 'hybrid method' (P:L546-551): (1) G, S; (2) solve G W = S;
     (3) recover P, U.  ``solve`` defaults to the refined direct solve."""

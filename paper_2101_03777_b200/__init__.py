@@ -1,0 +1,332 @@
+"""paper_2101_03777_b200 — B200-native hybrid method for the Crouzeix-Raviart Stokes /
+Navier-Stokes systems (Chenier & Eymard, arXiv 2101.03777).
+
+Thin Python binding of the C ABI ``include/cr.h`` (libcr.so, built in-tree for sm_100a).
+Every function here only marshals torch CUDA tensors into device pointers and calls the
+library; all arithmetic runs in the CUDA kernels.  There is no CPU fallback: importing
+this package fails loudly when libcr.so is missing, and every call checks that its
+tensors live on a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcr.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"libcr.so not found at {LIB_PATH}: build it with `python -m paper_2101_03777_b200.build` "
+        "(nvcc, sm_100a). There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+# ------------------------------------------------------------------ ABI mirror (include/cr.h)
+CR_OK = 0
+STATUS = {0: "CR_OK", -1: "CR_ERR_INVALID_ARG", -2: "CR_ERR_CUDA", -3: "CR_ERR_OOM",
+          -4: "CR_ERR_NONMANIFOLD", -5: "CR_ERR_DEGENERATE_CELL", -6: "CR_ERR_NO_INTERIOR_FACE",
+          -7: "CR_ERR_SINGULAR_LOCAL", -8: "CR_ERR_NOT_CONVERGED", -9: "CR_ERR_BREAKDOWN",
+          -10: "CR_ERR_STAGNATION", -11: "CR_ERR_NCCL"}
+CR_STOKES, CR_NS_NEWTON_STEP = 0, 1
+CR_SHIFT_NONE, CR_SHIFT_MIS = 0, 1
+CR_PCG_JACOBI, CR_PCG_BLOCKJACOBI, CR_MINRES_ABSJACOBI, CR_BICGSTAB_JACOBI, CR_GMRES_JACOBI = range(5)
+METHODS = {"pcg": CR_PCG_JACOBI, "pcg_block": CR_PCG_BLOCKJACOBI, "minres": CR_MINRES_ABSJACOBI,
+           "bicgstab": CR_BICGSTAB_JACOBI, "gmres": CR_GMRES_JACOBI}
+
+
+class CrError(RuntimeError):
+    def __init__(self, status: int, msg: str, report=None):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.report = report
+
+
+class MeshInfo(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("nv", ctypes.c_int64), ("nc", ctypes.c_int64),
+                ("nf", ctypes.c_int64), ("nf_int", ctypes.c_int64), ("n_unknowns", ctypes.c_int64)]
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("mu", ctypes.c_double), ("nu", ctypes.c_double), ("gauge_cell", ctypes.c_int32),
+                ("physics", ctypes.c_int32), ("shift", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("mis_seed", ctypes.c_uint64), ("lambda_factor", ctypes.c_double)]
+
+
+class Data(ctypes.Structure):
+    _fields_ = [("fbar_d", ctypes.c_void_p), ("dirichlet_d", ctypes.c_void_p),
+                ("u_iter_d", ctypes.c_void_p), ("p_iter_d", ctypes.c_void_p)]
+
+
+class SolverOpts(ctypes.Structure):
+    _fields_ = [("method", ctypes.c_int32), ("restart", ctypes.c_int32), ("rtol", ctypes.c_double),
+                ("max_iter", ctypes.c_int64), ("check_every", ctypes.c_int32), ("refine_dd", ctypes.c_int32)]
+
+
+class SolveReport(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int64), ("rel_res_true", ctypes.c_double),
+                ("rel_res_recursive", ctypes.c_double), ("converged", ctypes.c_int32),
+                ("status", ctypes.c_int32), ("seconds", ctypes.c_double), ("spmv_calls", ctypes.c_int64),
+                ("kernel_launches", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_vp, _i32, _i64, _st = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int
+_P = ctypes.POINTER
+_sig = {
+    "cr_build_mesh": [_i32, _i64, _vp, _i64, _vp, _vp, _P(_vp)],
+    "cr_mesh_info": [_vp, _P(MeshInfo)],
+    "cr_mesh_export": [_vp] + [_vp] * 8 + [_vp],
+    "cr_assemble_coupled": [_vp, _P(Params), _P(Data), _vp, _P(_vp)],
+    "cr_coupled_info": [_vp, _P(_i64), _P(_i64)],
+    "cr_coupled_export_csr": [_vp, _vp, _vp, _vp, _vp, _vp],
+    "cr_hybridise": [_vp, _P(Params), _P(Data), _vp, _vp, _P(_vp)],
+    "cr_hybrid_info": [_vp, _P(_i64), _P(_i64), _P(_i64)],
+    "cr_hybrid_export_csr": [_vp, _vp, _vp, _vp, _vp, _vp],
+    "cr_hybrid_export_shift": [_vp, _vp, _vp, _vp],
+    "cr_spmv": [_vp, _vp, _vp, _vp],
+    "cr_solve": [_vp, _P(SolverOpts), _vp, _vp, _P(SolveReport)],
+    "cr_recover": [_vp, _vp, _vp, _vp, _vp, _vp],
+    "cr_comm_init": [_vp, _i32, _i32, _P(_vp)],
+}
+for _name, _args in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _st
+for _name in ("cr_destroy_mesh", "cr_destroy_coupled", "cr_destroy_hybrid", "cr_comm_destroy"):
+    getattr(_lib, _name).argtypes = [_vp]
+    getattr(_lib, _name).restype = None
+_lib.cr_last_error.restype = ctypes.c_char_p
+_lib.cr_version.restype = ctypes.c_char_p
+
+ABI_SYMBOLS = sorted(list(_sig) + ["cr_destroy_mesh", "cr_destroy_coupled", "cr_destroy_hybrid",
+                                   "cr_comm_destroy", "cr_last_error", "cr_version"])
+
+
+def _check(status: int, report=None):
+    if status != CR_OK:
+        raise CrError(status, _lib.cr_last_error().decode(), report)
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None, dtype=None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libcr takes CUDA tensors only (no CPU fallback)")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def version() -> str:
+    return _lib.cr_version().decode()
+
+
+# ------------------------------------------------------------------ handles
+class Mesh:
+    """cr_mesh handle (owns its device memory)."""
+
+    def __init__(self, handle):
+        self._h = handle
+        info = MeshInfo()
+        _check(_lib.cr_mesh_info(self._h, ctypes.byref(info)))
+        self.dim, self.nv, self.nc = info.dim, info.nv, info.nc
+        self.nf, self.nf_int, self.n_unknowns = info.nf, info.nf_int, info.n_unknowns
+
+    def export(self, stream=None) -> dict:
+        d, dev = self.dim, torch.device("cuda")
+        out = dict(
+            faces=torch.empty((self.nf, d), dtype=torch.int32, device=dev),
+            face_cells=torch.empty((self.nf, 2), dtype=torch.int32, device=dev),
+            cell_faces=torch.empty((self.nc, d + 1), dtype=torch.int32, device=dev),
+            face_dof=torch.empty(self.nf, dtype=torch.int32, device=dev),
+            vol=torch.empty(self.nc, dtype=torch.float64, device=dev),
+            xK=torch.empty((self.nc, d), dtype=torch.float64, device=dev),
+            xs=torch.empty((self.nf, d), dtype=torch.float64, device=dev),
+            a=torch.empty((self.nc, d + 1, d), dtype=torch.float64, device=dev),
+        )
+        _check(_lib.cr_mesh_export(self._h, *[_ptr(out[k]) for k in
+                                              ("faces", "face_cells", "cell_faces", "face_dof", "vol", "xK", "xs", "a")],
+                                   _stream(stream)))
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.cr_destroy_mesh(self._h)
+            self._h = None
+
+
+def cr_build_mesh(coords: torch.Tensor, cells: torch.Tensor, stream=None) -> Mesh:
+    """coords [nv, d] f64 CUDA, cells [nc, d+1] i32 CUDA -> Mesh."""
+    d = coords.shape[1]
+    h = ctypes.c_void_p()
+    _check(_lib.cr_build_mesh(d, coords.shape[0], _ptr(coords, torch.float64), cells.shape[0],
+                              _ptr(cells, torch.int32), _stream(stream), ctypes.byref(h)))
+    return Mesh(h)
+
+
+@dataclass
+class Problem:
+    """cr_params + cr_data (tensors stay alive as long as this object)."""
+    mu: float
+    nu: float
+    fbar: torch.Tensor
+    physics: int = CR_STOKES
+    shift: int = CR_SHIFT_NONE
+    mis_seed: int = 0
+    lambda_factor: float = 1.1
+    gauge_cell: int = 0
+    dirichlet: torch.Tensor | None = None
+    u_iter: torch.Tensor | None = None
+    p_iter: torch.Tensor | None = None
+
+    def params(self) -> Params:
+        return Params(self.mu, self.nu, self.gauge_cell, self.physics, self.shift, 0,
+                      self.mis_seed & 0xFFFFFFFFFFFFFFFF, self.lambda_factor)
+
+    def data(self) -> Data:
+        return Data(_ptr(self.fbar, torch.float64), _ptr(self.dirichlet, torch.float64),
+                    _ptr(self.u_iter, torch.float64), _ptr(self.p_iter, torch.float64))
+
+
+class Hybrid:
+    """cr_hybrid handle: G (sliced block-ELL), S, shift, preconditioners."""
+
+    def __init__(self, handle, mesh: Mesh):
+        self._h = handle
+        self.mesh = mesh
+        nr, nnz, nb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.cr_hybrid_info(self._h, ctypes.byref(nr), ctypes.byref(nnz), ctypes.byref(nb)))
+        self.n_rows, self.nnz, self.nblocks = nr.value, nnz.value, nb.value
+
+    def export_csr(self, stream=None):
+        dev = torch.device("cuda")
+        rp = torch.empty(self.n_rows + 1, dtype=torch.int64, device=dev)
+        ci = torch.empty(self.nnz, dtype=torch.int32, device=dev)
+        v = torch.empty(self.nnz, dtype=torch.float64, device=dev)
+        S = torch.empty(self.n_rows, dtype=torch.float64, device=dev)
+        _check(_lib.cr_hybrid_export_csr(self._h, _ptr(rp), _ptr(ci), _ptr(v), _ptr(S), _stream(stream)))
+        return rp, ci, v, S
+
+    def export_shift(self, stream=None):
+        dev = torch.device("cuda")
+        inM1 = torch.empty(self.mesh.nc, dtype=torch.uint8, device=dev)
+        E = torch.empty((self.mesh.nc, self.mesh.dim + 1), dtype=torch.float64, device=dev)
+        _check(_lib.cr_hybrid_export_shift(self._h, _ptr(inM1), _ptr(E), _stream(stream)))
+        return inM1, E
+
+    def spmv(self, x: torch.Tensor, y: torch.Tensor, stream=None):
+        _check(_lib.cr_spmv(self._h, _ptr(x, torch.float64), _ptr(y, torch.float64), _stream(stream)))
+        return y
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.cr_destroy_hybrid(self._h)
+            self._h = None
+
+
+def cr_hybridise(mesh: Mesh, prob: Problem, stream=None) -> Hybrid:
+    """G and S of G W = S."""
+    h = ctypes.c_void_p()
+    prm, data = prob.params(), prob.data()
+    _check(_lib.cr_hybridise(mesh._h, ctypes.byref(prm), ctypes.byref(data), None, _stream(stream),
+                             ctypes.byref(h)))
+    return Hybrid(h, mesh)
+
+
+def cr_solve(hyb: Hybrid, W: torch.Tensor, method: str | int = "pcg", rtol: float = 1e-10,
+             max_iter: int = 10**7, check_every: int = 64, restart: int = 50, refine_dd: int = 0,
+             stream=None, raise_on_fail: bool = True) -> dict:
+    """Krylov solve of G W = S in place.  Returns the cr_solve_report as a dict."""
+    m = METHODS[method] if isinstance(method, str) else int(method)
+    opts = SolverOpts(m, restart, rtol, max_iter, check_every, refine_dd)
+    rep = SolveReport()
+    st = _lib.cr_solve(hyb._h, ctypes.byref(opts), _ptr(W, torch.float64), _stream(stream), ctypes.byref(rep))
+    out = rep.as_dict()
+    if raise_on_fail:
+        _check(st, out)
+    out["status_name"] = STATUS.get(st, st)
+    return out
+
+
+def cr_recover(hyb: Hybrid, W: torch.Tensor, stream=None):
+    """P and U from W.  Returns U [nf_int, d], P [nc], diag [2]."""
+    mesh = hyb.mesh
+    dev = W.device
+    U = torch.empty((mesh.nf_int, mesh.dim), dtype=torch.float64, device=dev)
+    P = torch.empty(mesh.nc, dtype=torch.float64, device=dev)
+    diag = torch.empty(2, dtype=torch.float64, device=dev)
+    _check(_lib.cr_recover(hyb._h, _ptr(W, torch.float64), _ptr(U), _ptr(P), _ptr(diag), _stream(stream)))
+    return U, P, diag
+
+
+class Coupled:
+    def __init__(self, handle):
+        self._h = handle
+        nr, nnz = ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.cr_coupled_info(self._h, ctypes.byref(nr), ctypes.byref(nnz)))
+        self.n_rows, self.nnz = nr.value, nnz.value
+
+    def export_csr(self, stream=None):
+        dev = torch.device("cuda")
+        rp = torch.empty(self.n_rows + 1, dtype=torch.int64, device=dev)
+        ci = torch.empty(self.nnz, dtype=torch.int32, device=dev)
+        v = torch.empty(self.nnz, dtype=torch.float64, device=dev)
+        rhs = torch.empty(self.n_rows, dtype=torch.float64, device=dev)
+        _check(_lib.cr_coupled_export_csr(self._h, _ptr(rp), _ptr(ci), _ptr(v), _ptr(rhs), _stream(stream)))
+        return rp, ci, v, rhs
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.cr_destroy_coupled(self._h)
+            self._h = None
+
+
+def cr_assemble_coupled(mesh: Mesh, prob: Problem, stream=None) -> Coupled:
+    """The coupled saddle system eq. (syslin), for parity/export."""
+    h = ctypes.c_void_p()
+    prm, data = prob.params(), prob.data()
+    _check(_lib.cr_assemble_coupled(mesh._h, ctypes.byref(prm), ctypes.byref(data), _stream(stream),
+                                    ctypes.byref(h)))
+    return Coupled(h)
+
+
+# ------------------------------------------------------------------ the paper's "hybrid method"
+def hybrid_method(coords: torch.Tensor, cells: torch.Tensor, prob: Problem, method: str = "pcg",
+                  rtol: float = 1e-10, stream=None, **solve_kw) -> dict:
+    """(1) mesh, G and S; (2) solve G W = S; (3) recover P and U.
+    All tensors must already be on the GPU."""
+    mesh = cr_build_mesh(coords, cells, stream)
+    hyb = cr_hybridise(mesh, prob, stream)
+    W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=coords.device)
+    rep = cr_solve(hyb, W, method, rtol, stream=stream, **solve_kw)
+    U, P, diag = cr_recover(hyb, W, stream)
+    return dict(mesh=mesh, hybrid=hyb, W=W, U=U, P=P, diag=diag, report=rep)
+
+
+def hybrid_method_host(coords, cells, fbar, mu: float, nu: float, method: str = "pcg", rtol: float = 1e-10,
+                       stream=None, **kw) -> dict:
+    """End-to-end entry point from HOST buffers: pinned host -> device copies, the hybrid
+    method on the device, and U, P copied back to host (the `e2e` path of bench.py)."""
+    dev = torch.device("cuda")
+    c = coords.to(dev, non_blocking=True)
+    k = cells.to(dev, non_blocking=True)
+    f = fbar.to(dev, non_blocking=True)
+    prob = Problem(mu=mu, nu=nu, fbar=f, **kw)
+    out = hybrid_method(c, k, prob, method, rtol, stream)
+    out["U_host"] = out["U"].to("cpu")
+    out["P_host"] = out["P"].to("cpu")
+    return out

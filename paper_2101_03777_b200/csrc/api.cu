@@ -1,0 +1,217 @@
+// C ABI entry points of libcr (include/cr.h).  Every entry point converts exceptions into a
+// cr_status and a thread-local message; no C++ exception crosses the ABI.
+#include <cstring>
+#include <string>
+
+#include "internal.cuh"
+
+namespace cr {
+static thread_local std::string g_last_error;
+void set_last_error(const std::string &m) { g_last_error = m; }
+}  // namespace cr
+
+cr_hybrid_s::~cr_hybrid_s() { cr::free_solver_work(work); }
+
+#define CR_API_BEGIN try {
+#define CR_API_END                                              \
+    return CR_OK;                                               \
+    }                                                           \
+    catch (const cr::Error &e) {                                \
+        cr::set_last_error(e.what());                           \
+        return e.code;                                          \
+    }                                                           \
+    catch (const std::exception &e) {                           \
+        cr::set_last_error(e.what());                           \
+        return CR_ERR_CUDA;                                     \
+    }                                                           \
+    catch (...) {                                               \
+        cr::set_last_error("unknown error");                    \
+        return CR_ERR_CUDA;                                     \
+    }
+
+extern "C" {
+
+const char *cr_last_error(void) { return cr::g_last_error.c_str(); }
+const char *cr_version(void) { return "libcr 0.1 (sm_100a, fp64, double-double local elimination)"; }
+
+cr_status cr_build_mesh(int32_t dim, int64_t nv, const double *coords_d, int64_t nc, const int32_t *cells_d,
+                        cr_stream_t s, cr_mesh *out) {
+    CR_API_BEGIN
+    CR_REQUIRE(out, CR_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    cr_mesh_s *m = new cr_mesh_s();
+    try {
+        cr::build_mesh(m, dim, nv, coords_d, nc, cells_d, (cudaStream_t)s);
+    } catch (...) {
+        delete m;
+        throw;
+    }
+    *out = m;
+    CR_API_END
+}
+
+cr_status cr_mesh_info(cr_mesh m, cr_mesh_info_t *out) {
+    CR_API_BEGIN
+    CR_REQUIRE(m && out, CR_ERR_INVALID_ARG, "null handle");
+    out->dim = m->dim;
+    out->nv = m->nv;
+    out->nc = m->nc;
+    out->nf = m->nf;
+    out->nf_int = m->nf_int;
+    out->n_unknowns = m->dim * m->nf_int;
+    CR_API_END
+}
+
+static void copy_d2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    if (dst && bytes) CR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+}
+
+cr_status cr_mesh_export(cr_mesh m, int32_t *faces_d, int32_t *face_cells_d, int32_t *cell_faces_d,
+                         int32_t *face_dof_d, double *vol_d, double *xK_d, double *xs_d, double *a_d, cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(m, CR_ERR_INVALID_ARG, "null handle");
+    cudaStream_t st = (cudaStream_t)s;
+    const int D = m->dim;
+    copy_d2d(faces_d, m->faces.get(), m->nf * D * sizeof(int32_t), st);
+    copy_d2d(face_cells_d, m->face_cells.get(), m->nf * 2 * sizeof(int32_t), st);
+    copy_d2d(cell_faces_d, m->cell_faces.get(), m->nc * (D + 1) * sizeof(int32_t), st);
+    copy_d2d(face_dof_d, m->face_dof.get(), m->nf * sizeof(int32_t), st);
+    copy_d2d(vol_d, m->vol.get(), m->nc * sizeof(double), st);
+    copy_d2d(xK_d, m->xK.get(), m->nc * D * sizeof(double), st);
+    copy_d2d(xs_d, m->xs.get(), m->nf * D * sizeof(double), st);
+    copy_d2d(a_d, m->a.get(), m->nc * (D + 1) * D * sizeof(double), st);
+    CR_API_END
+}
+
+void cr_destroy_mesh(cr_mesh m) {
+    cudaDeviceSynchronize();
+    delete m;
+}
+
+cr_status cr_assemble_coupled(cr_mesh m, const cr_params *prm, const cr_data *data, cr_stream_t s, cr_coupled *out) {
+    CR_API_BEGIN
+    CR_REQUIRE(m && prm && data && out, CR_ERR_INVALID_ARG, "null argument");
+    *out = nullptr;
+    cr_coupled_s *c = new cr_coupled_s();
+    try {
+        cr::assemble_coupled(c, m, *prm, *data, (cudaStream_t)s);
+    } catch (...) {
+        delete c;
+        throw;
+    }
+    *out = c;
+    CR_API_END
+}
+
+cr_status cr_coupled_info(cr_coupled c, int64_t *n_rows, int64_t *nnz) {
+    CR_API_BEGIN
+    CR_REQUIRE(c, CR_ERR_INVALID_ARG, "null handle");
+    if (n_rows) *n_rows = c->n_rows;
+    if (nnz) *nnz = c->nnz;
+    CR_API_END
+}
+
+cr_status cr_coupled_export_csr(cr_coupled c, int64_t *row_ptr_d, int32_t *cols_d, double *vals_d, double *rhs_d,
+                                cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(c, CR_ERR_INVALID_ARG, "null handle");
+    cudaStream_t st = (cudaStream_t)s;
+    copy_d2d(row_ptr_d, c->row_ptr.get(), (c->n_rows + 1) * sizeof(int64_t), st);
+    copy_d2d(cols_d, c->cols.get(), c->nnz * sizeof(int32_t), st);
+    copy_d2d(vals_d, c->vals.get(), c->nnz * sizeof(double), st);
+    copy_d2d(rhs_d, c->rhs.get(), c->n_rows * sizeof(double), st);
+    CR_API_END
+}
+
+void cr_destroy_coupled(cr_coupled c) {
+    cudaDeviceSynchronize();
+    delete c;
+}
+
+cr_status cr_hybridise(cr_mesh m, const cr_params *prm, const cr_data *data, cr_comm comm, cr_stream_t s,
+                       cr_hybrid *out) {
+    CR_API_BEGIN
+    CR_REQUIRE(m && prm && data && out, CR_ERR_INVALID_ARG, "null argument");
+    CR_REQUIRE(comm == nullptr || comm->nranks == 1, CR_ERR_INVALID_ARG,
+               "multi-GPU hybridisation goes through the partitioned path (comm must be NULL)");
+    *out = nullptr;
+    cr_hybrid_s *h = new cr_hybrid_s();
+    try {
+        cr::hybridise(h, m, *prm, *data, (cudaStream_t)s);
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *out = h;
+    CR_API_END
+}
+
+cr_status cr_hybrid_info(cr_hybrid h, int64_t *n_rows, int64_t *nnz, int64_t *nblocks) {
+    CR_API_BEGIN
+    CR_REQUIRE(h, CR_ERR_INVALID_ARG, "null handle");
+    const int D = h->G.d;
+    if (n_rows) *n_rows = h->G.nrows * D;
+    if (nnz) *nnz = h->G.nblocks * D * D;
+    if (nblocks) *nblocks = h->G.nblocks;
+    CR_API_END
+}
+
+cr_status cr_hybrid_export_csr(cr_hybrid h, int64_t *row_ptr_d, int32_t *cols_d, double *vals_d, double *S_d,
+                               cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(h && row_ptr_d && cols_d && vals_d, CR_ERR_INVALID_ARG, "null argument");
+    cr::hybrid_export_csr(h, row_ptr_d, cols_d, vals_d, S_d, (cudaStream_t)s);
+    CR_API_END
+}
+
+cr_status cr_hybrid_export_shift(cr_hybrid h, uint8_t *inM1_d, double *E_d, cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(h, CR_ERR_INVALID_ARG, "null handle");
+    const cr_mesh_s *m = h->mesh;
+    copy_d2d(inM1_d, h->inM1.get(), m->nc, (cudaStream_t)s);
+    copy_d2d(E_d, h->E.get(), m->nc * (m->dim + 1) * sizeof(double), (cudaStream_t)s);
+    CR_API_END
+}
+
+cr_status cr_spmv(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(h && x_d && y_d && x_d != y_d, CR_ERR_INVALID_ARG, "bad arguments");
+    cr::spmv(h->G, x_d, y_d, (cudaStream_t)s);
+    CR_API_END
+}
+
+void cr_destroy_hybrid(cr_hybrid h) {
+    cudaDeviceSynchronize();
+    delete h;
+}
+
+cr_status cr_solve(cr_hybrid h, const cr_solver_opts *opts, double *W_d, cr_stream_t s, cr_solve_report *rep) {
+    CR_API_BEGIN
+    CR_REQUIRE(h && opts && W_d, CR_ERR_INVALID_ARG, "null argument");
+    if (rep) std::memset(rep, 0, sizeof(*rep));
+    cr::solve(h, *opts, W_d, (cudaStream_t)s, rep);
+    CR_API_END
+}
+
+cr_status cr_recover(cr_hybrid h, const double *W_d, double *U_d, double *P_d, double *diag_d, cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(h && W_d && U_d && P_d, CR_ERR_INVALID_ARG, "null argument");
+    cr::recover(h, W_d, U_d, P_d, diag_d, (cudaStream_t)s);
+    CR_API_END
+}
+
+cr_status cr_comm_init(const void *nccl_unique_id, int32_t rank, int32_t nranks, cr_comm *out) {
+    CR_API_BEGIN
+    CR_REQUIRE(out && nranks >= 1 && rank >= 0 && rank < nranks, CR_ERR_INVALID_ARG, "bad communicator arguments");
+    (void)nccl_unique_id;
+    CR_REQUIRE(nranks == 1, CR_ERR_INVALID_ARG, "multi-rank communicators are created by the partitioned driver");
+    cr_comm_s *c = new cr_comm_s();
+    c->rank = rank;
+    c->nranks = nranks;
+    *out = c;
+    CR_API_END
+}
+
+void cr_comm_destroy(cr_comm c) { delete c; }
+
+}  // extern "C"

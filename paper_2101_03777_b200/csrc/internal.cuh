@@ -1,0 +1,156 @@
+// Internal declarations of libcr (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "cr.h"
+
+namespace cr {
+
+// ------------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+    cr_status code;
+    Error(cr_status c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string &m);
+
+#define CR_CUDA(call)                                                                      \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) {                                                           \
+            throw ::cr::Error(e_ == cudaErrorMemoryAllocation ? CR_ERR_OOM : CR_ERR_CUDA,  \
+                              std::string(#call) + ": " + cudaGetErrorString(e_));         \
+        }                                                                                  \
+    } while (0)
+
+#define CR_CHECK_LAUNCH() CR_CUDA(cudaGetLastError())
+
+#define CR_REQUIRE(cond, code, msg)                     \
+    do {                                                \
+        if (!(cond)) throw ::cr::Error((code), (msg));  \
+    } while (0)
+
+// ------------------------------------------------------------------ device buffer
+template <class T>
+struct DevBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    DevBuf(DevBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf &operator=(DevBuf &&o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count, cudaStream_t s) {
+        release();
+        n = count;
+        if (count == 0) return;
+        CR_CUDA(cudaMallocAsync((void **)&p, count * sizeof(T) + 16, s));
+    }
+    void zero(cudaStream_t s) { if (n) CR_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
+    void fill_bytes(int v, cudaStream_t s) { if (n) CR_CUDA(cudaMemsetAsync(p, v, n * sizeof(T), s)); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    T *get() const { return p; }
+};
+
+// error word written by kernels (first error wins)
+enum DevErr : int {
+    DE_OK = 0, DE_RANGE = 1, DE_DEGENERATE = 2, DE_NONMANIFOLD = 3, DE_NOINTERIOR = 4,
+    DE_SINGULAR = 5, DE_BZERO = 6
+};
+
+// grid sizing: B200 has 148 SMs; streaming kernels use a fixed grid (deterministic partials)
+constexpr int kSMs = 148;
+inline int grid_for(int64_t work, int threads, int max_blocks_per_sm = 8) {
+    int64_t b = (work + threads - 1) / threads;
+    int64_t cap = (int64_t)kSMs * max_blocks_per_sm;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+}  // namespace cr
+
+// ------------------------------------------------------------------ handles
+struct cr_mesh_s {
+    int dim = 0;
+    int64_t nv = 0, nc = 0, nf = 0, nf_int = 0;
+    cr::DevBuf<int32_t> faces, face_cells, cell_faces, face_dof, dof_face;
+    cr::DevBuf<double> vol, xK, xs, a;
+};
+
+// sliced block-ELL of G
+struct BlockEll {
+    int d = 0, W = 0;            // block size, blocks per row (2d+1)
+    int64_t nrows = 0;           // block rows = nf_int
+    int64_t nslices = 0;         // ceil(nrows / 32)
+    cr::DevBuf<int32_t> cols;    // [slice][slot][lane]
+    cr::DevBuf<double> vals;     // [slice][slot*d*d + i*d + j][lane]
+    int64_t nblocks = 0;         // true (unpadded) blocks
+};
+
+namespace cr { struct SolverWork; }
+
+struct cr_hybrid_s {
+    const cr_mesh_s *mesh = nullptr;
+    cr_params prm{};
+    int is_ns = 0;
+    // owned copies of the problem data (recovery needs them again)
+    cr::DevBuf<double> fbar, dir, uit, pit;
+    bool has_dir = false, has_uit = false, has_pit = false;
+    // shift
+    cr::DevBuf<uint8_t> inM1;
+    cr::DevBuf<double> lam, E;   // lam [nc], E [nc][d+1]
+    // G, S, preconditioners
+    BlockEll G;
+    cr::DevBuf<double> S, dinv, absdinv, bdinv;   // bdinv [nrows][d][d] inverse diagonal blocks
+    cr::DevBuf<uint8_t> rowlen;                   // true blocks per block row
+    cr::SolverWork *work = nullptr;
+    ~cr_hybrid_s();
+};
+
+struct cr_coupled_s {
+    int64_t n_rows = 0, nnz = 0;
+    cr::DevBuf<int64_t> row_ptr;
+    cr::DevBuf<int32_t> cols;
+    cr::DevBuf<double> vals, rhs;
+};
+
+struct cr_comm_s {
+    int rank = 0, nranks = 1;
+};
+
+namespace cr {
+// mesh.cu
+void build_mesh(cr_mesh_s *m, int dim, int64_t nv, const double *coords, int64_t nc,
+                const int32_t *cells, cudaStream_t s);
+// hybrid.cu
+void hybridise(cr_hybrid_s *h, const cr_mesh_s *m, const cr_params &prm, const cr_data &data,
+               cudaStream_t s);
+void hybrid_export_csr(const cr_hybrid_s *h, int64_t *row_ptr, int32_t *cols, double *vals, double *S,
+                       cudaStream_t s);
+void assemble_coupled(cr_coupled_s *c, const cr_mesh_s *m, const cr_params &prm, const cr_data &data,
+                      cudaStream_t s);
+void spmv(const BlockEll &G, const double *x, double *y, cudaStream_t s);
+// recover.cu
+void recover(const cr_hybrid_s *h, const double *W, double *U, double *P, double *diag, cudaStream_t s);
+// solve.cu
+void solve(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep);
+void free_solver_work(SolverWork *w);
+// shared: copy problem data into hybrid-owned buffers
+struct ProbView;
+ProbView prob_view(const cr_hybrid_s *h);
+void copy_problem_data(cr_hybrid_s *h, const cr_mesh_s *m, const cr_data &data, cudaStream_t s);
+}  // namespace cr

@@ -1,0 +1,898 @@
+// cr_solve: Krylov solvers for G W = S on the device (§4.2-4.3).
+//
+// Every solver keeps its scalars in a device-resident KState; each reduction is a
+// deterministic two-level sum (fixed grid, per-block partials, last block sums in block
+// order) whose last block also performs the scalar recurrence (alpha, beta, Givens, ...).
+// `check_every` iterations are captured once into a CUDA graph and replayed; after each
+// replay the host reads the state (one 128-byte D2H) to test convergence.  Kernels return
+// immediately once the state flag is set, so a converged graph replay costs ~launch time.
+//
+//   PCG       (SPD G, mu > 0):  3 kernels/iter: spmv+p.q | x,r update + z=M r + r.z, r.r | p = z + beta p
+//   MINRES    (symmetric, steady): spmv+z.q | Lanczos v, z=M v, z.v + Givens | w, x update
+//   BiCGStab  (nonsymmetric, NS): p,y | spmv+rhat.v | s,z | spmv+t.s,t.t | x,r update + rhat.r, r.r
+//   GMRES(m)  (nonsymmetric): Arnoldi with classical Gram-Schmidt twice, Givens on device
+// Stopping rule: TRUE relative residual ||S - G W|| / ||S|| <= rtol (reading 12).
+#include <cmath>
+#include <cstddef>
+#include <cstring>
+
+#include "internal.cuh"
+#include "spmv.cuh"
+
+namespace cr {
+
+enum { FLAG_RUN = 0, FLAG_CONV = 1, FLAG_BREAK = 2 };
+constexpr int kMaxRestart = 128;
+
+struct KState {
+    // ---- header: read back by the host after every graph replay
+    long long iters;
+    long long wx_iter;   // MINRES: last iteration whose w/x update ran
+    int flag;
+    int k;               // GMRES: Arnoldi steps done in the current cycle
+    unsigned tickets[8];
+    double rho, alpha, beta, pq, rr, bb, tol2;
+    // MINRES
+    double gamma, gamma_old, delta, eta, eta0, c, c_old, s, s_old;
+    double a1, a2, a3, cn, eta_w, gz;
+    // BiCGStab
+    double omega, rho_new, rv, ts, tt;
+    double hnorm;
+    // ---- GMRES arrays (device only)
+    double H[(kMaxRestart + 1) * kMaxRestart];
+    double cs[kMaxRestart], sn[kMaxRestart], g[kMaxRestart + 1], h[kMaxRestart + 1], y[kMaxRestart];
+};
+constexpr size_t kStateHeader = offsetof(KState, H);
+
+struct SolverWork {
+    int64_t N = 0;
+    int D = 0;
+    DevBuf<double> x, b, r, p, q, z, z2, v, v2, w, w2, y, t, rhat;
+    DevBuf<double> V;           // GMRES basis (m+1) x N
+    DevBuf<double> partials;
+    DevBuf<KState> st;
+    KState *hst = nullptr;      // pinned
+    cudaGraphExec_t graph = nullptr;
+    int graph_key = -1;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaStream_t cap = nullptr;   // private capture stream
+    ~SolverWork() {
+        if (cap) cudaStreamDestroy(cap);
+        if (graph) cudaGraphExecDestroy(graph);
+        if (hst) cudaFreeHost(hst);
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    }
+};
+
+void free_solver_work(SolverWork *w) { delete w; }
+
+constexpr int kT = 256;
+constexpr int kMaxPartials = 8;   // values per block
+
+#define GRID_STRIDE(r, n) for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < (n); r += (int64_t)gridDim.x * blockDim.x)
+
+// preconditioner application on one block row: z = M r
+template <int D, int PREC>
+__device__ __forceinline__ void apply_prec(const double *M, int64_t r, const double (&rv)[D], double (&zv)[D]) {
+    if constexpr (PREC == 1) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) acc = fma(M[(r * D + i) * D + j], rv[j], acc);
+            zv[i] = acc;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < D; ++i) zv[i] = M[r * D + i] * rv[i];
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void ld(const double *a, int64_t r, double (&v)[D]) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) v[i] = a[r * D + i];
+}
+template <int D>
+__device__ __forceinline__ void stv(double *a, int64_t r, const double (&v)[D]) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) a[r * D + i] = v[i];
+}
+
+// ------------------------------------------------------------------ generic
+// q = G x ; r = b - q ; partial |r|^2  (true residual)
+template <int D>
+__global__ void __launch_bounds__(kT) k_true_residual(EllView<D> G, const double *x, const double *b, double *r,
+                                                      KState *st, double *partials) {
+    double acc[1] = {0.0};
+    GRID_STRIDE(row, G.nrows) {
+        double y[D];
+        spmv_row<D>(G, row, x, y);
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double ri = b[row * D + i] - y[i];
+            r[row * D + i] = ri;
+            acc[0] += ri * ri;
+        }
+    }
+    reduce_and_finish<1>(acc, partials, &st->tickets[7], [&](double *t) { st->rr = t[0]; });
+}
+
+__global__ void k_norm2(const double *a, int64_t n, KState *st, double *partials) {
+    double acc[1] = {0.0};
+    GRID_STRIDE(i, n) acc[0] += a[i] * a[i];
+    reduce_and_finish<1>(acc, partials, &st->tickets[6], [&](double *t) { st->bb = t[0]; });
+}
+
+// ------------------------------------------------------------------ PCG
+template <int D, int PREC>
+__global__ void __launch_bounds__(kT) k_pcg_init(int64_t nrows, const double *b, const double *r, double *p,
+                                                 const double *M, double rtol, KState *st, double *partials) {
+    // r already holds b - G x (k_true_residual); z = M r ; p = z ; rho = r.z
+    double acc[2] = {0.0, 0.0};
+    GRID_STRIDE(row, nrows) {
+        double rv[D], zv[D];
+        ld<D>(r, row, rv);
+        apply_prec<D, PREC>(M, row, rv, zv);
+        stv<D>(p, row, zv);
+#pragma unroll
+        for (int i = 0; i < D; ++i) { acc[0] += rv[i] * zv[i]; acc[1] += rv[i] * rv[i]; }
+    }
+    reduce_and_finish<2>(acc, partials, &st->tickets[0], [&](double *t) {
+        st->rho = t[0];
+        st->rr = t[1];
+        st->tol2 = rtol * rtol * st->bb;
+        st->flag = (t[1] <= st->tol2) ? FLAG_CONV : FLAG_RUN;
+    });
+}
+
+template <int D>
+__global__ void __launch_bounds__(kT) k_pcg_spmv(EllView<D> G, const double *p, double *q, KState *st, double *partials) {
+    if (st->flag != FLAG_RUN) return;
+    double acc[1] = {0.0};
+    GRID_STRIDE(row, G.nrows) {
+        double y[D];
+        spmv_row<D>(G, row, p, y);
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            q[row * D + i] = y[i];
+            acc[0] += p[row * D + i] * y[i];
+        }
+    }
+    reduce_and_finish<1>(acc, partials, &st->tickets[1], [&](double *t) {
+        st->pq = t[0];
+        if (!(t[0] > 0.0)) st->flag = FLAG_BREAK;
+        else st->alpha = st->rho / t[0];
+    });
+}
+
+template <int D, int PREC>
+__global__ void __launch_bounds__(kT) k_pcg_update(int64_t nrows, double *x, double *r, const double *p, const double *q,
+                                                   const double *M, KState *st, double *partials) {
+    if (st->flag != FLAG_RUN) return;
+    const double alpha = st->alpha;
+    double acc[2] = {0.0, 0.0};
+    GRID_STRIDE(row, nrows) {
+        double rv[D], zv[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            x[row * D + i] = fma(alpha, p[row * D + i], x[row * D + i]);
+            rv[i] = fma(-alpha, q[row * D + i], r[row * D + i]);
+            r[row * D + i] = rv[i];
+        }
+        apply_prec<D, PREC>(M, row, rv, zv);
+#pragma unroll
+        for (int i = 0; i < D; ++i) { acc[0] += rv[i] * zv[i]; acc[1] += rv[i] * rv[i]; }
+    }
+    reduce_and_finish<2>(acc, partials, &st->tickets[2], [&](double *t) {
+        st->iters += 1;
+        st->rr = t[1];
+        st->beta = t[0] / st->rho;
+        st->rho = t[0];
+        if (t[1] <= st->tol2) st->flag = FLAG_CONV;
+    });
+}
+
+template <int D, int PREC>
+__global__ void __launch_bounds__(kT) k_pcg_pdir(int64_t nrows, double *p, const double *r, const double *M, const KState *st) {
+    if (st->flag != FLAG_RUN) return;
+    const double beta = st->beta;
+    GRID_STRIDE(row, nrows) {
+        double rv[D], zv[D];
+        ld<D>(r, row, rv);
+        apply_prec<D, PREC>(M, row, rv, zv);
+#pragma unroll
+        for (int i = 0; i < D; ++i) p[row * D + i] = fma(beta, p[row * D + i], zv[i]);
+    }
+}
+
+// ------------------------------------------------------------------ MINRES (preconditioned, SPD M)
+// Paige-Saunders recurrences in the Elman-Silvester-Wathen form (oracle/krylov.py minres):
+// z_j = M v_j / gamma_j; delta = z_j^t G z_j; v_{j+1} = G z_j - delta/gamma v_j - gamma/gamma_old v_{j-1}
+template <int D>
+__global__ void __launch_bounds__(kT) k_minres_init(int64_t nrows, const double *v, double *z, const double *M,
+                                                    double *w, double *w2, double *vold, KState *st, double *partials) {
+    double acc[1] = {0.0};
+    GRID_STRIDE(row, nrows) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double vi = v[row * D + i], zi = M[row * D + i] * vi;
+            z[row * D + i] = zi;
+            w[row * D + i] = 0.0;
+            w2[row * D + i] = 0.0;
+            vold[row * D + i] = 0.0;
+            acc[0] += zi * vi;
+        }
+    }
+    reduce_and_finish<1>(acc, partials, &st->tickets[0], [&](double *t) {
+        double gm = sqrt(fmax(t[0], 0.0));
+        st->gamma = gm;
+        st->gamma_old = 1.0;
+        st->eta = gm;
+        st->eta0 = gm;
+        st->s = st->s_old = 0.0;
+        st->c = st->c_old = 1.0;
+        st->flag = (gm == 0.0) ? FLAG_CONV : FLAG_RUN;
+    });
+}
+
+template <int D>
+__global__ void __launch_bounds__(kT) k_minres_spmv(EllView<D> G, const double *z, double *q, KState *st, double *partials) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->wx_iter = st->iters;   // previous w/x update has completed
+    if (st->flag != FLAG_RUN) return;
+    double acc[1] = {0.0};
+    GRID_STRIDE(row, G.nrows) {
+        double y[D];
+        spmv_row<D>(G, row, z, y);
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            q[row * D + i] = y[i];
+            acc[0] += z[row * D + i] * y[i];
+        }
+    }
+    reduce_and_finish<1>(acc, partials, &st->tickets[1], [&](double *t) {
+        st->delta = t[0] / (st->gamma * st->gamma);
+    });
+}
+
+// v_new (written over v_old) = q/gamma - delta/gamma v - gamma/gamma_old v_old ; z_new = M v_new
+template <int D>
+__global__ void __launch_bounds__(kT) k_minres_lanczos(int64_t nrows, const double *q, const double *v, double *vold_new,
+                                                       double *znew, const double *M, KState *st, double *partials) {
+    if (st->flag != FLAG_RUN) return;
+    const double gm = st->gamma, go = st->gamma_old, dl = st->delta;
+    const double c1 = 1.0 / gm, c2 = dl / gm, c3 = gm / go;
+    double acc[1] = {0.0};
+    GRID_STRIDE(row, nrows) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int64_t k = row * D + i;
+            double vn = q[k] * c1 - c2 * v[k] - c3 * vold_new[k];
+            double zn = M[k] * vn;
+            vold_new[k] = vn;
+            znew[k] = zn;
+            acc[0] += zn * vn;
+        }
+    }
+    reduce_and_finish<1>(acc, partials, &st->tickets[2], [&](double *t) {
+        const double gn = sqrt(fmax(t[0], 0.0));
+        const double gmo = st->gamma, dlo = st->delta;
+        const double a0 = st->c * dlo - st->c_old * st->s * gmo;
+        const double a1 = sqrt(a0 * a0 + gn * gn);
+        const double a2 = st->s * dlo + st->c_old * st->c * gmo;
+        const double a3 = st->s_old * gmo;
+        const double cn = a0 / a1, sn = gn / a1;
+        st->a1 = a1; st->a2 = a2; st->a3 = a3; st->cn = cn;
+        st->eta_w = st->eta;
+        st->gz = gmo;
+        st->eta = -sn * st->eta;
+        st->gamma_old = gmo;
+        st->gamma = gn;
+        st->c_old = st->c; st->c = cn;
+        st->s_old = st->s; st->s = sn;
+        st->iters += 1;
+        if (gn == 0.0) st->flag = FLAG_CONV;          // exact invariant subspace
+    });
+}
+
+// w_new (written over w_old) = (z/gz - a3 w_old - a2 w)/a1 ; x += cn eta_w w_new
+template <int D>
+__global__ void __launch_bounds__(kT) k_minres_wx(int64_t nrows, const double *z, const double *w, double *wold_new,
+                                                  double *x, const KState *st) {
+    if (st->flag == FLAG_BREAK) return;
+    if (st->wx_iter >= st->iters) return;   // no pending Lanczos step
+    const double inv_gz = 1.0 / st->gz, a1 = st->a1, a2 = st->a2, a3 = st->a3, f = st->cn * st->eta_w;
+    GRID_STRIDE(row, nrows) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int64_t k = row * D + i;
+            double wn = (z[k] * inv_gz - a3 * wold_new[k] - a2 * w[k]) / a1;
+            wold_new[k] = wn;
+            x[k] = fma(f, wn, x[k]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ BiCGStab (right Jacobi)
+template <int D>
+__global__ void __launch_bounds__(kT) k_bicg_init(int64_t nrows, const double *r, double *rhat, double *p, double *v,
+                                                  double rtol, KState *st, double *partials) {
+    double acc[1] = {0.0};
+    GRID_STRIDE(row, nrows) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int64_t k = row * D + i;
+            rhat[k] = r[k];
+            p[k] = 0.0;
+            v[k] = 0.0;
+            acc[0] += r[k] * r[k];
+        }
+    }
+    reduce_and_finish<1>(acc, partials, &st->tickets[0], [&](double *t) {
+        st->rho = 1.0; st->alpha = 1.0; st->omega = 1.0;
+        st->rho_new = t[0];
+        st->rr = t[0];
+        st->tol2 = rtol * rtol * st->bb;
+        st->flag = (t[0] <= st->tol2) ? FLAG_CONV : (t[0] == 0.0 ? FLAG_BREAK : FLAG_RUN);
+    });
+}
+
+template <int D>
+__global__ void __launch_bounds__(kT) k_bicg_pdir(int64_t nrows, const double *r, double *p, const double *v,
+                                                  double *y, const double *M, const KState *st) {
+    if (st->flag != FLAG_RUN) return;
+    const double beta = (st->rho_new / st->rho) * (st->alpha / st->omega), om = st->omega;
+    GRID_STRIDE(row, nrows) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int64_t k = row * D + i;
+            double pk = r[k] + beta * (p[k] - om * v[k]);
+            p[k] = pk;
+            y[k] = M[k] * pk;
+        }
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kT) k_bicg_spmv1(EllView<D> G, const double *y, double *v, const double *rhat,
+                                                   KState *st, double *partials) {
+    if (st->flag != FLAG_RUN) return;
+    double acc[1] = {0.0};
+    GRID_STRIDE(row, G.nrows) {
+        double o[D];
+        spmv_row<D>(G, row, y, o);
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            v[row * D + i] = o[i];
+            acc[0] += rhat[row * D + i] * o[i];
+        }
+    }
+    reduce_and_finish<1>(acc, partials, &st->tickets[1], [&](double *t) {
+        st->rv = t[0];
+        if (t[0] == 0.0) st->flag = FLAG_BREAK;
+        else st->alpha = st->rho_new / t[0];
+    });
+}
+
+template <int D>
+__global__ void __launch_bounds__(kT) k_bicg_s(int64_t nrows, double *r, const double *v, double *z, const double *M,
+                                               const KState *st) {
+    if (st->flag != FLAG_RUN) return;
+    const double al = st->alpha;
+    GRID_STRIDE(row, nrows) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int64_t k = row * D + i;
+            double sk = fma(-al, v[k], r[k]);
+            r[k] = sk;                 // r now holds s
+            z[k] = M[k] * sk;
+        }
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kT) k_bicg_spmv2(EllView<D> G, const double *z, double *t, const double *s,
+                                                   KState *st, double *partials) {
+    if (st->flag != FLAG_RUN) return;
+    double acc[2] = {0.0, 0.0};
+    GRID_STRIDE(row, G.nrows) {
+        double o[D];
+        spmv_row<D>(G, row, z, o);
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            t[row * D + i] = o[i];
+            acc[0] += o[i] * s[row * D + i];
+            acc[1] += o[i] * o[i];
+        }
+    }
+    reduce_and_finish<2>(acc, partials, &st->tickets[3], [&](double *t2) {
+        st->ts = t2[0];
+        st->tt = t2[1];
+        st->omega = t2[1] > 0.0 ? t2[0] / t2[1] : 0.0;
+    });
+}
+
+template <int D>
+__global__ void __launch_bounds__(kT) k_bicg_xr(int64_t nrows, double *x, double *r, const double *y, const double *z,
+                                                const double *t, const double *rhat, KState *st, double *partials) {
+    if (st->flag != FLAG_RUN) return;
+    const double al = st->alpha, om = st->omega;
+    double acc[2] = {0.0, 0.0};
+    GRID_STRIDE(row, nrows) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int64_t k = row * D + i;
+            x[k] = x[k] + al * y[k] + om * z[k];
+            double rk = fma(-om, t[k], r[k]);
+            r[k] = rk;
+            acc[0] += rhat[k] * rk;
+            acc[1] += rk * rk;
+        }
+    }
+    reduce_and_finish<2>(acc, partials, &st->tickets[4], [&](double *t2) {
+        st->iters += 1;
+        st->rho = st->rho_new;
+        st->rho_new = t2[0];
+        st->rr = t2[1];
+        if (t2[1] <= st->tol2) st->flag = FLAG_CONV;
+        else if (t2[0] == 0.0 || st->omega == 0.0) st->flag = FLAG_BREAK;
+    });
+}
+
+// ------------------------------------------------------------------ GMRES(m), right Jacobi
+__global__ void k_gmres_start(int64_t n, const double *r, double *V0, KState *st) {
+    // V0 = r / ||r|| (||r||^2 in st->rr); g = (beta, 0, ...)
+    const double beta = sqrt(st->rr);
+    const double inv = beta > 0 ? 1.0 / beta : 0.0;
+    GRID_STRIDE(i, n) V0[i] = r[i] * inv;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->g[0] = beta;
+        st->k = 0;
+        st->flag = (st->rr <= st->tol2) ? FLAG_CONV : FLAG_RUN;
+    }
+}
+
+__global__ void k_scale(int64_t n, const double *M, const double *a, double *out, const KState *st) {
+    if (st->flag != FLAG_RUN) return;
+    GRID_STRIDE(i, n) out[i] = M[i] * a[i];
+}
+
+template <int D>
+__global__ void __launch_bounds__(kT) k_spmv_guard(EllView<D> G, const double *x, double *y, const KState *st) {
+    if (st->flag != FLAG_RUN) return;
+    GRID_STRIDE(row, G.nrows) {
+        double o[D];
+        spmv_row<D>(G, row, x, o);
+#pragma unroll
+        for (int i = 0; i < D; ++i) y[row * D + i] = o[i];
+    }
+}
+
+// h[j] (+)= V_j . w for j = 0..k  (classical Gram-Schmidt pass), block-level partials per j
+__global__ void __launch_bounds__(kT) k_gmres_dots(int64_t n, int k, const double *V, const double *w, KState *st,
+                                                   double *partials, int accumulate) {
+    if (st->flag != FLAG_RUN) return;
+    __shared__ double sh[32];
+    __shared__ int s_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = 0; j <= k; ++j) {
+        double acc = 0.0;
+        GRID_STRIDE(i, n) acc += V[(int64_t)j * n + i] * w[i];
+        acc = warp_sum(acc);
+        if (lane == 0) sh[warp] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < nw; ++q) t += sh[q];
+            partials[(int64_t)blockIdx.x * (kMaxRestart + 1) + j] = t;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        unsigned tk = atomicAdd(&st->tickets[5], 1u);
+        s_last = (tk == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int j = 0; j <= k; ++j) {
+        double acc = 0.0;
+        for (int bidx = threadIdx.x; bidx < (int)gridDim.x; bidx += blockDim.x)
+            acc += __ldcg(partials + (int64_t)bidx * (kMaxRestart + 1) + j);
+        acc = warp_sum(acc);
+        __syncthreads();
+        if (lane == 0) sh[warp] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < nw; ++q) t += sh[q];
+            st->h[j] = accumulate ? st->h[j] + t : t;
+        }
+    }
+    if (threadIdx.x == 0) st->tickets[5] = 0u;
+}
+
+// w -= sum_j h_j V_j (only the increment of this pass: hnew - hold kept in y[])
+__global__ void __launch_bounds__(kT) k_gmres_orth(int64_t n, int k, const double *V, double *w, const KState *st, int pass) {
+    if (st->flag != FLAG_RUN) return;
+    GRID_STRIDE(i, n) {
+        double acc = w[i];
+        for (int j = 0; j <= k; ++j) acc -= (pass == 0 ? st->h[j] : st->h[j] - st->y[j]) * V[(int64_t)j * n + i];
+        w[i] = acc;
+    }
+}
+
+__global__ void k_gmres_keep_h(KState *st, int k) {
+    if (st->flag != FLAG_RUN) return;
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+        for (int j = 0; j <= k; ++j) st->y[j] = st->h[j];
+}
+
+// ||w|| then Givens update of column k (thread 0 of the last block)
+__global__ void __launch_bounds__(kT) k_gmres_norm_givens(int64_t n, int k, const double *w, KState *st, double *partials) {
+    if (st->flag != FLAG_RUN) return;
+    double acc[1] = {0.0};
+    GRID_STRIDE(i, n) acc[0] += w[i] * w[i];
+    reduce_and_finish<1>(acc, partials, &st->tickets[6], [&](double *t) {
+        const int m1 = kMaxRestart;
+        double hk1 = sqrt(t[0]);
+        st->hnorm = hk1;
+        double col[kMaxRestart + 1];
+        for (int j = 0; j <= k; ++j) col[j] = st->h[j];
+        col[k + 1] = hk1;
+        for (int j = 0; j < k; ++j) {
+            double a = st->cs[j] * col[j] + st->sn[j] * col[j + 1];
+            col[j + 1] = -st->sn[j] * col[j] + st->cs[j] * col[j + 1];
+            col[j] = a;
+        }
+        double den = hypot(col[k], col[k + 1]);
+        double cs = den > 0 ? col[k] / den : 1.0, sn = den > 0 ? col[k + 1] / den : 0.0;
+        st->cs[k] = cs;
+        st->sn[k] = sn;
+        col[k] = den;
+        for (int j = 0; j <= k; ++j) st->H[j * m1 + k] = col[j];
+        st->g[k + 1] = -sn * st->g[k];
+        st->g[k] = cs * st->g[k];
+        st->k = k + 1;
+        st->iters += 1;
+        if (fabs(st->g[k + 1]) * fabs(st->g[k + 1]) <= st->tol2 || hk1 == 0.0 || den == 0.0) st->flag = FLAG_CONV;
+    });
+}
+
+__global__ void k_gmres_next(int64_t n, const double *w, double *Vk1, const KState *st) {
+    if (st->flag != FLAG_RUN) return;
+    const double inv = 1.0 / st->hnorm;
+    GRID_STRIDE(i, n) Vk1[i] = w[i] * inv;
+}
+
+// y = H^{-1} g (upper triangular, st->k columns) ; x += M (V y)
+__global__ void k_gmres_solve_y(KState *st) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int k = st->k, m1 = kMaxRestart;
+    for (int i = k - 1; i >= 0; --i) {
+        double acc = st->g[i];
+        for (int j = i + 1; j < k; ++j) acc -= st->H[i * m1 + j] * st->y[j];
+        st->y[i] = acc / st->H[i * m1 + i];
+    }
+}
+
+__global__ void __launch_bounds__(kT) k_gmres_update_x(int64_t n, const double *V, const double *M, double *x, const KState *st) {
+    const int k = st->k;
+    GRID_STRIDE(i, n) {
+        double acc = 0.0;
+        for (int j = 0; j < k; ++j) acc += st->y[j] * V[(int64_t)j * n + i];
+        x[i] = fma(M[i], acc, x[i]);
+    }
+}
+
+// ------------------------------------------------------------------ host driver
+static void ensure_work(cr_hybrid_s *h, cudaStream_t s) {
+    const int D = h->G.d;
+    const int64_t N = h->G.nrows * D;
+    if (h->work && h->work->N == N) return;
+    delete h->work;
+    SolverWork *w = new SolverWork();
+    h->work = w;
+    w->N = N;
+    w->D = D;
+    for (DevBuf<double> *b : {&w->x, &w->b, &w->r, &w->p, &w->q, &w->z, &w->z2, &w->v, &w->v2, &w->w, &w->w2, &w->y,
+                              &w->t, &w->rhat}) {
+        b->alloc(N, s);
+        b->zero(s);
+    }
+    w->partials.alloc((size_t)kSMs * 16 * (kMaxRestart + 1), s);
+    w->st.alloc(1, s);
+    w->st.zero(s);
+    CR_CUDA(cudaMallocHost((void **)&w->hst, sizeof(KState)));
+    CR_CUDA(cudaEventCreate(&w->e0));
+    CR_CUDA(cudaEventCreate(&w->e1));
+    CR_CUDA(cudaStreamCreateWithFlags(&w->cap, cudaStreamNonBlocking));
+}
+
+struct Launcher {
+    cr_hybrid_s *h;
+    SolverWork *w;
+    cudaStream_t s;
+    int64_t launches = 0;
+    int64_t spmvs = 0;
+    int D;
+    int64_t nrows, N;
+    int grid_rows, grid_vec;
+};
+
+template <int D>
+static EllView<D> ell(const cr_hybrid_s *h) { return EllView<D>{h->G.cols.get(), h->G.vals.get(), h->G.nrows}; }
+
+static void read_state(SolverWork *w, cudaStream_t s) {
+    CR_CUDA(cudaMemcpyAsync(w->hst, w->st.get(), kStateHeader, cudaMemcpyDeviceToHost, s));
+    CR_CUDA(cudaStreamSynchronize(s));
+}
+
+template <int D>
+static void true_residual(Launcher &L, const double *x, double *r) {
+    k_true_residual<D><<<L.grid_rows, kT, 0, L.s>>>(ell<D>(L.h), x, L.w->b.get(), r, L.w->st.get(), L.w->partials.get());
+    CR_CHECK_LAUNCH();
+    ++L.launches;
+    ++L.spmvs;
+}
+
+// run `body` k times inside a CUDA graph (captured once per (method, k)), replay until done
+// The body launches on `ks`; it is captured on the work's private non-blocking stream (the
+// caller's stream may be the legacy default stream, which cannot capture) and the graph is
+// then launched on the caller's stream.
+template <class Body, class Done>
+static void graph_loop(Launcher &L, cudaStream_t &ks, int key, int k, Body body, Done done) {
+    SolverWork *w = L.w;
+    if (w->graph_key != key) {
+        if (w->graph) { cudaGraphExecDestroy(w->graph); w->graph = nullptr; }
+        cudaGraph_t g;
+        ks = w->cap;
+        CR_CUDA(cudaStreamBeginCapture(w->cap, cudaStreamCaptureModeThreadLocal));
+        int64_t l0 = L.launches, s0 = L.spmvs;
+        for (int i = 0; i < k; ++i) body(i);
+        L.launches = l0;
+        L.spmvs = s0;
+        CR_CUDA(cudaStreamEndCapture(w->cap, &g));
+        ks = L.s;
+        CR_CUDA(cudaGraphInstantiate(&w->graph, g, 0));
+        CR_CUDA(cudaGraphDestroy(g));
+        w->graph_key = key;
+    }
+    while (true) {
+        CR_CUDA(cudaGraphLaunch(w->graph, L.s));
+        read_state(w, L.s);
+        if (done()) break;
+    }
+}
+
+template <int D>
+static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep) {
+    ensure_work(h, s);
+    SolverWork *w = h->work;
+    Launcher L{h, w, s};
+    cudaStream_t ks = s;   // stream the captured bodies launch on (swapped during capture)
+    L.D = D;
+    L.nrows = h->G.nrows;
+    L.N = w->N;
+    L.grid_rows = grid_for(L.nrows, kT);
+    L.grid_vec = grid_for(L.N, kT);
+    const int64_t N = w->N, nrows = L.nrows;
+    const double rtol = o.rtol > 0 ? o.rtol : 1e-10;
+    const int64_t max_iter = o.max_iter > 0 ? o.max_iter : 10000000;
+    int kk = o.check_every > 0 ? o.check_every : 64;
+    kk = (kk + 1) & ~1;   // even: MINRES buffer rotation has period 2
+    double *x = w->x.get();
+    CR_CUDA(cudaMemcpyAsync(x, W, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CR_CUDA(cudaMemcpyAsync(w->b.get(), h->S.get(), N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CR_CUDA(cudaMemsetAsync(w->st.get(), 0, sizeof(KState), s));
+    CR_CUDA(cudaEventRecord(w->e0, s));
+    double *part = w->partials.get();
+    KState *st = w->st.get();
+    k_norm2<<<L.grid_vec, kT, 0, s>>>(w->b.get(), N, st, part);
+    CR_CHECK_LAUNCH();
+    ++L.launches;
+    cr_status status = CR_OK;
+    int replacements = 0;
+    const int method = o.method;
+
+    if (method == CR_PCG_JACOBI || method == CR_PCG_BLOCKJACOBI) {
+        const bool blk = method == CR_PCG_BLOCKJACOBI;
+        const double *M = blk ? h->bdinv.get() : h->dinv.get();
+        auto init = [&]() {
+            true_residual<D>(L, x, w->r.get());
+            if (blk) k_pcg_init<D, 1><<<L.grid_rows, kT, 0, s>>>(nrows, w->b.get(), w->r.get(), w->p.get(), M, rtol, st, part);
+            else k_pcg_init<D, 0><<<L.grid_rows, kT, 0, s>>>(nrows, w->b.get(), w->r.get(), w->p.get(), M, rtol, st, part);
+            CR_CHECK_LAUNCH();
+            ++L.launches;
+        };
+        init();
+        read_state(w, s);
+        if (w->hst->bb == 0.0) { CR_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), s)); }
+        while (w->hst->flag == FLAG_RUN) {
+            auto body = [&](int) {
+                k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part);
+                if (blk) {
+                    k_pcg_update<D, 1><<<L.grid_rows, kT, 0, ks>>>(nrows, x, w->r.get(), w->p.get(), w->q.get(), M, st, part);
+                    k_pcg_pdir<D, 1><<<L.grid_rows, kT, 0, ks>>>(nrows, w->p.get(), w->r.get(), M, st);
+                } else {
+                    k_pcg_update<D, 0><<<L.grid_rows, kT, 0, ks>>>(nrows, x, w->r.get(), w->p.get(), w->q.get(), M, st, part);
+                    k_pcg_pdir<D, 0><<<L.grid_rows, kT, 0, ks>>>(nrows, w->p.get(), w->r.get(), M, st);
+                }
+                CR_CHECK_LAUNCH();
+            };
+            int64_t it0 = w->hst->iters;
+            graph_loop(L, ks, method * 100000 + kk, kk, body, [&]() {
+                return w->hst->flag != FLAG_RUN || w->hst->iters >= max_iter;
+            });
+            int64_t dit = w->hst->iters - it0;
+            L.launches += 3 * ((dit + kk - 1) / kk) * kk;
+            L.spmvs += dit;
+            if (w->hst->flag == FLAG_CONV) {
+                // recursive residual converged: check the true residual (residual replacement)
+                init();
+                read_state(w, s);
+                if (w->hst->flag == FLAG_CONV || replacements >= 8) break;
+                ++replacements;
+            }
+            if (w->hst->flag == FLAG_BREAK) { status = CR_ERR_BREAKDOWN; break; }
+            if (w->hst->iters >= max_iter) { status = CR_ERR_NOT_CONVERGED; break; }
+        }
+    } else if (method == CR_MINRES_ABSJACOBI) {
+        const double *M = h->absdinv.get();
+        double *va = w->v.get(), *vb = w->v2.get(), *za = w->z.get(), *zb = w->z2.get();
+        double *wa = w->w.get(), *wb = w->w2.get();
+        // v = b - G x
+        true_residual<D>(L, x, va);
+        k_minres_init<D><<<L.grid_rows, kT, 0, s>>>(nrows, va, za, M, wa, wb, vb, st, part);
+        CR_CHECK_LAUNCH();
+        ++L.launches;
+        read_state(w, s);
+        const double bnorm = sqrt(w->hst->bb);
+        // iteration j uses (v=va, vold=vb, z=za, znew->zb, w=wa, wold->wb) then swaps
+        auto body = [&](int i) {
+            double *v = (i & 1) ? vb : va, *vold = (i & 1) ? va : vb;
+            double *z = (i & 1) ? zb : za, *zn = (i & 1) ? za : zb;
+            double *ww = (i & 1) ? wb : wa, *wold = (i & 1) ? wa : wb;
+            k_minres_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), z, w->q.get(), st, part);
+            k_minres_lanczos<D><<<L.grid_rows, kT, 0, ks>>>(nrows, w->q.get(), v, vold, zn, M, st, part);
+            k_minres_wx<D><<<L.grid_rows, kT, 0, ks>>>(nrows, z, ww, wold, x, st);
+            CR_CHECK_LAUNCH();
+        };
+        while (w->hst->flag == FLAG_RUN) {
+            int64_t it0 = w->hst->iters;
+            graph_loop(L, ks, method * 100000 + kk, kk, body, [&]() { return true; });
+            int64_t dit = w->hst->iters - it0;
+            L.launches += 3 * kk;
+            L.spmvs += dit;
+            // true residual check every graph replay (r goes to the scratch t buffer)
+            true_residual<D>(L, x, w->t.get());
+            read_state(w, s);
+            const double tr = sqrt(w->hst->rr);
+            if (tr <= rtol * bnorm) { w->hst->flag = FLAG_CONV; break; }
+            if (w->hst->flag != FLAG_RUN) {
+                status = w->hst->flag == FLAG_BREAK ? CR_ERR_BREAKDOWN : CR_ERR_STAGNATION;
+                break;
+            }
+            if (w->hst->iters >= max_iter) { status = CR_ERR_NOT_CONVERGED; break; }
+        }
+    } else if (method == CR_BICGSTAB_JACOBI) {
+        const double *M = h->dinv.get();
+        true_residual<D>(L, x, w->r.get());
+        k_bicg_init<D><<<L.grid_rows, kT, 0, s>>>(nrows, w->r.get(), w->rhat.get(), w->p.get(), w->v.get(), rtol, st, part);
+        CR_CHECK_LAUNCH();
+        ++L.launches;
+        read_state(w, s);
+        auto body = [&](int) {
+            k_bicg_pdir<D><<<L.grid_rows, kT, 0, ks>>>(nrows, w->r.get(), w->p.get(), w->v.get(), w->y.get(), M, st);
+            k_bicg_spmv1<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->y.get(), w->v.get(), w->rhat.get(), st, part);
+            k_bicg_s<D><<<L.grid_rows, kT, 0, ks>>>(nrows, w->r.get(), w->v.get(), w->z.get(), M, st);
+            k_bicg_spmv2<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->z.get(), w->t.get(), w->r.get(), st, part);
+            k_bicg_xr<D><<<L.grid_rows, kT, 0, ks>>>(nrows, x, w->r.get(), w->y.get(), w->z.get(), w->t.get(),
+                                                   w->rhat.get(), st, part);
+            CR_CHECK_LAUNCH();
+        };
+        while (w->hst->flag == FLAG_RUN) {
+            int64_t it0 = w->hst->iters;
+            graph_loop(L, ks, method * 100000 + kk, kk, body, [&]() {
+                return w->hst->flag != FLAG_RUN || w->hst->iters >= max_iter;
+            });
+            int64_t dit = w->hst->iters - it0;
+            L.launches += 5 * ((dit + kk - 1) / kk) * kk;
+            L.spmvs += 2 * dit;
+            if (w->hst->flag == FLAG_CONV) {
+                true_residual<D>(L, x, w->t.get());
+                read_state(w, s);
+                if (w->hst->rr <= w->hst->tol2 || replacements >= 8) { w->hst->flag = FLAG_CONV; break; }
+                ++replacements;   // restart from the true residual
+                true_residual<D>(L, x, w->r.get());
+                k_bicg_init<D><<<L.grid_rows, kT, 0, s>>>(nrows, w->r.get(), w->rhat.get(), w->p.get(), w->v.get(), rtol, st, part);
+                CR_CHECK_LAUNCH();
+                read_state(w, s);
+                continue;
+            }
+            if (w->hst->flag == FLAG_BREAK) { status = CR_ERR_BREAKDOWN; break; }
+            if (w->hst->iters >= max_iter) { status = CR_ERR_NOT_CONVERGED; break; }
+        }
+    } else if (method == CR_GMRES_JACOBI) {
+        const double *M = h->dinv.get();
+        int m = o.restart > 0 ? o.restart : 50;
+        CR_REQUIRE(m <= kMaxRestart, CR_ERR_INVALID_ARG, "GMRES restart must be <= 128");
+        if (w->V.n < (size_t)(m + 1) * N) w->V.alloc((size_t)(m + 1) * N, s);
+        double *V = w->V.get();
+        double best = INFINITY;
+        int stagn = 0;
+        auto cycle = [&](int) {
+            for (int k = 0; k < m; ++k) {
+                double *Vk = V + (int64_t)k * N;
+                k_scale<<<L.grid_vec, kT, 0, ks>>>(N, M, Vk, w->y.get(), st);
+                k_spmv_guard<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->y.get(), w->w.get(), st);
+                k_gmres_dots<<<L.grid_vec, kT, 0, ks>>>(N, k, V, w->w.get(), st, part, 0);
+                k_gmres_orth<<<L.grid_vec, kT, 0, ks>>>(N, k, V, w->w.get(), st, 0);
+                k_gmres_keep_h<<<1, 32, 0, ks>>>(st, k);
+                k_gmres_dots<<<L.grid_vec, kT, 0, ks>>>(N, k, V, w->w.get(), st, part, 1);
+                k_gmres_orth<<<L.grid_vec, kT, 0, ks>>>(N, k, V, w->w.get(), st, 1);
+                k_gmres_norm_givens<<<L.grid_vec, kT, 0, ks>>>(N, k, w->w.get(), st, part);
+                k_gmres_next<<<L.grid_vec, kT, 0, ks>>>(N, w->w.get(), V + (int64_t)(k + 1) * N, st);
+                CR_CHECK_LAUNCH();
+            }
+        };
+        while (true) {
+            true_residual<D>(L, x, w->r.get());
+            read_state(w, s);
+            const double rn = sqrt(w->hst->rr);
+            if (w->hst->bb == 0.0 || rn <= rtol * sqrt(w->hst->bb)) break;
+            if (rn >= best * (1.0 - 1e-12)) { if (++stagn >= 2) { status = CR_ERR_STAGNATION; break; } }
+            else stagn = 0;
+            best = fmin(best, rn);
+            if (w->hst->iters >= max_iter) { status = CR_ERR_NOT_CONVERGED; break; }
+            // set tol2 then start the cycle
+            KState tmp = *w->hst;
+            tmp.tol2 = rtol * rtol * tmp.bb;
+            CR_CUDA(cudaMemcpyAsync(&st->tol2, &tmp.tol2, sizeof(double), cudaMemcpyHostToDevice, s));
+            k_gmres_start<<<L.grid_vec, kT, 0, s>>>(N, w->r.get(), V, st);
+            CR_CHECK_LAUNCH();
+            graph_loop(L, ks, method * 100000 + m, 1, cycle, [&]() { return true; });
+            k_gmres_solve_y<<<1, 32, 0, s>>>(st);
+            k_gmres_update_x<<<L.grid_vec, kT, 0, s>>>(N, V, M, x, st);
+            CR_CHECK_LAUNCH();
+            read_state(w, s);
+            L.launches += 9 * m + 3;
+            L.spmvs += w->hst->k + 1;
+        }
+    } else {
+        throw Error(CR_ERR_INVALID_ARG, "unknown solver method");
+    }
+    CR_CUDA(cudaEventRecord(w->e1, s));
+    // final true residual
+    true_residual<D>(L, x, w->t.get());
+    read_state(w, s);
+    float ms = 0.f;
+    CR_CUDA(cudaEventElapsedTime(&ms, w->e0, w->e1));
+    const double bn = sqrt(w->hst->bb);
+    const double tr = bn > 0 ? sqrt(w->hst->rr) / bn : 0.0;
+    CR_CUDA(cudaMemcpyAsync(W, x, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CR_CUDA(cudaStreamSynchronize(s));
+    if (status == CR_OK && !(tr <= rtol)) status = CR_ERR_NOT_CONVERGED;
+    if (rep) {
+        rep->iterations = w->hst->iters;
+        rep->rel_res_true = tr;
+        rep->rel_res_recursive = (method == CR_MINRES_ABSJACOBI)
+                                     ? fabs(w->hst->eta) / (w->hst->eta0 > 0 ? w->hst->eta0 : 1.0)
+                                     : tr;
+        rep->converged = status == CR_OK;
+        rep->status = status;
+        rep->seconds = ms * 1e-3;
+        rep->spmv_calls = L.spmvs;
+        rep->kernel_launches = L.launches;
+    }
+    if (status != CR_OK) throw Error(status, "solver did not converge (see report)");
+}
+
+void solve(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep) {
+    if (h->G.d == 2) solve_t<2>(h, o, W, s, rep);
+    else solve_t<3>(h, o, W, s, rep);
+}
+
+}  // namespace cr

@@ -1,0 +1,270 @@
+"""GPU parity: the CUDA path (through the C ABI, via the thin binding) against the CPU
+oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star):
+  * connectivity, face numbering, MIS membership, sparsity patterns: bit-exact;
+  * assembled entries (G, S, coupled A/D/R/g): |dG_ij| <= 1e-12 max_j |G_ij| (row-relative);
+  * solved U and P: relative L2 <= 1e-8 against the oracle's refined direct solution,
+    solves driven to a true relative residual of 1e-12 (small cases) / 1e-10 (full size).
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch
+
+import cr_inputs as ci
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+import paper_2101_03777_b200 as P  # noqa: E402
+
+DEV = torch.device("cuda")
+
+
+def tg(x, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(x))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(DEV)
+
+
+def relL2(x, y):
+    return float(np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-300))
+
+
+def to_scipy(rp, ci_, v, n):
+    return sp.csr_matrix((v.cpu().numpy(), ci_.cpu().numpy(), rp.cpu().numpy()), shape=(n, n))
+
+
+def row_rel_err(Ag, Ao):
+    """max_i max_j |Ag_ij - Ao_ij| / max_j |Ao_ij|"""
+    Ag, Ao = Ag.tocsr(), Ao.tocsr()
+    Dm = (Ag - Ao).tocsr()
+    Dm.data = np.abs(Dm.data)
+    Aa = Ao.copy()
+    Aa.data = np.abs(Aa.data)
+    dm = np.asarray(Dm.max(axis=1).todense()).ravel()
+    am = np.asarray(Aa.max(axis=1).todense()).ravel()
+    return float(np.max(dm / np.where(am > 0, am, 1.0)))
+
+
+def same_pattern(Ag, Ao):
+    Ag, Ao = Ag.tocsr(), Ao.tocsr()
+    Ag.sort_indices(); Ao.sort_indices()
+    return np.array_equal(Ag.indptr, Ao.indptr) and np.array_equal(Ag.indices, Ao.indices)
+
+
+# ------------------------------------------------------------------ cases
+def make_case(dim, n, mu=1.0, nu=1.0, shift="none", jitter=0.2, seed=1, force="manufactured",
+              ns=False, dirichlet=False, k0=0):
+    if dim == 2:
+        coords, cells = ci.square_mesh(n, jitter, seed)
+    else:
+        coords, cells = ci.cube_mesh(n)
+    nc = cells.shape[0]
+    if force == "manufactured":
+        _, _, f = (ci.manufactured_2d if dim == 2 else ci.manufactured_3d)(mu, nu)
+        fbar = ci.cell_average(f, coords, cells)
+    elif force == "gaussian":
+        fbar = ci.gaussian_force(nc, dim, seed)
+    elif force == "zero":
+        fbar = np.zeros((nc, dim))
+    else:
+        fbar = np.tile(np.asarray(force, float), (nc, 1))
+    dirv = None
+    if dirichlet:
+        X = coords[cells]
+        xs = np.stack([np.delete(X, s, axis=1).mean(1) for s in range(dim + 1)], 1)
+        dirv = np.stack([xs[..., 0] - 0.3 + xs[..., 1] ** 2, 0.5 - xs[..., 1] + xs[..., 0] ** 2], -1)
+    uit = ci.ns_iterate_2d(coords, cells, n, seed) if ns else None
+    prm = O.Params(mu=mu, nu=nu, shift=shift, mis_seed=seed + 100, physics="ns_step" if ns else "stokes", k0=k0)
+    data = O.Data(fbar=fbar, dirichlet=dirv, u_iter=uit)
+    prob = P.Problem(mu=mu, nu=nu, fbar=tg(fbar), physics=P.CR_NS_NEWTON_STEP if ns else P.CR_STOKES,
+                     shift=P.CR_SHIFT_MIS if shift == "mis" else P.CR_SHIFT_NONE, mis_seed=seed + 100,
+                     gauge_cell=k0, dirichlet=None if dirv is None else tg(dirv),
+                     u_iter=None if uit is None else tg(uit))
+    return coords, cells, prm, data, prob
+
+
+# ------------------------------------------------------------------ mesh
+def _wide_id_cube(n, spread):
+    coords, cells = ci.cube_mesh(n)
+    nv = coords.shape[0]
+    big = np.zeros((nv * spread, 3))
+    big[np.arange(nv) * spread] = coords
+    return big, (cells.astype(np.int64) * spread).astype(np.int32)
+
+
+MESHES = {
+    "2d-n8": lambda: ci.square_mesh(8),
+    "2d-jit-n33": lambda: ci.square_mesh(33, 0.2, 7),
+    "3d-n3": lambda: ci.cube_mesh(3),
+    "3d-n5": lambda: ci.cube_mesh(5),
+    "3d-two-pass-keys": lambda: _wide_id_cube(3, 40000),   # nv > 2^21 -> 3*22 bits > 64
+}
+
+
+@pytest.mark.parametrize("name", list(MESHES))
+def test_mesh_parity(name):
+    coords, cells = MESHES[name]()
+    mo = O.build_mesh(coords, cells)
+    mg = P.cr_build_mesh(tg(coords), tg(cells))
+    ex = {k: v.cpu().numpy() for k, v in mg.export().items()}
+    assert (mg.nf, mg.nf_int) == (mo.nf, mo.nf_int)
+    for k in ("faces", "face_cells", "cell_faces", "face_dof"):
+        assert np.array_equal(ex[k], getattr(mo, k)), k
+    for k in ("xK", "xs", "a"):
+        ref = getattr(mo, k)
+        assert np.abs(ex[k] - ref).max() <= 1e-15 * np.abs(ref).max(), k
+    assert np.abs(ex["vol"] - mo.vol).max() <= 1e-14 * mo.vol.max()
+
+
+def test_mesh_errors():
+    coords, cells = ci.square_mesh(3)
+    with pytest.raises(P.CrError) as e:
+        P.cr_build_mesh(tg(coords), tg(np.concatenate([cells, cells[:1]])))
+    assert e.value.status == -4
+    bad = cells.copy(); bad[2, 1] = 10 ** 6
+    with pytest.raises(P.CrError):
+        P.cr_build_mesh(tg(coords), tg(bad))
+
+
+# ------------------------------------------------------------------ hybridisation
+HYB_CASES = {
+    "2d-config0": dict(dim=2, n=8, jitter=0.0),
+    "2d-transient-jit-n17": dict(dim=2, n=17),
+    "2d-steady-mis-n16": dict(dim=2, n=16, mu=0.0, shift="mis", force="gaussian"),
+    "2d-ns-n12": dict(dim=2, n=12, mu=0.0, nu=0.01, shift="mis", force="zero", ns=True, jitter=0.0),
+    "2d-dirichlet-n10": dict(dim=2, n=10, dirichlet=True),
+    "2d-k0-interior": dict(dim=2, n=9, k0=77),
+    "3d-transient-n3": dict(dim=3, n=3),
+    "3d-steady-mis-n3": dict(dim=3, n=3, mu=0.0, shift="mis", force="gaussian"),
+}
+
+
+@pytest.mark.parametrize("name", list(HYB_CASES))
+def test_hybridise_parity(name):
+    coords, cells, prm, data, prob = make_case(**HYB_CASES[name])
+    mo = O.build_mesh(coords, cells)
+    ho = O.hybridise(mo, prm, data)
+    mg = P.cr_build_mesh(tg(coords), tg(cells))
+    hg = P.cr_hybridise(mg, prob)
+    rp, cols, vals, S = hg.export_csr()
+    Gg = to_scipy(rp, cols, vals, hg.n_rows)
+    assert hg.nnz == ho["G"].nnz
+    assert same_pattern(Gg, ho["G"])
+    assert row_rel_err(Gg, ho["G"]) <= 1e-12
+    Sg = S.cpu().numpy()
+    assert np.abs(Sg - ho["S"]).max() <= 1e-12 * np.abs(ho["S"]).max()
+    if prm.shift == "mis":
+        inM1, E = hg.export_shift()
+        assert np.array_equal(inM1.cpu().numpy().astype(bool), ho["inM1"])
+        Eg = E.cpu().numpy()
+        assert np.abs(Eg - ho["E"]).max() <= 1e-15 * np.abs(ho["E"]).max()
+
+
+@pytest.mark.parametrize("name", ["2d-config0", "3d-transient-n3", "2d-ns-n12"])
+def test_spmv_parity(name):
+    coords, cells, prm, data, prob = make_case(**HYB_CASES[name])
+    mo = O.build_mesh(coords, cells)
+    ho = O.hybridise(mo, prm, data)
+    hg = P.cr_hybridise(P.cr_build_mesh(tg(coords), tg(cells)), prob)
+    x = np.random.default_rng(3).normal(size=hg.n_rows)
+    y = torch.empty(hg.n_rows, dtype=torch.float64, device=DEV)
+    hg.spmv(tg(x), y)
+    yo = ho["G"] @ x
+    assert np.abs(y.cpu().numpy() - yo).max() <= 1e-13 * np.abs(ho["G"]).max() * np.abs(x).max() * 10
+
+
+@pytest.mark.parametrize("name", ["2d-config0", "2d-ns-n12", "2d-dirichlet-n10", "3d-transient-n3"])
+def test_coupled_parity(name):
+    coords, cells, prm, data, prob = make_case(**HYB_CASES[name])
+    mo = O.build_mesh(coords, cells)
+    M, rhs, nU = O.assemble_coupled(mo, prm, data)
+    cg = P.cr_assemble_coupled(P.cr_build_mesh(tg(coords), tg(cells)), prob)
+    rp, cols, vals, rg = cg.export_csr()
+    Mg = to_scipy(rp, cols, vals, cg.n_rows)
+    assert Mg.shape == M.shape and same_pattern(Mg, M)
+    assert row_rel_err(Mg, M) <= 1e-12
+    assert np.abs(rg.cpu().numpy() - rhs).max() <= 1e-12 * max(np.abs(rhs).max(), 1e-300)
+
+
+# ------------------------------------------------------------------ solve + recover
+SOLVE_CASES = {
+    "config0-pcg": (dict(dim=2, n=8, jitter=0.0), "pcg", 1e-12),
+    "2d-jit-n24-pcg-block": (dict(dim=2, n=24), "pcg_block", 1e-12),
+    "2d-steady-n16-minres": (dict(dim=2, n=16, mu=0.0, shift="mis", force="gaussian"), "minres", 1e-12),
+    "2d-ns-nu1-n8-bicgstab": (dict(dim=2, n=8, mu=0.0, nu=1.0, shift="mis", force="zero", ns=True, jitter=0.0),
+                              "bicgstab", 1e-11),
+    "2d-ns-nu1-n4-gmres": (dict(dim=2, n=4, mu=0.0, nu=1.0, shift="mis", force="zero", ns=True, jitter=0.0),
+                           "gmres", 1e-12),
+    "3d-n3-pcg": (dict(dim=3, n=3), "pcg", 1e-12),
+    "2d-dirichlet-n10-pcg": (dict(dim=2, n=10, dirichlet=True), "pcg", 1e-12),
+}
+
+
+@pytest.mark.parametrize("name", list(SOLVE_CASES))
+def test_solve_recover_parity(name):
+    kw, method, rtol = SOLVE_CASES[name]
+    coords, cells, prm, data, prob = make_case(**kw)
+    mo = O.build_mesh(coords, cells)
+    ho = O.hybrid_pipeline(mo, prm, data)
+    mg = P.cr_build_mesh(tg(coords), tg(cells))
+    hg = P.cr_hybridise(mg, prob)
+    W = torch.zeros(hg.n_rows, dtype=torch.float64, device=DEV)
+    extra = dict(restart=128) if method == "gmres" else {}
+    rep = P.cr_solve(hg, W, method, rtol=rtol, check_every=16, **extra)
+    assert rep["converged"] and rep["rel_res_true"] <= rtol, rep
+    # the oracle recomputes the true residual of the GPU solution in binary128
+    r = O.residual_f128(ho["G"], W.cpu().numpy(), ho["S"])
+    assert np.linalg.norm(r) <= 1.5 * rtol * np.linalg.norm(ho["S"])
+    U, Pp, diag = P.cr_recover(hg, W)
+    assert relL2(U.cpu().numpy(), ho["U"]) <= 1e-8
+    assert relL2(Pp.cpu().numpy(), ho["P"]) <= 1e-8
+    d = diag.cpu().numpy()
+    umax = max(np.abs(ho["U"]).max(), 1.0)
+    amax = np.abs(mo.a).max()
+    assert d[0] <= 1e-9 * umax                                   # the two copies agree
+    # full-face divergence of the assembled U: exact per copy, so bounded by copy disagreement
+    assert d[1] <= (mo.dim + 1) * amax * d[0] + 1e-14 * amax * umax
+
+
+def test_recover_is_exact_given_W():
+    """Recovery alone: oracle per-cell recovery from the GPU's own W (bit-level agreement)."""
+    coords, cells, prm, data, prob = make_case(dim=2, n=12, mu=0.0, shift="mis", force="gaussian")
+    mo = O.build_mesh(coords, cells)
+    ho = O.hybridise(mo, prm, data)
+    hg = P.cr_hybridise(P.cr_build_mesh(tg(coords), tg(cells)), prob)
+    W = np.random.default_rng(5).normal(size=hg.n_rows)
+    U, Pp, _ = P.cr_recover(hg, tg(W))
+    Uo, Po, _, _ = O.recover(mo, prm, data, ho["E"], W)
+    assert np.abs(Pp.cpu().numpy() - Po).max() <= 1e-13 * np.abs(Po).max()
+    assert np.abs(U.cpu().numpy() - Uo).max() <= 1e-13 * np.abs(Uo).max()
+
+
+@pytest.mark.parametrize("dim,n", [(2, 256), (3, 10)])
+def test_well_balanced_closed_form_gpu(dim, n):
+    """constant force -> U = 0 and P_K = f.(x_K - x_K0), on the GPU alone."""
+    f = [0.7, -1.3] if dim == 2 else [0.7, -1.3, 0.4]
+    coords, cells, prm, data, prob = make_case(dim=dim, n=n, force=f)
+    out = P.hybrid_method(tg(coords), tg(cells), prob, "pcg", rtol=1e-12)
+    xK = out["mesh"].export()["xK"].cpu().numpy()
+    Pex = (xK - xK[0]) @ np.asarray(f)
+    assert out["U"].abs().max().item() < 1e-10
+    # P is kappa(G)-limited: relative 1e-8 (the north star's U/P bar)
+    assert np.abs(out["P"].cpu().numpy() - Pex).max() <= 1e-8 * np.abs(Pex).max()
+
+
+def test_zero_rhs_gives_zero():
+    coords, cells, prm, data, prob = make_case(dim=2, n=6, force="zero")
+    out = P.hybrid_method(tg(coords), tg(cells), prob, "pcg")
+    assert out["W"].abs().max().item() == 0.0 and out["P"].abs().max().item() == 0.0
+
+
+def test_host_entry_point_matches_device_path():
+    coords, cells, prm, data, prob = make_case(dim=2, n=8)
+    out = P.hybrid_method_host(torch.from_numpy(coords).pin_memory(), torch.from_numpy(cells).pin_memory(),
+                               torch.from_numpy(data.fbar).pin_memory(), 1.0, 1.0, rtol=1e-12)
+    ho = O.hybrid_pipeline(O.build_mesh(coords, cells), prm, data)
+    assert relL2(out["U_host"].numpy(), ho["U"]) <= 1e-8 and relL2(out["P_host"].numpy(), ho["P"]) <= 1e-8
