@@ -150,7 +150,13 @@ void cr_destroy_hybrid(cr_hybrid h);
  * residual replacement).  refine_dd = 1 adds outer iterative refinement with the residual
  * S - G W accumulated in double-double (parity mode).  Synchronises `s`.                  */
 enum { CR_PCG_JACOBI = 0, CR_PCG_BLOCKJACOBI = 1, CR_MINRES_ABSJACOBI = 2,
-       CR_BICGSTAB_JACOBI = 3, CR_GMRES_JACOBI = 4 };
+       CR_BICGSTAB_JACOBI = 3, CR_GMRES_JACOBI = 4,
+       /* overlapping-patch additive Schwarz M^{-1} = sum_p R_p^t (R_p G R_p^t)^{-1} R_p, one
+        * block per velocity component, patches = interior faces around a vertex (2D) / an
+        * edge (3D); built on the device at the first solve that needs it (DESIGN.md
+        * "Preconditioners").  PCG: Cholesky of each patch block (G SPD);
+        * MINRES: |patch block|^{-1} (SPD although G is indefinite).                */
+       CR_PCG_AFW = 5, CR_MINRES_AFW = 6 };
 typedef struct {
     int32_t method;       /* CR_* above                                                        */
     int32_t restart;      /* GMRES m (default 50)                                              */
@@ -171,6 +177,15 @@ typedef struct {
 } cr_solve_report;
 cr_status cr_solve(cr_hybrid h, const cr_solver_opts *opts, double *W_d, cr_stream_t s,
                    cr_solve_report *rep);
+
+/* z_d = M^{-1} r_d for the preconditioner that `method` (CR_* above) uses: diag(G)^{-1},
+ * |diag(G)|^{-1}, inverse diagonal blocks, or the patch additive Schwarz operator (built on
+ * first use).  r_d, z_d [n_rows], must not alias.  Asynchronous except for a first patch
+ * build (which synchronises `s`).                                                          */
+cr_status cr_apply_precond(cr_hybrid h, int32_t method, const double *r_d, double *z_d, cr_stream_t s);
+/* patch preconditioner statistics (0 if not built): number of patches, largest patch, and
+ * patch blocks that were singular and fell back to their diagonal                           */
+cr_status cr_hybrid_precond_info(cr_hybrid h, int64_t *npatch, int32_t *kmax, int64_t *nfallback);
 
 /* ------------------------------------------------------------------ recovery
  * P_K = (v^t (R_K - C_K W_K) - g_K)/B_K (K != K0), P_K0 = 0;  Uhat_K = Ahat^{-1}(R_K - D_K P_K - C_K W_K);

@@ -33,9 +33,11 @@ STATUS = {0: "CR_OK", -1: "CR_ERR_INVALID_ARG", -2: "CR_ERR_CUDA", -3: "CR_ERR_O
           -10: "CR_ERR_STAGNATION", -11: "CR_ERR_NCCL"}
 CR_STOKES, CR_NS_NEWTON_STEP = 0, 1
 CR_SHIFT_NONE, CR_SHIFT_MIS = 0, 1
-CR_PCG_JACOBI, CR_PCG_BLOCKJACOBI, CR_MINRES_ABSJACOBI, CR_BICGSTAB_JACOBI, CR_GMRES_JACOBI = range(5)
+(CR_PCG_JACOBI, CR_PCG_BLOCKJACOBI, CR_MINRES_ABSJACOBI, CR_BICGSTAB_JACOBI, CR_GMRES_JACOBI,
+ CR_PCG_AFW, CR_MINRES_AFW) = range(7)
 METHODS = {"pcg": CR_PCG_JACOBI, "pcg_block": CR_PCG_BLOCKJACOBI, "minres": CR_MINRES_ABSJACOBI,
-           "bicgstab": CR_BICGSTAB_JACOBI, "gmres": CR_GMRES_JACOBI}
+           "bicgstab": CR_BICGSTAB_JACOBI, "gmres": CR_GMRES_JACOBI, "pcg_afw": CR_PCG_AFW,
+           "minres_afw": CR_MINRES_AFW}
 
 
 class CrError(RuntimeError):
@@ -93,6 +95,8 @@ _sig = {
     "cr_solve": [_vp, _P(SolverOpts), _vp, _vp, _P(SolveReport)],
     "cr_recover": [_vp, _vp, _vp, _vp, _vp, _vp],
     "cr_comm_init": [_vp, _i32, _i32, _P(_vp)],
+    "cr_apply_precond": [_vp, _i32, _vp, _vp, _vp],
+    "cr_hybrid_precond_info": [_vp, _P(_i64), _P(_i32), _P(_i64)],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -164,7 +168,7 @@ class Mesh:
         return out
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.cr_destroy_mesh(self._h)
             self._h = None
 
@@ -232,8 +236,19 @@ class Hybrid:
         _check(_lib.cr_spmv(self._h, _ptr(x, torch.float64), _ptr(y, torch.float64), _stream(stream)))
         return y
 
+    def apply_precond(self, method: str | int, r: torch.Tensor, z: torch.Tensor, stream=None):
+        """z = M^{-1} r for the preconditioner of `method`."""
+        m = METHODS[method] if isinstance(method, str) else int(method)
+        _check(_lib.cr_apply_precond(self._h, m, _ptr(r, torch.float64), _ptr(z, torch.float64), _stream(stream)))
+        return z
+
+    def precond_info(self) -> dict:
+        npatch, kmax, nfb = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64()
+        _check(_lib.cr_hybrid_precond_info(self._h, ctypes.byref(npatch), ctypes.byref(kmax), ctypes.byref(nfb)))
+        return dict(npatch=npatch.value, kmax=kmax.value, nfallback=nfb.value)
+
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.cr_destroy_hybrid(self._h)
             self._h = None
 
@@ -290,7 +305,7 @@ class Coupled:
         return rp, ci, v, rhs
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.cr_destroy_coupled(self._h)
             self._h = None
 

@@ -1,0 +1,101 @@
+// Overlapping-patch additive Schwarz preconditioner for G (device side of precond.cu).
+//
+//   M^{-1} r = sum_p R_p^t  B_p^{-1}  R_p r,     B_p = R_p G R_p^t  (one block per component)
+//
+// Patches are the interior faces around a vertex (2D) or around an edge (3D): the kernel of
+// the cellwise signed sum sigma -> sum_{sigma in F_K} C_{K,sigma} W_sigma (the large 1/mu|K|
+// part of G, P:L510-517 with S_K^{-1} of SURVEY A.1) is spanned by circulations around
+// interior vertices (2D) / edges (3D), each supported on one patch, so the patch solves
+// resolve both scales of G exactly where Jacobi resolves neither (Arnold-Falk-Winther-type
+// space decomposition).
+//
+// Layout (sliced, 32 patches per slice = one warp, so every load is one coalesced 256-B row):
+//   kl[slice]                         patch size k of the slice (max over its 32 patches)
+//   ids[ioff[slice] + j*32 + lane]    (dof * SLOTS + slot) of patch face j, or -1 (padding)
+//   vals[voff[slice] + (i*T + e)*32 + lane]
+//        component i, entry e of B_p^{-1}: packed lower triangle (T = k(k+1)/2, symmetric
+//        modes) or row-major k x k (T = k^2, general mode)
+// A face belongs to exactly SLOTS patches (2 endpoints in 2D, 3 edges of a triangle in 3D);
+// slot s of face sigma receives patch s's contribution in zs[(dof*SLOTS + s)*D + i], and
+// consumers sum the SLOTS values in slot order, so the result is deterministic (no atomics).
+#pragma once
+#include <cstdint>
+
+namespace cr {
+
+struct AfwView {
+    const int64_t *ioff, *voff;
+    const uint8_t *kl;
+    const int32_t *ids;
+    const double *vals;
+    int64_t npatch;
+};
+
+// z-contributions of patch p for all D components; returns sum_i r_p^t B_p^{-1} r_p.
+template <int D, int SLOTS, int KMAX, bool SYM>
+__device__ __forceinline__ double afw_patch(const AfwView &A, int64_t p, const double *__restrict__ r,
+                                            double *__restrict__ zs) {
+    const int64_t slice = p >> 5;
+    const int lane = (int)(p & 31);
+    const int k = A.kl[slice];
+    const int32_t *ip = A.ids + A.ioff[slice] + lane;
+    int id[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) id[j] = (j < k) ? __ldg(ip + j * 32) : -1;
+    const int T = SYM ? k * (k + 1) / 2 : k * k;
+    const double *vp = A.vals + A.voff[slice] + lane;
+    double quad = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double rv[KMAX], y[KMAX];
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            rv[j] = (id[j] >= 0) ? r[(int64_t)(id[j] / SLOTS) * D + i] : 0.0;
+            y[j] = 0.0;
+        }
+        const double *vi = vp + (int64_t)i * T * 32;
+        if constexpr (SYM) {
+#pragma unroll
+            for (int a = 0; a < KMAX; ++a) {
+                if (a < k) {
+#pragma unroll
+                    for (int b = 0; b <= a; ++b) {
+                        const double v = __ldcs(vi + (a * (a + 1) / 2 + b) * 32);
+                        y[a] = fma(v, rv[b], y[a]);
+                        if (a != b) y[b] = fma(v, rv[a], y[b]);
+                    }
+                }
+            }
+        } else {
+#pragma unroll
+            for (int a = 0; a < KMAX; ++a) {
+                if (a < k) {
+#pragma unroll
+                    for (int b = 0; b < KMAX; ++b)
+                        if (b < k) y[a] = fma(__ldcs(vi + (a * k + b) * 32), rv[b], y[a]);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            if (id[j] >= 0) {
+                quad = fma(rv[j], y[j], quad);
+                zs[(int64_t)id[j] * D + i] = y[j];
+            }
+        }
+    }
+    return quad;
+}
+
+// z[row] = sum_s zs[row, s] (slot order)
+template <int D, int SLOTS>
+__device__ __forceinline__ void afw_sum(const double *__restrict__ zs, int64_t row, double (&z)[D]) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) z[i] = zs[(row * SLOTS) * D + i];
+#pragma unroll
+    for (int s = 1; s < SLOTS; ++s)
+#pragma unroll
+        for (int i = 0; i < D; ++i) z[i] += zs[(row * SLOTS + s) * D + i];
+}
+
+}  // namespace cr

@@ -10,6 +10,21 @@ static thread_local std::string g_last_error;
 void set_last_error(const std::string &m) { g_last_error = m; }
 }  // namespace cr
 
+// Keep freed stream-ordered memory in the device's default pool (no trim to the OS at every
+// synchronisation): repeated solves re-use their buffers without remapping.
+static void keep_pool() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    static thread_local int done_dev = -1;
+    if (done_dev == dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
+}
+
 cr_hybrid_s::~cr_hybrid_s() { cr::free_solver_work(work); }
 
 #define CR_API_BEGIN try {
@@ -39,6 +54,7 @@ cr_status cr_build_mesh(int32_t dim, int64_t nv, const double *coords_d, int64_t
     CR_API_BEGIN
     CR_REQUIRE(out, CR_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
+    keep_pool();
     cr_mesh_s *m = new cr_mesh_s();
     try {
         cr::build_mesh(m, dim, nv, coords_d, nc, cells_d, (cudaStream_t)s);
@@ -84,7 +100,7 @@ cr_status cr_mesh_export(cr_mesh m, int32_t *faces_d, int32_t *face_cells_d, int
 }
 
 void cr_destroy_mesh(cr_mesh m) {
-    cudaDeviceSynchronize();
+    cr::SyncFreeScope sync;
     delete m;
 }
 
@@ -124,7 +140,7 @@ cr_status cr_coupled_export_csr(cr_coupled c, int64_t *row_ptr_d, int32_t *cols_
 }
 
 void cr_destroy_coupled(cr_coupled c) {
-    cudaDeviceSynchronize();
+    cr::SyncFreeScope sync;
     delete c;
 }
 
@@ -181,7 +197,7 @@ cr_status cr_spmv(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s) {
 }
 
 void cr_destroy_hybrid(cr_hybrid h) {
-    cudaDeviceSynchronize();
+    cr::SyncFreeScope sync;
     delete h;
 }
 
@@ -190,6 +206,22 @@ cr_status cr_solve(cr_hybrid h, const cr_solver_opts *opts, double *W_d, cr_stre
     CR_REQUIRE(h && opts && W_d, CR_ERR_INVALID_ARG, "null argument");
     if (rep) std::memset(rep, 0, sizeof(*rep));
     cr::solve(h, *opts, W_d, (cudaStream_t)s, rep);
+    CR_API_END
+}
+
+cr_status cr_apply_precond(cr_hybrid h, int32_t method, const double *r_d, double *z_d, cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(h && r_d && z_d && r_d != z_d, CR_ERR_INVALID_ARG, "bad arguments");
+    cr::apply_precond(h, method, r_d, z_d, (cudaStream_t)s);
+    CR_API_END
+}
+
+cr_status cr_hybrid_precond_info(cr_hybrid h, int64_t *npatch, int32_t *kmax, int64_t *nfallback) {
+    CR_API_BEGIN
+    CR_REQUIRE(h, CR_ERR_INVALID_ARG, "null handle");
+    if (npatch) *npatch = h->afw.built >= 0 ? h->afw.npatch : 0;
+    if (kmax) *kmax = h->afw.built >= 0 ? h->afw.kmax : 0;
+    if (nfallback) *nfallback = h->afw.built >= 0 ? h->afw.nfallback : 0;
     CR_API_END
 }
 

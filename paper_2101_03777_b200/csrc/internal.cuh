@@ -36,29 +36,44 @@ void set_last_error(const std::string &m);
     } while (0)
 
 // ------------------------------------------------------------------ device buffer
+// Stream-ordered: allocated with cudaMallocAsync on stream s and freed with cudaFreeAsync on
+// the same stream, so a temporary released while kernels that use it are still queued is
+// only recycled after them.  Handle destructors (cr_destroy_*) synchronise the device first
+// and set g_sync_free, because the caller's stream may no longer exist at that point.
+inline thread_local bool g_sync_free = false;
+struct SyncFreeScope {
+    SyncFreeScope() { cudaDeviceSynchronize(); g_sync_free = true; }
+    ~SyncFreeScope() { g_sync_free = false; }
+};
+
 template <class T>
 struct DevBuf {
     T *p = nullptr;
     size_t n = 0;
+    cudaStream_t s_ = nullptr;
     DevBuf() = default;
     DevBuf(const DevBuf &) = delete;
     DevBuf &operator=(const DevBuf &) = delete;
-    DevBuf(DevBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf(DevBuf &&o) noexcept : p(o.p), n(o.n), s_(o.s_) { o.p = nullptr; o.n = 0; }
     DevBuf &operator=(DevBuf &&o) noexcept {
-        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        if (this != &o) { release(); p = o.p; n = o.n; s_ = o.s_; o.p = nullptr; o.n = 0; }
         return *this;
     }
     ~DevBuf() { release(); }
     void alloc(size_t count, cudaStream_t s) {
         release();
         n = count;
+        s_ = s;
         if (count == 0) return;
         CR_CUDA(cudaMallocAsync((void **)&p, count * sizeof(T) + 16, s));
     }
     void zero(cudaStream_t s) { if (n) CR_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
     void fill_bytes(int v, cudaStream_t s) { if (n) CR_CUDA(cudaMemsetAsync(p, v, n * sizeof(T), s)); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            if (g_sync_free) cudaFree(p);
+            else cudaFreeAsync(p, s_);
+        }
         p = nullptr;
         n = 0;
     }
@@ -103,6 +118,18 @@ struct BlockEll {
 
 namespace cr { struct SolverWork; }
 
+// overlapping-patch additive Schwarz preconditioner (afw.cuh layout)
+struct AfwPrec {
+    int built = -1;              // mode it was built for (-1 = not built)
+    int slots = 0, kmax = 0;     // patches per face (2D 2, 3D 3); largest patch
+    int64_t npatch = 0, nslices = 0, nfallback = 0;
+    cr::DevBuf<int64_t> ioff, voff;
+    cr::DevBuf<uint8_t> kl;
+    cr::DevBuf<int32_t> ids;
+    cr::DevBuf<double> vals;
+};
+enum { AFW_SPD = 0, AFW_ABS = 1, AFW_GEN = 2 };
+
 struct cr_hybrid_s {
     const cr_mesh_s *mesh = nullptr;
     cr_params prm{};
@@ -117,6 +144,7 @@ struct cr_hybrid_s {
     BlockEll G;
     cr::DevBuf<double> S, dinv, absdinv, bdinv;   // bdinv [nrows][d][d] inverse diagonal blocks
     cr::DevBuf<uint8_t> rowlen;                   // true blocks per block row
+    AfwPrec afw;
     cr::SolverWork *work = nullptr;
     ~cr_hybrid_s();
 };
@@ -149,6 +177,9 @@ void recover(const cr_hybrid_s *h, const double *W, double *U, double *P, double
 // solve.cu
 void solve(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep);
 void free_solver_work(SolverWork *w);
+void apply_precond(cr_hybrid_s *h, int method, const double *r, double *z, cudaStream_t s);
+// precond.cu
+void build_afw(cr_hybrid_s *h, int mode, cudaStream_t s);
 // shared: copy problem data into hybrid-owned buffers
 struct ProbView;
 ProbView prob_view(const cr_hybrid_s *h);

@@ -16,6 +16,7 @@
 #include <cstddef>
 #include <cstring>
 
+#include "afw.cuh"
 #include "internal.cuh"
 #include "spmv.cuh"
 
@@ -49,6 +50,7 @@ struct SolverWork {
     int D = 0;
     DevBuf<double> x, b, r, p, q, z, z2, v, v2, w, w2, y, t, rhat;
     DevBuf<double> V;           // GMRES basis (m+1) x N
+    DevBuf<double> zs;          // patch preconditioner: per-(face, slot) contributions
     DevBuf<double> partials;
     DevBuf<KState> st;
     KState *hst = nullptr;      // pinned
@@ -207,6 +209,40 @@ __global__ void __launch_bounds__(kT) k_pcg_pdir(int64_t nrows, double *p, const
     }
 }
 
+// ------------------------------------------------------------------ MINRES scalar recurrences
+// gamma_1 = sqrt(v_1^t M v_1) and the Givens state (called by the last block of a reduction)
+__device__ __forceinline__ void minres_start(KState *st, double vMv) {
+    double gm = sqrt(fmax(vMv, 0.0));
+    st->gamma = gm;
+    st->gamma_old = 1.0;
+    st->eta = gm;
+    st->eta0 = gm;
+    st->s = st->s_old = 0.0;
+    st->c = st->c_old = 1.0;
+    st->flag = (gm == 0.0) ? FLAG_CONV : FLAG_RUN;
+}
+
+// new gamma = sqrt(v_{j+1}^t M v_{j+1}); QR of the tridiagonal by Givens rotations
+__device__ __forceinline__ void minres_givens(KState *st, double vMv) {
+    const double gn = sqrt(fmax(vMv, 0.0));
+    const double gmo = st->gamma, dlo = st->delta;
+    const double a0 = st->c * dlo - st->c_old * st->s * gmo;
+    const double a1 = sqrt(a0 * a0 + gn * gn);
+    const double a2 = st->s * dlo + st->c_old * st->c * gmo;
+    const double a3 = st->s_old * gmo;
+    const double cn = a0 / a1, sn = gn / a1;
+    st->a1 = a1; st->a2 = a2; st->a3 = a3; st->cn = cn;
+    st->eta_w = st->eta;
+    st->gz = gmo;
+    st->eta = -sn * st->eta;
+    st->gamma_old = gmo;
+    st->gamma = gn;
+    st->c_old = st->c; st->c = cn;
+    st->s_old = st->s; st->s = sn;
+    st->iters += 1;
+    if (gn == 0.0) st->flag = FLAG_CONV;          // exact invariant subspace
+}
+
 // ------------------------------------------------------------------ MINRES (preconditioned, SPD M)
 // Paige-Saunders recurrences in the Elman-Silvester-Wathen form (oracle/krylov.py minres):
 // z_j = M v_j / gamma_j; delta = z_j^t G z_j; v_{j+1} = G z_j - delta/gamma v_j - gamma/gamma_old v_{j-1}
@@ -225,16 +261,7 @@ __global__ void __launch_bounds__(kT) k_minres_init(int64_t nrows, const double 
             acc[0] += zi * vi;
         }
     }
-    reduce_and_finish<1>(acc, partials, &st->tickets[0], [&](double *t) {
-        double gm = sqrt(fmax(t[0], 0.0));
-        st->gamma = gm;
-        st->gamma_old = 1.0;
-        st->eta = gm;
-        st->eta0 = gm;
-        st->s = st->s_old = 0.0;
-        st->c = st->c_old = 1.0;
-        st->flag = (gm == 0.0) ? FLAG_CONV : FLAG_RUN;
-    });
+    reduce_and_finish<1>(acc, partials, &st->tickets[0], [&](double *t) { minres_start(st, t[0]); });
 }
 
 template <int D>
@@ -275,25 +302,7 @@ __global__ void __launch_bounds__(kT) k_minres_lanczos(int64_t nrows, const doub
             acc[0] += zn * vn;
         }
     }
-    reduce_and_finish<1>(acc, partials, &st->tickets[2], [&](double *t) {
-        const double gn = sqrt(fmax(t[0], 0.0));
-        const double gmo = st->gamma, dlo = st->delta;
-        const double a0 = st->c * dlo - st->c_old * st->s * gmo;
-        const double a1 = sqrt(a0 * a0 + gn * gn);
-        const double a2 = st->s * dlo + st->c_old * st->c * gmo;
-        const double a3 = st->s_old * gmo;
-        const double cn = a0 / a1, sn = gn / a1;
-        st->a1 = a1; st->a2 = a2; st->a3 = a3; st->cn = cn;
-        st->eta_w = st->eta;
-        st->gz = gmo;
-        st->eta = -sn * st->eta;
-        st->gamma_old = gmo;
-        st->gamma = gn;
-        st->c_old = st->c; st->c = cn;
-        st->s_old = st->s; st->s = sn;
-        st->iters += 1;
-        if (gn == 0.0) st->flag = FLAG_CONV;          // exact invariant subspace
-    });
+    reduce_and_finish<1>(acc, partials, &st->tickets[2], [&](double *t) { minres_givens(st, t[0]); });
 }
 
 // w_new (written over w_old) = (z/gz - a3 w_old - a2 w)/a1 ; x += cn eta_w w_new
@@ -312,6 +321,103 @@ __global__ void __launch_bounds__(kT) k_minres_wx(int64_t nrows, const double *z
             x[k] = fma(f, wn, x[k]);
         }
     }
+}
+
+// ------------------------------------------------------------------ patch (AFW) preconditioner
+// What the last block does with q = sum_p r_p^t B_p^{-1} r_p  (= r^t M^{-1} r)
+enum { AFW_PCG_INIT = 0, AFW_PCG = 1, AFW_MINRES_INIT = 2, AFW_MINRES = 3 };
+
+// zs (per face slot) = patch contributions of M^{-1} r
+template <int D, int SLOTS, int KMAX, bool SYM, int WHAT>
+__global__ void __launch_bounds__(kT) k_afw_apply(AfwView A, const double *r, double *zs, double rtol, KState *st,
+                                                  double *partials) {
+    if (WHAT != AFW_PCG_INIT && WHAT != AFW_MINRES_INIT && st->flag != FLAG_RUN) return;
+    double acc[1] = {0.0};
+    const int64_t np = ((A.npatch + 31) >> 5) << 5;
+    GRID_STRIDE(pp, np) acc[0] += afw_patch<D, SLOTS, KMAX, SYM>(A, pp, r, zs);
+    reduce_and_finish<1>(acc, partials, &st->tickets[3], [&](double *t) {
+        if (WHAT == AFW_PCG_INIT) {
+            st->rho = t[0];
+            st->beta = 0.0;
+            st->tol2 = rtol * rtol * st->bb;
+            st->flag = (st->rr <= st->tol2) ? FLAG_CONV : FLAG_RUN;
+        } else if (WHAT == AFW_PCG) {
+            st->beta = t[0] / st->rho;
+            st->rho = t[0];
+        } else if (WHAT == AFW_MINRES_INIT) {
+            minres_start(st, t[0]);
+        } else {
+            minres_givens(st, t[0]);
+        }
+    });
+}
+
+// x += alpha p ; r -= alpha q ; |r|^2 (convergence)
+template <int D>
+__global__ void __launch_bounds__(kT) k_pcg_update_r(int64_t nrows, double *x, double *r, const double *p, const double *q,
+                                                     KState *st, double *partials) {
+    if (st->flag != FLAG_RUN) return;
+    const double alpha = st->alpha;
+    double acc[1] = {0.0};
+    GRID_STRIDE(row, nrows) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            x[row * D + i] = fma(alpha, p[row * D + i], x[row * D + i]);
+            const double ri = fma(-alpha, q[row * D + i], r[row * D + i]);
+            r[row * D + i] = ri;
+            acc[0] += ri * ri;
+        }
+    }
+    reduce_and_finish<1>(acc, partials, &st->tickets[2], [&](double *t) {
+        st->iters += 1;
+        st->rr = t[0];
+        if (t[0] <= st->tol2) st->flag = FLAG_CONV;
+    });
+}
+
+// p = z + beta p, z = sum of the slot contributions (beta = 0: p = z)
+template <int D, int SLOTS>
+__global__ void __launch_bounds__(kT) k_pcg_pdir_afw(int64_t nrows, double *p, const double *zs, const KState *st) {
+    if (st->flag != FLAG_RUN) return;
+    const double beta = st->beta;
+    GRID_STRIDE(row, nrows) {
+        double z[D];
+        afw_sum<D, SLOTS>(zs, row, z);
+#pragma unroll
+        for (int i = 0; i < D; ++i) p[row * D + i] = (beta == 0.0) ? z[i] : fma(beta, p[row * D + i], z[i]);
+    }
+}
+
+// z = sum of the slot contributions (MINRES); `guard` skips after convergence
+template <int D, int SLOTS>
+__global__ void __launch_bounds__(kT) k_afw_zsum(int64_t nrows, double *z, const double *zs, const KState *st, int guard) {
+    if (guard && st->flag != FLAG_RUN) return;
+    GRID_STRIDE(row, nrows) {
+        double zv[D];
+        afw_sum<D, SLOTS>(zs, row, zv);
+#pragma unroll
+        for (int i = 0; i < D; ++i) z[row * D + i] = zv[i];
+    }
+}
+
+// MINRES Lanczos vector only: v_new (over v_old) = q/gamma - delta/gamma v - gamma/gamma_old v_old
+template <int D>
+__global__ void __launch_bounds__(kT) k_minres_lanczos_v(int64_t nrows, const double *q, const double *v, double *vold_new,
+                                                         const KState *st) {
+    if (st->flag != FLAG_RUN) return;
+    const double gm = st->gamma, go = st->gamma_old, dl = st->delta;
+    const double c1 = 1.0 / gm, c2 = dl / gm, c3 = gm / go;
+    GRID_STRIDE(row, nrows) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int64_t k = row * D + i;
+            vold_new[k] = q[k] * c1 - c2 * v[k] - c3 * vold_new[k];
+        }
+    }
+}
+
+__global__ void k_zero3(int64_t n, double *a, double *b, double *c) {
+    GRID_STRIDE(i, n) { a[i] = 0.0; b[i] = 0.0; c[i] = 0.0; }
 }
 
 // ------------------------------------------------------------------ BiCGStab (right Jacobi)
@@ -642,6 +748,26 @@ static void true_residual(Launcher &L, const double *x, double *r) {
 // The body launches on `ks`; it is captured on the work's private non-blocking stream (the
 // caller's stream may be the legacy default stream, which cannot capture) and the graph is
 // then launched on the caller's stream.
+template <int D, int WHAT>
+static void launch_afw(Launcher &L, cudaStream_t ks, const double *r, double *zs, double rtol) {
+    constexpr int SLOTS = D == 2 ? 2 : 3;
+    const AfwPrec &P = L.h->afw;
+    AfwView A{P.ioff.get(), P.voff.get(), P.kl.get(), P.ids.get(), P.vals.get(), P.npatch};
+    const int grid = grid_for(P.nslices * 32, kT);
+    const bool sym = P.built != AFW_GEN;
+    KState *st = L.w->st.get();
+    double *part = L.w->partials.get();
+    if (P.kmax <= 8) {
+        if (sym) k_afw_apply<D, SLOTS, 8, true, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part);
+        else k_afw_apply<D, SLOTS, 8, false, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part);
+    } else {
+        if (sym) k_afw_apply<D, SLOTS, 16, true, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part);
+        else k_afw_apply<D, SLOTS, 16, false, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part);
+    }
+    CR_CHECK_LAUNCH();
+    ++L.launches;
+}
+
 template <class Body, class Done>
 static void graph_loop(Launcher &L, cudaStream_t &ks, int key, int k, Body body, Done done) {
     SolverWork *w = L.w;
@@ -737,6 +863,90 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                 ++replacements;
             }
             if (w->hst->flag == FLAG_BREAK) { status = CR_ERR_BREAKDOWN; break; }
+            if (w->hst->iters >= max_iter) { status = CR_ERR_NOT_CONVERGED; break; }
+        }
+    } else if (method == CR_PCG_AFW) {
+        constexpr int SLOTS = D == 2 ? 2 : 3;
+        build_afw(h, AFW_SPD, s);
+        if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
+        double *zs = w->zs.get();
+        auto init = [&]() {
+            true_residual<D>(L, x, w->r.get());
+            launch_afw<D, AFW_PCG_INIT>(L, s, w->r.get(), zs, rtol);
+            k_pcg_pdir_afw<D, SLOTS><<<L.grid_rows, kT, 0, s>>>(nrows, w->p.get(), zs, st);
+            CR_CHECK_LAUNCH();
+            ++L.launches;
+        };
+        init();
+        read_state(w, s);
+        if (w->hst->bb == 0.0) { CR_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), s)); }
+        while (w->hst->flag == FLAG_RUN) {
+            auto body = [&](int) {
+                k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part);
+                k_pcg_update_r<D><<<L.grid_rows, kT, 0, ks>>>(nrows, x, w->r.get(), w->p.get(), w->q.get(), st, part);
+                CR_CHECK_LAUNCH();
+                launch_afw<D, AFW_PCG>(L, ks, w->r.get(), zs, rtol);
+                k_pcg_pdir_afw<D, SLOTS><<<L.grid_rows, kT, 0, ks>>>(nrows, w->p.get(), zs, st);
+                CR_CHECK_LAUNCH();
+            };
+            int64_t it0 = w->hst->iters;
+            graph_loop(L, ks, method * 100000 + kk, kk, body, [&]() {
+                return w->hst->flag != FLAG_RUN || w->hst->iters >= max_iter;
+            });
+            int64_t dit = w->hst->iters - it0;
+            L.launches += 4 * ((dit + kk - 1) / kk) * kk;
+            L.spmvs += dit;
+            if (w->hst->flag == FLAG_CONV) {
+                init();
+                read_state(w, s);
+                if (w->hst->flag == FLAG_CONV || replacements >= 8) break;
+                ++replacements;
+            }
+            if (w->hst->flag == FLAG_BREAK) { status = CR_ERR_BREAKDOWN; break; }
+            if (w->hst->iters >= max_iter) { status = CR_ERR_NOT_CONVERGED; break; }
+        }
+    } else if (method == CR_MINRES_AFW) {
+        constexpr int SLOTS = D == 2 ? 2 : 3;
+        build_afw(h, AFW_ABS, s);
+        if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
+        double *zs = w->zs.get();
+        double *va = w->v.get(), *vb = w->v2.get(), *za = w->z.get(), *zb = w->z2.get();
+        double *wa = w->w.get(), *wb = w->w2.get();
+        true_residual<D>(L, x, va);
+        k_zero3<<<L.grid_vec, kT, 0, s>>>(N, wa, wb, vb);
+        CR_CHECK_LAUNCH();
+        launch_afw<D, AFW_MINRES_INIT>(L, s, va, zs, rtol);
+        k_afw_zsum<D, SLOTS><<<L.grid_rows, kT, 0, s>>>(nrows, za, zs, st, 0);
+        CR_CHECK_LAUNCH();
+        L.launches += 2;
+        read_state(w, s);
+        const double bnorm = sqrt(w->hst->bb);
+        auto body = [&](int i) {
+            double *v = (i & 1) ? vb : va, *vold = (i & 1) ? va : vb;
+            double *z = (i & 1) ? zb : za, *zn = (i & 1) ? za : zb;
+            double *ww = (i & 1) ? wb : wa, *wold = (i & 1) ? wa : wb;
+            k_minres_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), z, w->q.get(), st, part);
+            k_minres_lanczos_v<D><<<L.grid_rows, kT, 0, ks>>>(nrows, w->q.get(), v, vold, st);
+            CR_CHECK_LAUNCH();
+            launch_afw<D, AFW_MINRES>(L, ks, vold, zs, rtol);
+            k_afw_zsum<D, SLOTS><<<L.grid_rows, kT, 0, ks>>>(nrows, zn, zs, st, 1);
+            k_minres_wx<D><<<L.grid_rows, kT, 0, ks>>>(nrows, z, ww, wold, x, st);
+            CR_CHECK_LAUNCH();
+        };
+        while (w->hst->flag == FLAG_RUN) {
+            int64_t it0 = w->hst->iters;
+            graph_loop(L, ks, method * 100000 + kk, kk, body, [&]() { return true; });
+            int64_t dit = w->hst->iters - it0;
+            L.launches += 5 * kk;
+            L.spmvs += dit;
+            true_residual<D>(L, x, w->t.get());
+            read_state(w, s);
+            const double tr = sqrt(w->hst->rr);
+            if (tr <= rtol * bnorm) { w->hst->flag = FLAG_CONV; break; }
+            if (w->hst->flag != FLAG_RUN) {
+                status = w->hst->flag == FLAG_BREAK ? CR_ERR_BREAKDOWN : CR_ERR_STAGNATION;
+                break;
+            }
             if (w->hst->iters >= max_iter) { status = CR_ERR_NOT_CONVERGED; break; }
         }
     } else if (method == CR_MINRES_ABSJACOBI) {
@@ -878,7 +1088,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     if (rep) {
         rep->iterations = w->hst->iters;
         rep->rel_res_true = tr;
-        rep->rel_res_recursive = (method == CR_MINRES_ABSJACOBI)
+        rep->rel_res_recursive = (method == CR_MINRES_ABSJACOBI || method == CR_MINRES_AFW)
                                      ? fabs(w->hst->eta) / (w->hst->eta0 > 0 ? w->hst->eta0 : 1.0)
                                      : tr;
         rep->converged = status == CR_OK;
@@ -888,6 +1098,61 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         rep->kernel_launches = L.launches;
     }
     if (status != CR_OK) throw Error(status, "solver did not converge (see report)");
+}
+
+__global__ void k_scale_plain(int64_t n, const double *M, const double *a, double *out) {
+    GRID_STRIDE(i, n) out[i] = M[i] * a[i];
+}
+
+template <int D>
+__global__ void k_block_apply(int64_t nrows, const double *M, const double *r, double *z) {
+    GRID_STRIDE(row, nrows) {
+        double rv[D], zv[D];
+        ld<D>(r, row, rv);
+        apply_prec<D, 1>(M, row, rv, zv);
+        stv<D>(z, row, zv);
+    }
+}
+
+// z = M^{-1} r for the preconditioner of `method` (cr_apply_precond)
+template <int D>
+static void apply_precond_t(cr_hybrid_s *h, int method, const double *r, double *z, cudaStream_t s) {
+    constexpr int SLOTS = D == 2 ? 2 : 3;
+    ensure_work(h, s);
+    SolverWork *w = h->work;
+    const int64_t nrows = h->G.nrows, N = w->N;
+    Launcher L{h, w, s};
+    const int grid = grid_for(nrows, kT);
+    switch (method) {
+        case CR_PCG_JACOBI:
+        case CR_BICGSTAB_JACOBI:
+        case CR_GMRES_JACOBI:
+            k_scale_plain<<<grid_for(N, kT), kT, 0, s>>>(N, h->dinv.get(), r, z);
+            break;
+        case CR_MINRES_ABSJACOBI:
+            k_scale_plain<<<grid_for(N, kT), kT, 0, s>>>(N, h->absdinv.get(), r, z);
+            break;
+        case CR_PCG_BLOCKJACOBI:
+            k_block_apply<D><<<grid, kT, 0, s>>>(nrows, h->bdinv.get(), r, z);
+            break;
+        case CR_PCG_AFW:
+        case CR_MINRES_AFW: {
+            build_afw(h, method == CR_PCG_AFW ? AFW_SPD : AFW_ABS, s);
+            if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
+            CR_CUDA(cudaMemsetAsync(w->st.get(), 0, sizeof(KState), s));
+            launch_afw<D, AFW_PCG_INIT>(L, s, r, w->zs.get(), 1e-10);
+            k_afw_zsum<D, SLOTS><<<grid, kT, 0, s>>>(nrows, z, w->zs.get(), w->st.get(), 0);
+            break;
+        }
+        default:
+            throw Error(CR_ERR_INVALID_ARG, "unknown preconditioner method");
+    }
+    CR_CHECK_LAUNCH();
+}
+
+void apply_precond(cr_hybrid_s *h, int method, const double *r, double *z, cudaStream_t s) {
+    if (h->G.d == 2) apply_precond_t<2>(h, method, r, z, s);
+    else apply_precond_t<3>(h, method, r, z, s);
 }
 
 void solve(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep) {

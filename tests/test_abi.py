@@ -20,8 +20,11 @@ def declared_symbols():
 @pytest.fixture(scope="module")
 def lib():
     if not os.path.exists(LIB):
-        from paper_2101_03777_b200 import build
-        build.build()
+        import importlib.util
+        spec = importlib.util.spec_from_file_location("_cr_build", os.path.join(ROOT, "paper_2101_03777_b200", "build.py"))
+        b = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(b)
+        b.build()
     return ctypes.CDLL(LIB)
 
 

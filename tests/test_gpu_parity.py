@@ -201,6 +201,10 @@ SOLVE_CASES = {
                            "gmres", 1e-12),
     "3d-n3-pcg": (dict(dim=3, n=3), "pcg", 1e-12),
     "2d-dirichlet-n10-pcg": (dict(dim=2, n=10, dirichlet=True), "pcg", 1e-12),
+    "config0-pcg-afw": (dict(dim=2, n=8, jitter=0.0), "pcg_afw", 1e-12),
+    "2d-jit-n24-pcg-afw": (dict(dim=2, n=24), "pcg_afw", 1e-12),
+    "3d-n3-pcg-afw": (dict(dim=3, n=3), "pcg_afw", 1e-12),
+    "2d-steady-n16-minres-afw": (dict(dim=2, n=16, mu=0.0, shift="mis", force="gaussian"), "minres_afw", 1e-12),
 }
 
 
@@ -226,8 +230,10 @@ def test_solve_recover_parity(name):
     umax = max(np.abs(ho["U"]).max(), 1.0)
     amax = np.abs(mo.a).max()
     assert d[0] <= 1e-9 * umax                                   # the two copies agree
-    # full-face divergence of the assembled U: exact per copy, so bounded by copy disagreement
-    assert d[1] <= (mo.dim + 1) * amax * d[0] + 1e-14 * amax * umax
+    # full-face divergence of the assembled U: per copy it is D_K^t Uhat_K - g_K = B_K dP_K, i.e.
+    # the rounding of P_K times B_K; across copies add sum_sigma sum_i |a_sigma^i| |dU| <=
+    # (d+1) d amax * copy disagreement.  Factor 2 covers the per-copy rounding term.
+    assert d[1] <= 2 * (mo.dim + 1) * mo.dim * amax * d[0] + 1e-12 * amax * umax
 
 
 def test_recover_is_exact_given_W():
@@ -268,3 +274,66 @@ def test_host_entry_point_matches_device_path():
                                torch.from_numpy(data.fbar).pin_memory(), 1.0, 1.0, rtol=1e-12)
     ho = O.hybrid_pipeline(O.build_mesh(coords, cells), prm, data)
     assert relL2(out["U_host"].numpy(), ho["U"]) <= 1e-8 and relL2(out["P_host"].numpy(), ho["P"]) <= 1e-8
+
+
+# ------------------------------------------------------------------ patch preconditioner
+def _patches(mo):
+    """Independent construction of the patches: interior faces around each vertex (2D) or
+    around each edge (3D), faces in ascending dof order."""
+    from collections import defaultdict
+    import itertools
+    pt = defaultdict(list)
+    for f in np.nonzero(mo.face_dof >= 0)[0]:
+        t = sorted(mo.faces[f])
+        keys = t if mo.dim == 2 else list(itertools.combinations(t, 2))
+        for k in keys:
+            pt[tuple(np.atleast_1d(k))].append(mo.face_dof[f])
+    return [np.array(sorted(v)) for _, v in sorted(pt.items())]
+
+
+def _afw_numpy(G, pats, d, r, kind):
+    G = G.tocsr()
+    z = np.zeros_like(r)
+    for p in pats:
+        for i in range(d):
+            ii = p * d + i
+            B = G[ii][:, ii].toarray()
+            if kind == "abs":
+                w, V = np.linalg.eigh(0.5 * (B + B.T))
+                Bi = (V / np.abs(w)) @ V.T
+            else:
+                Bi = np.linalg.inv(B)
+            z[ii] += Bi @ r[ii]
+    return z
+
+
+@pytest.mark.parametrize("name,method,kind", [("2d-transient-jit-n17", "pcg_afw", "inv"),
+                                              ("3d-transient-n3", "pcg_afw", "inv"),
+                                              ("2d-steady-mis-n16", "minres_afw", "abs")])
+def test_patch_preconditioner_apply(name, method, kind):
+    """z = sum_p R_p^t B_p^{-1} R_p r on the GPU vs numpy from the oracle's G."""
+    coords, cells, prm, data, prob = make_case(**HYB_CASES[name])
+    mo = O.build_mesh(coords, cells)
+    ho = O.hybridise(mo, prm, data)
+    hg = P.cr_hybridise(P.cr_build_mesh(tg(coords), tg(cells)), prob)
+    r = np.random.default_rng(11).normal(size=hg.n_rows)
+    z = torch.empty(hg.n_rows, dtype=torch.float64, device=DEV)
+    hg.apply_precond(method, tg(r), z)
+    pats = _patches(mo)
+    info = hg.precond_info()
+    assert info["npatch"] == len(pats) and info["nfallback"] == 0
+    assert info["kmax"] == max(len(p) for p in pats)
+    zo = _afw_numpy(ho["G"], pats, mo.dim, r, kind)
+    assert relL2(z.cpu().numpy(), zo) <= 1e-9
+
+
+def test_patch_preconditioner_cuts_pcg_iterations():
+    """The patch preconditioner resolves the two scales of G: >= 4x fewer PCG iterations than
+    Jacobi at n = 32 (numpy experiment: 3186 vs 429)."""
+    coords, cells, prm, data, prob = make_case(dim=2, n=32, seed=2)
+    hg = P.cr_hybridise(P.cr_build_mesh(tg(coords), tg(cells)), prob)
+    its = {}
+    for m in ("pcg", "pcg_afw"):
+        W = torch.zeros(hg.n_rows, dtype=torch.float64, device=DEV)
+        its[m] = P.cr_solve(hg, W, m, rtol=1e-10)["iterations"]
+    assert its["pcg_afw"] * 4 <= its["pcg"], its
