@@ -5,9 +5,11 @@
 Workload (one "step"): BASELINE.json configs[1] — 2D transient Stokes, unit square,
 1024 x 1024 squares split into 2,097,152 triangles, interior vertices jittered by up to
 0.2h (seed 2), mu = nu = 1, manufactured fp64 force — run through the whole hot path:
-cr_build_mesh -> cr_hybridise -> cr_solve (Jacobi PCG to a TRUE relative residual of
-1e-10) -> cr_recover, inputs resident in HBM.  value = seconds per solve (time to
-solution, lower is better).
+cr_build_mesh -> cr_hybridise -> cr_solve (PCG to a TRUE relative residual of 1e-10, with
+the patch additive-Schwarz preconditioner) -> cr_recover,
+inputs resident in HBM.  value = seconds per step (time to solution, lower is better).
+The same step with Jacobi PCG (the north star's baseline solver) is timed once and reported
+under "pcg_jacobi".
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -32,6 +34,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "hybridised-system PCG time-to-solution; SpMV GB/s as % of B200 HBM peak"
 CONFIG_IDX = 1
+METHOD = "pcg_afw"
 # Jacobi-PCG iterations of configs[1] to a true 1e-10 residual, measured on B200 by this
 # bench (used only by --impl reference to extrapolate the oracle's per-iteration time).
 ITERS_CONFIG1_MEASURED = None
@@ -213,7 +216,7 @@ def main():
         mesh = P.cr_build_mesh(coords, cells)
         hyb = P.cr_hybridise(mesh, prob)
         W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=dev)
-        rep = P.cr_solve(hyb, W, "pcg", rtol=cfg.rtol, check_every=64)
+        rep = P.cr_solve(hyb, W, METHOD, rtol=cfg.rtol, check_every=64)
         U, Pp, diag = P.cr_recover(hyb, W)
         return mesh, hyb, rep, U, Pp, diag
 
@@ -243,22 +246,31 @@ def main():
     mesh, hyb, rep = out[0], out[1], reps[-1]
     N, nnz, nb = hyb.n_rows, hyb.nnz, hyb.nblocks
 
-    # ---- dominant kernel: the G SpMV, timed live with CUDA events on the launching stream
+    # ---- per-kernel rooflines: each kernel of the PCG step re-launched standalone on the same
+    # stream and timed with CUDA events (the in-solve launches live inside a CUDA graph)
+    peak, peak_src = measured_peaks()
+    N8 = 8 * N
+    pinfo = hyb.precond_info()
+    slots = 2 if mesh.dim == 2 else 3
+
+    def time_launch(fn, nrep=50):
+        for _ in range(5):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(nrep):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / nrep * 1e-3
+
     x = torch.randn(N, dtype=torch.float64, device=dev)
     y = torch.empty_like(x)
-    for _ in range(10):
-        hyb.spmv(x, y)
-    nrep = 50
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(nrep):
-        hyb.spmv(x, y)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    spmv_s = e0.elapsed_time(e1) / nrep * 1e-3
-    spmv_bytes = 8 * nnz + 4 * nb + 8 * N + 8 * N          # values + block cols + x once + y
-    peak, peak_src = measured_peaks()
-    achieved = spmv_bytes / spmv_s / 1e9
+    spmv_s = time_launch(lambda: hyb.spmv(x, y))
+    spmv_bytes = 8 * nnz + 4 * nb + N8 + N8          # values + block cols + x once + y
+    prec_s = time_launch(lambda: hyb.apply_precond(METHOD, x, y))
+    # patch operator + r read + slot contributions written, then read back and z written
+    prec_bytes = pinfo["bytes"] + N8 + slots * N8 + slots * N8 + N8
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "spmv_dram_bytes.json")
     if os.path.exists(tfile):
@@ -266,8 +278,13 @@ def main():
             traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    iter_bytes = 8 * nnz + 4 * nb + 9 * 8 * N               # PCG iteration, SURVEY §8(d)
+    # PCG-patch iteration: SpMV + update (x,p,r,q read; x,r write) + patch apply + p update
+    iter_bytes = spmv_bytes + 6 * N8 + (pinfo["bytes"] + N8 + slots * N8) + (slots * N8 + 2 * N8)
     iter_gbs = iter_bytes * rep["iterations"] / rep["seconds"] / 1e9 if rep["seconds"] > 0 else None
+
+    # ---- the north star's baseline solver on the same system (one timed solve)
+    Wj = torch.zeros(N, dtype=torch.float64, device=dev)
+    repj = P.cr_solve(hyb, Wj, "pcg", rtol=cfg.rtol, check_every=64)
 
     # ---- e2e through the public API from HOST buffers (pinned host -> device -> host)
     e2e = None
@@ -276,7 +293,7 @@ def main():
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        o2 = P.hybrid_method_host(coords_h, cells_h, fbar_h, cfg.mu, cfg.nu, "pcg", cfg.rtol)
+        o2 = P.hybrid_method_host(coords_h, cells_h, fbar_h, cfg.mu, cfg.nu, METHOD, cfg.rtol)
         b.record(stream)
         torch.cuda.synchronize()
         e2e_s = a.elapsed_time(b) * 1e-3
@@ -291,32 +308,40 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s = oracle_sample()
         nc_full = mesh.nc
-        v = oracle_extrapolate(s, nc_full, nnz, rep["iterations"])
+        v = oracle_extrapolate(s, nc_full, nnz, repj["iterations"])
         cpu = {"value": v, "unit": "s", "cores": 1, "kind": "oracle",
                "sample": (f"oracle on configs[1]-family mesh n={s['n']} ({s['nc']} cells): mesh+hybridise+recover "
                           f"timed in full ({s['mesh_s'] + s['hyb_s'] + s['rec_s']:.1f} s), PCG over {s['iters']} "
                           f"iterations ({s['iter_s'] * 1e3:.2f} ms/it); extrapolated per cell and per nnz x "
-                          f"{rep['iterations']} iterations to the full workload")}
+                          f"{repj['iterations']} Jacobi-PCG iterations (the oracle's solver, count measured on the B200 in this run) to the full workload")}
 
     launches = rep["kernel_launches"] + 25     # mesh (sort/scan/geometry ~15), hybridise 1, recover 3, copies
+    launches += 12 if METHOD == "pcg_afw" else 0   # patch build (pairs, sort, scans, setup)
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "configs[1] 2D transient Stokes n=%d jittered 0.2h, Jacobi-PCG to true 1e-10"
-                                   % (args.n or cfg.n),
+            "config": {"workload": "configs[1] 2D transient Stokes n=%d jittered 0.2h, patch-preconditioned PCG "
+                                   "to true 1e-10" % (args.n or cfg.n),
                        "cells": mesh.nc, "unknowns": N, "nnz_G": nnz, "blocks_G": nb,
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                        "l2": "working set > L2 (G = %.2f GB per SpMV) and a 256 MB L2 flush before each step"
                              % (8 * nnz / 1e9)},
-            "pcg": {"iterations": rep["iterations"], "rel_res_true": rep["rel_res_true"],
+            "pcg": {"method": METHOD, "iterations": rep["iterations"], "rel_res_true": rep["rel_res_true"],
                     "solve_s": rep["seconds"], "ms_per_iter": rep["seconds"] / max(rep["iterations"], 1) * 1e3,
-                    "iter_gbs": iter_gbs, "iter_bytes": iter_bytes},
+                    "iter_gbs": iter_gbs, "iter_bytes": iter_bytes, "precond": pinfo},
+            "pcg_jacobi": {"iterations": repj["iterations"], "rel_res_true": repj["rel_res_true"],
+                           "solve_s": repj["seconds"],
+                           "ms_per_iter": repj["seconds"] / max(repj["iterations"], 1) * 1e3},
             "roofline": {"kernel": "k_spmv (sliced block-ELL G x, same row code as the PCG SpMV)",
-                         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "bound": "hbm", "achieved": spmv_bytes / spmv_s / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": spmv_bytes / spmv_s / 1e9 / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes": spmv_bytes, "launch_s": spmv_s},
+            "roofline_precond": {"kernel": "k_afw_apply + k_afw_zsum (patch additive Schwarz z = M^-1 r)",
+                                 "bound": "hbm", "achieved": prec_bytes / prec_s / 1e9, "peak": peak,
+                                 "unit": "GB/s", "frac": prec_bytes / prec_s / 1e9 / peak,
+                                 "algorithmic_bytes": prec_bytes, "launch_s": prec_s},
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
             "e2e": e2e,

@@ -183,9 +183,11 @@ cr_status cr_solve(cr_hybrid h, const cr_solver_opts *opts, double *W_d, cr_stre
  * first use).  r_d, z_d [n_rows], must not alias.  Asynchronous except for a first patch
  * build (which synchronises `s`).                                                          */
 cr_status cr_apply_precond(cr_hybrid h, int32_t method, const double *r_d, double *z_d, cr_stream_t s);
-/* patch preconditioner statistics (0 if not built): number of patches, largest patch, and
- * patch blocks that were singular and fell back to their diagonal                           */
-cr_status cr_hybrid_precond_info(cr_hybrid h, int64_t *npatch, int32_t *kmax, int64_t *nfallback);
+/* patch preconditioner statistics (0 if not built): number of patches, largest patch, patch
+ * blocks that were singular and fell back to their diagonal, device bytes of the operator
+ * (what one application reads besides the vectors).  Any pointer may be NULL.               */
+cr_status cr_hybrid_precond_info(cr_hybrid h, int64_t *npatch, int32_t *kmax, int64_t *nfallback,
+                                 int64_t *bytes);
 
 /* ------------------------------------------------------------------ recovery
  * P_K = (v^t (R_K - C_K W_K) - g_K)/B_K (K != K0), P_K0 = 0;  Uhat_K = Ahat^{-1}(R_K - D_K P_K - C_K W_K);

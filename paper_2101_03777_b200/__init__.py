@@ -96,7 +96,7 @@ _sig = {
     "cr_recover": [_vp, _vp, _vp, _vp, _vp, _vp],
     "cr_comm_init": [_vp, _i32, _i32, _P(_vp)],
     "cr_apply_precond": [_vp, _i32, _vp, _vp, _vp],
-    "cr_hybrid_precond_info": [_vp, _P(_i64), _P(_i32), _P(_i64)],
+    "cr_hybrid_precond_info": [_vp, _P(_i64), _P(_i32), _P(_i64), _P(_i64)],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -243,9 +243,10 @@ class Hybrid:
         return z
 
     def precond_info(self) -> dict:
-        npatch, kmax, nfb = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64()
-        _check(_lib.cr_hybrid_precond_info(self._h, ctypes.byref(npatch), ctypes.byref(kmax), ctypes.byref(nfb)))
-        return dict(npatch=npatch.value, kmax=kmax.value, nfallback=nfb.value)
+        npatch, kmax, nfb, nby = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.cr_hybrid_precond_info(self._h, ctypes.byref(npatch), ctypes.byref(kmax), ctypes.byref(nfb),
+                                           ctypes.byref(nby)))
+        return dict(npatch=npatch.value, kmax=kmax.value, nfallback=nfb.value, bytes=nby.value)
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:

@@ -31,57 +31,57 @@ struct AfwView {
     int64_t npatch;
 };
 
-// z-contributions of patch p for all D components; returns sum_i r_p^t B_p^{-1} r_p.
+// z-contributions of one patch for one velocity component: thread t of a launch covers slice
+// t / (32 D), component (t / 32) % D, lane t % 32, so every load of ids / vals is one
+// coalesced warp row.  Returns r_p^(i)t B_p^{-1} r_p^(i) (its sum over p, i is r^t M^{-1} r).
 template <int D, int SLOTS, int KMAX, bool SYM>
-__device__ __forceinline__ double afw_patch(const AfwView &A, int64_t p, const double *__restrict__ r,
-                                            double *__restrict__ zs) {
-    const int64_t slice = p >> 5;
-    const int lane = (int)(p & 31);
+__device__ __forceinline__ double afw_patch_comp(const AfwView &A, int64_t t, const double *__restrict__ r,
+                                                 double *__restrict__ zs) {
+    const int lane = (int)(t & 31);
+    const int64_t w = t >> 5;
+    const int64_t slice = w / D;
+    const int i = (int)(w - slice * D);
     const int k = A.kl[slice];
     const int32_t *ip = A.ids + A.ioff[slice] + lane;
     int id[KMAX];
+    double rv[KMAX], y[KMAX];
 #pragma unroll
-    for (int j = 0; j < KMAX; ++j) id[j] = (j < k) ? __ldg(ip + j * 32) : -1;
+    for (int j = 0; j < KMAX; ++j) id[j] = (j < k) ? __ldcs(ip + j * 32) : -1;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        rv[j] = (id[j] >= 0) ? r[(int64_t)(id[j] / SLOTS) * D + i] : 0.0;
+        y[j] = 0.0;
+    }
     const int T = SYM ? k * (k + 1) / 2 : k * k;
-    const double *vp = A.vals + A.voff[slice] + lane;
+    const double *vi = A.vals + A.voff[slice] + lane + (int64_t)i * T * 32;
+    if constexpr (SYM) {
+#pragma unroll
+        for (int a = 0; a < KMAX; ++a) {
+            if (a < k) {
+#pragma unroll
+                for (int b = 0; b <= a; ++b) {
+                    const double v = __ldcs(vi + (a * (a + 1) / 2 + b) * 32);
+                    y[a] = fma(v, rv[b], y[a]);
+                    if (a != b) y[b] = fma(v, rv[a], y[b]);
+                }
+            }
+        }
+    } else {
+#pragma unroll
+        for (int a = 0; a < KMAX; ++a) {
+            if (a < k) {
+#pragma unroll
+                for (int b = 0; b < KMAX; ++b)
+                    if (b < k) y[a] = fma(__ldcs(vi + (a * k + b) * 32), rv[b], y[a]);
+            }
+        }
+    }
     double quad = 0.0;
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-        double rv[KMAX], y[KMAX];
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j) {
-            rv[j] = (id[j] >= 0) ? r[(int64_t)(id[j] / SLOTS) * D + i] : 0.0;
-            y[j] = 0.0;
-        }
-        const double *vi = vp + (int64_t)i * T * 32;
-        if constexpr (SYM) {
-#pragma unroll
-            for (int a = 0; a < KMAX; ++a) {
-                if (a < k) {
-#pragma unroll
-                    for (int b = 0; b <= a; ++b) {
-                        const double v = __ldcs(vi + (a * (a + 1) / 2 + b) * 32);
-                        y[a] = fma(v, rv[b], y[a]);
-                        if (a != b) y[b] = fma(v, rv[a], y[b]);
-                    }
-                }
-            }
-        } else {
-#pragma unroll
-            for (int a = 0; a < KMAX; ++a) {
-                if (a < k) {
-#pragma unroll
-                    for (int b = 0; b < KMAX; ++b)
-                        if (b < k) y[a] = fma(__ldcs(vi + (a * k + b) * 32), rv[b], y[a]);
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j) {
-            if (id[j] >= 0) {
-                quad = fma(rv[j], y[j], quad);
-                zs[(int64_t)id[j] * D + i] = y[j];
-            }
+    for (int j = 0; j < KMAX; ++j) {
+        if (id[j] >= 0) {
+            quad = fma(rv[j], y[j], quad);
+            zs[(int64_t)id[j] * D + i] = y[j];
         }
     }
     return quad;

@@ -216,9 +216,13 @@ cr_status cr_apply_precond(cr_hybrid h, int32_t method, const double *r_d, doubl
     CR_API_END
 }
 
-cr_status cr_hybrid_precond_info(cr_hybrid h, int64_t *npatch, int32_t *kmax, int64_t *nfallback) {
+cr_status cr_hybrid_precond_info(cr_hybrid h, int64_t *npatch, int32_t *kmax, int64_t *nfallback, int64_t *bytes) {
     CR_API_BEGIN
     CR_REQUIRE(h, CR_ERR_INVALID_ARG, "null handle");
+    if (bytes)
+        *bytes = h->afw.built >= 0 ? (int64_t)(h->afw.vals.n * sizeof(double) + h->afw.ids.n * sizeof(int32_t) +
+                                               h->afw.kl.n + 2 * h->afw.ioff.n * sizeof(int64_t))
+                                   : 0;
     if (npatch) *npatch = h->afw.built >= 0 ? h->afw.npatch : 0;
     if (kmax) *kmax = h->afw.built >= 0 ? h->afw.kmax : 0;
     if (nfallback) *nfallback = h->afw.built >= 0 ? h->afw.nfallback : 0;

@@ -196,6 +196,105 @@ __global__ void __launch_bounds__(kT) k_pcg_update(int64_t nrows, double *x, dou
     });
 }
 
+// Jacobi PCG, flat double2 form: x += alpha p ; r -= alpha q ; z = dinv r ; r.z, r.r
+__global__ void __launch_bounds__(kT, 4) k_pcg_update_jac(int64_t N, double *__restrict__ x, double *__restrict__ r,
+                                                       const double *__restrict__ p, const double *__restrict__ q,
+                                                       const double *__restrict__ dinv, KState *st, double *partials) {
+    if (st->flag != FLAG_RUN) return;
+    const double alpha = st->alpha;
+    double acc[2] = {0.0, 0.0};
+    const int64_t n2 = N >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+    double2 *x2 = reinterpret_cast<double2 *>(x), *r2 = reinterpret_cast<double2 *>(r);
+    const double2 *p2 = reinterpret_cast<const double2 *>(p), *q2 = reinterpret_cast<const double2 *>(q);
+    const double2 *d2 = reinterpret_cast<const double2 *>(dinv);
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n2; i += 4 * stride) {
+        double2 pv[4], qv[4], xv[4], rv[4], dv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            pv[u] = __ldcs(p2 + i + u * stride);
+            qv[u] = __ldcs(q2 + i + u * stride);
+            xv[u] = __ldcs(x2 + i + u * stride);
+            rv[u] = __ldcs(r2 + i + u * stride);
+            dv[u] = d2[i + u * stride];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            xv[u].x = fma(alpha, pv[u].x, xv[u].x);
+            xv[u].y = fma(alpha, pv[u].y, xv[u].y);
+            rv[u].x = fma(-alpha, qv[u].x, rv[u].x);
+            rv[u].y = fma(-alpha, qv[u].y, rv[u].y);
+            acc[0] = fma(rv[u].x, dv[u].x * rv[u].x, acc[0]);
+            acc[0] = fma(rv[u].y, dv[u].y * rv[u].y, acc[0]);
+            acc[1] = fma(rv[u].x, rv[u].x, acc[1]);
+            acc[1] = fma(rv[u].y, rv[u].y, acc[1]);
+            __stcs(x2 + i + u * stride, xv[u]);
+            r2[i + u * stride] = rv[u];
+        }
+    }
+    for (; i < n2; i += stride) {
+        double2 pv = p2[i], qv = q2[i], xv = x2[i], rv = r2[i], dv = d2[i];
+        xv.x = fma(alpha, pv.x, xv.x);
+        xv.y = fma(alpha, pv.y, xv.y);
+        rv.x = fma(-alpha, qv.x, rv.x);
+        rv.y = fma(-alpha, qv.y, rv.y);
+        acc[0] = fma(rv.x, dv.x * rv.x, acc[0]);
+        acc[0] = fma(rv.y, dv.y * rv.y, acc[0]);
+        acc[1] = fma(rv.x, rv.x, acc[1]);
+        acc[1] = fma(rv.y, rv.y, acc[1]);
+        x2[i] = xv;
+        r2[i] = rv;
+    }
+    if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t k = N - 1;
+        x[k] = fma(alpha, p[k], x[k]);
+        const double rk = fma(-alpha, q[k], r[k]);
+        r[k] = rk;
+        acc[0] = fma(rk, dinv[k] * rk, acc[0]);
+        acc[1] = fma(rk, rk, acc[1]);
+    }
+    reduce_and_finish<2>(acc, partials, &st->tickets[2], [&](double *t) {
+        st->iters += 1;
+        st->rr = t[1];
+        st->beta = t[0] / st->rho;
+        st->rho = t[0];
+        if (t[1] <= st->tol2) st->flag = FLAG_CONV;
+    });
+}
+
+// Jacobi PCG, flat double2 form: p = dinv r + beta p
+__global__ void __launch_bounds__(kT) k_pcg_pdir_jac(int64_t N, double *__restrict__ p, const double *__restrict__ r,
+                                                     const double *__restrict__ dinv, const KState *st) {
+    if (st->flag != FLAG_RUN) return;
+    const double beta = st->beta;
+    const int64_t n2 = N >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+    double2 *p2 = reinterpret_cast<double2 *>(p);
+    const double2 *r2 = reinterpret_cast<const double2 *>(r), *d2 = reinterpret_cast<const double2 *>(dinv);
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n2; i += 4 * stride) {
+        double2 pv[4], rv[4], dv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            pv[u] = __ldcs(p2 + i + u * stride);
+            rv[u] = r2[i + u * stride];
+            dv[u] = d2[i + u * stride];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            pv[u].x = fma(beta, pv[u].x, dv[u].x * rv[u].x);
+            pv[u].y = fma(beta, pv[u].y, dv[u].y * rv[u].y);
+            p2[i + u * stride] = pv[u];
+        }
+    }
+    for (; i < n2; i += stride) {
+        double2 pv = p2[i], rv = r2[i], dv = d2[i];
+        pv.x = fma(beta, pv.x, dv.x * rv.x);
+        pv.y = fma(beta, pv.y, dv.y * rv.y);
+        p2[i] = pv;
+    }
+    if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[N - 1] = fma(beta, p[N - 1], dinv[N - 1] * r[N - 1]);
+}
+
 template <int D, int PREC>
 __global__ void __launch_bounds__(kT) k_pcg_pdir(int64_t nrows, double *p, const double *r, const double *M, const KState *st) {
     if (st->flag != FLAG_RUN) return;
@@ -333,8 +432,8 @@ __global__ void __launch_bounds__(kT) k_afw_apply(AfwView A, const double *r, do
                                                   double *partials) {
     if (WHAT != AFW_PCG_INIT && WHAT != AFW_MINRES_INIT && st->flag != FLAG_RUN) return;
     double acc[1] = {0.0};
-    const int64_t np = ((A.npatch + 31) >> 5) << 5;
-    GRID_STRIDE(pp, np) acc[0] += afw_patch<D, SLOTS, KMAX, SYM>(A, pp, r, zs);
+    const int64_t nt = ((A.npatch + 31) >> 5) * 32 * D;     // one thread per (patch, component)
+    GRID_STRIDE(t, nt) acc[0] += afw_patch_comp<D, SLOTS, KMAX, SYM>(A, t, r, zs);
     reduce_and_finish<1>(acc, partials, &st->tickets[3], [&](double *t) {
         if (WHAT == AFW_PCG_INIT) {
             st->rho = t[0];
@@ -352,21 +451,56 @@ __global__ void __launch_bounds__(kT) k_afw_apply(AfwView A, const double *r, do
     });
 }
 
-// x += alpha p ; r -= alpha q ; |r|^2 (convergence)
-template <int D>
-__global__ void __launch_bounds__(kT) k_pcg_update_r(int64_t nrows, double *x, double *r, const double *p, const double *q,
+// x += alpha p ; r -= alpha q ; |r|^2 (convergence).  Flat over the N = D*nrows entries in
+// 16-byte double2 units, 4 independent units in flight per thread (memory-level parallelism).
+__global__ void __launch_bounds__(kT, 4) k_pcg_update_r(int64_t N, double *__restrict__ x, double *__restrict__ r,
+                                                     const double *__restrict__ p, const double *__restrict__ q,
                                                      KState *st, double *partials) {
     if (st->flag != FLAG_RUN) return;
     const double alpha = st->alpha;
     double acc[1] = {0.0};
-    GRID_STRIDE(row, nrows) {
+    const int64_t n2 = N >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+    double2 *x2 = reinterpret_cast<double2 *>(x), *r2 = reinterpret_cast<double2 *>(r);
+    const double2 *p2 = reinterpret_cast<const double2 *>(p), *q2 = reinterpret_cast<const double2 *>(q);
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n2; i += 4 * stride) {
+        double2 pv[4], qv[4], xv[4], rv[4];
 #pragma unroll
-        for (int i = 0; i < D; ++i) {
-            x[row * D + i] = fma(alpha, p[row * D + i], x[row * D + i]);
-            const double ri = fma(-alpha, q[row * D + i], r[row * D + i]);
-            r[row * D + i] = ri;
-            acc[0] += ri * ri;
+        for (int u = 0; u < 4; ++u) {
+            pv[u] = __ldcs(p2 + i + u * stride);
+            qv[u] = __ldcs(q2 + i + u * stride);
+            xv[u] = __ldcs(x2 + i + u * stride);
+            rv[u] = __ldcs(r2 + i + u * stride);
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            xv[u].x = fma(alpha, pv[u].x, xv[u].x);
+            xv[u].y = fma(alpha, pv[u].y, xv[u].y);
+            rv[u].x = fma(-alpha, qv[u].x, rv[u].x);
+            rv[u].y = fma(-alpha, qv[u].y, rv[u].y);
+            acc[0] = fma(rv[u].x, rv[u].x, acc[0]);
+            acc[0] = fma(rv[u].y, rv[u].y, acc[0]);
+            __stcs(x2 + i + u * stride, xv[u]);
+            r2[i + u * stride] = rv[u];
+        }
+    }
+    for (; i < n2; i += stride) {
+        double2 pv = p2[i], qv = q2[i], xv = x2[i], rv = r2[i];
+        xv.x = fma(alpha, pv.x, xv.x);
+        xv.y = fma(alpha, pv.y, xv.y);
+        rv.x = fma(-alpha, qv.x, rv.x);
+        rv.y = fma(-alpha, qv.y, rv.y);
+        acc[0] = fma(rv.x, rv.x, acc[0]);
+        acc[0] = fma(rv.y, rv.y, acc[0]);
+        x2[i] = xv;
+        r2[i] = rv;
+    }
+    if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t k = N - 1;
+        x[k] = fma(alpha, p[k], x[k]);
+        const double rk = fma(-alpha, q[k], r[k]);
+        r[k] = rk;
+        acc[0] = fma(rk, rk, acc[0]);
     }
     reduce_and_finish<1>(acc, partials, &st->tickets[2], [&](double *t) {
         st->iters += 1;
@@ -377,14 +511,49 @@ __global__ void __launch_bounds__(kT) k_pcg_update_r(int64_t nrows, double *x, d
 
 // p = z + beta p, z = sum of the slot contributions (beta = 0: p = z)
 template <int D, int SLOTS>
-__global__ void __launch_bounds__(kT) k_pcg_pdir_afw(int64_t nrows, double *p, const double *zs, const KState *st) {
+__global__ void __launch_bounds__(kT) k_pcg_pdir_afw(int64_t nrows, double *__restrict__ p, const double *__restrict__ zs,
+                                                     const KState *st) {
     if (st->flag != FLAG_RUN) return;
     const double beta = st->beta;
-    GRID_STRIDE(row, nrows) {
-        double z[D];
-        afw_sum<D, SLOTS>(zs, row, z);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if constexpr (D == 2) {
+        double2 *p2 = reinterpret_cast<double2 *>(p);
+        const double2 *z2 = reinterpret_cast<const double2 *>(zs);
+        int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        for (; row + 3 * stride < nrows; row += 4 * stride) {
+            double2 pv[4], zv[4][SLOTS];
 #pragma unroll
-        for (int i = 0; i < D; ++i) p[row * D + i] = (beta == 0.0) ? z[i] : fma(beta, p[row * D + i], z[i]);
+            for (int u = 0; u < 4; ++u) {
+                pv[u] = __ldcs(p2 + row + u * stride);
+#pragma unroll
+                for (int sl = 0; sl < SLOTS; ++sl) zv[u][sl] = __ldcs(z2 + (row + u * stride) * SLOTS + sl);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                double zx = zv[u][0].x, zy = zv[u][0].y;
+#pragma unroll
+                for (int sl = 1; sl < SLOTS; ++sl) { zx += zv[u][sl].x; zy += zv[u][sl].y; }
+                pv[u].x = (beta == 0.0) ? zx : fma(beta, pv[u].x, zx);
+                pv[u].y = (beta == 0.0) ? zy : fma(beta, pv[u].y, zy);
+                p2[row + u * stride] = pv[u];
+            }
+        }
+        for (; row < nrows; row += stride) {
+            double2 pv = p2[row];
+            double zx = 0.0, zy = 0.0;
+#pragma unroll
+            for (int sl = 0; sl < SLOTS; ++sl) { const double2 zz = z2[row * SLOTS + sl]; zx += zz.x; zy += zz.y; }
+            pv.x = (beta == 0.0) ? zx : fma(beta, pv.x, zx);
+            pv.y = (beta == 0.0) ? zy : fma(beta, pv.y, zy);
+            p2[row] = pv;
+        }
+    } else {
+        GRID_STRIDE(row, nrows) {
+            double z[D];
+            afw_sum<D, SLOTS>(zs, row, z);
+#pragma unroll
+            for (int i = 0; i < D; ++i) p[row * D + i] = (beta == 0.0) ? z[i] : fma(beta, p[row * D + i], z[i]);
+        }
     }
 }
 
@@ -753,11 +922,14 @@ static void launch_afw(Launcher &L, cudaStream_t ks, const double *r, double *zs
     constexpr int SLOTS = D == 2 ? 2 : 3;
     const AfwPrec &P = L.h->afw;
     AfwView A{P.ioff.get(), P.voff.get(), P.kl.get(), P.ids.get(), P.vals.get(), P.npatch};
-    const int grid = grid_for(P.nslices * 32, kT);
+    const int grid = grid_for(P.nslices * 32 * D, kT);
     const bool sym = P.built != AFW_GEN;
     KState *st = L.w->st.get();
     double *part = L.w->partials.get();
-    if (P.kmax <= 8) {
+    if (P.kmax <= 6) {
+        if (sym) k_afw_apply<D, SLOTS, 6, true, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part);
+        else k_afw_apply<D, SLOTS, 6, false, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part);
+    } else if (P.kmax <= 8) {
         if (sym) k_afw_apply<D, SLOTS, 8, true, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part);
         else k_afw_apply<D, SLOTS, 8, false, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part);
     } else {
@@ -843,8 +1015,8 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                     k_pcg_update<D, 1><<<L.grid_rows, kT, 0, ks>>>(nrows, x, w->r.get(), w->p.get(), w->q.get(), M, st, part);
                     k_pcg_pdir<D, 1><<<L.grid_rows, kT, 0, ks>>>(nrows, w->p.get(), w->r.get(), M, st);
                 } else {
-                    k_pcg_update<D, 0><<<L.grid_rows, kT, 0, ks>>>(nrows, x, w->r.get(), w->p.get(), w->q.get(), M, st, part);
-                    k_pcg_pdir<D, 0><<<L.grid_rows, kT, 0, ks>>>(nrows, w->p.get(), w->r.get(), M, st);
+                    k_pcg_update_jac<<<L.grid_vec, kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), M, st, part);
+                    k_pcg_pdir_jac<<<L.grid_vec, kT, 0, ks>>>(N, w->p.get(), w->r.get(), M, st);
                 }
                 CR_CHECK_LAUNCH();
             };
@@ -883,7 +1055,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         while (w->hst->flag == FLAG_RUN) {
             auto body = [&](int) {
                 k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part);
-                k_pcg_update_r<D><<<L.grid_rows, kT, 0, ks>>>(nrows, x, w->r.get(), w->p.get(), w->q.get(), st, part);
+                k_pcg_update_r<<<L.grid_vec, kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), st, part);
                 CR_CHECK_LAUNCH();
                 launch_afw<D, AFW_PCG>(L, ks, w->r.get(), zs, rtol);
                 k_pcg_pdir_afw<D, SLOTS><<<L.grid_rows, kT, 0, ks>>>(nrows, w->p.get(), zs, st);
