@@ -13,8 +13,10 @@ under "pcg_jacobi".
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-For N > 1 (torchrun, one rank per GPU) every rank solves its own replica of the workload
-(no data-path collective), timed on the device, max over ranks.
+For N > 1 (torchrun, one rank per GPU) the SAME problem is partitioned: each rank owns a slab
+of face rows of G, exchanges SpMV ghosts with its neighbours (NCCL send/recv) and allreduces
+the Krylov dot products (strong scaling); timed on the device, max over
+ranks.
 --impl reference times the CPU oracle (oracle/, numpy/scipy + binary128 C) on the host
 cores on a bounded sample of the same workload and extrapolates per unit.
 """
@@ -37,7 +39,7 @@ CONFIG_IDX = 1
 METHOD = "pcg_afw"
 # Jacobi-PCG iterations of configs[1] to a true 1e-10 residual, measured on B200 by this
 # bench (used only by --impl reference to extrapolate the oracle's per-iteration time).
-ITERS_CONFIG1_MEASURED = None
+ITERS_CONFIG1_MEASURED = 162221   # Jacobi PCG, configs[1], B200 bench r01 (profiles/r01_bench_*.log)
 
 
 def measured_peaks():
@@ -159,7 +161,7 @@ def run_reference(args):
                    f"nnz x {iters_full} iterations (B200-measured count) to n=1024")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "configs[1] 2D transient Stokes n=1024 jittered, Jacobi-PCG to 1e-10",
                        "cells": nc, "unknowns": N},
             "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "oracle", "sample": sample_desc},
@@ -195,8 +197,13 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        # libcr's own NCCL communicator (halo send/recv + allreduce inside its CUDA graphs)
+        uid = [P.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = P.Comm.nccl(uid[0], rank, world)
 
     def barrier():
         if world > 1:
@@ -214,7 +221,7 @@ def main():
     def step():
         prob = P.Problem(mu=cfg.mu, nu=cfg.nu, fbar=fbar)
         mesh = P.cr_build_mesh(coords, cells)
-        hyb = P.cr_hybridise(mesh, prob)
+        hyb = P.cr_hybridise(mesh, prob, comm=comm)
         W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=dev)
         rep = P.cr_solve(hyb, W, METHOD, rtol=cfg.rtol, check_every=64)
         U, Pp, diag = P.cr_recover(hyb, W)
@@ -293,7 +300,7 @@ def main():
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        o2 = P.hybrid_method_host(coords_h, cells_h, fbar_h, cfg.mu, cfg.nu, METHOD, cfg.rtol)
+        o2 = P.hybrid_method_host(coords_h, cells_h, fbar_h, cfg.mu, cfg.nu, METHOD, cfg.rtol, comm=comm)
         b.record(stream)
         torch.cuda.synchronize()
         e2e_s = a.elapsed_time(b) * 1e-3
@@ -320,12 +327,13 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "configs[1] 2D transient Stokes n=%d jittered 0.2h, patch-preconditioned PCG "
                                    "to true 1e-10" % (args.n or cfg.n),
                        "cells": mesh.nc, "unknowns": N, "nnz_G": nnz, "blocks_G": nb,
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"face rows partitioned over {world} GPUs (NCCL halo send/recv + allreduce)"
+                                       if world > 1 else "1 GPU"),
                        "l2": "working set > L2 (G = %.2f GB per SpMV) and a 256 MB L2 flush before each step"
                              % (8 * nnz / 1e9)},
             "pcg": {"method": METHOD, "iterations": rep["iterations"], "rel_res_true": rep["rel_res_true"],

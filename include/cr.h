@@ -60,6 +60,7 @@ typedef struct cr_mesh_s *cr_mesh;
 typedef struct cr_coupled_s *cr_coupled;
 typedef struct cr_hybrid_s *cr_hybrid;
 typedef struct cr_comm_s *cr_comm;
+typedef struct cr_loopback_s *cr_loopback;
 
 /* ------------------------------------------------------------------ mesh
  * coords_d [nv][dim] f64, cells_d [nc][dim+1] i32 (0-based vertex ids, any orientation).
@@ -132,9 +133,11 @@ void cr_destroy_coupled(cr_coupled c);
  * Synchronises `s`.  Errors: NO_INTERIOR_FACE, SINGULAR_LOCAL, INVALID_ARG, OOM, CUDA.   */
 cr_status cr_hybridise(cr_mesh m, const cr_params *prm, const cr_data *data, cr_comm comm,
                        cr_stream_t s, cr_hybrid *out);
-/* n_rows = dim*nf_int; nnz = scalar nonzeros of G (explicit zeros of the stencil included) */
+/* n_rows = dim*nf_int (partitioned: dim * owned rows); nnz = scalar nonzeros of G (explicit
+ * zeros of the stencil included; partitioned: of the owned rows)                            */
 cr_status cr_hybrid_info(cr_hybrid h, int64_t *n_rows, int64_t *nnz, int64_t *nblocks);
-/* canonical scalar CSR of G (int64 row_ptr_d [n_rows+1], cols ascending) and S_d [n_rows] */
+/* canonical scalar CSR of G (int64 row_ptr_d [n_rows+1], cols ascending) and S_d [n_rows];
+ * partitioned: the owned rows, with GLOBAL column indices                                   */
 cr_status cr_hybrid_export_csr(cr_hybrid h, int64_t *row_ptr_d, int32_t *cols_d, double *vals_d,
                                double *S_d, cr_stream_t s);
 /* MIS membership inM1_d [nc] (u8) and E_d [nc][dim+1] (shift per local face); either may be NULL */
@@ -197,9 +200,40 @@ cr_status cr_hybrid_precond_info(cr_hybrid h, int64_t *npatch, int32_t *kmax, in
 cr_status cr_recover(cr_hybrid h, const double *W_d, double *U_d, double *P_d, double *diag_d,
                      cr_stream_t s);
 
-/* ------------------------------------------------------------------ multi-GPU (reserved) */
+/* ------------------------------------------------------------------ multi-GPU
+ * One process per GPU.  Rank q of P owns the contiguous block rows [floor(q F/P), floor((q+1)F/P))
+ * of G (F = nf_int, lexicographic face order = slabs); every rank builds the whole mesh, assembles
+ * and stores only its rows (columns renumbered: owned rows first, then ghosts in ascending global
+ * order) and exchanges ghost entries of the SpMV input with the ranks that own them.  Partitioned
+ * handles come from cr_hybridise(..., comm, ...) with comm->nranks > 1; then n_rows of
+ * cr_hybrid_info, the W_d of cr_solve and the x/y of cr_spmv are LOCAL (owned rows x dim);
+ * cr_recover gathers W and returns the GLOBAL U [nf_int][dim] and P [nc] on every rank.
+ * Distributed cr_solve supports the PCG methods (CR_PCG_JACOBI, CR_PCG_AFW; the patch
+ * preconditioner uses the patches restricted to the owned faces).                            */
+/* 128-byte NCCL unique id (rank 0 creates it and broadcasts it, e.g. with torch.distributed) */
+cr_status cr_nccl_unique_id(void *out128);
+/* NCCL communicator (nranks > 1; NCCL is dlopen'ed: import torch first) or a trivial one (1)  */
 cr_status cr_comm_init(const void *nccl_unique_id, int32_t rank, int32_t nranks, cr_comm *out);
+/* In-process loopback group: nranks host threads of ONE process share one GPU, exchanging
+ * through device copies and host barriers (no NCCL, no CUDA graphs).  For testing the
+ * partitioned path on a single GPU; each thread uses its own comm from cr_comm_init_loopback. */
+cr_status cr_loopback_create(int32_t nranks, cr_loopback *out);
+void cr_loopback_destroy(cr_loopback g);
+cr_status cr_comm_init_loopback(cr_loopback g, int32_t rank, cr_comm *out);
 void cr_comm_destroy(cr_comm c);
+/* partition of a hybrid handle: owned global block rows [row0, row1), ghosts, global rows    */
+cr_status cr_hybrid_partition_info(cr_hybrid h, int64_t *row0, int64_t *row1, int64_t *nghost,
+                                   int64_t *nglobal);
+/* The partition plan on the HOST (no GPU): for rank `rank` of `nranks`, row_range [2], per-peer
+ * recv_counts / send_counts [nranks] (block rows), then, if non-NULL, ghosts [sum recv_counts]
+ * (ascending global block rows) and send_rows [sum send_counts] (global block rows, by peer,
+ * ascending).  Arrays as exported by cr_mesh_export plus dof_face [nf_int] (the face of each
+ * interior dof).  Call once with ghosts = send_rows = NULL to size them.                    */
+cr_status cr_partition_plan(int32_t dim, int64_t nf_int, const int32_t *cell_faces_h,
+                            const int32_t *face_cells_h, const int32_t *face_dof_h,
+                            const int32_t *dof_face_h, int32_t rank, int32_t nranks,
+                            int64_t *row_range, int64_t *recv_counts, int64_t *send_counts,
+                            int32_t *ghosts, int32_t *send_rows);
 
 const char *cr_last_error(void);
 const char *cr_version(void);

@@ -95,6 +95,11 @@ _sig = {
     "cr_solve": [_vp, _P(SolverOpts), _vp, _vp, _P(SolveReport)],
     "cr_recover": [_vp, _vp, _vp, _vp, _vp, _vp],
     "cr_comm_init": [_vp, _i32, _i32, _P(_vp)],
+    "cr_nccl_unique_id": [_vp],
+    "cr_loopback_create": [_i32, _P(_vp)],
+    "cr_comm_init_loopback": [_vp, _i32, _P(_vp)],
+    "cr_hybrid_partition_info": [_vp, _P(_i64), _P(_i64), _P(_i64), _P(_i64)],
+    "cr_partition_plan": [_i32, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp],
     "cr_apply_precond": [_vp, _i32, _vp, _vp, _vp],
     "cr_hybrid_precond_info": [_vp, _P(_i64), _P(_i32), _P(_i64), _P(_i64)],
 }
@@ -102,14 +107,14 @@ for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
     _f.argtypes = _args
     _f.restype = _st
-for _name in ("cr_destroy_mesh", "cr_destroy_coupled", "cr_destroy_hybrid", "cr_comm_destroy"):
+for _name in ("cr_destroy_mesh", "cr_destroy_coupled", "cr_destroy_hybrid", "cr_comm_destroy", "cr_loopback_destroy"):
     getattr(_lib, _name).argtypes = [_vp]
     getattr(_lib, _name).restype = None
 _lib.cr_last_error.restype = ctypes.c_char_p
 _lib.cr_version.restype = ctypes.c_char_p
 
 ABI_SYMBOLS = sorted(list(_sig) + ["cr_destroy_mesh", "cr_destroy_coupled", "cr_destroy_hybrid",
-                                   "cr_comm_destroy", "cr_last_error", "cr_version"])
+                                   "cr_comm_destroy", "cr_loopback_destroy", "cr_last_error", "cr_version"])
 
 
 def _check(status: int, report=None):
@@ -216,6 +221,12 @@ class Hybrid:
         _check(_lib.cr_hybrid_info(self._h, ctypes.byref(nr), ctypes.byref(nnz), ctypes.byref(nb)))
         self.n_rows, self.nnz, self.nblocks = nr.value, nnz.value, nb.value
 
+    def partition_info(self) -> dict:
+        r0, r1, ng, nglob = (ctypes.c_int64() for _ in range(4))
+        _check(_lib.cr_hybrid_partition_info(self._h, ctypes.byref(r0), ctypes.byref(r1), ctypes.byref(ng),
+                                             ctypes.byref(nglob)))
+        return dict(row0=r0.value, row1=r1.value, nghost=ng.value, nglobal=nglob.value)
+
     def export_csr(self, stream=None):
         dev = torch.device("cuda")
         rp = torch.empty(self.n_rows + 1, dtype=torch.int64, device=dev)
@@ -254,13 +265,81 @@ class Hybrid:
             self._h = None
 
 
-def cr_hybridise(mesh: Mesh, prob: Problem, stream=None) -> Hybrid:
-    """G and S of G W = S."""
+def cr_hybridise(mesh: Mesh, prob: Problem, stream=None, comm: "Comm | None" = None) -> Hybrid:
+    """G and S of G W = S.  With a multi-rank ``comm`` only this rank's rows."""
     h = ctypes.c_void_p()
     prm, data = prob.params(), prob.data()
-    _check(_lib.cr_hybridise(mesh._h, ctypes.byref(prm), ctypes.byref(data), None, _stream(stream),
-                             ctypes.byref(h)))
-    return Hybrid(h, mesh)
+    _check(_lib.cr_hybridise(mesh._h, ctypes.byref(prm), ctypes.byref(data), comm._h if comm else None,
+                             _stream(stream), ctypes.byref(h)))
+    hy = Hybrid(h, mesh)
+    hy.comm = comm          # keep the communicator alive as long as the handle
+    return hy
+
+
+# ------------------------------------------------------------------ multi-GPU (SURVEY §8(e))
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (call on rank 0, broadcast to the others)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.cr_nccl_unique_id(buf))
+    return buf.raw
+
+
+class LoopbackGroup:
+    """In-process group of ``n`` ranks sharing one GPU (testing the partitioned path)."""
+
+    def __init__(self, n: int):
+        self._h = ctypes.c_void_p()
+        _check(_lib.cr_loopback_create(n, ctypes.byref(self._h)))
+        self.n = n
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.cr_loopback_destroy(self._h)
+            self._h = None
+
+
+class Comm:
+    """cr_comm handle: NCCL (one process per GPU) or in-process loopback."""
+
+    def __init__(self, handle, rank: int, nranks: int, keep=None):
+        self._h, self.rank, self.nranks, self._keep = handle, rank, nranks, keep
+
+    @classmethod
+    def nccl(cls, unique_id: bytes, rank: int, nranks: int) -> "Comm":
+        h = ctypes.c_void_p()
+        _check(_lib.cr_comm_init(ctypes.c_char_p(unique_id), rank, nranks, ctypes.byref(h)))
+        return cls(h, rank, nranks)
+
+    @classmethod
+    def loopback(cls, group: LoopbackGroup, rank: int) -> "Comm":
+        h = ctypes.c_void_p()
+        _check(_lib.cr_comm_init_loopback(group._h, rank, ctypes.byref(h)))
+        return cls(h, rank, group.n, keep=group)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.cr_comm_destroy(self._h)
+            self._h = None
+
+
+def partition_plan(dim: int, cell_faces, face_cells, face_dof, rank: int, nranks: int) -> dict:
+    """Host partition plan (no GPU): numpy int32 arrays as exported by the mesh."""
+    import numpy as np
+    cf = np.ascontiguousarray(cell_faces, dtype=np.int32)
+    fc = np.ascontiguousarray(face_cells, dtype=np.int32)
+    fd = np.ascontiguousarray(face_dof, dtype=np.int32)
+    df = np.ascontiguousarray(np.nonzero(fd >= 0)[0], dtype=np.int32)
+    nf_int = len(df)
+    rr = np.zeros(2, np.int64)
+    rc = np.zeros(nranks, np.int64)
+    sc = np.zeros(nranks, np.int64)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    args = (dim, nf_int, p(cf), p(fc), p(fd), p(df), rank, nranks, p(rr), p(rc), p(sc))
+    _check(_lib.cr_partition_plan(*args, None, None))
+    gh = np.zeros(int(rc.sum()), np.int32)
+    sr = np.zeros(int(sc.sum()), np.int32)
+    _check(_lib.cr_partition_plan(*args, p(gh), p(sr)))
+    return dict(row0=int(rr[0]), row1=int(rr[1]), recv_counts=rc, send_counts=sc, ghosts=gh, send_rows=sr)
 
 
 def cr_solve(hyb: Hybrid, W: torch.Tensor, method: str | int = "pcg", rtol: float = 1e-10,
@@ -279,7 +358,8 @@ def cr_solve(hyb: Hybrid, W: torch.Tensor, method: str | int = "pcg", rtol: floa
 
 
 def cr_recover(hyb: Hybrid, W: torch.Tensor, stream=None):
-    """P and U from W.  Returns U [nf_int, d], P [nc], diag [2]."""
+    """P and U from W.  Returns U [nf_int, d], P [nc], diag [2]
+    (global arrays on every rank of a partitioned handle; W holds this rank's rows)."""
     mesh = hyb.mesh
     dev = W.device
     U = torch.empty((mesh.nf_int, mesh.dim), dtype=torch.float64, device=dev)
@@ -322,11 +402,12 @@ def cr_assemble_coupled(mesh: Mesh, prob: Problem, stream=None) -> Coupled:
 
 # ------------------------------------------------------------------ the paper's "hybrid method"
 def hybrid_method(coords: torch.Tensor, cells: torch.Tensor, prob: Problem, method: str = "pcg",
-                  rtol: float = 1e-10, stream=None, **solve_kw) -> dict:
+                  rtol: float = 1e-10, stream=None, comm: Comm | None = None, **solve_kw) -> dict:
     """(1) mesh, G and S; (2) solve G W = S; (3) recover P and U.
-    All tensors must already be on the GPU."""
+    All tensors must already be on the GPU.  With a multi-rank ``comm`` (one call per rank)
+    each rank holds and solves its rows of G; U and P come back whole on every rank."""
     mesh = cr_build_mesh(coords, cells, stream)
-    hyb = cr_hybridise(mesh, prob, stream)
+    hyb = cr_hybridise(mesh, prob, stream, comm)
     W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=coords.device)
     rep = cr_solve(hyb, W, method, rtol, stream=stream, **solve_kw)
     U, P, diag = cr_recover(hyb, W, stream)
@@ -334,7 +415,7 @@ def hybrid_method(coords: torch.Tensor, cells: torch.Tensor, prob: Problem, meth
 
 
 def hybrid_method_host(coords, cells, fbar, mu: float, nu: float, method: str = "pcg", rtol: float = 1e-10,
-                       stream=None, **kw) -> dict:
+                       stream=None, comm: Comm | None = None, **kw) -> dict:
     """End-to-end entry point from HOST buffers: pinned host -> device copies, the hybrid
     method on the device, and U, P copied back to host (the `e2e` path of bench.py)."""
     dev = torch.device("cuda")
@@ -342,7 +423,7 @@ def hybrid_method_host(coords, cells, fbar, mu: float, nu: float, method: str = 
     k = cells.to(dev, non_blocking=True)
     f = fbar.to(dev, non_blocking=True)
     prob = Problem(mu=mu, nu=nu, fbar=f, **kw)
-    out = hybrid_method(c, k, prob, method, rtol, stream)
+    out = hybrid_method(c, k, prob, method, rtol, stream, comm)
     out["U_host"] = out["U"].to("cpu")
     out["P_host"] = out["P"].to("cpu")
     return out

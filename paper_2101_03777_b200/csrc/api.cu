@@ -148,12 +148,10 @@ cr_status cr_hybridise(cr_mesh m, const cr_params *prm, const cr_data *data, cr_
                        cr_hybrid *out) {
     CR_API_BEGIN
     CR_REQUIRE(m && prm && data && out, CR_ERR_INVALID_ARG, "null argument");
-    CR_REQUIRE(comm == nullptr || comm->nranks == 1, CR_ERR_INVALID_ARG,
-               "multi-GPU hybridisation goes through the partitioned path (comm must be NULL)");
     *out = nullptr;
     cr_hybrid_s *h = new cr_hybrid_s();
     try {
-        cr::hybridise(h, m, *prm, *data, (cudaStream_t)s);
+        cr::hybridise(h, m, *prm, *data, comm, (cudaStream_t)s);
     } catch (...) {
         delete h;
         throw;
@@ -169,6 +167,17 @@ cr_status cr_hybrid_info(cr_hybrid h, int64_t *n_rows, int64_t *nnz, int64_t *nb
     if (n_rows) *n_rows = h->G.nrows * D;
     if (nnz) *nnz = h->G.nblocks * D * D;
     if (nblocks) *nblocks = h->G.nblocks;
+    CR_API_END
+}
+
+cr_status cr_hybrid_partition_info(cr_hybrid h, int64_t *row0, int64_t *row1, int64_t *nghost, int64_t *nglobal) {
+    CR_API_BEGIN
+    CR_REQUIRE(h, CR_ERR_INVALID_ARG, "null handle");
+    const bool on = h->part.on;
+    if (row0) *row0 = on ? h->part.row0 : 0;
+    if (row1) *row1 = on ? h->part.row1 : h->G.nrows;
+    if (nghost) *nghost = on ? h->part.nghost : 0;
+    if (nglobal) *nglobal = on ? h->part.nglobal : h->G.nrows;
     CR_API_END
 }
 
@@ -192,7 +201,8 @@ cr_status cr_hybrid_export_shift(cr_hybrid h, uint8_t *inM1_d, double *E_d, cr_s
 cr_status cr_spmv(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s) {
     CR_API_BEGIN
     CR_REQUIRE(h && x_d && y_d && x_d != y_d, CR_ERR_INVALID_ARG, "bad arguments");
-    cr::spmv(h->G, x_d, y_d, (cudaStream_t)s);
+    if (h->part.on) cr::spmv_part(h, x_d, y_d, (cudaStream_t)s);
+    else cr::spmv(h->G, x_d, y_d, (cudaStream_t)s);
     CR_API_END
 }
 
@@ -235,19 +245,5 @@ cr_status cr_recover(cr_hybrid h, const double *W_d, double *U_d, double *P_d, d
     cr::recover(h, W_d, U_d, P_d, diag_d, (cudaStream_t)s);
     CR_API_END
 }
-
-cr_status cr_comm_init(const void *nccl_unique_id, int32_t rank, int32_t nranks, cr_comm *out) {
-    CR_API_BEGIN
-    CR_REQUIRE(out && nranks >= 1 && rank >= 0 && rank < nranks, CR_ERR_INVALID_ARG, "bad communicator arguments");
-    (void)nccl_unique_id;
-    CR_REQUIRE(nranks == 1, CR_ERR_INVALID_ARG, "multi-rank communicators are created by the partitioned driver");
-    cr_comm_s *c = new cr_comm_s();
-    c->rank = rank;
-    c->nranks = nranks;
-    *out = c;
-    CR_API_END
-}
-
-void cr_comm_destroy(cr_comm c) { delete c; }
 
 }  // extern "C"

@@ -205,11 +205,11 @@ __device__ __forceinline__ void finish_row(const AsmOut &o, int64_t r, int slot,
 
 template <int D>
 __global__ void __launch_bounds__(128) k_assemble_stokes(MeshView mv, ProbView p, const int32_t *dof_face,
-                                                         int64_t nrows, AsmOut o) {
+                                                         int64_t nrows, int64_t row0, const int32_t *g2l, AsmOut o) {
     constexpr int NF = D + 1;
     unsigned long long nb_local = 0;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
-        const int f = dof_face[r];
+        const int f = dof_face[row0 + r];
         double diag[D][D], Sr[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) {
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(128) k_assemble_stokes(MeshView mv, ProbView p
 #pragma unroll
                         for (int j = 0; j < D; ++j) diag[i][j] += b[i][j];
                 } else {
-                    write_block<D>(o, r, slot++, (int32_t)c.dof[lq], b);
+                    write_block<D>(o, r, slot++, g2l ? g2l[c.dof[lq]] : (int32_t)c.dof[lq], b);
                 }
             }
         }
@@ -287,10 +287,10 @@ __global__ void __launch_bounds__(128) k_assemble_stokes(MeshView mv, ProbView p
 
 template <int D>
 __global__ void __launch_bounds__(64) k_assemble_ns(MeshView mv, ProbView p, const int32_t *dof_face,
-                                                    int64_t nrows, AsmOut o) {
+                                                         int64_t nrows, int64_t row0, const int32_t *g2l, AsmOut o) {
     unsigned long long nb_local = 0;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
-        const int f = dof_face[r];
+        const int f = dof_face[row0 + r];
         double diag[D][D], Sr[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) {
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(64) k_assemble_ns(MeshView mv, ProbView p, con
 #pragma unroll
                         for (int j = 0; j < D; ++j) diag[i][j] += b[i][j];
                 } else {
-                    write_block<D>(o, r, slot++, (int32_t)c.dof[lq], b);
+                    write_block<D>(o, r, slot++, g2l ? g2l[c.dof[lq]] : (int32_t)c.dof[lq], b);
                 }
             }
         }
@@ -409,7 +409,10 @@ static cr_status status_of(int e) {
 template <int D>
 static void hybridise_t(cr_hybrid_s *h, const cr_mesh_s *m, cudaStream_t s) {
     const int T = 256;
-    const int64_t nc = m->nc, nrows = m->nf_int;
+    const int64_t nc = m->nc;
+    const int64_t nrows = h->part.on ? h->part.nloc : m->nf_int;
+    const int64_t row0 = h->part.on ? h->part.row0 : 0;
+    const int32_t *g2l = h->part.on ? h->part.g2l.get() : nullptr;
     MeshView mv = mesh_view(m);
     DevBuf<int> err;
     err.alloc(1, s);
@@ -466,9 +469,9 @@ static void hybridise_t(cr_hybrid_s *h, const cr_mesh_s *m, cudaStream_t s) {
              h->bdinv.get(), nb.get(), err.get()};
     ProbView p = prob_view(h);
     if (!h->is_ns) {
-        k_assemble_stokes<D><<<grid_for(nrows, 128, 16), 128, 0, s>>>(mv, p, m->dof_face.get(), nrows, o);
+        k_assemble_stokes<D><<<grid_for(nrows, 128, 16), 128, 0, s>>>(mv, p, m->dof_face.get(), nrows, row0, g2l, o);
     } else {
-        k_assemble_ns<D><<<grid_for(nrows, 64, 16), 64, 0, s>>>(mv, p, m->dof_face.get(), nrows, o);
+        k_assemble_ns<D><<<grid_for(nrows, 64, 16), 64, 0, s>>>(mv, p, m->dof_face.get(), nrows, row0, g2l, o);
     }
     CR_CHECK_LAUNCH();
     int e = read_int(err.get(), s);
@@ -479,7 +482,8 @@ static void hybridise_t(cr_hybrid_s *h, const cr_mesh_s *m, cudaStream_t s) {
     G.nblocks = (int64_t)hnb;
 }
 
-void hybridise(cr_hybrid_s *h, const cr_mesh_s *m, const cr_params &prm, const cr_data &data, cudaStream_t s) {
+void hybridise(cr_hybrid_s *h, const cr_mesh_s *m, const cr_params &prm, const cr_data &data, cr_comm_s *comm,
+               cudaStream_t s) {
     CR_REQUIRE(prm.physics == CR_STOKES || prm.physics == CR_NS_NEWTON_STEP, CR_ERR_INVALID_ARG, "bad physics");
     CR_REQUIRE(prm.shift == CR_SHIFT_NONE || prm.shift == CR_SHIFT_MIS, CR_ERR_INVALID_ARG, "bad shift");
     CR_REQUIRE(prm.gauge_cell >= 0 && prm.gauge_cell < m->nc, CR_ERR_INVALID_ARG, "gauge cell out of range");
@@ -491,6 +495,8 @@ void hybridise(cr_hybrid_s *h, const cr_mesh_s *m, const cr_params &prm, const c
     h->is_ns = prm.physics == CR_NS_NEWTON_STEP;
     CR_REQUIRE(!h->is_ns || data.u_iter_d, CR_ERR_INVALID_ARG, "NS step needs u_iter_d");
     copy_problem_data(h, m, data, s);
+    h->comm = comm;
+    if (comm && comm->nranks > 1) setup_part(h, m, comm, s);
     if (m->dim == 2) hybridise_t<2>(h, m, s);
     else hybridise_t<3>(h, m, s);
 }
@@ -504,14 +510,18 @@ __global__ void k_csr_counts(int64_t nrows, const uint8_t *rowlen, int64_t *cnt)
 
 template <int D>
 __global__ void k_csr_fill(EllView<D> G, const uint8_t *rowlen, const int64_t *base, const double *S,
-                           int64_t *row_ptr, int32_t *cols, double *vals, double *Sout) {
+                           const int32_t *l2g, int64_t *row_ptr, int32_t *cols, double *vals, double *Sout) {
     constexpr int W = 2 * D + 1, B2 = D * D;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < G.nrows; r += (int64_t)gridDim.x * blockDim.x) {
         const int nb = rowlen[r];
         const int64_t slice = r >> 5;
         const int lane = (int)(r & 31);
         int bc[W], bs[W];
-        for (int k = 0; k < nb; ++k) { bc[k] = G.cols[slice * (W * 32) + k * 32 + lane]; bs[k] = k; }
+        for (int k = 0; k < nb; ++k) {
+            const int32_t c = G.cols[slice * (W * 32) + k * 32 + lane];
+            bc[k] = l2g ? l2g[c] : c;   // partitioned: export GLOBAL block columns
+            bs[k] = k;
+        }
         for (int i = 1; i < nb; ++i)            // insertion sort by block column
             for (int j = i; j > 0 && bc[j - 1] > bc[j]; --j) {
                 int t = bc[j]; bc[j] = bc[j - 1]; bc[j - 1] = t;
@@ -535,6 +545,7 @@ void hybrid_export_csr(const cr_hybrid_s *h, int64_t *row_ptr, int32_t *cols, do
                        cudaStream_t s) {
     const int D = h->G.d;
     const int64_t nrows = h->G.nrows;
+    const int32_t *l2g = h->part.on ? h->part.l2g.get() : nullptr;
     DevBuf<int64_t> cnt, base;
     cnt.alloc(nrows, s);
     base.alloc(nrows, s);
@@ -549,10 +560,10 @@ void hybrid_export_csr(const cr_hybrid_s *h, int64_t *row_ptr, int32_t *cols, do
     CR_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, cnt.get(), base.get(), (int)nrows, s));
     if (D == 2) {
         EllView<2> G{h->G.cols.get(), h->G.vals.get(), nrows};
-        k_csr_fill<2><<<grid_for(nrows, T), T, 0, s>>>(G, h->rowlen.get(), base.get(), h->S.get(), row_ptr, cols, vals, S);
+        k_csr_fill<2><<<grid_for(nrows, T), T, 0, s>>>(G, h->rowlen.get(), base.get(), h->S.get(), l2g, row_ptr, cols, vals, S);
     } else {
         EllView<3> G{h->G.cols.get(), h->G.vals.get(), nrows};
-        k_csr_fill<3><<<grid_for(nrows, T), T, 0, s>>>(G, h->rowlen.get(), base.get(), h->S.get(), row_ptr, cols, vals, S);
+        k_csr_fill<3><<<grid_for(nrows, T), T, 0, s>>>(G, h->rowlen.get(), base.get(), h->S.get(), l2g, row_ptr, cols, vals, S);
     }
     CR_CHECK_LAUNCH();
     int64_t nnz = h->G.nblocks * D * D;

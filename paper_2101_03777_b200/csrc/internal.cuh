@@ -118,6 +118,45 @@ struct BlockEll {
 
 namespace cr { struct SolverWork; }
 
+namespace cr {
+// host partition plan (partition.cu)
+struct PartPlan {
+    int rank = 0, nranks = 1;
+    int64_t row0 = 0, row1 = 0;
+    std::vector<int64_t> ghosts;                  // ascending global block rows
+    std::vector<int64_t> recv_counts, send_counts;  // per peer (block rows)
+    std::vector<int32_t> send_rows;               // global block rows, by peer then ascending
+};
+void plan_partition(int dim, int64_t nf_int, const int32_t *cell_faces, const int32_t *face_cells,
+                    const int32_t *face_dof, const int32_t *dof_face, int rank, int nranks, PartPlan &pl);
+int64_t part_row0(int64_t nrows, int rank, int nranks);
+
+// device-side partition of a hybrid system (empty when not partitioned)
+struct Part {
+    bool on = false;
+    int rank = 0, nranks = 1;
+    int64_t row0 = 0, row1 = 0, nloc = 0, nghost = 0, nglobal = 0;
+    std::vector<int64_t> rcount, roff, scount, soff;   // per peer, block rows
+    std::vector<int64_t> all_row0;                     // row0 of every rank, + nglobal
+    int64_t nsend = 0;
+    DevBuf<int32_t> send_rows;   // LOCAL row of each packed send entry
+    DevBuf<int32_t> g2l;         // [nglobal] global block row -> local index (owned, then ghosts) or -1
+    DevBuf<int32_t> l2g;         // [nloc + nghost]
+    DevBuf<double> sendbuf;      // [nsend * D]
+};
+
+// collectives of the partitioned path (comm.cu)
+struct Comm {
+    int rank = 0, nranks = 1;
+    virtual ~Comm() {}
+    virtual bool capturable() const = 0;
+    virtual void allreduce(double *d, int n, bool max, cudaStream_t s) = 0;
+    virtual void halo(const Part &P, const double *sendbuf, double *xghost, int D, cudaStream_t s) = 0;
+    virtual void allgatherv(const double *local, double *full, const std::vector<int64_t> &counts,
+                            const std::vector<int64_t> &displs, cudaStream_t s) = 0;
+};
+}  // namespace cr
+
 // overlapping-patch additive Schwarz preconditioner (afw.cuh layout)
 struct AfwPrec {
     int built = -1;              // mode it was built for (-1 = not built)
@@ -145,6 +184,8 @@ struct cr_hybrid_s {
     cr::DevBuf<double> S, dinv, absdinv, bdinv;   // bdinv [nrows][d][d] inverse diagonal blocks
     cr::DevBuf<uint8_t> rowlen;                   // true blocks per block row
     AfwPrec afw;
+    cr::Part part;               // row partition (multi-GPU); part.on == false on one GPU
+    cr_comm_s *comm = nullptr;   // borrowed
     cr::SolverWork *work = nullptr;
     ~cr_hybrid_s();
 };
@@ -158,6 +199,7 @@ struct cr_coupled_s {
 
 struct cr_comm_s {
     int rank = 0, nranks = 1;
+    cr::Comm *impl = nullptr;   // null for a single rank
 };
 
 namespace cr {
@@ -165,8 +207,10 @@ namespace cr {
 void build_mesh(cr_mesh_s *m, int dim, int64_t nv, const double *coords, int64_t nc,
                 const int32_t *cells, cudaStream_t s);
 // hybrid.cu
-void hybridise(cr_hybrid_s *h, const cr_mesh_s *m, const cr_params &prm, const cr_data &data,
+void hybridise(cr_hybrid_s *h, const cr_mesh_s *m, const cr_params &prm, const cr_data &data, cr_comm_s *comm,
                cudaStream_t s);
+// partition.cu
+void setup_part(cr_hybrid_s *h, const cr_mesh_s *m, cr_comm_s *comm, cudaStream_t s);
 void hybrid_export_csr(const cr_hybrid_s *h, int64_t *row_ptr, int32_t *cols, double *vals, double *S,
                        cudaStream_t s);
 void assemble_coupled(cr_coupled_s *c, const cr_mesh_s *m, const cr_params &prm, const cr_data &data,
@@ -178,6 +222,7 @@ void recover(const cr_hybrid_s *h, const double *W, double *U, double *P, double
 void solve(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep);
 void free_solver_work(SolverWork *w);
 void apply_precond(cr_hybrid_s *h, int method, const double *r, double *z, cudaStream_t s);
+void spmv_part(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s);
 // precond.cu
 void build_afw(cr_hybrid_s *h, int mode, cudaStream_t s);
 // shared: copy problem data into hybrid-owned buffers

@@ -265,7 +265,8 @@ static void build_afw_t(cr_hybrid_s *h, int mode, cudaStream_t s) {
     DevBuf<uint64_t> k0, k1;
     DevBuf<uint32_t> v0, v1;
     k0.alloc(n, s); k1.alloc(n, s); v0.alloc(n, s); v1.alloc(n, s);
-    k_patch_pairs<D><<<grid_for(nrows, T), T, 0, s>>>(m->faces.get(), m->dof_face.get(), nrows, bits, k0.get(), v0.get());
+    k_patch_pairs<D><<<grid_for(nrows, T), T, 0, s>>>(m->faces.get(), m->dof_face.get() + (h->part.on ? h->part.row0 : 0),
+                                                       nrows, bits, k0.get(), v0.get());
     CR_CHECK_LAUNCH();
     const int end_bit = D == 2 ? bits : 2 * bits;
     size_t tb = 0;

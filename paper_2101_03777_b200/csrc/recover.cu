@@ -126,6 +126,18 @@ __global__ void k_cell_divergence(MeshView mv, const double *dir, int64_t nc, co
 void recover(const cr_hybrid_s *h, const double *W, double *U, double *P, double *diag, cudaStream_t s) {
     const cr_mesh_s *m = h->mesh;
     const int D = m->dim;
+    DevBuf<double> Wfull;
+    if (h->part.on) {   // every rank recovers the whole mesh from the gathered W (once per solve)
+        const Part &Pt = h->part;
+        std::vector<int64_t> cnt(Pt.nranks), dsp(Pt.nranks);
+        for (int q = 0; q < Pt.nranks; ++q) {
+            dsp[q] = Pt.all_row0[q] * D;
+            cnt[q] = (Pt.all_row0[q + 1] - Pt.all_row0[q]) * D;
+        }
+        Wfull.alloc(Pt.nglobal * D, s);
+        h->comm->impl->allgatherv(W, Wfull.get(), cnt, dsp, s);
+        W = Wfull.get();
+    }
     const int64_t nc = m->nc, nrows = m->nf_int;
     MeshView mv = mesh_view(m);
     ProbView p = prob_view(h);

@@ -32,6 +32,7 @@ struct KState {
     int flag;
     int k;               // GMRES: Arnoldi steps done in the current cycle
     unsigned tickets[8];
+    double red[4];       // distributed mode: this rank's reduction values, allreduced in place
     double rho, alpha, beta, pq, rr, bb, tol2;
     // MINRES
     double gamma, gamma_old, delta, eta, eta0, c, c_old, s, s_old;
@@ -102,11 +103,82 @@ __device__ __forceinline__ void stv(double *a, int64_t r, const double (&v)[D]) 
     for (int i = 0; i < D; ++i) a[r * D + i] = v[i];
 }
 
+// ------------------------------------------------------------------ scalar recurrences
+// Applied by the last block of a reduction on one GPU, or by k_fin after the allreduce of
+// the per-rank values in st->red on several (the same code either way).
+enum FinKind { FIN_BB, FIN_RR, FIN_PCG_INIT, FIN_PQ, FIN_UPD_PC, FIN_UPD_R, FIN_AFW_PCG_INIT, FIN_AFW_PCG };
+
+__device__ __forceinline__ void apply_fin(KState *st, int kind, const double *t, double rtol) {
+    switch (kind) {
+        case FIN_BB: st->bb = t[0]; break;
+        case FIN_RR: st->rr = t[0]; break;
+        case FIN_PCG_INIT:   // t = (r.z, r.r)
+            st->rho = t[0];
+            st->rr = t[1];
+            st->tol2 = rtol * rtol * st->bb;
+            st->flag = (t[1] <= st->tol2) ? FLAG_CONV : FLAG_RUN;
+            break;
+        case FIN_PQ:         // t = p.q
+            st->pq = t[0];
+            if (!(t[0] > 0.0)) st->flag = FLAG_BREAK;
+            else st->alpha = st->rho / t[0];
+            break;
+        case FIN_UPD_PC:     // t = (r.z, r.r)
+            st->iters += 1;
+            st->rr = t[1];
+            st->beta = t[0] / st->rho;
+            st->rho = t[0];
+            if (t[1] <= st->tol2) st->flag = FLAG_CONV;
+            break;
+        case FIN_UPD_R:      // t = r.r
+            st->iters += 1;
+            st->rr = t[0];
+            if (t[0] <= st->tol2) st->flag = FLAG_CONV;
+            break;
+        case FIN_AFW_PCG_INIT:   // t = r^t M^{-1} r
+            st->rho = t[0];
+            st->beta = 0.0;
+            st->tol2 = rtol * rtol * st->bb;
+            st->flag = (st->rr <= st->tol2) ? FLAG_CONV : FLAG_RUN;
+            break;
+        case FIN_AFW_PCG:
+            st->beta = t[0] / st->rho;
+            st->rho = t[0];
+            break;
+    }
+}
+
+template <int NV>
+__device__ __forceinline__ void fin_or_store(KState *st, int kind, const double *t, double rtol, int dist) {
+    if (dist) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) st->red[i] = t[i];
+    } else {
+        apply_fin(st, kind, t, rtol);
+    }
+}
+
+// distributed mode: the recurrence after the allreduce (a converged state stays frozen)
+__global__ void k_fin(KState *st, int kind, double rtol) {
+    const bool init = kind == FIN_BB || kind == FIN_RR || kind == FIN_PCG_INIT || kind == FIN_AFW_PCG_INIT;
+    if (!init && st->flag != FLAG_RUN) return;
+    apply_fin(st, kind, st->red, rtol);
+}
+
+// pack the owned rows peers need: buf[k] = x[send_rows[k]]
+template <int D>
+__global__ void k_halo_pack(int64_t n, const int32_t *rows, const double *x, double *buf) {
+    GRID_STRIDE(k, n) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) buf[k * D + i] = x[(int64_t)rows[k] * D + i];
+    }
+}
+
 // ------------------------------------------------------------------ generic
 // q = G x ; r = b - q ; partial |r|^2  (true residual)
 template <int D>
 __global__ void __launch_bounds__(kT) k_true_residual(EllView<D> G, const double *x, const double *b, double *r,
-                                                      KState *st, double *partials) {
+                                                      KState *st, double *partials, int dist) {
     double acc[1] = {0.0};
     GRID_STRIDE(row, G.nrows) {
         double y[D];
@@ -118,19 +190,19 @@ __global__ void __launch_bounds__(kT) k_true_residual(EllView<D> G, const double
             acc[0] += ri * ri;
         }
     }
-    reduce_and_finish<1>(acc, partials, &st->tickets[7], [&](double *t) { st->rr = t[0]; });
+    reduce_and_finish<1>(acc, partials, &st->tickets[7], [&](double *t) { fin_or_store<1>(st, FIN_RR, t, 0.0, dist); });
 }
 
-__global__ void k_norm2(const double *a, int64_t n, KState *st, double *partials) {
+__global__ void k_norm2(const double *a, int64_t n, KState *st, double *partials, int dist) {
     double acc[1] = {0.0};
     GRID_STRIDE(i, n) acc[0] += a[i] * a[i];
-    reduce_and_finish<1>(acc, partials, &st->tickets[6], [&](double *t) { st->bb = t[0]; });
+    reduce_and_finish<1>(acc, partials, &st->tickets[6], [&](double *t) { fin_or_store<1>(st, FIN_BB, t, 0.0, dist); });
 }
 
 // ------------------------------------------------------------------ PCG
 template <int D, int PREC>
 __global__ void __launch_bounds__(kT) k_pcg_init(int64_t nrows, const double *b, const double *r, double *p,
-                                                 const double *M, double rtol, KState *st, double *partials) {
+                                                 const double *M, double rtol, KState *st, double *partials, int dist) {
     // r already holds b - G x (k_true_residual); z = M r ; p = z ; rho = r.z
     double acc[2] = {0.0, 0.0};
     GRID_STRIDE(row, nrows) {
@@ -141,16 +213,11 @@ __global__ void __launch_bounds__(kT) k_pcg_init(int64_t nrows, const double *b,
 #pragma unroll
         for (int i = 0; i < D; ++i) { acc[0] += rv[i] * zv[i]; acc[1] += rv[i] * rv[i]; }
     }
-    reduce_and_finish<2>(acc, partials, &st->tickets[0], [&](double *t) {
-        st->rho = t[0];
-        st->rr = t[1];
-        st->tol2 = rtol * rtol * st->bb;
-        st->flag = (t[1] <= st->tol2) ? FLAG_CONV : FLAG_RUN;
-    });
+    reduce_and_finish<2>(acc, partials, &st->tickets[0], [&](double *t) { fin_or_store<2>(st, FIN_PCG_INIT, t, rtol, dist); });
 }
 
 template <int D>
-__global__ void __launch_bounds__(kT) k_pcg_spmv(EllView<D> G, const double *p, double *q, KState *st, double *partials) {
+__global__ void __launch_bounds__(kT) k_pcg_spmv(EllView<D> G, const double *p, double *q, KState *st, double *partials, int dist) {
     if (st->flag != FLAG_RUN) return;
     double acc[1] = {0.0};
     GRID_STRIDE(row, G.nrows) {
@@ -162,16 +229,12 @@ __global__ void __launch_bounds__(kT) k_pcg_spmv(EllView<D> G, const double *p, 
             acc[0] += p[row * D + i] * y[i];
         }
     }
-    reduce_and_finish<1>(acc, partials, &st->tickets[1], [&](double *t) {
-        st->pq = t[0];
-        if (!(t[0] > 0.0)) st->flag = FLAG_BREAK;
-        else st->alpha = st->rho / t[0];
-    });
+    reduce_and_finish<1>(acc, partials, &st->tickets[1], [&](double *t) { fin_or_store<1>(st, FIN_PQ, t, 0.0, dist); });
 }
 
 template <int D, int PREC>
 __global__ void __launch_bounds__(kT) k_pcg_update(int64_t nrows, double *x, double *r, const double *p, const double *q,
-                                                   const double *M, KState *st, double *partials) {
+                                                   const double *M, KState *st, double *partials, int dist) {
     if (st->flag != FLAG_RUN) return;
     const double alpha = st->alpha;
     double acc[2] = {0.0, 0.0};
@@ -187,19 +250,14 @@ __global__ void __launch_bounds__(kT) k_pcg_update(int64_t nrows, double *x, dou
 #pragma unroll
         for (int i = 0; i < D; ++i) { acc[0] += rv[i] * zv[i]; acc[1] += rv[i] * rv[i]; }
     }
-    reduce_and_finish<2>(acc, partials, &st->tickets[2], [&](double *t) {
-        st->iters += 1;
-        st->rr = t[1];
-        st->beta = t[0] / st->rho;
-        st->rho = t[0];
-        if (t[1] <= st->tol2) st->flag = FLAG_CONV;
-    });
+    reduce_and_finish<2>(acc, partials, &st->tickets[2], [&](double *t) { fin_or_store<2>(st, FIN_UPD_PC, t, 0.0, dist); });
 }
 
 // Jacobi PCG, flat double2 form: x += alpha p ; r -= alpha q ; z = dinv r ; r.z, r.r
 __global__ void __launch_bounds__(kT, 4) k_pcg_update_jac(int64_t N, double *__restrict__ x, double *__restrict__ r,
                                                        const double *__restrict__ p, const double *__restrict__ q,
-                                                       const double *__restrict__ dinv, KState *st, double *partials) {
+                                                       const double *__restrict__ dinv, KState *st, double *partials,
+                                                       int dist) {
     if (st->flag != FLAG_RUN) return;
     const double alpha = st->alpha;
     double acc[2] = {0.0, 0.0};
@@ -253,13 +311,7 @@ __global__ void __launch_bounds__(kT, 4) k_pcg_update_jac(int64_t N, double *__r
         acc[0] = fma(rk, dinv[k] * rk, acc[0]);
         acc[1] = fma(rk, rk, acc[1]);
     }
-    reduce_and_finish<2>(acc, partials, &st->tickets[2], [&](double *t) {
-        st->iters += 1;
-        st->rr = t[1];
-        st->beta = t[0] / st->rho;
-        st->rho = t[0];
-        if (t[1] <= st->tol2) st->flag = FLAG_CONV;
-    });
+    reduce_and_finish<2>(acc, partials, &st->tickets[2], [&](double *t) { fin_or_store<2>(st, FIN_UPD_PC, t, 0.0, dist); });
 }
 
 // Jacobi PCG, flat double2 form: p = dinv r + beta p
@@ -429,20 +481,16 @@ enum { AFW_PCG_INIT = 0, AFW_PCG = 1, AFW_MINRES_INIT = 2, AFW_MINRES = 3 };
 // zs (per face slot) = patch contributions of M^{-1} r
 template <int D, int SLOTS, int KMAX, bool SYM, int WHAT>
 __global__ void __launch_bounds__(kT) k_afw_apply(AfwView A, const double *r, double *zs, double rtol, KState *st,
-                                                  double *partials) {
+                                                  double *partials, int dist) {
     if (WHAT != AFW_PCG_INIT && WHAT != AFW_MINRES_INIT && st->flag != FLAG_RUN) return;
     double acc[1] = {0.0};
     const int64_t nt = ((A.npatch + 31) >> 5) * 32 * D;     // one thread per (patch, component)
     GRID_STRIDE(t, nt) acc[0] += afw_patch_comp<D, SLOTS, KMAX, SYM>(A, t, r, zs);
     reduce_and_finish<1>(acc, partials, &st->tickets[3], [&](double *t) {
         if (WHAT == AFW_PCG_INIT) {
-            st->rho = t[0];
-            st->beta = 0.0;
-            st->tol2 = rtol * rtol * st->bb;
-            st->flag = (st->rr <= st->tol2) ? FLAG_CONV : FLAG_RUN;
+            fin_or_store<1>(st, FIN_AFW_PCG_INIT, t, rtol, dist);
         } else if (WHAT == AFW_PCG) {
-            st->beta = t[0] / st->rho;
-            st->rho = t[0];
+            fin_or_store<1>(st, FIN_AFW_PCG, t, rtol, dist);
         } else if (WHAT == AFW_MINRES_INIT) {
             minres_start(st, t[0]);
         } else {
@@ -455,7 +503,7 @@ __global__ void __launch_bounds__(kT) k_afw_apply(AfwView A, const double *r, do
 // 16-byte double2 units, 4 independent units in flight per thread (memory-level parallelism).
 __global__ void __launch_bounds__(kT, 4) k_pcg_update_r(int64_t N, double *__restrict__ x, double *__restrict__ r,
                                                      const double *__restrict__ p, const double *__restrict__ q,
-                                                     KState *st, double *partials) {
+                                                     KState *st, double *partials, int dist) {
     if (st->flag != FLAG_RUN) return;
     const double alpha = st->alpha;
     double acc[1] = {0.0};
@@ -502,11 +550,7 @@ __global__ void __launch_bounds__(kT, 4) k_pcg_update_r(int64_t N, double *__res
         r[k] = rk;
         acc[0] = fma(rk, rk, acc[0]);
     }
-    reduce_and_finish<1>(acc, partials, &st->tickets[2], [&](double *t) {
-        st->iters += 1;
-        st->rr = t[0];
-        if (t[0] <= st->tol2) st->flag = FLAG_CONV;
-    });
+    reduce_and_finish<1>(acc, partials, &st->tickets[2], [&](double *t) { fin_or_store<1>(st, FIN_UPD_R, t, 0.0, dist); });
 }
 
 // p = z + beta p, z = sum of the slot contributions (beta = 0: p = z)
@@ -866,6 +910,8 @@ __global__ void __launch_bounds__(kT) k_gmres_update_x(int64_t n, const double *
 static void ensure_work(cr_hybrid_s *h, cudaStream_t s) {
     const int D = h->G.d;
     const int64_t N = h->G.nrows * D;
+    // SpMV inputs carry the ghost rows of a partitioned system after the owned ones
+    const int64_t Nalloc = (h->G.nrows + (h->part.on ? h->part.nghost : 0)) * D;
     if (h->work && h->work->N == N) return;
     delete h->work;
     SolverWork *w = new SolverWork();
@@ -874,7 +920,7 @@ static void ensure_work(cr_hybrid_s *h, cudaStream_t s) {
     w->D = D;
     for (DevBuf<double> *b : {&w->x, &w->b, &w->r, &w->p, &w->q, &w->z, &w->z2, &w->v, &w->v2, &w->w, &w->w2, &w->y,
                               &w->t, &w->rhat}) {
-        b->alloc(N, s);
+        b->alloc(Nalloc, s);
         b->zero(s);
     }
     w->partials.alloc((size_t)kSMs * 16 * (kMaxRestart + 1), s);
@@ -895,6 +941,29 @@ struct Launcher {
     int D;
     int64_t nrows, N;
     int grid_rows, grid_vec;
+    int dist = 0;           // partitioned over several ranks
+    Comm *comm = nullptr;
+
+    // after a reducing kernel: allreduce this rank's values and apply the recurrence
+    void reduced(cudaStream_t ks, int nv, int kind, double rtol) {
+        if (!dist) return;
+        comm->allreduce(w->st.get()->red, nv, false, ks);
+        k_fin<<<1, 32, 0, ks>>>(w->st.get(), kind, rtol);
+        CR_CHECK_LAUNCH();
+        ++launches;
+    }
+    // ghost rows of an SpMV input from the ranks that own them
+    void halo(cudaStream_t ks, double *v) {
+        if (!dist) return;
+        const Part &P = h->part;
+        if (P.nsend) {
+            if (D == 2) k_halo_pack<2><<<grid_for(P.nsend, kT), kT, 0, ks>>>(P.nsend, P.send_rows.get(), v, P.sendbuf.get());
+            else k_halo_pack<3><<<grid_for(P.nsend, kT), kT, 0, ks>>>(P.nsend, P.send_rows.get(), v, P.sendbuf.get());
+            CR_CHECK_LAUNCH();
+            ++launches;
+        }
+        comm->halo(P, P.sendbuf.get(), v + P.nloc * D, D, ks);
+    }
 };
 
 template <int D>
@@ -906,9 +975,12 @@ static void read_state(SolverWork *w, cudaStream_t s) {
 }
 
 template <int D>
-static void true_residual(Launcher &L, const double *x, double *r) {
-    k_true_residual<D><<<L.grid_rows, kT, 0, L.s>>>(ell<D>(L.h), x, L.w->b.get(), r, L.w->st.get(), L.w->partials.get());
+static void true_residual(Launcher &L, double *x, double *r) {
+    L.halo(L.s, x);
+    k_true_residual<D><<<L.grid_rows, kT, 0, L.s>>>(ell<D>(L.h), x, L.w->b.get(), r, L.w->st.get(), L.w->partials.get(),
+                                                   L.dist);
     CR_CHECK_LAUNCH();
+    L.reduced(L.s, 1, FIN_RR, 0.0);
     ++L.launches;
     ++L.spmvs;
 }
@@ -927,22 +999,33 @@ static void launch_afw(Launcher &L, cudaStream_t ks, const double *r, double *zs
     KState *st = L.w->st.get();
     double *part = L.w->partials.get();
     if (P.kmax <= 6) {
-        if (sym) k_afw_apply<D, SLOTS, 6, true, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part);
-        else k_afw_apply<D, SLOTS, 6, false, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part);
+        if (sym) k_afw_apply<D, SLOTS, 6, true, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        else k_afw_apply<D, SLOTS, 6, false, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
     } else if (P.kmax <= 8) {
-        if (sym) k_afw_apply<D, SLOTS, 8, true, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part);
-        else k_afw_apply<D, SLOTS, 8, false, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part);
+        if (sym) k_afw_apply<D, SLOTS, 8, true, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        else k_afw_apply<D, SLOTS, 8, false, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
     } else {
-        if (sym) k_afw_apply<D, SLOTS, 16, true, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part);
-        else k_afw_apply<D, SLOTS, 16, false, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part);
+        if (sym) k_afw_apply<D, SLOTS, 16, true, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        else k_afw_apply<D, SLOTS, 16, false, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
     }
     CR_CHECK_LAUNCH();
     ++L.launches;
+    if (WHAT == AFW_PCG_INIT) L.reduced(ks, 1, FIN_AFW_PCG_INIT, rtol);
+    if (WHAT == AFW_PCG) L.reduced(ks, 1, FIN_AFW_PCG, rtol);
 }
 
 template <class Body, class Done>
 static void graph_loop(Launcher &L, cudaStream_t &ks, int key, int k, Body body, Done done) {
     SolverWork *w = L.w;
+    if (L.dist && !L.comm->capturable()) {   // host-synchronising collectives: no graph
+        ks = L.s;
+        while (true) {
+            for (int i = 0; i < k; ++i) body(i);
+            read_state(w, L.s);
+            if (done()) break;
+        }
+        return;
+    }
     if (w->graph_key != key) {
         if (w->graph) { cudaGraphExecDestroy(w->graph); w->graph = nullptr; }
         cudaGraph_t g;
@@ -976,6 +1059,10 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     L.N = w->N;
     L.grid_rows = grid_for(L.nrows, kT);
     L.grid_vec = grid_for(L.N, kT);
+    L.dist = h->part.on ? 1 : 0;
+    L.comm = h->part.on ? h->comm->impl : nullptr;
+    CR_REQUIRE(!L.dist || o.method == CR_PCG_JACOBI || o.method == CR_PCG_BLOCKJACOBI || o.method == CR_PCG_AFW,
+               CR_ERR_INVALID_ARG, "a partitioned (multi-GPU) solve supports the PCG methods only");
     const int64_t N = w->N, nrows = L.nrows;
     const double rtol = o.rtol > 0 ? o.rtol : 1e-10;
     const int64_t max_iter = o.max_iter > 0 ? o.max_iter : 10000000;
@@ -988,8 +1075,9 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     CR_CUDA(cudaEventRecord(w->e0, s));
     double *part = w->partials.get();
     KState *st = w->st.get();
-    k_norm2<<<L.grid_vec, kT, 0, s>>>(w->b.get(), N, st, part);
+    k_norm2<<<L.grid_vec, kT, 0, s>>>(w->b.get(), N, st, part, L.dist);
     CR_CHECK_LAUNCH();
+    L.reduced(s, 1, FIN_BB, 0.0);
     ++L.launches;
     cr_status status = CR_OK;
     int replacements = 0;
@@ -1000,9 +1088,10 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         const double *M = blk ? h->bdinv.get() : h->dinv.get();
         auto init = [&]() {
             true_residual<D>(L, x, w->r.get());
-            if (blk) k_pcg_init<D, 1><<<L.grid_rows, kT, 0, s>>>(nrows, w->b.get(), w->r.get(), w->p.get(), M, rtol, st, part);
-            else k_pcg_init<D, 0><<<L.grid_rows, kT, 0, s>>>(nrows, w->b.get(), w->r.get(), w->p.get(), M, rtol, st, part);
+            if (blk) k_pcg_init<D, 1><<<L.grid_rows, kT, 0, s>>>(nrows, w->b.get(), w->r.get(), w->p.get(), M, rtol, st, part, L.dist);
+            else k_pcg_init<D, 0><<<L.grid_rows, kT, 0, s>>>(nrows, w->b.get(), w->r.get(), w->p.get(), M, rtol, st, part, L.dist);
             CR_CHECK_LAUNCH();
+            L.reduced(s, 2, FIN_PCG_INIT, rtol);
             ++L.launches;
         };
         init();
@@ -1010,12 +1099,19 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         if (w->hst->bb == 0.0) { CR_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), s)); }
         while (w->hst->flag == FLAG_RUN) {
             auto body = [&](int) {
-                k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part);
+                L.halo(ks, w->p.get());
+                k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part, L.dist);
+                CR_CHECK_LAUNCH();
+                L.reduced(ks, 1, FIN_PQ, rtol);
                 if (blk) {
-                    k_pcg_update<D, 1><<<L.grid_rows, kT, 0, ks>>>(nrows, x, w->r.get(), w->p.get(), w->q.get(), M, st, part);
+                    k_pcg_update<D, 1><<<L.grid_rows, kT, 0, ks>>>(nrows, x, w->r.get(), w->p.get(), w->q.get(), M, st, part, L.dist);
+                    CR_CHECK_LAUNCH();
+                    L.reduced(ks, 2, FIN_UPD_PC, rtol);
                     k_pcg_pdir<D, 1><<<L.grid_rows, kT, 0, ks>>>(nrows, w->p.get(), w->r.get(), M, st);
                 } else {
-                    k_pcg_update_jac<<<L.grid_vec, kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), M, st, part);
+                    k_pcg_update_jac<<<L.grid_vec, kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), M, st, part, L.dist);
+                    CR_CHECK_LAUNCH();
+                    L.reduced(ks, 2, FIN_UPD_PC, rtol);
                     k_pcg_pdir_jac<<<L.grid_vec, kT, 0, ks>>>(N, w->p.get(), w->r.get(), M, st);
                 }
                 CR_CHECK_LAUNCH();
@@ -1054,9 +1150,13 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         if (w->hst->bb == 0.0) { CR_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), s)); }
         while (w->hst->flag == FLAG_RUN) {
             auto body = [&](int) {
-                k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part);
-                k_pcg_update_r<<<L.grid_vec, kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), st, part);
+                L.halo(ks, w->p.get());
+                k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part, L.dist);
                 CR_CHECK_LAUNCH();
+                L.reduced(ks, 1, FIN_PQ, rtol);
+                k_pcg_update_r<<<L.grid_vec, kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), st, part, L.dist);
+                CR_CHECK_LAUNCH();
+                L.reduced(ks, 1, FIN_UPD_R, rtol);
                 launch_afw<D, AFW_PCG>(L, ks, w->r.get(), zs, rtol);
                 k_pcg_pdir_afw<D, SLOTS><<<L.grid_rows, kT, 0, ks>>>(nrows, w->p.get(), zs, st);
                 CR_CHECK_LAUNCH();
@@ -1320,6 +1420,26 @@ static void apply_precond_t(cr_hybrid_s *h, int method, const double *r, double 
             throw Error(CR_ERR_INVALID_ARG, "unknown preconditioner method");
     }
     CR_CHECK_LAUNCH();
+}
+
+// y = G x on a partitioned handle: x (owned rows) -> work vector, halo, SpMV of the owned rows
+template <int D>
+static void spmv_part_t(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s) {
+    ensure_work(h, s);
+    SolverWork *w = h->work;
+    Launcher L{h, w, s};
+    L.D = D;
+    L.dist = 1;
+    L.comm = h->comm->impl;
+    double *xt = w->t.get();
+    CR_CUDA(cudaMemcpyAsync(xt, x, w->N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    L.halo(s, xt);
+    spmv(h->G, xt, y, s);
+}
+
+void spmv_part(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s) {
+    if (h->G.d == 2) spmv_part_t<2>(h, x, y, s);
+    else spmv_part_t<3>(h, x, y, s);
 }
 
 void apply_precond(cr_hybrid_s *h, int method, const double *r, double *z, cudaStream_t s) {

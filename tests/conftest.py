@@ -11,10 +11,18 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+    config.addinivalue_line("markers", "timeout(seconds): per-test time limit (pytest-timeout)")
 
 
 @pytest.fixture(scope="session", autouse=True)
 def _build_oracle():
     import oracle
     oracle.build()
+    lib = os.path.join(ROOT, "paper_2101_03777_b200", "libcr.so")
+    if not os.path.exists(lib):   # nvcc cross-compiles on a CPU box too
+        import importlib.util
+        spec = importlib.util.spec_from_file_location("_cr_build", os.path.join(ROOT, "paper_2101_03777_b200", "build.py"))
+        b = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(b)
+        b.build()
     yield

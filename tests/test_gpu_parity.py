@@ -337,3 +337,59 @@ def test_patch_preconditioner_cuts_pcg_iterations():
         W = torch.zeros(hg.n_rows, dtype=torch.float64, device=DEV)
         its[m] = P.cr_solve(hg, W, m, rtol=1e-10)["iterations"]
     assert its["pcg_afw"] * 4 <= its["pcg"], its
+
+
+# ------------------------------------------------------------------ partitioned path (multi-GPU)
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("dim,n,nranks,method", [(2, 12, 2, "pcg"), (2, 12, 3, "pcg_afw"), (2, 10, 2, "pcg_block"),
+                                                 (3, 3, 2, "pcg_afw"), (3, 4, 4, "pcg")])
+def test_partitioned_loopback(dim, n, nranks, method):
+    """The row-partitioned path (local assembly with renumbered columns, halo exchange before
+    every SpMV, allreduced dot products, W gathered for the recovery) with `nranks` ranks as
+    threads of this process on one GPU (loopback communicator): each rank's rows of
+    G and S equal the oracle's, and every rank recovers the oracle's U and P."""
+    import threading
+    coords, cells, prm, data, prob = make_case(dim=dim, n=n)
+    mo = O.build_mesh(coords, cells)
+    ho = O.hybrid_pipeline(mo, prm, data)
+    grp = P.LoopbackGroup(nranks)
+    res, errs = [None] * nranks, []
+
+    def run(rank):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                comm = P.Comm.loopback(grp, rank)
+                c, k = tg(coords), tg(cells)
+                out = P.hybrid_method(c, k, prob, method, rtol=1e-12, stream=st, comm=comm, check_every=16)
+                rp, cols, vals, S = out["hybrid"].export_csr(st)
+                st.synchronize()
+                res[rank] = dict(out=out, info=out["hybrid"].partition_info(), rp=rp.cpu().numpy(),
+                                 cols=cols.cpu().numpy(), vals=vals.cpu().numpy(), S=S.cpu().numpy(),
+                                 U=out["U"].cpu().numpy(), P=out["P"].cpu().numpy())
+        except Exception as e:   # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    d = mo.dim
+    Go = ho["G"].tocsr()
+    rows_seen = 0
+    for rank, r in enumerate(res):
+        inf = r["info"]
+        assert inf["nglobal"] == mo.nf_int
+        r0, r1 = inf["row0"], inf["row1"]
+        rows_seen += r1 - r0
+        Gl = sp.csr_matrix((r["vals"], r["cols"], r["rp"]), shape=((r1 - r0) * d, mo.nf_int * d))
+        Gref = Go[r0 * d:r1 * d]
+        assert same_pattern(Gl, Gref)
+        assert row_rel_err(Gl, Gref) <= 1e-12
+        assert np.abs(r["S"] - ho["S"][r0 * d:r1 * d]).max() <= 1e-12 * np.abs(ho["S"]).max()
+        assert relL2(r["U"], ho["U"]) <= 1e-8 and relL2(r["P"], ho["P"]) <= 1e-8
+        assert np.array_equal(r["U"], res[0]["U"]) and np.array_equal(r["P"], res[0]["P"])
+        assert r["out"]["report"]["converged"]
+    assert rows_seen == mo.nf_int
