@@ -144,14 +144,21 @@ cr_status cr_hybrid_export_csr(cr_hybrid h, int64_t *row_ptr_d, int32_t *cols_d,
 cr_status cr_hybrid_export_shift(cr_hybrid h, uint8_t *inM1_d, double *E_d, cr_stream_t s);
 /* y = G x (the solver's SpMV kernel; x_d, y_d [n_rows], must not alias).  Asynchronous. */
 cr_status cr_spmv(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s);
+/* y = G x with the matrix-free factored operator (built on first use; transient Stokes,
+ * unpartitioned handles): G = sum_K H_K C_K[I (x) Shat_K^{-1} - u_K u_K^t]C_K H_K^t, u = w/sqrt(B)
+ * (P:L508-517); x_d, y_d [n_rows], must not alias.  Asynchronous after the first build.    */
+cr_status cr_spmv_mf(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s);
+/* matrix-free operator statistics (0 if not built): cells (padded to 32) and device bytes     */
+cr_status cr_hybrid_mf_info(cr_hybrid h, int64_t *ncells, int64_t *bytes);
 void cr_destroy_hybrid(cr_hybrid h);
 
 /* ------------------------------------------------------------------ solve
  * Solves G W = S.  W_d [n_rows] holds the initial guess on entry (use zeros) and the solution
  * on exit.  Stopping rule: TRUE relative residual ||S - G W||_2 / ||S||_2 <= rtol (recomputed
  * at exit; recursive-residual convergence triggers a true-residual check and, if it fails, a
- * residual replacement).  refine_dd = 1 adds outer iterative refinement with the residual
- * S - G W accumulated in double-double (parity mode).  Synchronises `s`.                  */
+ * residual replacement).  matrix_free = 1 applies G as sum_K H_K G_K H_K^t from per-cell factors
+ * (Shat_K^{-1}, w_K / sqrt(B_K)) instead of the assembled block-ELL (transient Stokes
+ * PCG methods only; the residual is then that of the factored operator).  Synchronises `s`.  */
 enum { CR_PCG_JACOBI = 0, CR_PCG_BLOCKJACOBI = 1, CR_MINRES_ABSJACOBI = 2,
        CR_BICGSTAB_JACOBI = 3, CR_GMRES_JACOBI = 4,
        /* overlapping-patch additive Schwarz M^{-1} = sum_p R_p^t (R_p G R_p^t)^{-1} R_p, one
@@ -166,7 +173,7 @@ typedef struct {
     double rtol;          /* default 1e-10                                                     */
     int64_t max_iter;     /* total Krylov iterations cap                                       */
     int32_t check_every;  /* iterations per captured CUDA graph between host checks (def 64)   */
-    int32_t refine_dd;    /* 0/1                                                               */
+    int32_t matrix_free;  /* 0: assembled G; 1: matrix-free factored G (see above)             */
 } cr_solver_opts;
 typedef struct {
     int64_t iterations;
@@ -205,14 +212,16 @@ cr_status cr_recover(cr_hybrid h, const double *W_d, double *U_d, double *P_d, d
  * of G (F = nf_int, lexicographic face order = slabs); every rank builds the whole mesh, assembles
  * and stores only its rows (columns renumbered: owned rows first, then ghosts in ascending global
  * order) and exchanges ghost entries of the SpMV input with the ranks that own them.  Partitioned
- * handles come from cr_hybridise(..., comm, ...) with comm->nranks > 1; then n_rows of
+ * handles come from cr_hybridise(..., comm, ...) with an NCCL or loopback comm; then n_rows of
  * cr_hybrid_info, the W_d of cr_solve and the x/y of cr_spmv are LOCAL (owned rows x dim);
  * cr_recover gathers W and returns the GLOBAL U [nf_int][dim] and P [nc] on every rank.
  * Distributed cr_solve supports the PCG methods (CR_PCG_JACOBI, CR_PCG_AFW; the patch
  * preconditioner uses the patches restricted to the owned faces).                            */
 /* 128-byte NCCL unique id (rank 0 creates it and broadcasts it, e.g. with torch.distributed) */
 cr_status cr_nccl_unique_id(void *out128);
-/* NCCL communicator (nranks > 1; NCCL is dlopen'ed: import torch first) or a trivial one (1)  */
+/* NCCL communicator (NCCL is dlopen'ed: import torch first).  nccl_unique_id = NULL with
+ * nranks = 1 gives a trivial communicator (unpartitioned handles); with an id, even a single
+ * rank takes the partitioned path (all collectives through NCCL).                            */
 cr_status cr_comm_init(const void *nccl_unique_id, int32_t rank, int32_t nranks, cr_comm *out);
 /* In-process loopback group: nranks host threads of ONE process share one GPU, exchanging
  * through device copies and host barriers (no NCCL, no CUDA graphs).  For testing the

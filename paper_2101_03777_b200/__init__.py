@@ -65,7 +65,7 @@ class Data(ctypes.Structure):
 
 class SolverOpts(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int32), ("restart", ctypes.c_int32), ("rtol", ctypes.c_double),
-                ("max_iter", ctypes.c_int64), ("check_every", ctypes.c_int32), ("refine_dd", ctypes.c_int32)]
+                ("max_iter", ctypes.c_int64), ("check_every", ctypes.c_int32), ("matrix_free", ctypes.c_int32)]
 
 
 class SolveReport(ctypes.Structure):
@@ -92,6 +92,8 @@ _sig = {
     "cr_hybrid_export_csr": [_vp, _vp, _vp, _vp, _vp, _vp],
     "cr_hybrid_export_shift": [_vp, _vp, _vp, _vp],
     "cr_spmv": [_vp, _vp, _vp, _vp],
+    "cr_spmv_mf": [_vp, _vp, _vp, _vp],
+    "cr_hybrid_mf_info": [_vp, _P(_i64), _P(_i64)],
     "cr_solve": [_vp, _P(SolverOpts), _vp, _vp, _P(SolveReport)],
     "cr_recover": [_vp, _vp, _vp, _vp, _vp, _vp],
     "cr_comm_init": [_vp, _i32, _i32, _P(_vp)],
@@ -247,6 +249,16 @@ class Hybrid:
         _check(_lib.cr_spmv(self._h, _ptr(x, torch.float64), _ptr(y, torch.float64), _stream(stream)))
         return y
 
+    def spmv_mf(self, x: torch.Tensor, y: torch.Tensor, stream=None):
+        """y = G x with the matrix-free factored operator."""
+        _check(_lib.cr_spmv_mf(self._h, _ptr(x, torch.float64), _ptr(y, torch.float64), _stream(stream)))
+        return y
+
+    def mf_info(self) -> dict:
+        nc, nb = ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.cr_hybrid_mf_info(self._h, ctypes.byref(nc), ctypes.byref(nb)))
+        return dict(ncells=nc.value, bytes=nb.value)
+
     def apply_precond(self, method: str | int, r: torch.Tensor, z: torch.Tensor, stream=None):
         """z = M^{-1} r for the preconditioner of `method`."""
         m = METHODS[method] if isinstance(method, str) else int(method)
@@ -343,11 +355,11 @@ def partition_plan(dim: int, cell_faces, face_cells, face_dof, rank: int, nranks
 
 
 def cr_solve(hyb: Hybrid, W: torch.Tensor, method: str | int = "pcg", rtol: float = 1e-10,
-             max_iter: int = 10**7, check_every: int = 64, restart: int = 50, refine_dd: int = 0,
+             max_iter: int = 10**7, check_every: int = 64, restart: int = 50, matrix_free: int = 0,
              stream=None, raise_on_fail: bool = True) -> dict:
     """Krylov solve of G W = S in place.  Returns the cr_solve_report as a dict."""
     m = METHODS[method] if isinstance(method, str) else int(method)
-    opts = SolverOpts(m, restart, rtol, max_iter, check_every, refine_dd)
+    opts = SolverOpts(m, restart, rtol, max_iter, check_every, int(matrix_free))
     rep = SolveReport()
     st = _lib.cr_solve(hyb._h, ctypes.byref(opts), _ptr(W, torch.float64), _stream(stream), ctypes.byref(rep))
     out = rep.as_dict()

@@ -206,6 +206,22 @@ cr_status cr_spmv(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s) {
     CR_API_END
 }
 
+cr_status cr_spmv_mf(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(h && x_d && y_d && x_d != y_d, CR_ERR_INVALID_ARG, "bad arguments");
+    cr::spmv_mf(h, x_d, y_d, (cudaStream_t)s);
+    CR_API_END
+}
+
+cr_status cr_hybrid_mf_info(cr_hybrid h, int64_t *ncells, int64_t *bytes) {
+    CR_API_BEGIN
+    CR_REQUIRE(h, CR_ERR_INVALID_ARG, "null handle");
+    const bool b = h->mf.built;
+    if (ncells) *ncells = b ? h->mf.ncells : 0;
+    if (bytes) *bytes = b ? (int64_t)(h->mf.v.n * sizeof(double) + h->mf.ids.n * sizeof(int32_t) + h->mf.sg.n) : 0;
+    CR_API_END
+}
+
 void cr_destroy_hybrid(cr_hybrid h) {
     cr::SyncFreeScope sync;
     delete h;

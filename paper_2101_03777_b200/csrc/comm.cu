@@ -210,7 +210,9 @@ cr_status cr_comm_init(const void *nccl_unique_id, int32_t rank, int32_t nranks,
     cr_comm_s *c = new cr_comm_s();
     c->rank = rank;
     c->nranks = nranks;
-    if (nranks > 1) {
+    // with a unique id the communicator is NCCL-backed even for one rank (hybrids built with it
+    // take the partitioned path: used to exercise the NCCL calls inside the solver graphs)
+    if (nranks > 1 || nccl_unique_id) {
         CR_REQUIRE(nccl_unique_id, CR_ERR_INVALID_ARG, "nranks > 1 needs the NCCL unique id of rank 0");
         auto *nc = new cr::NcclComm();
         nc->rank = rank;

@@ -496,7 +496,7 @@ void hybridise(cr_hybrid_s *h, const cr_mesh_s *m, const cr_params &prm, const c
     CR_REQUIRE(!h->is_ns || data.u_iter_d, CR_ERR_INVALID_ARG, "NS step needs u_iter_d");
     copy_problem_data(h, m, data, s);
     h->comm = comm;
-    if (comm && comm->nranks > 1) setup_part(h, m, comm, s);
+    if (comm && comm->impl) setup_part(h, m, comm, s);
     if (m->dim == 2) hybridise_t<2>(h, m, s);
     else hybridise_t<3>(h, m, s);
 }

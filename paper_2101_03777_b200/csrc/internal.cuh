@@ -169,6 +169,15 @@ struct AfwPrec {
 };
 enum { AFW_SPD = 0, AFW_ABS = 1, AFW_GEN = 2 };
 
+// matrix-free factored G (mf.cuh layout)
+struct MfOp {
+    bool built = false;
+    int64_t ncells = 0;          // padded to a multiple of 32
+    cr::DevBuf<int32_t> ids;
+    cr::DevBuf<uint8_t> sg;
+    cr::DevBuf<double> v;
+};
+
 struct cr_hybrid_s {
     const cr_mesh_s *mesh = nullptr;
     cr_params prm{};
@@ -184,6 +193,7 @@ struct cr_hybrid_s {
     cr::DevBuf<double> S, dinv, absdinv, bdinv;   // bdinv [nrows][d][d] inverse diagonal blocks
     cr::DevBuf<uint8_t> rowlen;                   // true blocks per block row
     AfwPrec afw;
+    MfOp mf;
     cr::Part part;               // row partition (multi-GPU); part.on == false on one GPU
     cr_comm_s *comm = nullptr;   // borrowed
     cr::SolverWork *work = nullptr;
@@ -223,8 +233,11 @@ void solve(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, c
 void free_solver_work(SolverWork *w);
 void apply_precond(cr_hybrid_s *h, int method, const double *r, double *z, cudaStream_t s);
 void spmv_part(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s);
+void spmv_mf(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s);
 // precond.cu
 void build_afw(cr_hybrid_s *h, int mode, cudaStream_t s);
+// mf.cu
+void build_mf(cr_hybrid_s *h, cudaStream_t s);
 // shared: copy problem data into hybrid-owned buffers
 struct ProbView;
 ProbView prob_view(const cr_hybrid_s *h);

@@ -1,0 +1,142 @@
+// Setup of the matrix-free factored operator (layout and algebra in mf.cuh).  One thread per
+// cell recomputes the cell's elimination in double-double (the same LDL^t as the assembly,
+// local.cuh), forms Shat_K^{-1} column by column, splits off the 1/(mu|K|) 1 1^t part for
+// cells with all faces interior (transient), scales w by 1/sqrt(B_K), and rounds once.
+#include <cub/cub.cuh>
+
+#include "local.cuh"
+#include "mf.cuh"
+
+namespace cr {
+
+// cells with at least one owned interior face (all cells when not partitioned)
+template <int D>
+__global__ void k_mf_flag(MeshView mv, int64_t nc, int64_t row0, int64_t row1, uint8_t *flag) {
+    constexpr int NF = D + 1;
+    for (int64_t K = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; K < nc; K += (int64_t)gridDim.x * blockDim.x) {
+        uint8_t f = 0;
+#pragma unroll
+        for (int l = 0; l < NF; ++l) {
+            const int dof = mv.face_dof[mv.cell_faces[K * NF + l]];
+            if (dof >= row0 && dof < row1) f = 1;
+        }
+        flag[K] = f;
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) k_mf_build(MeshView mv, ProbView p, const int32_t *cells, int64_t ncell,
+                                                  const int32_t *g2l, int32_t *ids, uint8_t *sg, double *v, int *err) {
+    using LY = MfLayout<D>;
+    constexpr int NF = LY::NF, NT = LY::NT, NE = LY::NE;
+    const int64_t npad = ((ncell + 31) >> 5) << 5;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < npad; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t slice = t >> 5;
+        const int lane = (int)(t & 31);
+        int32_t *ip = ids + slice * (NF * 32) + lane;
+        double *vp = v + slice * ((int64_t)NE * 32) + lane;
+        if (t >= ncell) {   // padding lane of the last slice: no faces, zero operator
+            for (int l = 0; l < NF; ++l) ip[l * 32] = -1;
+            sg[t] = 0;
+            for (int e = 0; e < NE; ++e) vp[e * 32] = 0.0;
+            continue;
+        }
+        const int64_t K = cells[t];
+        Cell<D> c;
+        load_cell<D>(mv, K, c);
+        StokesElim<D> e;
+        stokes_eliminate<D>(c, p, e);
+        if (e.status != DE_OK) { atomicCAS(err, DE_OK, e.status); continue; }
+        unsigned mask = 0;
+        for (int l = 0; l < NF; ++l) {
+            const int dof = c.dof[l];
+            ip[l * 32] = dof < 0 ? -1 : (g2l ? g2l[dof] : dof);
+            if (c.C[l] < 0) mask |= 1u << l;
+        }
+        sg[t] = (uint8_t)mask;
+        // Shat^{-1} (compact s x s) by solves with unit vectors, expanded to local faces
+        dd Si[NF][NF];
+        for (int a = 0; a < NF; ++a)
+            for (int b = 0; b < NF; ++b) Si[a][b] = dd_of(0.0);
+        for (int q = 0; q < c.s; ++q) {
+            dd col[NF];
+            for (int r = 0; r < c.s; ++r) col[r] = dd_of(r == q ? 1.0 : 0.0);
+            ldl_solve<D>(e, c.s, col);
+            for (int r = 0; r < c.s; ++r) Si[c.map[r]][c.map[q]] = col[r];
+        }
+        const bool split = (c.s == NF) && p.mu > 0.0 && !p.E;
+        dd cb = dd_of(0.0);
+        if (split) cb = dd_of(1.0) / (two_prod(p.mu, c.vol));   // 1/(alpha (d+1)), alpha = mu|K|/(d+1)
+        vp[0] = dd_round(cb);
+        for (int a = 0; a < NF; ++a)
+            for (int b = 0; b <= a; ++b) vp[(1 + a * (a + 1) / 2 + b) * 32] = dd_round(Si[a][b] - cb);
+        // u = w / sqrt(B) (K0: no pressure unknown, no projection)
+        const bool k0 = (K == p.k0);
+        dd sq = dd_of(0.0);
+        if (!k0) {
+            const double s0 = sqrt(e.B.hi);
+            sq = dd_of(s0) + (e.B - two_prod(s0, s0)) / (2.0 * s0);   // one Newton step in dd
+        }
+        for (int i = 0; i < D; ++i)
+            for (int l = 0; l < NF; ++l) vp[(1 + NT + i * NF + l) * 32] = 0.0;
+        if (!k0)
+            for (int i = 0; i < D; ++i)
+                for (int q = 0; q < c.s; ++q) vp[(1 + NT + i * NF + c.map[q]) * 32] = dd_round(e.w[i][q] / sq);
+    }
+}
+
+template <int D>
+static void build_mf_t(cr_hybrid_s *h, cudaStream_t s) {
+    using LY = MfLayout<D>;
+    const cr_mesh_s *m = h->mesh;
+    MfOp &M = h->mf;
+    const int64_t nc = m->nc;
+    const int T = 256;
+    MeshView mv = mesh_view(m);
+    ProbView p = prob_view(h);
+    const int64_t row0 = h->part.on ? h->part.row0 : 0, row1 = h->part.on ? h->part.row1 : m->nf_int;
+    DevBuf<uint8_t> flag;
+    flag.alloc(nc, s);
+    k_mf_flag<D><<<grid_for(nc, T), T, 0, s>>>(mv, nc, row0, row1, flag.get());
+    CR_CHECK_LAUNCH();
+    DevBuf<int32_t> list;
+    list.alloc(nc, s);
+    DevBuf<int64_t> nsel;
+    nsel.alloc(1, s);
+    size_t tb = 0;
+    cub::CountingInputIterator<int32_t> it(0);
+    CR_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flag.get(), list.get(), nsel.get(), (int64_t)nc, s));
+    DevBuf<uint8_t> tmp;
+    tmp.alloc(tb, s);
+    CR_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tb, it, flag.get(), list.get(), nsel.get(), (int64_t)nc, s));
+    int64_t ncell = 0;
+    CR_CUDA(cudaMemcpyAsync(&ncell, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CR_CUDA(cudaStreamSynchronize(s));
+    const int64_t nsl = (ncell + 31) / 32;
+    M.ncells = nsl * 32;
+    M.ids.alloc(nsl * 32 * LY::NF, s);
+    M.sg.alloc(nsl * 32, s);
+    M.v.alloc(nsl * 32 * LY::NE, s);
+    DevBuf<int> err;
+    err.alloc(1, s);
+    err.zero(s);
+    k_mf_build<D><<<grid_for(nsl * 32, 128, 16), 128, 0, s>>>(mv, p, list.get(), ncell,
+                                                               h->part.on ? h->part.g2l.get() : nullptr, M.ids.get(),
+                                                               M.sg.get(), M.v.get(), err.get());
+    CR_CHECK_LAUNCH();
+    int he = 0;
+    CR_CUDA(cudaMemcpyAsync(&he, err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    CR_CUDA(cudaStreamSynchronize(s));
+    CR_REQUIRE(he == DE_OK, CR_ERR_SINGULAR_LOCAL, "local elimination failed while building the matrix-free operator");
+    M.built = true;
+}
+
+void build_mf(cr_hybrid_s *h, cudaStream_t s) {
+    if (h->mf.built) return;
+    CR_REQUIRE(!h->is_ns && h->prm.shift == CR_SHIFT_NONE && h->prm.mu > 0.0, CR_ERR_INVALID_ARG,
+               "the matrix-free operator covers transient Stokes (mu > 0, no shift) only");
+    if (h->mesh->dim == 2) build_mf_t<2>(h, s);
+    else build_mf_t<3>(h, s);
+}
+
+}  // namespace cr

@@ -18,6 +18,7 @@
 
 #include "afw.cuh"
 #include "internal.cuh"
+#include "mf.cuh"
 #include "spmv.cuh"
 
 namespace cr {
@@ -172,6 +173,30 @@ __global__ void k_halo_pack(int64_t n, const int32_t *rows, const double *x, dou
 #pragma unroll
         for (int i = 0; i < D; ++i) buf[k * D + i] = x[(int64_t)rows[k] * D + i];
     }
+}
+
+// ------------------------------------------------------------------ matrix-free G (mf.cuh)
+// q += G_mf x over this rank's cells (q pre-zeroed); REDUCE: p.q -> alpha (FIN_PQ)
+template <int D, bool REDUCE>
+__global__ void __launch_bounds__(kT) k_mf_spmv(MfView M, const double *x, double *q, int64_t nown, KState *st,
+                                                double *partials, int dist) {
+    if (REDUCE && st->flag != FLAG_RUN) return;
+    double acc[1] = {0.0};
+    GRID_STRIDE(t, M.ncells) acc[0] += mf_cell<D>(M, t, x, q, nown);
+    if (REDUCE)
+        reduce_and_finish<1>(acc, partials, &st->tickets[1], [&](double *t) { fin_or_store<1>(st, FIN_PQ, t, 0.0, dist); });
+}
+
+// r = b - q, |r|^2 (FIN_RR)
+__global__ void __launch_bounds__(kT) k_resid_vec(int64_t N, const double *b, const double *q, double *r, KState *st,
+                                                  double *partials, int dist) {
+    double acc[1] = {0.0};
+    GRID_STRIDE(i, N) {
+        const double ri = b[i] - q[i];
+        r[i] = ri;
+        acc[0] = fma(ri, ri, acc[0]);
+    }
+    reduce_and_finish<1>(acc, partials, &st->tickets[7], [&](double *t) { fin_or_store<1>(st, FIN_RR, t, 0.0, dist); });
 }
 
 // ------------------------------------------------------------------ generic
@@ -943,6 +968,7 @@ struct Launcher {
     int grid_rows, grid_vec;
     int dist = 0;           // partitioned over several ranks
     Comm *comm = nullptr;
+    int mf = 0;             // matrix-free factored G
 
     // after a reducing kernel: allreduce this rank's values and apply the recurrence
     void reduced(cudaStream_t ks, int nv, int kind, double rtol) {
@@ -975,7 +1001,34 @@ static void read_state(SolverWork *w, cudaStream_t s) {
 }
 
 template <int D>
+static MfView mf_view(const cr_hybrid_s *h) {
+    return MfView{h->mf.ids.get(), h->mf.sg.get(), h->mf.v.get(), h->mf.ncells};
+}
+
+// q = G_mf x (q zeroed first); REDUCE also reduces x.q -> alpha
+template <int D, bool REDUCE>
+static void mf_apply(Launcher &L, cudaStream_t ks, const double *x, double *q, double rtol) {
+    CR_CUDA(cudaMemsetAsync(q, 0, L.N * sizeof(double), ks));
+    k_mf_spmv<D, REDUCE><<<grid_for(L.h->mf.ncells, kT), kT, 0, ks>>>(mf_view<D>(L.h), x, q, L.nrows, L.w->st.get(),
+                                                                      L.w->partials.get(), L.dist);
+    CR_CHECK_LAUNCH();
+    ++L.launches;
+    if (REDUCE) L.reduced(ks, 1, FIN_PQ, rtol);
+}
+
+template <int D>
 static void true_residual(Launcher &L, double *x, double *r) {
+    if (L.mf) {
+        L.halo(L.s, x);
+        mf_apply<D, false>(L, L.s, x, L.w->q.get(), 0.0);
+        k_resid_vec<<<L.grid_vec, kT, 0, L.s>>>(L.N, L.w->b.get(), L.w->q.get(), r, L.w->st.get(), L.w->partials.get(),
+                                               L.dist);
+        CR_CHECK_LAUNCH();
+        L.reduced(L.s, 1, FIN_RR, 0.0);
+        ++L.launches;
+        ++L.spmvs;
+        return;
+    }
     L.halo(L.s, x);
     k_true_residual<D><<<L.grid_rows, kT, 0, L.s>>>(ell<D>(L.h), x, L.w->b.get(), r, L.w->st.get(), L.w->partials.get(),
                                                    L.dist);
@@ -1063,6 +1116,10 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     L.comm = h->part.on ? h->comm->impl : nullptr;
     CR_REQUIRE(!L.dist || o.method == CR_PCG_JACOBI || o.method == CR_PCG_BLOCKJACOBI || o.method == CR_PCG_AFW,
                CR_ERR_INVALID_ARG, "a partitioned (multi-GPU) solve supports the PCG methods only");
+    L.mf = o.matrix_free ? 1 : 0;
+    CR_REQUIRE(!L.mf || o.method == CR_PCG_JACOBI || o.method == CR_PCG_BLOCKJACOBI || o.method == CR_PCG_AFW,
+               CR_ERR_INVALID_ARG, "matrix_free supports the PCG methods only");
+    if (L.mf) build_mf(h, s);
     const int64_t N = w->N, nrows = L.nrows;
     const double rtol = o.rtol > 0 ? o.rtol : 1e-10;
     const int64_t max_iter = o.max_iter > 0 ? o.max_iter : 10000000;
@@ -1100,9 +1157,13 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         while (w->hst->flag == FLAG_RUN) {
             auto body = [&](int) {
                 L.halo(ks, w->p.get());
-                k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part, L.dist);
-                CR_CHECK_LAUNCH();
-                L.reduced(ks, 1, FIN_PQ, rtol);
+                if (L.mf) {
+                    mf_apply<D, true>(L, ks, w->p.get(), w->q.get(), rtol);
+                } else {
+                    k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part, L.dist);
+                    CR_CHECK_LAUNCH();
+                    L.reduced(ks, 1, FIN_PQ, rtol);
+                }
                 if (blk) {
                     k_pcg_update<D, 1><<<L.grid_rows, kT, 0, ks>>>(nrows, x, w->r.get(), w->p.get(), w->q.get(), M, st, part, L.dist);
                     CR_CHECK_LAUNCH();
@@ -1117,7 +1178,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                 CR_CHECK_LAUNCH();
             };
             int64_t it0 = w->hst->iters;
-            graph_loop(L, ks, method * 100000 + kk, kk, body, [&]() {
+            graph_loop(L, ks, method * 100000 + L.mf * 50000 + kk, kk, body, [&]() {
                 return w->hst->flag != FLAG_RUN || w->hst->iters >= max_iter;
             });
             int64_t dit = w->hst->iters - it0;
@@ -1151,9 +1212,13 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         while (w->hst->flag == FLAG_RUN) {
             auto body = [&](int) {
                 L.halo(ks, w->p.get());
-                k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part, L.dist);
-                CR_CHECK_LAUNCH();
-                L.reduced(ks, 1, FIN_PQ, rtol);
+                if (L.mf) {
+                    mf_apply<D, true>(L, ks, w->p.get(), w->q.get(), rtol);
+                } else {
+                    k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part, L.dist);
+                    CR_CHECK_LAUNCH();
+                    L.reduced(ks, 1, FIN_PQ, rtol);
+                }
                 k_pcg_update_r<<<L.grid_vec, kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), st, part, L.dist);
                 CR_CHECK_LAUNCH();
                 L.reduced(ks, 1, FIN_UPD_R, rtol);
@@ -1162,7 +1227,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                 CR_CHECK_LAUNCH();
             };
             int64_t it0 = w->hst->iters;
-            graph_loop(L, ks, method * 100000 + kk, kk, body, [&]() {
+            graph_loop(L, ks, method * 100000 + L.mf * 50000 + kk, kk, body, [&]() {
                 return w->hst->flag != FLAG_RUN || w->hst->iters >= max_iter;
             });
             int64_t dit = w->hst->iters - it0;
@@ -1207,7 +1272,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         };
         while (w->hst->flag == FLAG_RUN) {
             int64_t it0 = w->hst->iters;
-            graph_loop(L, ks, method * 100000 + kk, kk, body, [&]() { return true; });
+            graph_loop(L, ks, method * 100000 + L.mf * 50000 + kk, kk, body, [&]() { return true; });
             int64_t dit = w->hst->iters - it0;
             L.launches += 5 * kk;
             L.spmvs += dit;
@@ -1244,7 +1309,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         };
         while (w->hst->flag == FLAG_RUN) {
             int64_t it0 = w->hst->iters;
-            graph_loop(L, ks, method * 100000 + kk, kk, body, [&]() { return true; });
+            graph_loop(L, ks, method * 100000 + L.mf * 50000 + kk, kk, body, [&]() { return true; });
             int64_t dit = w->hst->iters - it0;
             L.launches += 3 * kk;
             L.spmvs += dit;
@@ -1277,7 +1342,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         };
         while (w->hst->flag == FLAG_RUN) {
             int64_t it0 = w->hst->iters;
-            graph_loop(L, ks, method * 100000 + kk, kk, body, [&]() {
+            graph_loop(L, ks, method * 100000 + L.mf * 50000 + kk, kk, body, [&]() {
                 return w->hst->flag != FLAG_RUN || w->hst->iters >= max_iter;
             });
             int64_t dit = w->hst->iters - it0;
@@ -1440,6 +1505,24 @@ static void spmv_part_t(cr_hybrid_s *h, const double *x, double *y, cudaStream_t
 void spmv_part(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s) {
     if (h->G.d == 2) spmv_part_t<2>(h, x, y, s);
     else spmv_part_t<3>(h, x, y, s);
+}
+
+// y = G_mf x (matrix-free factored operator) on an unpartitioned handle
+template <int D>
+static void spmv_mf_t(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s) {
+    ensure_work(h, s);
+    build_mf(h, s);
+    Launcher L{h, h->work, s};
+    L.D = D;
+    L.nrows = h->G.nrows;
+    L.N = h->work->N;
+    mf_apply<D, false>(L, s, x, y, 0.0);
+}
+
+void spmv_mf(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s) {
+    CR_REQUIRE(!h->part.on, CR_ERR_INVALID_ARG, "cr_spmv_mf: unpartitioned handles only");
+    if (h->G.d == 2) spmv_mf_t<2>(h, x, y, s);
+    else spmv_mf_t<3>(h, x, y, s);
 }
 
 void apply_precond(cr_hybrid_s *h, int method, const double *r, double *z, cudaStream_t s) {

@@ -177,6 +177,26 @@ def test_spmv_parity(name):
     assert np.abs(y.cpu().numpy() - yo).max() <= 1e-13 * np.abs(ho["G"]).max() * np.abs(x).max() * 10
 
 
+@pytest.mark.parametrize("name", ["2d-config0", "2d-transient-jit-n17", "2d-dirichlet-n10", "2d-k0-interior",
+                                  "3d-transient-n3"])
+def test_matrix_free_spmv_parity(name):
+    """y = sum_K H_K G_K H_K^t x from per-cell factors (Shat^{-1} split as 1/(mu|K|) 11^t + T,
+    u = w/sqrt(B)) against the oracle's assembled G (entries rounded once from binary128)."""
+    coords, cells, prm, data, prob = make_case(**HYB_CASES[name])
+    mo = O.build_mesh(coords, cells)
+    ho = O.hybridise(mo, prm, data)
+    hg = P.cr_hybridise(P.cr_build_mesh(tg(coords), tg(cells)), prob)
+    x = np.random.default_rng(7).normal(size=hg.n_rows)
+    y = torch.empty(hg.n_rows, dtype=torch.float64, device=DEV)
+    hg.spmv_mf(tg(x), y)
+    yo = ho["G"] @ x
+    Ga = abs(ho["G"])
+    bound = 1e-14 * (Ga @ np.abs(x))            # rounding of G's entries, row by row
+    assert np.all(np.abs(y.cpu().numpy() - yo) <= 4 * bound + 1e-300)
+    info = hg.mf_info()
+    assert info["ncells"] >= mo.nc and info["bytes"] > 0
+
+
 @pytest.mark.parametrize("name", ["2d-config0", "2d-ns-n12", "2d-dirichlet-n10", "3d-transient-n3"])
 def test_coupled_parity(name):
     coords, cells, prm, data, prob = make_case(**HYB_CASES[name])
@@ -208,9 +228,19 @@ SOLVE_CASES = {
 }
 
 
-@pytest.mark.parametrize("name", list(SOLVE_CASES))
+MF_CASES = {   # the matrix-free factored operator (transient Stokes)
+    "config0-pcg-mf": (dict(dim=2, n=8, jitter=0.0), "pcg", 1e-12),
+    "2d-jit-n24-pcg-afw-mf": (dict(dim=2, n=24), "pcg_afw", 1e-12),
+    "3d-n3-pcg-afw-mf": (dict(dim=3, n=3), "pcg_afw", 1e-12),
+    "2d-dirichlet-n10-pcg-afw-mf": (dict(dim=2, n=10, dirichlet=True), "pcg_afw", 1e-12),
+    "2d-k0-interior-pcg-mf": (dict(dim=2, n=9, k0=77), "pcg", 1e-12),
+}
+
+
+@pytest.mark.parametrize("name", list(SOLVE_CASES) + list(MF_CASES))
 def test_solve_recover_parity(name):
-    kw, method, rtol = SOLVE_CASES[name]
+    mf = name in MF_CASES
+    kw, method, rtol = MF_CASES[name] if mf else SOLVE_CASES[name]
     coords, cells, prm, data, prob = make_case(**kw)
     mo = O.build_mesh(coords, cells)
     ho = O.hybrid_pipeline(mo, prm, data)
@@ -218,7 +248,7 @@ def test_solve_recover_parity(name):
     hg = P.cr_hybridise(mg, prob)
     W = torch.zeros(hg.n_rows, dtype=torch.float64, device=DEV)
     extra = dict(restart=128) if method == "gmres" else {}
-    rep = P.cr_solve(hg, W, method, rtol=rtol, check_every=16, **extra)
+    rep = P.cr_solve(hg, W, method, rtol=rtol, check_every=16, matrix_free=int(mf), **extra)
     assert rep["converged"] and rep["rel_res_true"] <= rtol, rep
     # the oracle recomputes the true residual of the GPU solution in binary128
     r = O.residual_f128(ho["G"], W.cpu().numpy(), ho["S"])
@@ -342,7 +372,8 @@ def test_patch_preconditioner_cuts_pcg_iterations():
 # ------------------------------------------------------------------ partitioned path (multi-GPU)
 @pytest.mark.timeout(600)
 @pytest.mark.parametrize("dim,n,nranks,method", [(2, 12, 2, "pcg"), (2, 12, 3, "pcg_afw"), (2, 10, 2, "pcg_block"),
-                                                 (3, 3, 2, "pcg_afw"), (3, 4, 4, "pcg")])
+                                                 (3, 3, 2, "pcg_afw"), (3, 4, 4, "pcg"), (2, 12, 3, "pcg_afw_mf"),
+                                                 (3, 3, 2, "pcg_mf")])
 def test_partitioned_loopback(dim, n, nranks, method):
     """The row-partitioned path (local assembly with renumbered columns, halo exchange before
     every SpMV, allreduced dot products, W gathered for the recovery) with `nranks` ranks as
@@ -361,7 +392,9 @@ def test_partitioned_loopback(dim, n, nranks, method):
             with torch.cuda.stream(st):
                 comm = P.Comm.loopback(grp, rank)
                 c, k = tg(coords), tg(cells)
-                out = P.hybrid_method(c, k, prob, method, rtol=1e-12, stream=st, comm=comm, check_every=16)
+                mf = method.endswith("_mf")
+                out = P.hybrid_method(c, k, prob, method[:-3] if mf else method, rtol=1e-12, stream=st, comm=comm,
+                                      check_every=16, matrix_free=int(mf))
                 rp, cols, vals, S = out["hybrid"].export_csr(st)
                 st.synchronize()
                 res[rank] = dict(out=out, info=out["hybrid"].partition_info(), rp=rp.cpu().numpy(),
@@ -393,3 +426,16 @@ def test_partitioned_loopback(dim, n, nranks, method):
         assert np.array_equal(r["U"], res[0]["U"]) and np.array_equal(r["P"], res[0]["P"])
         assert r["out"]["report"]["converged"]
     assert rows_seen == mo.nf_int
+
+
+def test_nccl_single_rank_partitioned_path():
+    """The NCCL communicator (dlopen'ed libnccl, allreduce + send/recv enqueued inside the
+    solver's CUDA graphs) on one rank: same answer as the unpartitioned solve."""
+    coords, cells, prm, data, prob = make_case(dim=2, n=12)
+    comm = P.Comm.nccl(P.nccl_unique_id(), 0, 1)
+    out = P.hybrid_method(tg(coords), tg(cells), prob, "pcg_afw", rtol=1e-12, comm=comm, check_every=8)
+    ref = P.hybrid_method(tg(coords), tg(cells), prob, "pcg_afw", rtol=1e-12, check_every=8)
+    assert out["hybrid"].partition_info()["nghost"] == 0
+    assert out["report"]["iterations"] == ref["report"]["iterations"]
+    assert relL2(out["U"].cpu().numpy(), ref["U"].cpu().numpy()) <= 1e-12
+    assert relL2(out["P"].cpu().numpy(), ref["P"].cpu().numpy()) <= 1e-10
