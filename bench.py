@@ -6,8 +6,9 @@ Workload (one "step"): BASELINE.json configs[1] — 2D transient Stokes, unit sq
 1024 x 1024 squares split into 2,097,152 triangles, interior vertices jittered by up to
 0.2h (seed 2), mu = nu = 1, manufactured fp64 force — run through the whole hot path:
 cr_build_mesh -> cr_hybridise -> cr_solve (PCG to a TRUE relative residual of 1e-10, with
-the patch additive-Schwarz preconditioner) -> cr_recover,
-inputs resident in HBM.  value = seconds per step (time to solution, lower is better).
+the two-level preconditioner (patch additive Schwarz + a coarse "stress x area vector" space)
+and the matrix-free factored G)
+-> cr_recover, inputs resident in HBM.  value = seconds per step (time to solution, lower is better).
 The same step with Jacobi PCG (the north star's baseline solver) is timed once and reported
 under "pcg_jacobi".
 
@@ -36,7 +37,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "hybridised-system PCG time-to-solution; SpMV GB/s as % of B200 HBM peak"
 CONFIG_IDX = 1
-METHOD = "pcg_afw"
+METHOD = "pcg_afw2"  # patch additive Schwarz + coarse "stress x area" correction
+MATRIX_FREE = 1      # G applied from per-cell factors
+COARSE = 32          # coarse grid intervals per direction
 # Jacobi-PCG iterations of configs[1] to a true 1e-10 residual, measured on B200 by this
 # bench (used only by --impl reference to extrapolate the oracle's per-iteration time).
 ITERS_CONFIG1_MEASURED = 162221   # Jacobi PCG, configs[1], B200 bench r01 (profiles/r01_bench_*.log)
@@ -223,7 +226,7 @@ def main():
         mesh = P.cr_build_mesh(coords, cells)
         hyb = P.cr_hybridise(mesh, prob, comm=comm)
         W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=dev)
-        rep = P.cr_solve(hyb, W, METHOD, rtol=cfg.rtol, check_every=64)
+        rep = P.cr_solve(hyb, W, METHOD, rtol=cfg.rtol, check_every=64, matrix_free=MATRIX_FREE, coarse=COARSE)
         U, Pp, diag = P.cr_recover(hyb, W)
         return mesh, hyb, rep, U, Pp, diag
 
@@ -275,7 +278,10 @@ def main():
     y = torch.empty_like(x)
     spmv_s = time_launch(lambda: hyb.spmv(x, y))
     spmv_bytes = 8 * nnz + 4 * nb + N8 + N8          # values + block cols + x once + y
-    prec_s = time_launch(lambda: hyb.apply_precond(METHOD, x, y))
+    mf_s = time_launch(lambda: hyb.spmv_mf(x, y))
+    minfo = hyb.mf_info()
+    mf_bytes = minfo["bytes"] + N8 + N8              # per-cell factors + x once + q once
+    prec_s = time_launch(lambda: hyb.apply_precond("pcg_afw", x, y))
     # patch operator + r read + slot contributions written, then read back and z written
     prec_bytes = pinfo["bytes"] + N8 + slots * N8 + slots * N8 + N8
     traffic = None
@@ -285,11 +291,30 @@ def main():
             traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    # PCG-patch iteration: SpMV + update (x,p,r,q read; x,r write) + patch apply + p update
-    iter_bytes = spmv_bytes + 6 * N8 + (pinfo["bytes"] + N8 + slots * N8) + (slots * N8 + 2 * N8)
+    # PCG-two-level iteration: G apply + update (x,p,r,q read; x,r write) + patch apply + coarse
+    # (restriction reads r and the fp32 row basis, E^-1 once) + p update (+ basis again)
+    g_bytes = mf_bytes if MATRIX_FREE else spmv_bytes
+    nE = 4 * (COARSE + 1) ** 2 if mesh.dim == 2 else 9 * (COARSE + 1) ** 3
+    coarse_bytes = N8 + 8 * N + 8 * nE * nE + 8 * N     # r, (x, a) fp32, E^-1, (x, a) again
+    iter_bytes = g_bytes + 6 * N8 + (pinfo["bytes"] + N8 + slots * N8) + coarse_bytes + (slots * N8 + 2 * N8)
     iter_gbs = iter_bytes * rep["iterations"] / rep["seconds"] / 1e9 if rep["seconds"] > 0 else None
 
-    # ---- the north star's baseline solver on the same system (one timed solve)
+    def roof(kernel, bytes_, sec, traffic_=None):
+        return {"kernel": kernel, "bound": "hbm", "achieved": bytes_ / sec / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": bytes_ / sec / 1e9 / peak, "traffic": traffic_, "peak_source": peak_src,
+                "algorithmic_bytes": bytes_, "launch_s": sec}
+
+    kernels = {
+        "mf": roof("k_mf_spmv (matrix-free factored G x, per-cell factors, the in-solve G apply)", mf_bytes, mf_s),
+        "precond": roof("k_afw_apply + k_afw_zsum (patch additive Schwarz z = M^-1 r)", prec_bytes, prec_s),
+        "spmv": roof("k_spmv (assembled sliced block-ELL G x, same row code as the assembled PCG SpMV)",
+                     spmv_bytes, spmv_s, traffic),
+    }
+    dominant = "mf" if mf_s >= prec_s else "precond"
+
+    # ---- one-level patch PCG (assembled G), and the north star's baseline solver (Jacobi PCG)
+    Wa = torch.zeros(N, dtype=torch.float64, device=dev)
+    repa = P.cr_solve(hyb, Wa, "pcg_afw", rtol=cfg.rtol, check_every=64, matrix_free=0)
     Wj = torch.zeros(N, dtype=torch.float64, device=dev)
     repj = P.cr_solve(hyb, Wj, "pcg", rtol=cfg.rtol, check_every=64)
 
@@ -300,7 +325,8 @@ def main():
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        o2 = P.hybrid_method_host(coords_h, cells_h, fbar_h, cfg.mu, cfg.nu, METHOD, cfg.rtol, comm=comm)
+        o2 = P.hybrid_method_host(coords_h, cells_h, fbar_h, cfg.mu, cfg.nu, METHOD, cfg.rtol, comm=comm,
+                                  matrix_free=MATRIX_FREE, coarse=COARSE)
         b.record(stream)
         torch.cuda.synchronize()
         e2e_s = a.elapsed_time(b) * 1e-3
@@ -323,33 +349,34 @@ def main():
                           f"{repj['iterations']} Jacobi-PCG iterations (the oracle's solver, count measured on the B200 in this run) to the full workload")}
 
     launches = rep["kernel_launches"] + 25     # mesh (sort/scan/geometry ~15), hybridise 1, recover 3, copies
-    launches += 12 if METHOD == "pcg_afw" else 0   # patch build (pairs, sort, scans, setup)
+    launches += 12   # patch build (pairs, sort, scans, setup)
+    nE_ = 4 * (COARSE + 1) ** 2 if mesh.dim == 2 else 9 * (COARSE + 1) ** 3
+    launches += (5 ** mesh.dim) * mesh.dim ** 2 * 5 + 5 * ((nE_ + 31) // 32) + 10   # coarse E assembly + inversion
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "configs[1] 2D transient Stokes n=%d jittered 0.2h, patch-preconditioned PCG "
-                                   "to true 1e-10" % (args.n or cfg.n),
+            "config": {"workload": "configs[1] 2D transient Stokes n=%d jittered 0.2h, two-level-preconditioned "
+                                   "PCG to true 1e-10" % (args.n or cfg.n),
                        "cells": mesh.nc, "unknowns": N, "nnz_G": nnz, "blocks_G": nb,
                        "parallelism": (f"face rows partitioned over {world} GPUs (NCCL halo send/recv + allreduce)"
                                        if world > 1 else "1 GPU"),
                        "l2": "working set > L2 (G = %.2f GB per SpMV) and a 256 MB L2 flush before each step"
                              % (8 * nnz / 1e9)},
-            "pcg": {"method": METHOD, "iterations": rep["iterations"], "rel_res_true": rep["rel_res_true"],
-                    "solve_s": rep["seconds"], "ms_per_iter": rep["seconds"] / max(rep["iterations"], 1) * 1e3,
-                    "iter_gbs": iter_gbs, "iter_bytes": iter_bytes, "precond": pinfo},
+            "pcg": {"method": METHOD, "matrix_free": MATRIX_FREE, "coarse_intervals": COARSE,
+                    "iterations": rep["iterations"],
+                    "rel_res_true": rep["rel_res_true"], "solve_s": rep["seconds"],
+                    "ms_per_iter": rep["seconds"] / max(rep["iterations"], 1) * 1e3,
+                    "iter_gbs": iter_gbs, "iter_bytes": iter_bytes, "precond": pinfo, "mf": minfo},
+            "pcg_patch_assembled_G": {"iterations": repa["iterations"], "rel_res_true": repa["rel_res_true"],
+                                "solve_s": repa["seconds"],
+                                "ms_per_iter": repa["seconds"] / max(repa["iterations"], 1) * 1e3},
             "pcg_jacobi": {"iterations": repj["iterations"], "rel_res_true": repj["rel_res_true"],
                            "solve_s": repj["seconds"],
                            "ms_per_iter": repj["seconds"] / max(repj["iterations"], 1) * 1e3},
-            "roofline": {"kernel": "k_spmv (sliced block-ELL G x, same row code as the PCG SpMV)",
-                         "bound": "hbm", "achieved": spmv_bytes / spmv_s / 1e9, "peak": peak, "unit": "GB/s",
-                         "frac": spmv_bytes / spmv_s / 1e9 / peak, "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes": spmv_bytes, "launch_s": spmv_s},
-            "roofline_precond": {"kernel": "k_afw_apply + k_afw_zsum (patch additive Schwarz z = M^-1 r)",
-                                 "bound": "hbm", "achieved": prec_bytes / prec_s / 1e9, "peak": peak,
-                                 "unit": "GB/s", "frac": prec_bytes / prec_s / 1e9 / peak,
-                                 "algorithmic_bytes": prec_bytes, "launch_s": prec_s},
+            "roofline": kernels[dominant],
+            "roofline_kernels": kernels,
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
             "e2e": e2e,

@@ -166,7 +166,11 @@ enum { CR_PCG_JACOBI = 0, CR_PCG_BLOCKJACOBI = 1, CR_MINRES_ABSJACOBI = 2,
         * edge (3D); built on the device at the first solve that needs it (DESIGN.md
         * "Preconditioners").  PCG: Cholesky of each patch block (G SPD);
         * MINRES: |patch block|^{-1} (SPD although G is indefinite).                */
-       CR_PCG_AFW = 5, CR_MINRES_AFW = 6 };
+       CR_PCG_AFW = 5, CR_MINRES_AFW = 6,
+       /* two-level: the patch preconditioner plus the coarse correction Z (Z^t G Z)^{-1} Z^t,
+        * Z_(j,k,l): W^(k) = a_sigma^(l) phi_j(x_sigma) on a uniform grid of `coarse` intervals
+        * per direction; E = Z^t G Z assembled and inverted on the device.   */
+       CR_PCG_AFW2 = 7 };
 typedef struct {
     int32_t method;       /* CR_* above                                                        */
     int32_t restart;      /* GMRES m (default 50)                                              */
@@ -174,6 +178,7 @@ typedef struct {
     int64_t max_iter;     /* total Krylov iterations cap                                       */
     int32_t check_every;  /* iterations per captured CUDA graph between host checks (def 64)   */
     int32_t matrix_free;  /* 0: assembled G; 1: matrix-free factored G (see above)             */
+    int32_t coarse;       /* CR_PCG_AFW2: coarse intervals per direction (0: 16 in 2D, 8 in 3D) */
 } cr_solver_opts;
 typedef struct {
     int64_t iterations;

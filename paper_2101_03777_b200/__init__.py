@@ -34,10 +34,10 @@ STATUS = {0: "CR_OK", -1: "CR_ERR_INVALID_ARG", -2: "CR_ERR_CUDA", -3: "CR_ERR_O
 CR_STOKES, CR_NS_NEWTON_STEP = 0, 1
 CR_SHIFT_NONE, CR_SHIFT_MIS = 0, 1
 (CR_PCG_JACOBI, CR_PCG_BLOCKJACOBI, CR_MINRES_ABSJACOBI, CR_BICGSTAB_JACOBI, CR_GMRES_JACOBI,
- CR_PCG_AFW, CR_MINRES_AFW) = range(7)
+ CR_PCG_AFW, CR_MINRES_AFW, CR_PCG_AFW2) = range(8)
 METHODS = {"pcg": CR_PCG_JACOBI, "pcg_block": CR_PCG_BLOCKJACOBI, "minres": CR_MINRES_ABSJACOBI,
            "bicgstab": CR_BICGSTAB_JACOBI, "gmres": CR_GMRES_JACOBI, "pcg_afw": CR_PCG_AFW,
-           "minres_afw": CR_MINRES_AFW}
+           "minres_afw": CR_MINRES_AFW, "pcg_afw2": CR_PCG_AFW2}
 
 
 class CrError(RuntimeError):
@@ -65,7 +65,8 @@ class Data(ctypes.Structure):
 
 class SolverOpts(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int32), ("restart", ctypes.c_int32), ("rtol", ctypes.c_double),
-                ("max_iter", ctypes.c_int64), ("check_every", ctypes.c_int32), ("matrix_free", ctypes.c_int32)]
+                ("max_iter", ctypes.c_int64), ("check_every", ctypes.c_int32), ("matrix_free", ctypes.c_int32),
+                ("coarse", ctypes.c_int32)]
 
 
 class SolveReport(ctypes.Structure):
@@ -355,11 +356,11 @@ def partition_plan(dim: int, cell_faces, face_cells, face_dof, rank: int, nranks
 
 
 def cr_solve(hyb: Hybrid, W: torch.Tensor, method: str | int = "pcg", rtol: float = 1e-10,
-             max_iter: int = 10**7, check_every: int = 64, restart: int = 50, matrix_free: int = 0,
+             max_iter: int = 10**7, check_every: int = 64, restart: int = 50, matrix_free: int = 0, coarse: int = 0,
              stream=None, raise_on_fail: bool = True) -> dict:
     """Krylov solve of G W = S in place.  Returns the cr_solve_report as a dict."""
     m = METHODS[method] if isinstance(method, str) else int(method)
-    opts = SolverOpts(m, restart, rtol, max_iter, check_every, int(matrix_free))
+    opts = SolverOpts(m, restart, rtol, max_iter, check_every, int(matrix_free), int(coarse))
     rep = SolveReport()
     st = _lib.cr_solve(hyb._h, ctypes.byref(opts), _ptr(W, torch.float64), _stream(stream), ctypes.byref(rep))
     out = rep.as_dict()
@@ -427,7 +428,7 @@ def hybrid_method(coords: torch.Tensor, cells: torch.Tensor, prob: Problem, meth
 
 
 def hybrid_method_host(coords, cells, fbar, mu: float, nu: float, method: str = "pcg", rtol: float = 1e-10,
-                       stream=None, comm: Comm | None = None, **kw) -> dict:
+                       stream=None, comm: Comm | None = None, matrix_free: int = 0, coarse: int = 0, **kw) -> dict:
     """End-to-end entry point from HOST buffers: pinned host -> device copies, the hybrid
     method on the device, and U, P copied back to host (the `e2e` path of bench.py)."""
     dev = torch.device("cuda")
@@ -435,7 +436,7 @@ def hybrid_method_host(coords, cells, fbar, mu: float, nu: float, method: str = 
     k = cells.to(dev, non_blocking=True)
     f = fbar.to(dev, non_blocking=True)
     prob = Problem(mu=mu, nu=nu, fbar=f, **kw)
-    out = hybrid_method(c, k, prob, method, rtol, stream, comm)
+    out = hybrid_method(c, k, prob, method, rtol, stream, comm, matrix_free=matrix_free, coarse=coarse)
     out["U_host"] = out["U"].to("cpu")
     out["P_host"] = out["P"].to("cpu")
     return out

@@ -3,10 +3,12 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "coarse.cuh"
 #include "cr.h"
 
 namespace cr {
@@ -169,6 +171,21 @@ struct AfwPrec {
 };
 enum { AFW_SPD = 0, AFW_ABS = 1, AFW_GEN = 2 };
 
+// two-level coarse correction (coarse.cu)
+struct CoarseOp {
+    int built = 0;               // H it was built for (0 = not built)
+    int requested = 0;           // H asked for when it was built
+    cr::CoarseGrid g;
+    int64_t nE = 0, nchunk = 0;
+    cr::DevBuf<float> fx, fa;
+    cr::DevBuf<int32_t> perm;
+    cr::DevBuf<int64_t> chunk_start, cell_chunk;
+    cr::DevBuf<double> part, c, y, Einv;
+    cr::CoarseView view() const {
+        return cr::CoarseView{g, fx.get(), fa.get(), perm.get(), chunk_start.get(), cell_chunk.get(), nE};
+    }
+};
+
 // matrix-free factored G (mf.cuh layout)
 struct MfOp {
     bool built = false;
@@ -194,6 +211,7 @@ struct cr_hybrid_s {
     cr::DevBuf<uint8_t> rowlen;                   // true blocks per block row
     AfwPrec afw;
     MfOp mf;
+    CoarseOp coarse;
     cr::Part part;               // row partition (multi-GPU); part.on == false on one GPU
     cr_comm_s *comm = nullptr;   // borrowed
     cr::SolverWork *work = nullptr;
@@ -238,6 +256,10 @@ void spmv_mf(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s);
 void build_afw(cr_hybrid_s *h, int mode, cudaStream_t s);
 // mf.cu
 void build_mf(cr_hybrid_s *h, cudaStream_t s);
+// coarse.cu
+void build_coarse(cr_hybrid_s *h, int H, const std::function<void(const double *, double *)> &applyG, cudaStream_t s);
+void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double *partials, unsigned *ticket,
+                           cudaStream_t s);
 // shared: copy problem data into hybrid-owned buffers
 struct ProbView;
 ProbView prob_view(const cr_hybrid_s *h);

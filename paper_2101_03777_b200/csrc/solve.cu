@@ -34,6 +34,7 @@ struct KState {
     int k;               // GMRES: Arnoldi steps done in the current cycle
     unsigned tickets[8];
     double red[4];       // distributed mode: this rank's reduction values, allreduced in place
+    double qc;           // two-level: c^t E^{-1} c of the coarse correction (global)
     double rho, alpha, beta, pq, rr, bb, tol2;
     // MINRES
     double gamma, gamma_old, delta, eta, eta0, c, c_old, s, s_old;
@@ -107,7 +108,8 @@ __device__ __forceinline__ void stv(double *a, int64_t r, const double (&v)[D]) 
 // ------------------------------------------------------------------ scalar recurrences
 // Applied by the last block of a reduction on one GPU, or by k_fin after the allreduce of
 // the per-rank values in st->red on several (the same code either way).
-enum FinKind { FIN_BB, FIN_RR, FIN_PCG_INIT, FIN_PQ, FIN_UPD_PC, FIN_UPD_R, FIN_AFW_PCG_INIT, FIN_AFW_PCG };
+enum FinKind { FIN_BB, FIN_RR, FIN_PCG_INIT, FIN_PQ, FIN_UPD_PC, FIN_UPD_R, FIN_AFW_PCG_INIT, FIN_AFW_PCG,
+               FIN_AFW2_PCG_INIT, FIN_AFW2_PCG };
 
 __device__ __forceinline__ void apply_fin(KState *st, int kind, const double *t, double rtol) {
     switch (kind) {
@@ -146,6 +148,16 @@ __device__ __forceinline__ void apply_fin(KState *st, int kind, const double *t,
             st->beta = t[0] / st->rho;
             st->rho = t[0];
             break;
+        case FIN_AFW2_PCG_INIT:  // r^t M2^{-1} r = fine part + coarse part
+            st->rho = t[0] + st->qc;
+            st->beta = 0.0;
+            st->tol2 = rtol * rtol * st->bb;
+            st->flag = (st->rr <= st->tol2) ? FLAG_CONV : FLAG_RUN;
+            break;
+        case FIN_AFW2_PCG:
+            st->beta = (t[0] + st->qc) / st->rho;
+            st->rho = t[0] + st->qc;
+            break;
     }
 }
 
@@ -161,7 +173,8 @@ __device__ __forceinline__ void fin_or_store(KState *st, int kind, const double 
 
 // distributed mode: the recurrence after the allreduce (a converged state stays frozen)
 __global__ void k_fin(KState *st, int kind, double rtol) {
-    const bool init = kind == FIN_BB || kind == FIN_RR || kind == FIN_PCG_INIT || kind == FIN_AFW_PCG_INIT;
+    const bool init = kind == FIN_BB || kind == FIN_RR || kind == FIN_PCG_INIT || kind == FIN_AFW_PCG_INIT ||
+                      kind == FIN_AFW2_PCG_INIT;
     if (!init && st->flag != FLAG_RUN) return;
     apply_fin(st, kind, st->red, rtol);
 }
@@ -501,13 +514,13 @@ __global__ void __launch_bounds__(kT) k_minres_wx(int64_t nrows, const double *z
 
 // ------------------------------------------------------------------ patch (AFW) preconditioner
 // What the last block does with q = sum_p r_p^t B_p^{-1} r_p  (= r^t M^{-1} r)
-enum { AFW_PCG_INIT = 0, AFW_PCG = 1, AFW_MINRES_INIT = 2, AFW_MINRES = 3 };
+enum { AFW_PCG_INIT = 0, AFW_PCG = 1, AFW_MINRES_INIT = 2, AFW_MINRES = 3, AFW_PCG2_INIT = 4, AFW_PCG2 = 5 };
 
 // zs (per face slot) = patch contributions of M^{-1} r
 template <int D, int SLOTS, int KMAX, bool SYM, int WHAT>
 __global__ void __launch_bounds__(kT) k_afw_apply(AfwView A, const double *r, double *zs, double rtol, KState *st,
                                                   double *partials, int dist) {
-    if (WHAT != AFW_PCG_INIT && WHAT != AFW_MINRES_INIT && st->flag != FLAG_RUN) return;
+    if (WHAT != AFW_PCG_INIT && WHAT != AFW_MINRES_INIT && WHAT != AFW_PCG2_INIT && st->flag != FLAG_RUN) return;
     double acc[1] = {0.0};
     const int64_t nt = ((A.npatch + 31) >> 5) * 32 * D;     // one thread per (patch, component)
     GRID_STRIDE(t, nt) acc[0] += afw_patch_comp<D, SLOTS, KMAX, SYM>(A, t, r, zs);
@@ -516,6 +529,10 @@ __global__ void __launch_bounds__(kT) k_afw_apply(AfwView A, const double *r, do
             fin_or_store<1>(st, FIN_AFW_PCG_INIT, t, rtol, dist);
         } else if (WHAT == AFW_PCG) {
             fin_or_store<1>(st, FIN_AFW_PCG, t, rtol, dist);
+        } else if (WHAT == AFW_PCG2_INIT) {
+            fin_or_store<1>(st, FIN_AFW2_PCG_INIT, t, rtol, dist);
+        } else if (WHAT == AFW_PCG2) {
+            fin_or_store<1>(st, FIN_AFW2_PCG, t, rtol, dist);
         } else if (WHAT == AFW_MINRES_INIT) {
             minres_start(st, t[0]);
         } else {
@@ -622,6 +639,24 @@ __global__ void __launch_bounds__(kT) k_pcg_pdir_afw(int64_t nrows, double *__re
             afw_sum<D, SLOTS>(zs, row, z);
 #pragma unroll
             for (int i = 0; i < D; ++i) p[row * D + i] = (beta == 0.0) ? z[i] : fma(beta, p[row * D + i], z[i]);
+        }
+    }
+}
+
+// two-level: p = (sum of the slot contributions) + Z y + beta p
+template <int D, int SLOTS>
+__global__ void __launch_bounds__(kT) k_pcg_pdir_afw2(int64_t nrows, double *__restrict__ p, const double *__restrict__ zs,
+                                                      CoarseView C, const double *__restrict__ y, const KState *st) {
+    if (st->flag != FLAG_RUN) return;
+    const double beta = st->beta;
+    GRID_STRIDE(row, nrows) {
+        double z[D], zc[D];
+        afw_sum<D, SLOTS>(zs, row, z);
+        coarse_prolong<D>(C, row, y, zc);
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const double zi = z[i] + zc[i];
+            p[row * D + i] = (beta == 0.0) ? zi : fma(beta, p[row * D + i], zi);
         }
     }
 }
@@ -1065,6 +1100,8 @@ static void launch_afw(Launcher &L, cudaStream_t ks, const double *r, double *zs
     ++L.launches;
     if (WHAT == AFW_PCG_INIT) L.reduced(ks, 1, FIN_AFW_PCG_INIT, rtol);
     if (WHAT == AFW_PCG) L.reduced(ks, 1, FIN_AFW_PCG, rtol);
+    if (WHAT == AFW_PCG2_INIT) L.reduced(ks, 1, FIN_AFW2_PCG_INIT, rtol);
+    if (WHAT == AFW_PCG2) L.reduced(ks, 1, FIN_AFW2_PCG, rtol);
 }
 
 template <class Body, class Done>
@@ -1114,11 +1151,11 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     L.grid_vec = grid_for(L.N, kT);
     L.dist = h->part.on ? 1 : 0;
     L.comm = h->part.on ? h->comm->impl : nullptr;
-    CR_REQUIRE(!L.dist || o.method == CR_PCG_JACOBI || o.method == CR_PCG_BLOCKJACOBI || o.method == CR_PCG_AFW,
-               CR_ERR_INVALID_ARG, "a partitioned (multi-GPU) solve supports the PCG methods only");
+    const bool pcg_family = o.method == CR_PCG_JACOBI || o.method == CR_PCG_BLOCKJACOBI || o.method == CR_PCG_AFW ||
+                            o.method == CR_PCG_AFW2;
+    CR_REQUIRE(!L.dist || pcg_family, CR_ERR_INVALID_ARG, "a partitioned (multi-GPU) solve supports the PCG methods only");
     L.mf = o.matrix_free ? 1 : 0;
-    CR_REQUIRE(!L.mf || o.method == CR_PCG_JACOBI || o.method == CR_PCG_BLOCKJACOBI || o.method == CR_PCG_AFW,
-               CR_ERR_INVALID_ARG, "matrix_free supports the PCG methods only");
+    CR_REQUIRE(!L.mf || pcg_family, CR_ERR_INVALID_ARG, "matrix_free supports the PCG methods only");
     if (L.mf) build_mf(h, s);
     const int64_t N = w->N, nrows = L.nrows;
     const double rtol = o.rtol > 0 ? o.rtol : 1e-10;
@@ -1232,6 +1269,68 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
             });
             int64_t dit = w->hst->iters - it0;
             L.launches += 4 * ((dit + kk - 1) / kk) * kk;
+            L.spmvs += dit;
+            if (w->hst->flag == FLAG_CONV) {
+                init();
+                read_state(w, s);
+                if (w->hst->flag == FLAG_CONV || replacements >= 8) break;
+                ++replacements;
+            }
+            if (w->hst->flag == FLAG_BREAK) { status = CR_ERR_BREAKDOWN; break; }
+            if (w->hst->iters >= max_iter) { status = CR_ERR_NOT_CONVERGED; break; }
+        }
+    } else if (method == CR_PCG_AFW2) {
+        constexpr int SLOTS = D == 2 ? 2 : 3;
+        build_afw(h, AFW_SPD, s);
+        const int H = o.coarse > 0 ? o.coarse : (D == 2 ? 16 : 8);
+        build_coarse(h, H, [&](const double *z, double *Y) {
+            L.halo(s, const_cast<double *>(z));
+            if (L.mf) mf_apply<D, false>(L, s, z, Y, 0.0);
+            else spmv(h->G, z, Y, s);
+        }, s);
+        if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
+        double *zs = w->zs.get();
+        const CoarseView CV = h->coarse.view();
+        double *yc = h->coarse.y.get();
+        auto coarse = [&](cudaStream_t q) {
+            coarse_restrict_solve(h, w->r.get(), &st->qc, part, &st->tickets[4], q);
+            L.launches += 3;
+        };
+        auto init = [&]() {
+            true_residual<D>(L, x, w->r.get());
+            coarse(s);
+            launch_afw<D, AFW_PCG2_INIT>(L, s, w->r.get(), zs, rtol);
+            k_pcg_pdir_afw2<D, SLOTS><<<L.grid_rows, kT, 0, s>>>(nrows, w->p.get(), zs, CV, yc, st);
+            CR_CHECK_LAUNCH();
+            ++L.launches;
+        };
+        init();
+        read_state(w, s);
+        if (w->hst->bb == 0.0) { CR_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), s)); }
+        while (w->hst->flag == FLAG_RUN) {
+            auto body = [&](int) {
+                L.halo(ks, w->p.get());
+                if (L.mf) {
+                    mf_apply<D, true>(L, ks, w->p.get(), w->q.get(), rtol);
+                } else {
+                    k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part, L.dist);
+                    CR_CHECK_LAUNCH();
+                    L.reduced(ks, 1, FIN_PQ, rtol);
+                }
+                k_pcg_update_r<<<L.grid_vec, kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), st, part, L.dist);
+                CR_CHECK_LAUNCH();
+                L.reduced(ks, 1, FIN_UPD_R, rtol);
+                coarse(ks);
+                launch_afw<D, AFW_PCG2>(L, ks, w->r.get(), zs, rtol);
+                k_pcg_pdir_afw2<D, SLOTS><<<L.grid_rows, kT, 0, ks>>>(nrows, w->p.get(), zs, CV, yc, st);
+                CR_CHECK_LAUNCH();
+            };
+            int64_t it0 = w->hst->iters;
+            graph_loop(L, ks, method * 100000 + L.mf * 50000 + kk, kk, body, [&]() {
+                return w->hst->flag != FLAG_RUN || w->hst->iters >= max_iter;
+            });
+            int64_t dit = w->hst->iters - it0;
+            L.launches += 7 * ((dit + kk - 1) / kk) * kk;
             L.spmvs += dit;
             if (w->hst->flag == FLAG_CONV) {
                 init();
@@ -1472,6 +1571,18 @@ static void apply_precond_t(cr_hybrid_s *h, int method, const double *r, double 
         case CR_PCG_BLOCKJACOBI:
             k_block_apply<D><<<grid, kT, 0, s>>>(nrows, h->bdinv.get(), r, z);
             break;
+        case CR_PCG_AFW2: {
+            build_afw(h, AFW_SPD, s);
+            build_coarse(h, D == 2 ? 16 : 8, [&](const double *zz, double *Y) { spmv(h->G, zz, Y, s); }, s);
+            if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
+            CR_CUDA(cudaMemsetAsync(w->st.get(), 0, sizeof(KState), s));
+            coarse_restrict_solve(h, r, &w->st.get()->qc, w->partials.get(), &w->st.get()->tickets[4], s);
+            launch_afw<D, AFW_PCG_INIT>(L, s, r, w->zs.get(), 1e-10);
+            CR_CUDA(cudaMemsetAsync(w->st.get(), 0, sizeof(KState), s));   // flag RUN, beta 0: p = z
+            k_pcg_pdir_afw2<D, SLOTS><<<grid, kT, 0, s>>>(nrows, z, w->zs.get(), h->coarse.view(), h->coarse.y.get(),
+                                                         w->st.get());
+            break;
+        }
         case CR_PCG_AFW:
         case CR_MINRES_AFW: {
             build_afw(h, method == CR_PCG_AFW ? AFW_SPD : AFW_ABS, s);
