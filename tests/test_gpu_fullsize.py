@@ -132,7 +132,8 @@ def test_config1_full_size():
     eG, eS = sampled_rows(mo, prm, data, E, hg, 200)
     assert eG <= 1e-12 and eS <= 1e-12, (eG, eS)
     W = torch.zeros(hg.n_rows, dtype=torch.float64, device=DEV)
-    rep = P.cr_solve(hg, W, "pcg_afw", rtol=cfg.rtol, check_every=64)
+    # the bench's solver: two-level PCG on the matrix-free factored G
+    rep = P.cr_solve(hg, W, "pcg_afw2", rtol=cfg.rtol, check_every=64, matrix_free=1, coarse=32)
     assert rep["converged"] and rep["rel_res_true"] <= cfg.rtol
     U, Pp, diag = P.cr_recover(hg, W)
     eP, eU = sampled_recovery(mo, prm, data, E, W.cpu().numpy(), U.cpu().numpy(), Pp.cpu().numpy(), 400)
@@ -147,15 +148,18 @@ def test_config1_full_size():
 
 @pytest.mark.parametrize("dim,n", [(2, 1024)])
 def test_well_balanced_full_size(dim, n):
-    """P:L559 at the bench size: constant f -> U = 0 and P_K = f.(x_K - x_K0)."""
+    """P:L559 at the bench size: constant f -> U = 0 and P_K = f.(x_K - x_K0), through the
+    bench's solver (two-level PCG, matrix-free G).  The factored G keeps the O(|K|) part of each
+    Shat_K^{-1} exact, so P reaches the 1e-8 bar; the assembled fp64 G stalls at ~8e-7 here
+    (DESIGN.md §5.2)."""
     coords, cells = ci.square_mesh(n, 0.2, 2)
     f = np.array([0.7, -1.3])
     prob = P.Problem(mu=1.0, nu=1.0, fbar=tg(np.tile(f, (cells.shape[0], 1))))
-    out = P.hybrid_method(tg(coords), tg(cells), prob, "pcg_afw", rtol=1e-10)
+    out = P.hybrid_method(tg(coords), tg(cells), prob, "pcg_afw2", rtol=1e-10, matrix_free=1, coarse=32)
     xK = out["mesh"].export()["xK"].cpu().numpy()
     Pex = (xK - xK[0]) @ f
     assert out["U"].abs().max().item() <= 1e-8
-    assert np.abs(out["P"].cpu().numpy() - Pex).max() <= 1e-7 * np.abs(Pex).max()
+    assert np.abs(out["P"].cpu().numpy() - Pex).max() <= 1e-8 * np.abs(Pex).max()
 
 
 # ------------------------------------------------------------------ configs[2], configs[3]: shifted systems
@@ -195,7 +199,7 @@ def test_config4_3d_full_size():
     eG, eS = sampled_rows(mo, prm, data, E, hg, 100)
     assert eG <= 1e-12 and eS <= 1e-12, (eG, eS)
     W = torch.zeros(hg.n_rows, dtype=torch.float64, device=DEV)
-    rep = P.cr_solve(hg, W, "pcg_afw", rtol=cfg.rtol, check_every=64)
+    rep = P.cr_solve(hg, W, "pcg_afw2", rtol=cfg.rtol, check_every=64, matrix_free=1, coarse=8)
     assert rep["converged"] and rep["rel_res_true"] <= cfg.rtol
     U, Pp, diag = P.cr_recover(hg, W)
     eP, eU = sampled_recovery(mo, prm, data, E, W.cpu().numpy(), U.cpu().numpy(), Pp.cpu().numpy(), 200)
