@@ -53,42 +53,69 @@ __global__ void k_coarse_faces(const int32_t *dof_face, int64_t row0, int64_t nr
 }
 
 // partial restriction of one chunk: the 2^D nodes of its coarse cell x D^2 tensor components.
-// 2^D consecutive threads share a row (one per corner node, D^2 accumulators each); lanes of the
-// same corner are reduced by shuffles, then across warps in shared memory (fixed trees).
+// 2D: one thread per row with all 16 accumulators; 3D: the 2^D = 8 corner nodes of a row are
+// split over 8 consecutive threads (9 accumulators each).  Rows are read 4 at a time per thread
+// (independent loads in flight); lanes of the same corner are reduced by shuffles, then across
+// warps in shared memory (fixed trees: deterministic).
 template <int D>
 __global__ void __launch_bounds__(256) k_coarse_restrict(CoarseView C, const double *r, double *part) {
-    constexpr int NN = 1 << D, DD = D * D, NV = NN * DD, SL = 256 / NN;
+    constexpr int NN = 1 << D, DD = D * D, NV = NN * DD;
+    constexpr int TPR = D == 2 ? 1 : NN;            // threads per row
+    constexpr int NA = D == 2 ? NV : DD;            // accumulators per thread
+    constexpr int SL = 256 / TPR, U = 4;
     const int64_t ch = blockIdx.x;
     const int64_t b = C.chunk_start[ch], e = C.chunk_start[ch + 1];
-    const int n = threadIdx.x % NN, slot = threadIdx.x / NN;
-    double acc[DD];
+    const int n3 = threadIdx.x % TPR, slot = threadIdx.x / TPR;
+    double acc[NA];
 #pragma unroll
-    for (int v = 0; v < DD; ++v) acc[v] = 0.0;
-    for (int64_t t = b + slot; t < e; t += SL) {
-        const int64_t row = C.perm[t];
-        int ic[D];
-        float xi[D];
-        coarse_locate<D>(C.g, C.fx + row * D, ic, xi);
-        double wn = 1.0, av[D], rv[D];
+    for (int v = 0; v < NA; ++v) acc[v] = 0.0;
+    for (int64_t t0 = b + slot; t0 < e; t0 += (int64_t)SL * U) {
+        int64_t row[U];
 #pragma unroll
-        for (int i = 0; i < D; ++i) {
-            wn *= ((n >> i) & 1) ? (double)xi[i] : 1.0 - (double)xi[i];
-            av[i] = C.fa[row * D + i];
-            rv[i] = r[row * D + i];
+        for (int u = 0; u < U; ++u) {
+            const int64_t t = t0 + (int64_t)u * SL;
+            row[u] = t < e ? (int64_t)C.perm[t] : -1;
         }
+        float xv[U][D], av[U][D];
+        double rv[U][D];
 #pragma unroll
-        for (int k = 0; k < D; ++k)
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int l = 0; l < D; ++l) acc[k * D + l] = fma(wn * av[l], rv[k], acc[k * D + l]);
+            for (int i = 0; i < D; ++i) {
+                const bool ok = row[u] >= 0;
+                xv[u][i] = ok ? C.fx[row[u] * D + i] : 0.f;
+                av[u][i] = ok ? C.fa[row[u] * D + i] : 0.f;
+                rv[u][i] = ok ? r[row[u] * D + i] : 0.0;
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            int ic[D];
+            float xi[D];
+            coarse_locate<D>(C.g, xv[u], ic, xi);
+#pragma unroll
+            for (int nn = 0; nn < (D == 2 ? NN : 1); ++nn) {
+                const int n = D == 2 ? nn : n3;
+                double wn = 1.0;
+#pragma unroll
+                for (int i = 0; i < D; ++i) wn *= ((n >> i) & 1) ? (double)xi[i] : 1.0 - (double)xi[i];
+#pragma unroll
+                for (int k = 0; k < D; ++k)
+#pragma unroll
+                    for (int l = 0; l < D; ++l) {
+                        const int v = (D == 2 ? nn * DD : 0) + k * D + l;
+                        acc[v] = fma(wn * (double)av[u][l], rv[u][k], acc[v]);
+                    }
+            }
+        }
     }
     __shared__ double sh[8][NV];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int v = 0; v < DD; ++v) {
+    for (int v = 0; v < NA; ++v) {
         double x = acc[v];
 #pragma unroll
-        for (int o = 16; o >= NN; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if (lane < NN) sh[warp][lane * DD + v] = x;
+        for (int o = 16; o >= TPR; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane < TPR) sh[warp][(D == 2 ? 0 : lane * DD) + v] = x;
     }
     __syncthreads();
     for (int v = threadIdx.x; v < NV; v += blockDim.x) {
@@ -126,21 +153,24 @@ __global__ void k_coarse_gather(CoarseView C, const double *part, double *c) {
     }
 }
 
-// y = Einv c (one warp per row), q = c^t y (last block) -> st->qc
-__global__ void __launch_bounds__(256) k_coarse_gemv(const double *Einv, int64_t nE, const double *c, double *y,
+// y = Einv c (one 128-thread block per row), q = c^t y -> *qout (block partials, last block sums)
+__global__ void __launch_bounds__(128) k_coarse_gemv(const double *Einv, int64_t nE, const double *c, double *y,
                                                      double *qout, double *partials, unsigned *ticket) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     double acc[1] = {0.0};
-    for (int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); row < nE; row += warps) {
+    __shared__ double sh[4];
+    for (int64_t row = blockIdx.x; row < nE; row += gridDim.x) {
         const double *er = Einv + row * nE;
         double s = 0.0;
-        for (int64_t j = lane; j < nE; j += 32) s = fma(er[j], c[j], s);
+        for (int64_t j = threadIdx.x; j < nE; j += blockDim.x) s = fma(__ldcs(er + j), c[j], s);
         s = warp_sum(s);
-        if (lane == 0) {
-            y[row] = s;
-            acc[0] = fma(c[row], s, acc[0]);
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const double t = (sh[0] + sh[1]) + (sh[2] + sh[3]);
+            y[row] = t;
+            acc[0] = fma(c[row], t, acc[0]);
         }
+        __syncthreads();
     }
     reduce_and_finish<1>(acc, partials, ticket, [&](double *t) { *qout = t[0]; });
 }
@@ -474,7 +504,8 @@ void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double
     }
     CR_CHECK_LAUNCH();
     if (h->part.on) h->comm->impl->allreduce(C.c.get(), (int)C.nE, false, s);
-    k_coarse_gemv<<<grid_for(C.nE * 32, T), T, 0, s>>>(C.Einv.get(), C.nE, C.c.get(), C.y.get(), qout, partials, ticket);
+    k_coarse_gemv<<<(unsigned)std::min<int64_t>(C.nE, kSMs * 16), 128, 0, s>>>(C.Einv.get(), C.nE, C.c.get(), C.y.get(),
+                                                                              qout, partials, ticket);
     CR_CHECK_LAUNCH();
 }
 

@@ -90,6 +90,28 @@ enum DevErr : int {
 
 // grid sizing: B200 has 148 SMs; streaming kernels use a fixed grid (deterministic partials)
 constexpr int kSMs = 148;
+
+// Grid of exactly one wave of resident blocks (occupancy of `kernel` at `threads` per block) for
+// grid-stride kernels: a second, partial wave would leave SMs idle while it drains.  Cached per
+// kernel; the grid only depends on the kernel and the GPU, so block partials stay deterministic.
+template <class F>
+inline int occ_grid(F kernel, int threads, int64_t work) {
+    static thread_local std::vector<std::pair<const void *, int>> cache;
+    const void *key = reinterpret_cast<const void *>(kernel);
+    int nb = 0;
+    for (auto &kv : cache)
+        if (kv.first == key) nb = kv.second;
+    if (nb == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, 0) != cudaSuccess || nb < 1) nb = 1;
+        nb = nb > 16 ? 16 : nb;
+        cache.emplace_back(key, nb);
+    }
+    int64_t b = (work + threads - 1) / threads;
+    const int64_t cap = (int64_t)kSMs * nb;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (int)b;
+}
 inline int grid_for(int64_t work, int threads, int max_blocks_per_sm = 8) {
     int64_t b = (work + threads - 1) / threads;
     int64_t cap = (int64_t)kSMs * max_blocks_per_sm;

@@ -1044,7 +1044,7 @@ static MfView mf_view(const cr_hybrid_s *h) {
 template <int D, bool REDUCE>
 static void mf_apply(Launcher &L, cudaStream_t ks, const double *x, double *q, double rtol) {
     CR_CUDA(cudaMemsetAsync(q, 0, L.N * sizeof(double), ks));
-    k_mf_spmv<D, REDUCE><<<grid_for(L.h->mf.ncells, kT), kT, 0, ks>>>(mf_view<D>(L.h), x, q, L.nrows, L.w->st.get(),
+    k_mf_spmv<D, REDUCE><<<occ_grid(k_mf_spmv<D, REDUCE>, kT, L.h->mf.ncells), kT, 0, ks>>>(mf_view<D>(L.h), x, q, L.nrows, L.w->st.get(),
                                                                       L.w->partials.get(), L.dist);
     CR_CHECK_LAUNCH();
     ++L.launches;
@@ -1082,19 +1082,19 @@ static void launch_afw(Launcher &L, cudaStream_t ks, const double *r, double *zs
     constexpr int SLOTS = D == 2 ? 2 : 3;
     const AfwPrec &P = L.h->afw;
     AfwView A{P.ioff.get(), P.voff.get(), P.kl.get(), P.ids.get(), P.vals.get(), P.npatch};
-    const int grid = grid_for(P.nslices * 32 * D, kT);
+    const int64_t nt = P.nslices * 32 * D;
     const bool sym = P.built != AFW_GEN;
     KState *st = L.w->st.get();
     double *part = L.w->partials.get();
     if (P.kmax <= 6) {
-        if (sym) k_afw_apply<D, SLOTS, 6, true, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
-        else k_afw_apply<D, SLOTS, 6, false, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        if (sym) k_afw_apply<D, SLOTS, 6, true, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 6, true, WHAT>, kT, nt), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        else k_afw_apply<D, SLOTS, 6, false, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 6, false, WHAT>, kT, nt), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
     } else if (P.kmax <= 8) {
-        if (sym) k_afw_apply<D, SLOTS, 8, true, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
-        else k_afw_apply<D, SLOTS, 8, false, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        if (sym) k_afw_apply<D, SLOTS, 8, true, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 8, true, WHAT>, kT, nt), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        else k_afw_apply<D, SLOTS, 8, false, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 8, false, WHAT>, kT, nt), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
     } else {
-        if (sym) k_afw_apply<D, SLOTS, 16, true, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
-        else k_afw_apply<D, SLOTS, 16, false, WHAT><<<grid, kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        if (sym) k_afw_apply<D, SLOTS, 16, true, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 16, true, WHAT>, kT, nt), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        else k_afw_apply<D, SLOTS, 16, false, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 16, false, WHAT>, kT, nt), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
     }
     CR_CHECK_LAUNCH();
     ++L.launches;
@@ -1197,7 +1197,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                 if (L.mf) {
                     mf_apply<D, true>(L, ks, w->p.get(), w->q.get(), rtol);
                 } else {
-                    k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part, L.dist);
+                    k_pcg_spmv<D><<<occ_grid(k_pcg_spmv<D>, kT, L.nrows), kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part, L.dist);
                     CR_CHECK_LAUNCH();
                     L.reduced(ks, 1, FIN_PQ, rtol);
                 }
@@ -1207,10 +1207,10 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                     L.reduced(ks, 2, FIN_UPD_PC, rtol);
                     k_pcg_pdir<D, 1><<<L.grid_rows, kT, 0, ks>>>(nrows, w->p.get(), w->r.get(), M, st);
                 } else {
-                    k_pcg_update_jac<<<L.grid_vec, kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), M, st, part, L.dist);
+                    k_pcg_update_jac<<<occ_grid(k_pcg_update_jac, kT, L.N / 2), kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), M, st, part, L.dist);
                     CR_CHECK_LAUNCH();
                     L.reduced(ks, 2, FIN_UPD_PC, rtol);
-                    k_pcg_pdir_jac<<<L.grid_vec, kT, 0, ks>>>(N, w->p.get(), w->r.get(), M, st);
+                    k_pcg_pdir_jac<<<occ_grid(k_pcg_pdir_jac, kT, L.N / 2), kT, 0, ks>>>(N, w->p.get(), w->r.get(), M, st);
                 }
                 CR_CHECK_LAUNCH();
             };
@@ -1252,15 +1252,15 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                 if (L.mf) {
                     mf_apply<D, true>(L, ks, w->p.get(), w->q.get(), rtol);
                 } else {
-                    k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part, L.dist);
+                    k_pcg_spmv<D><<<occ_grid(k_pcg_spmv<D>, kT, L.nrows), kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part, L.dist);
                     CR_CHECK_LAUNCH();
                     L.reduced(ks, 1, FIN_PQ, rtol);
                 }
-                k_pcg_update_r<<<L.grid_vec, kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), st, part, L.dist);
+                k_pcg_update_r<<<occ_grid(k_pcg_update_r, kT, L.N / 2), kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), st, part, L.dist);
                 CR_CHECK_LAUNCH();
                 L.reduced(ks, 1, FIN_UPD_R, rtol);
                 launch_afw<D, AFW_PCG>(L, ks, w->r.get(), zs, rtol);
-                k_pcg_pdir_afw<D, SLOTS><<<L.grid_rows, kT, 0, ks>>>(nrows, w->p.get(), zs, st);
+                k_pcg_pdir_afw<D, SLOTS><<<occ_grid(k_pcg_pdir_afw<D, SLOTS>, kT, nrows), kT, 0, ks>>>(nrows, w->p.get(), zs, st);
                 CR_CHECK_LAUNCH();
             };
             int64_t it0 = w->hst->iters;
@@ -1313,16 +1313,16 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                 if (L.mf) {
                     mf_apply<D, true>(L, ks, w->p.get(), w->q.get(), rtol);
                 } else {
-                    k_pcg_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part, L.dist);
+                    k_pcg_spmv<D><<<occ_grid(k_pcg_spmv<D>, kT, L.nrows), kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part, L.dist);
                     CR_CHECK_LAUNCH();
                     L.reduced(ks, 1, FIN_PQ, rtol);
                 }
-                k_pcg_update_r<<<L.grid_vec, kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), st, part, L.dist);
+                k_pcg_update_r<<<occ_grid(k_pcg_update_r, kT, L.N / 2), kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), st, part, L.dist);
                 CR_CHECK_LAUNCH();
                 L.reduced(ks, 1, FIN_UPD_R, rtol);
                 coarse(ks);
                 launch_afw<D, AFW_PCG2>(L, ks, w->r.get(), zs, rtol);
-                k_pcg_pdir_afw2<D, SLOTS><<<L.grid_rows, kT, 0, ks>>>(nrows, w->p.get(), zs, CV, yc, st);
+                k_pcg_pdir_afw2<D, SLOTS><<<occ_grid(k_pcg_pdir_afw2<D, SLOTS>, kT, nrows), kT, 0, ks>>>(nrows, w->p.get(), zs, CV, yc, st);
                 CR_CHECK_LAUNCH();
             };
             int64_t it0 = w->hst->iters;
