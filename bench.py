@@ -136,8 +136,19 @@ def oracle_extrapolate(s: dict, nc_full: int, nnz_full: int, iters_full: int) ->
     return (s["mesh_s"] + s["hyb_s"] + s["rec_s"]) * f + s["iter_s"] * (nnz_full / s["nnz"]) * iters_full
 
 
-def full_sizes():
-    n = 1024
+def workload_config(n, world):
+    """The `config` object of both arms (identical by construction; closed-form sizes of the
+    structured n x n triangulation)."""
+    nc, nnz, nb, N = full_sizes(n)
+    return {"workload": "configs[1] 2D transient Stokes n=%d jittered 0.2h, two-level-preconditioned PCG to "
+                        "true 1e-10" % n,
+            "cells": nc, "unknowns": N, "nnz_G": nnz, "blocks_G": nb,
+            "parallelism": (f"face rows partitioned over {world} GPUs (NCCL halo send/recv + allreduce)"
+                            if world > 1 else "1 GPU"),
+            "l2": "working set > L2 (G = %.2f GB per SpMV) and a 256 MB L2 flush before each step" % (8 * nnz / 1e9)}
+
+
+def full_sizes(n=1024):
     nc = 2 * n * n
     nf_int = 3 * n * n - 2 * n
     nb = nf_int + 12 * (n - 1) ** 2 + 8 * (n - 1)
@@ -165,8 +176,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "configs[1] 2D transient Stokes n=1024 jittered, Jacobi-PCG to 1e-10",
-                       "cells": nc, "unknowns": N},
+            "config": workload_config(1024, args.gpus),
             "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "oracle", "sample": sample_desc},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -282,6 +292,7 @@ def main():
     minfo = hyb.mf_info()
     mf_bytes = minfo["bytes"] + N8 + N8              # per-cell factors + x once + q once
     prec_s = time_launch(lambda: hyb.apply_precond("pcg_afw", x, y))
+    prec2_s = time_launch(lambda: hyb.apply_precond(METHOD, x, y))
     # patch operator + r read + slot contributions written, then read back and z written
     prec_bytes = pinfo["bytes"] + N8 + slots * N8 + slots * N8 + N8
     traffic = None
@@ -304,9 +315,12 @@ def main():
                 "frac": bytes_ / sec / 1e9 / peak, "traffic": traffic_, "peak_source": peak_src,
                 "algorithmic_bytes": bytes_, "launch_s": sec}
 
+    prec2_bytes = prec_bytes + coarse_bytes
     kernels = {
         "mf": roof("k_mf_spmv (matrix-free factored G x, per-cell factors, the in-solve G apply)", mf_bytes, mf_s),
         "precond": roof("k_afw_apply + k_afw_zsum (patch additive Schwarz z = M^-1 r)", prec_bytes, prec_s),
+        "precond_two_level": roof("coarse restrict + gather + E^-1 GEMV + patch apply + combine (z = M2^-1 r)",
+                                  prec2_bytes, prec2_s),
         "spmv": roof("k_spmv (assembled sliced block-ELL G x, same row code as the assembled PCG SpMV)",
                      spmv_bytes, spmv_s, traffic),
     }
@@ -357,13 +371,7 @@ def main():
             "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "configs[1] 2D transient Stokes n=%d jittered 0.2h, two-level-preconditioned "
-                                   "PCG to true 1e-10" % (args.n or cfg.n),
-                       "cells": mesh.nc, "unknowns": N, "nnz_G": nnz, "blocks_G": nb,
-                       "parallelism": (f"face rows partitioned over {world} GPUs (NCCL halo send/recv + allreduce)"
-                                       if world > 1 else "1 GPU"),
-                       "l2": "working set > L2 (G = %.2f GB per SpMV) and a 256 MB L2 flush before each step"
-                             % (8 * nnz / 1e9)},
+            "config": workload_config(args.n or cfg.n, world),
             "pcg": {"method": METHOD, "matrix_free": MATRIX_FREE, "coarse_intervals": COARSE,
                     "iterations": rep["iterations"],
                     "rel_res_true": rep["rel_res_true"], "solve_s": rep["seconds"],

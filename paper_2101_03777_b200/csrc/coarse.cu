@@ -153,15 +153,38 @@ __global__ void k_coarse_gather(CoarseView C, const double *part, double *c) {
     }
 }
 
-// y = Einv c (one 128-thread block per row), q = c^t y -> *qout (block partials, last block sums)
+// y = Einv c (one 128-thread block per row, 16-byte loads, 4 in flight per thread),
+// q = c^t y -> *qout (block partials, last block sums)
 __global__ void __launch_bounds__(128) k_coarse_gemv(const double *Einv, int64_t nE, const double *c, double *y,
                                                      double *qout, double *partials, unsigned *ticket) {
     double acc[1] = {0.0};
     __shared__ double sh[4];
+    const int64_t n2 = nE >> 1;   // nE = D^2 (H+1)^D is even for D = 2; odd tails handled below
+    const double2 *c2 = reinterpret_cast<const double2 *>(c);
     for (int64_t row = blockIdx.x; row < nE; row += gridDim.x) {
         const double *er = Einv + row * nE;
-        double s = 0.0;
-        for (int64_t j = threadIdx.x; j < nE; j += blockDim.x) s = fma(__ldcs(er + j), c[j], s);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (((row * nE) & 1) == 0) {
+            const double2 *e2 = reinterpret_cast<const double2 *>(er);
+            int64_t j = threadIdx.x;
+            for (; j + 3 * 128 < n2; j += 4 * 128) {
+                const double2 a0 = __ldcs(e2 + j), a1 = __ldcs(e2 + j + 128), a2 = __ldcs(e2 + j + 256),
+                              a3 = __ldcs(e2 + j + 384);
+                const double2 b0 = c2[j], b1 = c2[j + 128], b2 = c2[j + 256], b3 = c2[j + 384];
+                s0 = fma(a0.x, b0.x, fma(a0.y, b0.y, s0));
+                s1 = fma(a1.x, b1.x, fma(a1.y, b1.y, s1));
+                s2 = fma(a2.x, b2.x, fma(a2.y, b2.y, s2));
+                s3 = fma(a3.x, b3.x, fma(a3.y, b3.y, s3));
+            }
+            for (; j < n2; j += 128) {
+                const double2 a0 = __ldcs(e2 + j), b0 = c2[j];
+                s0 = fma(a0.x, b0.x, fma(a0.y, b0.y, s0));
+            }
+            if ((nE & 1) && threadIdx.x == 0) s0 = fma(er[nE - 1], c[nE - 1], s0);
+        } else {
+            for (int64_t j = threadIdx.x; j < nE; j += 128) s0 = fma(__ldcs(er + j), c[j], s0);
+        }
+        double s = (s0 + s1) + (s2 + s3);
         s = warp_sum(s);
         if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
         __syncthreads();
@@ -504,8 +527,8 @@ void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double
     }
     CR_CHECK_LAUNCH();
     if (h->part.on) h->comm->impl->allreduce(C.c.get(), (int)C.nE, false, s);
-    k_coarse_gemv<<<(unsigned)std::min<int64_t>(C.nE, kSMs * 16), 128, 0, s>>>(C.Einv.get(), C.nE, C.c.get(), C.y.get(),
-                                                                              qout, partials, ticket);
+    k_coarse_gemv<<<occ_grid(k_coarse_gemv, 128, C.nE * 128), 128, 0, s>>>(C.Einv.get(), C.nE, C.c.get(), C.y.get(),
+                                                                           qout, partials, ticket);
     CR_CHECK_LAUNCH();
 }
 

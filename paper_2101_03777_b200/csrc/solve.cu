@@ -1573,7 +1573,9 @@ static void apply_precond_t(cr_hybrid_s *h, int method, const double *r, double 
             break;
         case CR_PCG_AFW2: {
             build_afw(h, AFW_SPD, s);
-            build_coarse(h, D == 2 ? 16 : 8, [&](const double *zz, double *Y) { spmv(h->G, zz, Y, s); }, s);
+            // the coarse grid of the last two-level solve, else the default
+            const int Hc = h->coarse.requested > 0 ? h->coarse.requested : (D == 2 ? 16 : 8);
+            build_coarse(h, Hc, [&](const double *zz, double *Y) { spmv(h->G, zz, Y, s); }, s);
             if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
             CR_CUDA(cudaMemsetAsync(w->st.get(), 0, sizeof(KState), s));
             coarse_restrict_solve(h, r, &w->st.get()->qc, w->partials.get(), &w->st.get()->tickets[4], s);
