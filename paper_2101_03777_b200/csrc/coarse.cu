@@ -263,29 +263,28 @@ __global__ void k_symmetrize(double *E, int64_t n) {
 //   A_KK = Pk.
 constexpr int kGB = 32;
 
-// Pk = inverse of the b x b diagonal block (one CTA, shared memory, scalar Gauss-Jordan)
-__global__ void k_gj_diag(const double *E, int64_t n, int64_t k0, int b, double *Pk, int *bad) {
-    __shared__ double A[kGB][2 * kGB];
-    for (int t = threadIdx.x; t < b * 2 * b; t += blockDim.x) {
-        const int i = t / (2 * b), j = t % (2 * b);
-        A[i][j] = j < b ? E[(k0 + i) * n + k0 + j] : (j - b == i ? 1.0 : 0.0);
-    }
-    __syncthreads();
-    __shared__ double colc[kGB];
+// Pk = inverse of the b x b diagonal block: one warp, lane i owns row i of [A | I] in shared
+// memory (scalar Gauss-Jordan, no pivoting: the block is a Schur complement of an SPD matrix)
+__global__ void __launch_bounds__(32) k_gj_diag(const double *E, int64_t n, int64_t k0, int b, double *Pk, int *bad) {
+    __shared__ double A[kGB][2 * kGB + 1];
+    const int i = threadIdx.x;
+    for (int j = 0; j < 2 * b; ++j)
+        A[i][j] = (i < b) ? (j < b ? E[(k0 + i) * n + k0 + j] : (j - b == i ? 1.0 : 0.0)) : 0.0;
+    __syncwarp();
     for (int c = 0; c < b; ++c) {
         const double piv = A[c][c];
-        if (threadIdx.x == 0 && !(piv > 0.0)) atomicExch(bad, 1);
-        if (threadIdx.x < b) colc[threadIdx.x] = A[threadIdx.x][c];   // before row c or column c change
-        __syncthreads();
-        for (int j = threadIdx.x; j < 2 * b; j += blockDim.x) A[c][j] /= piv;
-        __syncthreads();
-        for (int t = threadIdx.x; t < b * 2 * b; t += blockDim.x) {
-            const int i = t / (2 * b), j = t % (2 * b);
-            if (i != c) A[i][j] -= colc[i] * A[c][j];
-        }
-        __syncthreads();
+        if (i == 0 && !(piv > 0.0)) atomicExch(bad, 1);
+        const double f = (i < b && i != c) ? A[i][c] / piv : 0.0;
+        __syncwarp();
+        if (i < b && i != c)
+            for (int j = 0; j < 2 * b; ++j) A[i][j] -= f * A[c][j];
+        __syncwarp();
+        if (i == c)
+            for (int j = 0; j < 2 * b; ++j) A[c][j] /= piv;
+        __syncwarp();
     }
-    for (int t = threadIdx.x; t < b * b; t += blockDim.x) Pk[t] = A[t / b][b + t % b];
+    if (i < b)
+        for (int j = 0; j < b; ++j) Pk[i * b + j] = A[i][b + j];
 }
 
 // X[i][c] = sum_m A[i][k0+m] Pk[m][c]  (all rows i; block rows give Pk itself up to rounding)
@@ -329,17 +328,24 @@ __global__ void __launch_bounds__(256) k_gj_update(double *E, int64_t n, int64_t
         }
 }
 
-// pivot rows A_KJ = Pk A_KJ (J outside the block), pivot columns A_IK = -X_I, A_KK = Pk
-__global__ void k_gj_rows(double *E, int64_t n, int64_t k0, int b, const double *Pk, const double *X) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+// pivot rows A_KJ = Pk A_KJ (J outside the block): one thread per (r, j); the column is read
+// by the b threads of the same j (cached)
+__global__ void k_gj_rows(double *E, int64_t n, int64_t k0, int b, const double *Pk, const double *X, double *tmp) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * b; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / b;
+        const int r = (int)(t - j * b);
         if (j >= k0 && j < k0 + b) continue;
-        double col[kGB];
-        for (int m = 0; m < b; ++m) col[m] = E[(k0 + m) * n + j];
-        for (int r = 0; r < b; ++r) {
-            double s = 0.0;
-            for (int m = 0; m < b; ++m) s = fma(Pk[r * b + m], col[m], s);
-            E[(k0 + r) * n + j] = s;
-        }
+        double s = 0.0;
+        for (int m = 0; m < b; ++m) s = fma(Pk[r * b + m], E[(k0 + m) * n + j], s);
+        tmp[t] = s;
+    }
+}
+__global__ void k_gj_rows_store(double *E, int64_t n, int64_t k0, int b, const double *tmp) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * b; t += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(t / n);
+        const int64_t j = t - (int64_t)r * n;
+        if (j >= k0 && j < k0 + b) continue;
+        E[(k0 + r) * n + j] = tmp[j * b + r];
     }
 }
 __global__ void k_gj_cols(double *E, int64_t n, int64_t k0, int b, const double *Pk, const double *X) {
@@ -468,19 +474,21 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
             }
     k_symmetrize<<<grid_for(C.nE * C.nE, T, 64), T, 0, s>>>(C.Einv.get(), C.nE);
     CR_CHECK_LAUNCH();
-    DevBuf<double> Pk, X;
+    DevBuf<double> Pk, X, RT;
     Pk.alloc(kGB * kGB, s);
     X.alloc(C.nE * kGB, s);
+    RT.alloc(C.nE * kGB, s);
     DevBuf<int> bad;
     bad.alloc(1, s);
     bad.zero(s);
     const unsigned tiles = (unsigned)((C.nE + 63) / 64);
     for (int64_t k0 = 0; k0 < C.nE; k0 += kGB) {
         const int b = (int)std::min<int64_t>(kGB, C.nE - k0);
-        k_gj_diag<<<1, 256, 0, s>>>(C.Einv.get(), C.nE, k0, b, Pk.get(), bad.get());
+        k_gj_diag<<<1, 32, 0, s>>>(C.Einv.get(), C.nE, k0, b, Pk.get(), bad.get());
         k_gj_colpanel<<<grid_for(C.nE * b, T), T, 0, s>>>(C.Einv.get(), C.nE, k0, b, Pk.get(), X.get());
         k_gj_update<<<dim3(tiles, tiles), 256, 0, s>>>(C.Einv.get(), C.nE, k0, b, X.get());
-        k_gj_rows<<<grid_for(C.nE, 128), 128, 0, s>>>(C.Einv.get(), C.nE, k0, b, Pk.get(), X.get());
+        k_gj_rows<<<grid_for(C.nE * b, T), T, 0, s>>>(C.Einv.get(), C.nE, k0, b, Pk.get(), X.get(), RT.get());
+        k_gj_rows_store<<<grid_for(C.nE * b, T), T, 0, s>>>(C.Einv.get(), C.nE, k0, b, RT.get());
         k_gj_cols<<<grid_for(C.nE * b, T), T, 0, s>>>(C.Einv.get(), C.nE, k0, b, Pk.get(), X.get());
     }
     CR_CHECK_LAUNCH();
