@@ -448,6 +448,7 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
     C.part.alloc(std::max<int64_t>(C.nchunk, 1) * NV, s);
     C.c.alloc(C.nE, s);
     C.y.alloc(C.nE, s);
+    C.gpart.alloc((size_t)kSMs * 32, s);
     C.Einv.alloc(C.nE * C.nE, s);
     C.Einv.zero(s);
     // E = Z^t G Z by colours

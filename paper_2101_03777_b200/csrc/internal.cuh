@@ -203,6 +203,7 @@ struct CoarseOp {
     cr::DevBuf<int32_t> perm;
     cr::DevBuf<int64_t> chunk_start, cell_chunk;
     cr::DevBuf<double> part, c, y, Einv;
+    cr::DevBuf<double> gpart;    // block partials of the coarse GEMV (its own: it runs concurrently)
     cr::CoarseView view() const {
         return cr::CoarseView{g, fx.get(), fa.get(), perm.get(), chunk_start.get(), cell_chunk.get(), nE};
     }

@@ -35,6 +35,7 @@ struct KState {
     unsigned tickets[8];
     double red[4];       // distributed mode: this rank's reduction values, allreduced in place
     double qc;           // two-level: c^t E^{-1} c of the coarse correction (global)
+    double qf;           // two-level: r^t M_patch^{-1} r of the patch part (global)
     double rho, alpha, beta, pq, rr, bb, tol2;
     // MINRES
     double gamma, gamma_old, delta, eta, eta0, c, c_old, s, s_old;
@@ -61,7 +62,12 @@ struct SolverWork {
     int graph_key = -1;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     cudaStream_t cap = nullptr;   // private capture stream
+    cudaStream_t side = nullptr;  // two-level: the coarse path runs here, concurrently with the patches
+    cudaEvent_t fork = nullptr, join = nullptr;
     ~SolverWork() {
+        if (side) cudaStreamDestroy(side);
+        if (fork) cudaEventDestroy(fork);
+        if (join) cudaEventDestroy(join);
         if (cap) cudaStreamDestroy(cap);
         if (graph) cudaGraphExecDestroy(graph);
         if (hst) cudaFreeHost(hst);
@@ -109,7 +115,7 @@ __device__ __forceinline__ void stv(double *a, int64_t r, const double (&v)[D]) 
 // Applied by the last block of a reduction on one GPU, or by k_fin after the allreduce of
 // the per-rank values in st->red on several (the same code either way).
 enum FinKind { FIN_BB, FIN_RR, FIN_PCG_INIT, FIN_PQ, FIN_UPD_PC, FIN_UPD_R, FIN_AFW_PCG_INIT, FIN_AFW_PCG,
-               FIN_AFW2_PCG_INIT, FIN_AFW2_PCG };
+               FIN_AFW2_PCG_INIT, FIN_AFW2_PCG, FIN_AFW2_QF_INIT, FIN_AFW2_QF, FIN_PQ2 };
 
 __device__ __forceinline__ void apply_fin(KState *st, int kind, const double *t, double rtol) {
     switch (kind) {
@@ -158,6 +164,21 @@ __device__ __forceinline__ void apply_fin(KState *st, int kind, const double *t,
             st->beta = (t[0] + st->qc) / st->rho;
             st->rho = t[0] + st->qc;
             break;
+        // two-level with the coarse path on a second stream: the patch and coarse quadratic forms
+        // land in qf / qc; the direction update forms beta = (qf + qc) / rho itself and the next
+        // p.q reduction makes rho = qf + qc current (FIN_PQ2)
+        case FIN_AFW2_QF_INIT:
+            st->qf = t[0];
+            st->tol2 = rtol * rtol * st->bb;
+            st->flag = (st->rr <= st->tol2) ? FLAG_CONV : FLAG_RUN;
+            break;
+        case FIN_AFW2_QF: st->qf = t[0]; break;
+        case FIN_PQ2:
+            st->rho = st->qf + st->qc;
+            st->pq = t[0];
+            if (!(t[0] > 0.0)) st->flag = FLAG_BREAK;
+            else st->alpha = st->rho / t[0];
+            break;
     }
 }
 
@@ -174,7 +195,7 @@ __device__ __forceinline__ void fin_or_store(KState *st, int kind, const double 
 // distributed mode: the recurrence after the allreduce (a converged state stays frozen)
 __global__ void k_fin(KState *st, int kind, double rtol) {
     const bool init = kind == FIN_BB || kind == FIN_RR || kind == FIN_PCG_INIT || kind == FIN_AFW_PCG_INIT ||
-                      kind == FIN_AFW2_PCG_INIT;
+                      kind == FIN_AFW2_PCG_INIT || kind == FIN_AFW2_QF_INIT;
     if (!init && st->flag != FLAG_RUN) return;
     apply_fin(st, kind, st->red, rtol);
 }
@@ -192,12 +213,12 @@ __global__ void k_halo_pack(int64_t n, const int32_t *rows, const double *x, dou
 // q += G_mf x over this rank's cells (q pre-zeroed); REDUCE: p.q -> alpha (FIN_PQ)
 template <int D, bool REDUCE>
 __global__ void __launch_bounds__(kT) k_mf_spmv(MfView M, const double *x, double *q, int64_t nown, KState *st,
-                                                double *partials, int dist) {
+                                                double *partials, int dist, int pqkind) {
     if (REDUCE && st->flag != FLAG_RUN) return;
     double acc[1] = {0.0};
     GRID_STRIDE(t, M.ncells) acc[0] += mf_cell<D>(M, t, x, q, nown);
     if (REDUCE)
-        reduce_and_finish<1>(acc, partials, &st->tickets[1], [&](double *t) { fin_or_store<1>(st, FIN_PQ, t, 0.0, dist); });
+        reduce_and_finish<1>(acc, partials, &st->tickets[1], [&](double *t) { fin_or_store<1>(st, pqkind, t, 0.0, dist); });
 }
 
 // r = b - q, |r|^2 (FIN_RR)
@@ -255,7 +276,8 @@ __global__ void __launch_bounds__(kT) k_pcg_init(int64_t nrows, const double *b,
 }
 
 template <int D>
-__global__ void __launch_bounds__(kT) k_pcg_spmv(EllView<D> G, const double *p, double *q, KState *st, double *partials, int dist) {
+__global__ void __launch_bounds__(kT) k_pcg_spmv(EllView<D> G, const double *p, double *q, KState *st, double *partials, int dist,
+                                                int pqkind = FIN_PQ) {
     if (st->flag != FLAG_RUN) return;
     double acc[1] = {0.0};
     GRID_STRIDE(row, G.nrows) {
@@ -267,7 +289,7 @@ __global__ void __launch_bounds__(kT) k_pcg_spmv(EllView<D> G, const double *p, 
             acc[0] += p[row * D + i] * y[i];
         }
     }
-    reduce_and_finish<1>(acc, partials, &st->tickets[1], [&](double *t) { fin_or_store<1>(st, FIN_PQ, t, 0.0, dist); });
+    reduce_and_finish<1>(acc, partials, &st->tickets[1], [&](double *t) { fin_or_store<1>(st, pqkind, t, 0.0, dist); });
 }
 
 template <int D, int PREC>
@@ -530,9 +552,9 @@ __global__ void __launch_bounds__(kT) k_afw_apply(AfwView A, const double *r, do
         } else if (WHAT == AFW_PCG) {
             fin_or_store<1>(st, FIN_AFW_PCG, t, rtol, dist);
         } else if (WHAT == AFW_PCG2_INIT) {
-            fin_or_store<1>(st, FIN_AFW2_PCG_INIT, t, rtol, dist);
+            fin_or_store<1>(st, FIN_AFW2_QF_INIT, t, rtol, dist);
         } else if (WHAT == AFW_PCG2) {
-            fin_or_store<1>(st, FIN_AFW2_PCG, t, rtol, dist);
+            fin_or_store<1>(st, FIN_AFW2_QF, t, rtol, dist);
         } else if (WHAT == AFW_MINRES_INIT) {
             minres_start(st, t[0]);
         } else {
@@ -646,9 +668,10 @@ __global__ void __launch_bounds__(kT) k_pcg_pdir_afw(int64_t nrows, double *__re
 // two-level: p = (sum of the slot contributions) + Z y + beta p
 template <int D, int SLOTS>
 __global__ void __launch_bounds__(kT) k_pcg_pdir_afw2(int64_t nrows, double *__restrict__ p, const double *__restrict__ zs,
-                                                      CoarseView C, const double *__restrict__ y, const KState *st) {
+                                                      CoarseView C, const double *__restrict__ y, const KState *st,
+                                                      int first) {
     if (st->flag != FLAG_RUN) return;
-    const double beta = st->beta;
+    const double beta = first ? 0.0 : (st->qf + st->qc) / st->rho;
     GRID_STRIDE(row, nrows) {
         double z[D], zc[D];
         afw_sum<D, SLOTS>(zs, row, z);
@@ -990,6 +1013,9 @@ static void ensure_work(cr_hybrid_s *h, cudaStream_t s) {
     CR_CUDA(cudaEventCreate(&w->e0));
     CR_CUDA(cudaEventCreate(&w->e1));
     CR_CUDA(cudaStreamCreateWithFlags(&w->cap, cudaStreamNonBlocking));
+    CR_CUDA(cudaStreamCreateWithFlags(&w->side, cudaStreamNonBlocking));
+    CR_CUDA(cudaEventCreateWithFlags(&w->fork, cudaEventDisableTiming));
+    CR_CUDA(cudaEventCreateWithFlags(&w->join, cudaEventDisableTiming));
 }
 
 struct Launcher {
@@ -1042,13 +1068,13 @@ static MfView mf_view(const cr_hybrid_s *h) {
 
 // q = G_mf x (q zeroed first); REDUCE also reduces x.q -> alpha
 template <int D, bool REDUCE>
-static void mf_apply(Launcher &L, cudaStream_t ks, const double *x, double *q, double rtol) {
+static void mf_apply(Launcher &L, cudaStream_t ks, const double *x, double *q, double rtol, int pqkind = FIN_PQ) {
     CR_CUDA(cudaMemsetAsync(q, 0, L.N * sizeof(double), ks));
     k_mf_spmv<D, REDUCE><<<occ_grid(k_mf_spmv<D, REDUCE>, kT, L.h->mf.ncells), kT, 0, ks>>>(mf_view<D>(L.h), x, q, L.nrows, L.w->st.get(),
-                                                                      L.w->partials.get(), L.dist);
+                                                                      L.w->partials.get(), L.dist, pqkind);
     CR_CHECK_LAUNCH();
     ++L.launches;
-    if (REDUCE) L.reduced(ks, 1, FIN_PQ, rtol);
+    if (REDUCE) L.reduced(ks, 1, pqkind, rtol);
 }
 
 template <int D>
@@ -1100,8 +1126,8 @@ static void launch_afw(Launcher &L, cudaStream_t ks, const double *r, double *zs
     ++L.launches;
     if (WHAT == AFW_PCG_INIT) L.reduced(ks, 1, FIN_AFW_PCG_INIT, rtol);
     if (WHAT == AFW_PCG) L.reduced(ks, 1, FIN_AFW_PCG, rtol);
-    if (WHAT == AFW_PCG2_INIT) L.reduced(ks, 1, FIN_AFW2_PCG_INIT, rtol);
-    if (WHAT == AFW_PCG2) L.reduced(ks, 1, FIN_AFW2_PCG, rtol);
+    if (WHAT == AFW_PCG2_INIT) L.reduced(ks, 1, FIN_AFW2_QF_INIT, rtol);
+    if (WHAT == AFW_PCG2) L.reduced(ks, 1, FIN_AFW2_QF, rtol);
 }
 
 template <class Body, class Done>
@@ -1292,15 +1318,31 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         double *zs = w->zs.get();
         const CoarseView CV = h->coarse.view();
         double *yc = h->coarse.y.get();
-        auto coarse = [&](cudaStream_t q) {
-            coarse_restrict_solve(h, w->r.get(), &st->qc, part, &st->tickets[4], q);
+        // coarse path (restriction, gather, E^-1 GEMV) forked onto a side stream so it overlaps the
+        // patch solves; joined before the direction update.  Partitioned runs stay on one stream
+        // (NCCL collectives of one communicator must not be reordered between ranks).
+        const bool fork = !L.dist;
+        double *cpart = h->coarse.gpart.get();
+        auto coarse_begin = [&](cudaStream_t q) {
+            cudaStream_t cs = q;
+            if (fork) {
+                CR_CUDA(cudaEventRecord(w->fork, q));
+                CR_CUDA(cudaStreamWaitEvent(w->side, w->fork, 0));
+                cs = w->side;
+            }
+            coarse_restrict_solve(h, w->r.get(), &st->qc, fork ? cpart : part, &st->tickets[4], cs);
+            if (fork) CR_CUDA(cudaEventRecord(w->join, w->side));
             L.launches += 3;
+        };
+        auto coarse_end = [&](cudaStream_t q) {
+            if (fork) CR_CUDA(cudaStreamWaitEvent(q, w->join, 0));
         };
         auto init = [&]() {
             true_residual<D>(L, x, w->r.get());
-            coarse(s);
+            coarse_begin(s);
             launch_afw<D, AFW_PCG2_INIT>(L, s, w->r.get(), zs, rtol);
-            k_pcg_pdir_afw2<D, SLOTS><<<L.grid_rows, kT, 0, s>>>(nrows, w->p.get(), zs, CV, yc, st);
+            coarse_end(s);
+            k_pcg_pdir_afw2<D, SLOTS><<<L.grid_rows, kT, 0, s>>>(nrows, w->p.get(), zs, CV, yc, st, 1);
             CR_CHECK_LAUNCH();
             ++L.launches;
         };
@@ -1311,18 +1353,20 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
             auto body = [&](int) {
                 L.halo(ks, w->p.get());
                 if (L.mf) {
-                    mf_apply<D, true>(L, ks, w->p.get(), w->q.get(), rtol);
+                    mf_apply<D, true>(L, ks, w->p.get(), w->q.get(), rtol, FIN_PQ2);
                 } else {
-                    k_pcg_spmv<D><<<occ_grid(k_pcg_spmv<D>, kT, L.nrows), kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part, L.dist);
+                    k_pcg_spmv<D><<<occ_grid(k_pcg_spmv<D>, kT, L.nrows), kT, 0, ks>>>(ell<D>(h), w->p.get(), w->q.get(), st, part,
+                                                                                     L.dist, FIN_PQ2);
                     CR_CHECK_LAUNCH();
-                    L.reduced(ks, 1, FIN_PQ, rtol);
+                    L.reduced(ks, 1, FIN_PQ2, rtol);
                 }
                 k_pcg_update_r<<<occ_grid(k_pcg_update_r, kT, L.N / 2), kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), st, part, L.dist);
                 CR_CHECK_LAUNCH();
                 L.reduced(ks, 1, FIN_UPD_R, rtol);
-                coarse(ks);
+                coarse_begin(ks);
                 launch_afw<D, AFW_PCG2>(L, ks, w->r.get(), zs, rtol);
-                k_pcg_pdir_afw2<D, SLOTS><<<occ_grid(k_pcg_pdir_afw2<D, SLOTS>, kT, nrows), kT, 0, ks>>>(nrows, w->p.get(), zs, CV, yc, st);
+                coarse_end(ks);
+                k_pcg_pdir_afw2<D, SLOTS><<<occ_grid(k_pcg_pdir_afw2<D, SLOTS>, kT, nrows), kT, 0, ks>>>(nrows, w->p.get(), zs, CV, yc, st, 0);
                 CR_CHECK_LAUNCH();
             };
             int64_t it0 = w->hst->iters;
@@ -1582,7 +1626,7 @@ static void apply_precond_t(cr_hybrid_s *h, int method, const double *r, double 
             launch_afw<D, AFW_PCG_INIT>(L, s, r, w->zs.get(), 1e-10);
             CR_CUDA(cudaMemsetAsync(w->st.get(), 0, sizeof(KState), s));   // flag RUN, beta 0: p = z
             k_pcg_pdir_afw2<D, SLOTS><<<grid, kT, 0, s>>>(nrows, z, w->zs.get(), h->coarse.view(), h->coarse.y.get(),
-                                                         w->st.get());
+                                                         w->st.get(), 1);
             break;
         }
         case CR_PCG_AFW:
