@@ -333,6 +333,9 @@ def main():
     repj = P.cr_solve(hyb, Wj, "pcg", rtol=cfg.rtol, check_every=64)
 
     # ---- e2e through the public API from HOST buffers (pinned host -> device -> host)
+    # (the handles of the timed steps are released first, as a caller's next solve would)
+    nc_full, ndim = mesh.nc, mesh.dim
+    del out, hyb, mesh, Wa, Wj, x, y
     e2e = None
     if not args.no_e2e:
         torch.cuda.synchronize()
@@ -354,7 +357,6 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s = oracle_sample()
-        nc_full = mesh.nc
         v = oracle_extrapolate(s, nc_full, nnz, repj["iterations"])
         cpu = {"value": v, "unit": "s", "cores": 1, "kind": "oracle",
                "sample": (f"oracle on configs[1]-family mesh n={s['n']} ({s['nc']} cells): mesh+hybridise+recover "
@@ -364,8 +366,8 @@ def main():
 
     launches = rep["kernel_launches"] + 25     # mesh (sort/scan/geometry ~15), hybridise 1, recover 3, copies
     launches += 12   # patch build (pairs, sort, scans, setup)
-    nE_ = 4 * (COARSE + 1) ** 2 if mesh.dim == 2 else 9 * (COARSE + 1) ** 3
-    launches += (5 ** mesh.dim) * mesh.dim ** 2 * 5 + 5 * ((nE_ + 31) // 32) + 10   # coarse E assembly + inversion
+    nE_ = 4 * (COARSE + 1) ** 2 if ndim == 2 else 9 * (COARSE + 1) ** 3
+    launches += (5 ** ndim) * ndim ** 2 * 5 + 5 * ((nE_ + 31) // 32) + 10   # coarse E assembly + inversion
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,

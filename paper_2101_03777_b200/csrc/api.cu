@@ -219,7 +219,8 @@ cr_status cr_hybrid_mf_info(cr_hybrid h, int64_t *ncells, int64_t *bytes) {
     const bool b = h->mf.built;
     if (ncells) *ncells = b ? h->mf.ncells : 0;
     if (bytes)
-        *bytes = b ? (int64_t)(h->mf.v.n * sizeof(double) + h->mf.ids.n * sizeof(int32_t) + h->mf.sg.n) : 0;
+        *bytes = b ? (int64_t)(h->mf.v.n * sizeof(double) + h->mf.ids.n * sizeof(int32_t) + h->mf.sg.n + h->mf.nb.n)
+                   : 0;
     CR_API_END
 }
 

@@ -53,19 +53,18 @@ __global__ void k_coarse_faces(const int32_t *dof_face, int64_t row0, int64_t nr
 }
 
 // partial restriction of one chunk: the 2^D nodes of its coarse cell x D^2 tensor components.
-// 2D: one thread per row with all 16 accumulators; 3D: the 2^D = 8 corner nodes of a row are
-// split over 8 consecutive threads (9 accumulators each).  Rows are read 4 at a time per thread
-// (independent loads in flight); lanes of the same corner are reduced by shuffles, then across
-// warps in shared memory (fixed trees: deterministic).
+// One thread per row with all 2^D D^2 accumulators (16 in 2D, 72 in 3D); rows are read 4 at a time
+// per thread (independent loads in flight); warp shuffles then shared memory reduce the block
+// (fixed trees: deterministic).
 template <int D>
 __global__ void __launch_bounds__(256) k_coarse_restrict(CoarseView C, const double *r, double *part) {
     constexpr int NN = 1 << D, DD = D * D, NV = NN * DD;
-    constexpr int TPR = D == 2 ? 1 : NN;            // threads per row
-    constexpr int NA = D == 2 ? NV : DD;            // accumulators per thread
+    constexpr int TPR = 1;                           // threads per row
+    constexpr int NA = NV;                           // accumulators per thread
     constexpr int SL = 256 / TPR, U = 4;
     const int64_t ch = blockIdx.x;
     const int64_t b = C.chunk_start[ch], e = C.chunk_start[ch + 1];
-    const int n3 = threadIdx.x % TPR, slot = threadIdx.x / TPR;
+    const int slot = threadIdx.x / TPR;
     double acc[NA];
 #pragma unroll
     for (int v = 0; v < NA; ++v) acc[v] = 0.0;
@@ -92,19 +91,18 @@ __global__ void __launch_bounds__(256) k_coarse_restrict(CoarseView C, const dou
             int ic[D];
             float xi[D];
             coarse_locate<D>(C.g, xv[u], ic, xi);
+            double ar[DD];   // r^(k) a^(l)
 #pragma unroll
-            for (int nn = 0; nn < (D == 2 ? NN : 1); ++nn) {
-                const int n = D == 2 ? nn : n3;
+            for (int k = 0; k < D; ++k)
+#pragma unroll
+                for (int l = 0; l < D; ++l) ar[k * D + l] = (double)av[u][l] * rv[u][k];
+#pragma unroll
+            for (int n = 0; n < NN; ++n) {
                 double wn = 1.0;
 #pragma unroll
                 for (int i = 0; i < D; ++i) wn *= ((n >> i) & 1) ? (double)xi[i] : 1.0 - (double)xi[i];
 #pragma unroll
-                for (int k = 0; k < D; ++k)
-#pragma unroll
-                    for (int l = 0; l < D; ++l) {
-                        const int v = (D == 2 ? nn * DD : 0) + k * D + l;
-                        acc[v] = fma(wn * (double)av[u][l], rv[u][k], acc[v]);
-                    }
+                for (int v = 0; v < DD; ++v) acc[n * DD + v] = fma(wn, ar[v], acc[n * DD + v]);
             }
         }
     }
@@ -115,7 +113,7 @@ __global__ void __launch_bounds__(256) k_coarse_restrict(CoarseView C, const dou
         double x = acc[v];
 #pragma unroll
         for (int o = 16; o >= TPR; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if (lane < TPR) sh[warp][(D == 2 ? 0 : lane * DD) + v] = x;
+        if (lane < TPR) sh[warp][v] = x;
     }
     __syncthreads();
     for (int v = threadIdx.x; v < NV; v += blockDim.x) {

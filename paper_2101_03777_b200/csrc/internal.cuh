@@ -216,6 +216,7 @@ struct MfOp {
     cr::DevBuf<int32_t> ids;
     cr::DevBuf<uint8_t> sg;
     cr::DevBuf<double> v;
+    cr::DevBuf<uint8_t> nb;      // in-warp face partners (mf.cuh)
 };
 
 struct cr_hybrid_s {

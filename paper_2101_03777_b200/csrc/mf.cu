@@ -85,6 +85,41 @@ __global__ void __launch_bounds__(128) k_mf_build(MeshView mv, ProbView p, const
     }
 }
 
+__global__ void k_mf_slot(const int32_t *list, int64_t n, int32_t *slot) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        slot[list[t]] = (int32_t)t;
+}
+
+// nb code of (slot t, local face l): the other cell of the face, if stored in the same 32-slot slice
+template <int D>
+__global__ void k_mf_partners(MeshView mv, const int32_t *list, int64_t ncell, int64_t npad, const int32_t *slot,
+                              uint8_t *nb) {
+    constexpr int NF = D + 1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < npad; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t slice = t >> 5;
+        const int lane = (int)(t & 31);
+        for (int l = 0; l < NF; ++l) {
+            uint8_t code = 0;
+            if (t < ncell) {
+                const int64_t K = list[t];
+                const int64_t f = mv.cell_faces[K * NF + l];
+                const int64_t c0 = mv.face_cells[2 * f], c1 = mv.face_cells[2 * f + 1];
+                if (c1 >= 0 && mv.face_dof[f] >= 0) {
+                    const int64_t L = (c0 == K) ? c1 : c0;
+                    const int64_t tL = slot[L];
+                    if (tL >= 0 && (tL >> 5) == slice) {
+                        int lp = 0;
+                        for (int q = 0; q < NF; ++q)
+                            if (mv.cell_faces[L * NF + q] == (int32_t)f) lp = q;
+                        code = (uint8_t)(0x80u | ((unsigned)lp << 5) | (unsigned)(tL & 31));
+                    }
+                }
+            }
+            nb[slice * (NF * 32) + l * 32 + lane] = code;
+        }
+    }
+}
+
 template <int D>
 static void build_mf_t(cr_hybrid_s *h, cudaStream_t s) {
     using LY = MfLayout<D>;
@@ -123,6 +158,15 @@ static void build_mf_t(cr_hybrid_s *h, cudaStream_t s) {
     k_mf_build<D><<<grid_for(nsl * 32, 128, 16), 128, 0, s>>>(mv, p, list.get(), ncell,
                                                                h->part.on ? h->part.g2l.get() : nullptr, M.ids.get(),
                                                                M.sg.get(), M.v.get(), err.get());
+    CR_CHECK_LAUNCH();
+    // in-warp face partners
+    DevBuf<int32_t> slot;
+    slot.alloc(nc, s);
+    slot.fill_bytes(0xFF, s);
+    k_mf_slot<<<grid_for(ncell, T), T, 0, s>>>(list.get(), ncell, slot.get());
+    CR_CHECK_LAUNCH();
+    M.nb.alloc(nsl * 32 * LY::NF, s);
+    k_mf_partners<D><<<grid_for(nsl * 32, T), T, 0, s>>>(mv, list.get(), ncell, nsl * 32, slot.get(), M.nb.get());
     CR_CHECK_LAUNCH();
     int he = 0;
     CR_CUDA(cudaMemcpyAsync(&he, err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -29,12 +29,16 @@ struct MfView {
     const int32_t *ids;
     const uint8_t *sg;
     const double *v;
+    const uint8_t *nb;  // [slice][l][lane]: 0x80 | l' << 5 | lane' when the other cell of face l is in
+                        // the same 32-cell slice (as its local face l'), else 0
     int64_t ncells;     // cells processed (padded to slices of 32 with ids = -1)
 };
 
-// y_K = G_K x_K scattered into q (q pre-zeroed: exactly two cells add into each interior face, so
-// 0 + a + b rounds the same in either order -> deterministic).  Returns this cell's share of
-// p^t G p counted on rows < nown (owned rows).
+// y_K = G_K x_K scattered into q (q pre-zeroed).  A face whose two cells sit in the same warp
+// (32 consecutive cells: most faces inside a structured row of squares / a Kuhn cube) is summed
+// in registers through shuffles and stored once by the lower cell; the others get one atomicAdd
+// from each side.  Either way exactly two contributions meet, and 0 + a + b rounds the same in
+// either order -> deterministic.  Returns this cell's share of p^t G p on rows < nown (owned).
 template <int D>
 __device__ __forceinline__ double mf_cell(const MfView &M, int64_t t, const double *__restrict__ x,
                                           double *__restrict__ q, int64_t nown) {
@@ -84,12 +88,16 @@ __device__ __forceinline__ double mf_cell(const MfView &M, int64_t t, const doub
 #pragma unroll
         for (int l = 0; l < NF; ++l) pu = fma(u[i][l], xs[i][l], pu);
     double quad = 0.0;
+    unsigned nbc[NF];
+#pragma unroll
+    for (int a = 0; a < NF; ++a) nbc[a] = M.nb[slice * (NF * 32) + a * 32 + lane];
 #pragma unroll
     for (int i = 0; i < D; ++i) {
         double sum = 0.0;
 #pragma unroll
         for (int l = 0; l < NF; ++l) sum += xs[i][l];
         const double cb = c * sum;
+        double out[NF];
 #pragma unroll
         for (int a = 0; a < NF; ++a) {
             double y = cb;
@@ -99,9 +107,29 @@ __device__ __forceinline__ double mf_cell(const MfView &M, int64_t t, const doub
                 y = fma(T[e], xs[i][b], y);
             }
             y = fma(-u[i][a], pu, y);
-            if (id[a] >= 0 && id[a] < nown) {
-                quad = fma(xs[i][a], y, quad);
-                atomicAdd(q + (int64_t)id[a] * D + i, cs[a] * y);
+            if (id[a] >= 0 && id[a] < nown) quad = fma(xs[i][a], y, quad);
+            out[a] = cs[a] * y;
+        }
+        // the partner's contribution to each in-warp shared face (round b2 publishes face b2)
+        double part[NF];
+#pragma unroll
+        for (int a = 0; a < NF; ++a) part[a] = 0.0;
+#pragma unroll
+        for (int b2 = 0; b2 < NF; ++b2)
+#pragma unroll
+            for (int a = 0; a < NF; ++a) {
+                const int src = (nbc[a] & 0x80u) ? (int)(nbc[a] & 31u) : lane;
+                const double v = __shfl_sync(0xffffffffu, out[b2], src);
+                if ((nbc[a] & 0x80u) && (int)((nbc[a] >> 5) & 3u) == b2) part[a] = v;
+            }
+#pragma unroll
+        for (int a = 0; a < NF; ++a) {
+            if (id[a] < 0 || id[a] >= nown) continue;
+            double *dst = q + (int64_t)id[a] * D + i;
+            if (nbc[a] & 0x80u) {
+                if ((int)(nbc[a] & 31u) > lane) *dst = out[a] + part[a];   // lower cell stores the pair
+            } else {
+                atomicAdd(dst, out[a]);
             }
         }
     }

@@ -1063,7 +1063,7 @@ static void read_state(SolverWork *w, cudaStream_t s) {
 
 template <int D>
 static MfView mf_view(const cr_hybrid_s *h) {
-    return MfView{h->mf.ids.get(), h->mf.sg.get(), h->mf.v.get(), h->mf.ncells};
+    return MfView{h->mf.ids.get(), h->mf.sg.get(), h->mf.v.get(), h->mf.nb.get(), h->mf.ncells};
 }
 
 // q = G_mf x (q zeroed first); REDUCE also reduces x.q -> alpha
