@@ -5,9 +5,31 @@
 
 #include "internal.cuh"
 
+#include <chrono>
+#include <cstdlib>
+
 namespace cr {
 static thread_local std::string g_last_error;
 void set_last_error(const std::string &m) { g_last_error = m; }
+
+static double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+Trace::Trace(cudaStream_t st) : s(st) {
+    const char *e = std::getenv("CR_TRACE");
+    on = e && e[0] == '1';
+    if (on) {
+        cudaStreamSynchronize(s);
+        t0 = now_s();
+    }
+}
+void Trace::mark(const char *what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const double t = now_s();
+    std::fprintf(stderr, "[cr_trace] %-28s %9.3f ms\n", what, (t - t0) * 1e3);
+    t0 = t;
+}
 }  // namespace cr
 
 // Keep freed stream-ordered memory in the device's default pool (no trim to the OS at every

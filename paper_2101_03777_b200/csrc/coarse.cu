@@ -363,6 +363,7 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
     const int64_t nrows = h->G.nrows, row0 = h->part.on ? h->part.row0 : 0;
     const int T = 256;
     C.g.H = H;
+    Trace tr(s);
     {
         // min / max of the vertex coordinates by CUB
         DevBuf<double> lo, hi;
@@ -443,6 +444,7 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
         CR_CUDA(cudaMemcpyAsync(C.cell_chunk.get(), cell_chunk.data(), cell_chunk.size() * 8, cudaMemcpyHostToDevice, s));
         CR_CUDA(cudaStreamSynchronize(s));
     }
+    tr.mark("coarse: rows, sort, chunks");
     C.part.alloc(std::max<int64_t>(C.nchunk, 1) * NV, s);
     C.c.alloc(C.nE, s);
     C.y.alloc(C.nE, s);
@@ -471,6 +473,7 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
                 k_coarse_scatterE<D><<<grid_for(C.nE, T), T, 0, s>>>(C.nE, H, colour, k, l, C.c.get(), C.Einv.get());
                 CR_CHECK_LAUNCH();
             }
+    tr.mark("coarse: E = Z^t G Z");
     k_symmetrize<<<grid_for(C.nE * C.nE, T, 64), T, 0, s>>>(C.Einv.get(), C.nE);
     CR_CHECK_LAUNCH();
     DevBuf<double> Pk, X, RT;
@@ -494,6 +497,7 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
     int hb = 0;
     CR_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     CR_CUDA(cudaStreamSynchronize(s));
+    tr.mark("coarse: E^-1 (Gauss-Jordan)");
     CR_REQUIRE(hb == 0, CR_ERR_SINGULAR_LOCAL, "coarse matrix Z^t G Z is not positive definite");
     C.built = H;
 }

@@ -120,6 +120,15 @@ inline int grid_for(int64_t work, int threads, int max_blocks_per_sm = 8) {
     return (int)b;
 }
 
+// CR_TRACE=1: host wall time of setup phases on stderr (synchronises the stream at each mark)
+struct Trace {
+    bool on = false;
+    double t0 = 0.0;
+    cudaStream_t s = nullptr;
+    explicit Trace(cudaStream_t st);
+    void mark(const char *what);
+};
+
 }  // namespace cr
 
 // ------------------------------------------------------------------ handles

@@ -1182,7 +1182,9 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     CR_REQUIRE(!L.dist || pcg_family, CR_ERR_INVALID_ARG, "a partitioned (multi-GPU) solve supports the PCG methods only");
     L.mf = o.matrix_free ? 1 : 0;
     CR_REQUIRE(!L.mf || pcg_family, CR_ERR_INVALID_ARG, "matrix_free supports the PCG methods only");
+    Trace trc(s);
     if (L.mf) build_mf(h, s);
+    trc.mark("matrix-free factors");
     const int64_t N = w->N, nrows = L.nrows;
     const double rtol = o.rtol > 0 ? o.rtol : 1e-10;
     const int64_t max_iter = o.max_iter > 0 ? o.max_iter : 10000000;
@@ -1308,12 +1310,14 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     } else if (method == CR_PCG_AFW2) {
         constexpr int SLOTS = D == 2 ? 2 : 3;
         build_afw(h, AFW_SPD, s);
+        trc.mark("patch preconditioner");
         const int H = o.coarse > 0 ? o.coarse : (D == 2 ? 16 : 8);
         build_coarse(h, H, [&](const double *z, double *Y) {
             L.halo(s, const_cast<double *>(z));
             if (L.mf) mf_apply<D, false>(L, s, z, Y, 0.0);
             else spmv(h->G, z, Y, s);
         }, s);
+        trc.mark("coarse space (E, E^-1)");
         if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
         double *zs = w->zs.get();
         const CoarseView CV = h->coarse.view();
@@ -1348,7 +1352,9 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         };
         init();
         read_state(w, s);
+        trc.mark("initial residual");
         if (w->hst->bb == 0.0) { CR_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), s)); }
+        bool first_replay = true;
         while (w->hst->flag == FLAG_RUN) {
             auto body = [&](int) {
                 L.halo(ks, w->p.get());
@@ -1373,6 +1379,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
             graph_loop(L, ks, method * 100000 + L.mf * 50000 + kk, kk, body, [&]() {
                 return w->hst->flag != FLAG_RUN || w->hst->iters >= max_iter;
             });
+            if (first_replay) { trc.mark("iterations (incl. graph capture)"); first_replay = false; }
             int64_t dit = w->hst->iters - it0;
             L.launches += 7 * ((dit + kk - 1) / kk) * kk;
             L.spmvs += dit;
