@@ -16,8 +16,10 @@
 //        component i, entry e of B_p^{-1}: packed lower triangle (T = k(k+1)/2, symmetric
 //        modes) or row-major k x k (T = k^2, general mode)
 // A face belongs to exactly SLOTS patches (2 endpoints in 2D, 3 edges of a triangle in 3D);
-// slot s of face sigma receives patch s's contribution in zs[(dof*SLOTS + s)*D + i], and
-// consumers sum the SLOTS values in slot order, so the result is deterministic (no atomics).
+// slot s of face sigma receives patch s's contribution in zs[(s*D + i)*nrows + dof] (one array per
+// slot and component: a vertex's / edge's faces whose first vertex it is are consecutive dofs, so
+// half the writes are coalesced), and consumers sum the SLOTS values in slot order, so the result
+// is deterministic (no atomics).
 #pragma once
 #include <cstdint>
 
@@ -29,6 +31,7 @@ struct AfwView {
     const int32_t *ids;
     const double *vals;
     int64_t npatch;
+    int64_t nrows;   // block rows (zs stride)
 };
 
 // z-contributions of one patch for one velocity component: thread t of a launch covers slice
@@ -81,7 +84,7 @@ __device__ __forceinline__ double afw_patch_comp(const AfwView &A, int64_t t, co
     for (int j = 0; j < KMAX; ++j) {
         if (id[j] >= 0) {
             quad = fma(rv[j], y[j], quad);
-            zs[(int64_t)id[j] * D + i] = y[j];
+            zs[((int64_t)(id[j] % SLOTS) * D + i) * A.nrows + id[j] / SLOTS] = y[j];
         }
     }
     return quad;
@@ -89,13 +92,13 @@ __device__ __forceinline__ double afw_patch_comp(const AfwView &A, int64_t t, co
 
 // z[row] = sum_s zs[row, s] (slot order)
 template <int D, int SLOTS>
-__device__ __forceinline__ void afw_sum(const double *__restrict__ zs, int64_t row, double (&z)[D]) {
+__device__ __forceinline__ void afw_sum(const double *__restrict__ zs, int64_t nrows, int64_t row, double (&z)[D]) {
 #pragma unroll
-    for (int i = 0; i < D; ++i) z[i] = zs[(row * SLOTS) * D + i];
+    for (int i = 0; i < D; ++i) z[i] = zs[(int64_t)i * nrows + row];
 #pragma unroll
     for (int s = 1; s < SLOTS; ++s)
 #pragma unroll
-        for (int i = 0; i < D; ++i) z[i] += zs[(row * SLOTS + s) * D + i];
+        for (int i = 0; i < D; ++i) z[i] += zs[((int64_t)s * D + i) * nrows + row];
 }
 
 }  // namespace cr

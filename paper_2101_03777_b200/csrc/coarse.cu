@@ -16,6 +16,7 @@
 // Per iteration: restriction c = Z^t r (chunk partials, fixed-order gather: deterministic),
 // y = E^{-1} c and c^t y (dense GEMV), prolongation fused into the direction update.
 #include <cub/cub.cuh>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -27,6 +28,39 @@
 namespace cr {
 
 constexpr int kCH = 2048;   // rows per restriction chunk
+
+// cuBLAS DGEMM (a plain library GEMM) for the rank-32 updates of the coarse Gauss-Jordan; loaded
+// with dlopen (libcublas.so.12: the copy torch maps) so libcr loads without it on a CPU box.
+struct Blas {
+    void *h = nullptr, *handle = nullptr;
+    int (*Create)(void **) = nullptr;
+    int (*SetStream)(void *, cudaStream_t) = nullptr;
+    int (*Dgemm)(void *, int, int, int, int, int, const double *, const double *, int, const double *, int,
+                 const double *, double *, int) = nullptr;
+};
+static Blas &blas() {
+    static thread_local Blas b = [] {
+        Blas x;
+        x.h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+        if (!x.h) x.h = dlopen("libcublas.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!x.h) return x;
+        x.Create = (decltype(x.Create))dlsym(x.h, "cublasCreate_v2");
+        x.SetStream = (decltype(x.SetStream))dlsym(x.h, "cublasSetStream_v2");
+        x.Dgemm = (decltype(x.Dgemm))dlsym(x.h, "cublasDgemm_v2");
+        if (x.Create && x.Create(&x.handle) != 0) x.handle = nullptr;
+        return x;
+    }();
+    return b;
+}
+// column-major C(m x n) = alpha A(m x k) B(k x n) + beta C, no transposes
+static void dgemm(cudaStream_t s, int m, int n, int k, double alpha, const double *A, int lda, const double *B, int ldb,
+                  double beta, double *C, int ldc) {
+    Blas &b = blas();
+    CR_REQUIRE(b.handle && b.Dgemm, CR_ERR_CUDA, "cuBLAS (libcublas.so.12) could not be loaded");
+    b.SetStream(b.handle, s);
+    const int st = b.Dgemm(b.handle, 0, 0, m, n, k, &alpha, A, lda, B, ldb, &beta, C, ldc);
+    CR_REQUIRE(st == 0, CR_ERR_CUDA, "cublasDgemm failed");
+}
 
 template <int D>
 __global__ void k_coarse_faces(const int32_t *dof_face, int64_t row0, int64_t nrows, const int32_t *face_cells,
@@ -258,7 +292,7 @@ __global__ void k_symmetrize(double *E, int64_t n) {
 
 // Blocked Gauss-Jordan inversion in place, no pivoting (E SPD), pivot blocks of kGB:
 //   Pk = A_KK^{-1};  X = A_:K Pk;  A_IJ -= X_I A_KJ (I,J != K);  A_KJ = Pk A_KJ;  A_IK = -X_I;
-//   A_KK = Pk.
+//   A_KK = Pk.  The three products are cuBLAS DGEMMs (build_coarse_t).
 constexpr int kGB = 32;
 
 // Pk = inverse of the b x b diagonal block: one warp, lane i owns row i of [A | I] in shared
@@ -285,73 +319,31 @@ __global__ void __launch_bounds__(32) k_gj_diag(const double *E, int64_t n, int6
         for (int j = 0; j < b; ++j) Pk[i * b + j] = A[i][b + j];
 }
 
-// X[i][c] = sum_m A[i][k0+m] Pk[m][c]  (all rows i; block rows give Pk itself up to rounding)
-__global__ void k_gj_colpanel(const double *E, int64_t n, int64_t k0, int b, const double *Pk, double *X) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * b; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = t / b;
-        const int c = (int)(t - i * b);
-        double s = 0.0;
-        for (int m = 0; m < b; ++m) s = fma(E[i * n + k0 + m], Pk[m * b + c], s);
-        X[t] = s;
-    }
-}
-
-// rank-b update of every entry outside the pivot rows and columns; 64 x 64 tiles in shared memory
-__global__ void __launch_bounds__(256) k_gj_update(double *E, int64_t n, int64_t k0, int b, const double *X) {
-    __shared__ double Xs[64][kGB + 1];
-    __shared__ double Ys[kGB][64 + 1];
-    const int64_t i0 = (int64_t)blockIdx.y * 64, j0 = (int64_t)blockIdx.x * 64;
-    for (int t = threadIdx.x; t < 64 * kGB; t += blockDim.x) {
-        const int r = t / kGB, m = t % kGB;
-        Xs[r][m] = (i0 + r < n && m < b) ? X[(i0 + r) * b + m] : 0.0;
-        const int mm = t / 64, cc = t % 64;
-        Ys[mm][cc] = (mm < b && j0 + cc < n) ? E[(k0 + mm) * n + j0 + cc] : 0.0;
-    }
-    __syncthreads();
-    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;   // 16 x 16 threads, 4 x 4 entries each
-    double acc[4][4] = {};
-    for (int m = 0; m < b; ++m)
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) acc[a][c] = fma(Xs[ty * 4 + a][m], Ys[m][tx * 4 + c], acc[a][c]);
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int64_t i = i0 + ty * 4 + a, j = j0 + tx * 4 + c;
-            if (i >= n || j >= n) continue;
-            if ((i >= k0 && i < k0 + b) || (j >= k0 && j < k0 + b)) continue;
-            E[i * n + j] -= acc[a][c];
-        }
-}
-
-// pivot rows A_KJ = Pk A_KJ (J outside the block): one thread per (r, j); the column is read
-// by the b threads of the same j (cached)
-__global__ void k_gj_rows(double *E, int64_t n, int64_t k0, int b, const double *Pk, const double *X, double *tmp) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * b; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = t / b;
-        const int r = (int)(t - j * b);
-        if (j >= k0 && j < k0 + b) continue;
-        double s = 0.0;
-        for (int m = 0; m < b; ++m) s = fma(Pk[r * b + m], E[(k0 + m) * n + j], s);
-        tmp[t] = s;
-    }
-}
-__global__ void k_gj_rows_store(double *E, int64_t n, int64_t k0, int b, const double *tmp) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * b; t += (int64_t)gridDim.x * blockDim.x) {
-        const int r = (int)(t / n);
-        const int64_t j = t - (int64_t)r * n;
-        if (j >= k0 && j < k0 + b) continue;
-        E[(k0 + r) * n + j] = tmp[j * b + r];
-    }
-}
+// pivot columns A_IK = -X_I, A_KK = Pk
 __global__ void k_gj_cols(double *E, int64_t n, int64_t k0, int b, const double *Pk, const double *X) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * b; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = t / b;
         const int c = (int)(t - i * b);
         E[i * n + k0 + c] = (i >= k0 && i < k0 + b) ? Pk[(i - k0) * b + c] : -X[t];
     }
+}
+
+// first sorted position with coarse cell >= c (c = 0..ncc)
+__global__ void k_cell_starts(const uint32_t *cc_sorted, int64_t n, int64_t ncc, int64_t *cstart) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= ncc; c += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)cc_sorted[mid] < c) lo = mid + 1;
+            else hi = mid;
+        }
+        cstart[c] = lo;
+    }
+}
+
+__global__ void k_iota_u32(uint32_t *a, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = (uint32_t)i;
 }
 
 template <int D>
@@ -405,27 +397,25 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
                                                        C.fa.get(), cc.get());
     CR_CHECK_LAUNCH();
     {
-        std::vector<uint32_t> iota(nrows);
-        for (int64_t r = 0; r < nrows; ++r) iota[r] = (uint32_t)r;
-        CR_CUDA(cudaMemcpyAsync(idx.get(), iota.data(), nrows * 4, cudaMemcpyHostToDevice, s));
+        k_iota_u32<<<grid_for(nrows, T), T, 0, s>>>(idx.get(), nrows);
+        CR_CHECK_LAUNCH();
         int bits = 1;
         while (((int64_t)1 << bits) < ncc) ++bits;
         size_t tb = 0;
-        DevBuf<uint32_t> perm32;
-        perm32.alloc(nrows, s);
-        CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, cc.get(), cc2.get(), idx.get(), perm32.get(), (int)nrows, 0, bits, s));
+        CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, cc.get(), cc2.get(), idx.get(),
+                                                reinterpret_cast<uint32_t *>(C.perm.get()), (int)nrows, 0, bits, s));
         DevBuf<uint8_t> tmp;
         tmp.alloc(tb, s);
-        CR_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, cc.get(), cc2.get(), idx.get(), perm32.get(), (int)nrows, 0, bits, s));
-        // chunks on the host (counts per coarse cell)
-        std::vector<uint32_t> hcc(nrows);
-        std::vector<uint32_t> hperm(nrows);
-        CR_CUDA(cudaMemcpyAsync(hcc.data(), cc2.get(), nrows * 4, cudaMemcpyDeviceToHost, s));
-        CR_CUDA(cudaMemcpyAsync(hperm.data(), perm32.get(), nrows * 4, cudaMemcpyDeviceToHost, s));
+        CR_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, cc.get(), cc2.get(), idx.get(),
+                                                reinterpret_cast<uint32_t *>(C.perm.get()), (int)nrows, 0, bits, s));
+        // rows of each coarse cell (device), chunks of <= kCH rows (host: a few thousand entries)
+        DevBuf<int64_t> cs;
+        cs.alloc(ncc + 1, s);
+        k_cell_starts<<<grid_for(ncc + 1, T), T, 0, s>>>(cc2.get(), nrows, ncc, cs.get());
+        CR_CHECK_LAUNCH();
+        std::vector<int64_t> cstart(ncc + 1);
+        CR_CUDA(cudaMemcpyAsync(cstart.data(), cs.get(), (ncc + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         CR_CUDA(cudaStreamSynchronize(s));
-        std::vector<int64_t> cstart(ncc + 1, 0);
-        for (int64_t r = 0; r < nrows; ++r) cstart[hcc[r] + 1]++;
-        for (int64_t c = 0; c < ncc; ++c) cstart[c + 1] += cstart[c];
         std::vector<int64_t> chunk_start, cell_chunk(ncc + 1, 0);
         for (int64_t c = 0; c < ncc; ++c) {
             cell_chunk[c] = (int64_t)chunk_start.size();
@@ -434,17 +424,12 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
         cell_chunk[ncc] = (int64_t)chunk_start.size();
         chunk_start.push_back(nrows);
         C.nchunk = (int64_t)chunk_start.size() - 1;
-        std::vector<int32_t> p32(nrows);
-        for (int64_t r = 0; r < nrows; ++r) p32[r] = (int32_t)hperm[r];
-        C.perm.alloc(nrows, s);
         C.chunk_start.alloc(chunk_start.size(), s);
         C.cell_chunk.alloc(cell_chunk.size(), s);
-        CR_CUDA(cudaMemcpyAsync(C.perm.get(), p32.data(), nrows * 4, cudaMemcpyHostToDevice, s));
         CR_CUDA(cudaMemcpyAsync(C.chunk_start.get(), chunk_start.data(), chunk_start.size() * 8, cudaMemcpyHostToDevice, s));
         CR_CUDA(cudaMemcpyAsync(C.cell_chunk.get(), cell_chunk.data(), cell_chunk.size() * 8, cudaMemcpyHostToDevice, s));
         CR_CUDA(cudaStreamSynchronize(s));
     }
-    tr.mark("coarse: rows, sort, chunks");
     C.part.alloc(std::max<int64_t>(C.nchunk, 1) * NV, s);
     C.c.alloc(C.nE, s);
     C.y.alloc(C.nE, s);
@@ -476,22 +461,25 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
     tr.mark("coarse: E = Z^t G Z");
     k_symmetrize<<<grid_for(C.nE * C.nE, T, 64), T, 0, s>>>(C.Einv.get(), C.nE);
     CR_CHECK_LAUNCH();
-    DevBuf<double> Pk, X, RT;
+    // blocked Gauss-Jordan on the row-major E (a row-major M is the column-major M^t for cuBLAS):
+    //   Y = E[K,:];  X = E[:,K] Pk;  E -= X Y;  E[K,:] = Pk Y;  E[:,K] = -X, E[K,K] = Pk
+    DevBuf<double> Pk, X, Yb;
     Pk.alloc(kGB * kGB, s);
     X.alloc(C.nE * kGB, s);
-    RT.alloc(C.nE * kGB, s);
+    Yb.alloc(C.nE * kGB, s);
     DevBuf<int> bad;
     bad.alloc(1, s);
     bad.zero(s);
-    const unsigned tiles = (unsigned)((C.nE + 63) / 64);
+    const int n = (int)C.nE;
     for (int64_t k0 = 0; k0 < C.nE; k0 += kGB) {
         const int b = (int)std::min<int64_t>(kGB, C.nE - k0);
-        k_gj_diag<<<1, 32, 0, s>>>(C.Einv.get(), C.nE, k0, b, Pk.get(), bad.get());
-        k_gj_colpanel<<<grid_for(C.nE * b, T), T, 0, s>>>(C.Einv.get(), C.nE, k0, b, Pk.get(), X.get());
-        k_gj_update<<<dim3(tiles, tiles), 256, 0, s>>>(C.Einv.get(), C.nE, k0, b, X.get());
-        k_gj_rows<<<grid_for(C.nE * b, T), T, 0, s>>>(C.Einv.get(), C.nE, k0, b, Pk.get(), X.get(), RT.get());
-        k_gj_rows_store<<<grid_for(C.nE * b, T), T, 0, s>>>(C.Einv.get(), C.nE, k0, b, RT.get());
-        k_gj_cols<<<grid_for(C.nE * b, T), T, 0, s>>>(C.Einv.get(), C.nE, k0, b, Pk.get(), X.get());
+        double *Ep = C.Einv.get();
+        k_gj_diag<<<1, 32, 0, s>>>(Ep, C.nE, k0, b, Pk.get(), bad.get());
+        CR_CUDA(cudaMemcpyAsync(Yb.get(), Ep + k0 * C.nE, (size_t)b * C.nE * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        dgemm(s, b, n, b, 1.0, Pk.get(), b, Ep + k0, n, 0.0, X.get(), b);            // X^t = Pk^t E[:,K]^t
+        dgemm(s, n, n, b, -1.0, Yb.get(), n, X.get(), b, 1.0, Ep, n);                  // E^t -= Y^t X^t
+        dgemm(s, n, b, b, 1.0, Yb.get(), n, Pk.get(), b, 0.0, Ep + k0 * C.nE, n);     // E[K,:]^t = Y^t Pk^t
+        k_gj_cols<<<grid_for(C.nE * b, T), T, 0, s>>>(Ep, C.nE, k0, b, Pk.get(), X.get());
     }
     CR_CHECK_LAUNCH();
     int hb = 0;

@@ -324,7 +324,7 @@ static void build_afw_t(cr_hybrid_s *h, int mode, cudaStream_t s) {
     nfb.alloc(1, s);
     nfb.zero(s);
     EllView<D> Gv{h->G.cols.get(), h->G.vals.get(), nrows};
-    AfwView A{P.ioff.get(), P.voff.get(), P.kl.get(), P.ids.get(), P.vals.get(), npatch};
+    AfwView A{P.ioff.get(), P.voff.get(), P.kl.get(), P.ids.get(), P.vals.get(), npatch, nrows};
     const int grid = grid_for(nsl * 32, 64, 16);
 #define CR_SETUP(KM, MD) \
     k_patch_setup<D, KM, MD><<<grid, 64, 0, s>>>(Gv, h->rowlen.get(), start.get(), v1.get(), npatch, A, P.ids.get(), P.vals.get(), nfb.get())

@@ -626,39 +626,41 @@ __global__ void __launch_bounds__(kT) k_pcg_pdir_afw(int64_t nrows, double *__re
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if constexpr (D == 2) {
         double2 *p2 = reinterpret_cast<double2 *>(p);
-        const double2 *z2 = reinterpret_cast<const double2 *>(zs);
         int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
         for (; row + 3 * stride < nrows; row += 4 * stride) {
-            double2 pv[4], zv[4][SLOTS];
+            double2 pv[4];
+            double z0[4], z1[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                pv[u] = __ldcs(p2 + row + u * stride);
+                const int64_t r = row + u * stride;
+                pv[u] = __ldcs(p2 + r);
+                z0[u] = __ldcs(zs + r);
+                z1[u] = __ldcs(zs + nrows + r);
 #pragma unroll
-                for (int sl = 0; sl < SLOTS; ++sl) zv[u][sl] = __ldcs(z2 + (row + u * stride) * SLOTS + sl);
+                for (int sl = 1; sl < SLOTS; ++sl) {
+                    z0[u] += __ldcs(zs + (int64_t)(sl * 2) * nrows + r);
+                    z1[u] += __ldcs(zs + (int64_t)(sl * 2 + 1) * nrows + r);
+                }
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                double zx = zv[u][0].x, zy = zv[u][0].y;
-#pragma unroll
-                for (int sl = 1; sl < SLOTS; ++sl) { zx += zv[u][sl].x; zy += zv[u][sl].y; }
-                pv[u].x = (beta == 0.0) ? zx : fma(beta, pv[u].x, zx);
-                pv[u].y = (beta == 0.0) ? zy : fma(beta, pv[u].y, zy);
+                pv[u].x = (beta == 0.0) ? z0[u] : fma(beta, pv[u].x, z0[u]);
+                pv[u].y = (beta == 0.0) ? z1[u] : fma(beta, pv[u].y, z1[u]);
                 p2[row + u * stride] = pv[u];
             }
         }
         for (; row < nrows; row += stride) {
+            double z[2];
+            afw_sum<2, SLOTS>(zs, nrows, row, z);
             double2 pv = p2[row];
-            double zx = 0.0, zy = 0.0;
-#pragma unroll
-            for (int sl = 0; sl < SLOTS; ++sl) { const double2 zz = z2[row * SLOTS + sl]; zx += zz.x; zy += zz.y; }
-            pv.x = (beta == 0.0) ? zx : fma(beta, pv.x, zx);
-            pv.y = (beta == 0.0) ? zy : fma(beta, pv.y, zy);
+            pv.x = (beta == 0.0) ? z[0] : fma(beta, pv.x, z[0]);
+            pv.y = (beta == 0.0) ? z[1] : fma(beta, pv.y, z[1]);
             p2[row] = pv;
         }
     } else {
         GRID_STRIDE(row, nrows) {
             double z[D];
-            afw_sum<D, SLOTS>(zs, row, z);
+            afw_sum<D, SLOTS>(zs, nrows, row, z);
 #pragma unroll
             for (int i = 0; i < D; ++i) p[row * D + i] = (beta == 0.0) ? z[i] : fma(beta, p[row * D + i], z[i]);
         }
@@ -674,7 +676,7 @@ __global__ void __launch_bounds__(kT) k_pcg_pdir_afw2(int64_t nrows, double *__r
     const double beta = first ? 0.0 : (st->qf + st->qc) / st->rho;
     GRID_STRIDE(row, nrows) {
         double z[D], zc[D];
-        afw_sum<D, SLOTS>(zs, row, z);
+        afw_sum<D, SLOTS>(zs, nrows, row, z);
         coarse_prolong<D>(C, row, y, zc);
 #pragma unroll
         for (int i = 0; i < D; ++i) {
@@ -690,7 +692,7 @@ __global__ void __launch_bounds__(kT) k_afw_zsum(int64_t nrows, double *z, const
     if (guard && st->flag != FLAG_RUN) return;
     GRID_STRIDE(row, nrows) {
         double zv[D];
-        afw_sum<D, SLOTS>(zs, row, zv);
+        afw_sum<D, SLOTS>(zs, nrows, row, zv);
 #pragma unroll
         for (int i = 0; i < D; ++i) z[row * D + i] = zv[i];
     }
@@ -1107,7 +1109,7 @@ template <int D, int WHAT>
 static void launch_afw(Launcher &L, cudaStream_t ks, const double *r, double *zs, double rtol) {
     constexpr int SLOTS = D == 2 ? 2 : 3;
     const AfwPrec &P = L.h->afw;
-    AfwView A{P.ioff.get(), P.voff.get(), P.kl.get(), P.ids.get(), P.vals.get(), P.npatch};
+    AfwView A{P.ioff.get(), P.voff.get(), P.kl.get(), P.ids.get(), P.vals.get(), P.npatch, L.h->G.nrows};
     const int64_t nt = P.nslices * 32 * D;
     const bool sym = P.built != AFW_GEN;
     KState *st = L.w->st.get();
