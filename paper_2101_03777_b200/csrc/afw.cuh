@@ -57,7 +57,22 @@ __device__ __forceinline__ double afw_patch_comp(const AfwView &A, int64_t t, co
     }
     const int T = SYM ? k * (k + 1) / 2 : k * k;
     const double *vi = A.vals + A.voff[slice] + lane + (int64_t)i * T * 32;
-    if constexpr (SYM) {
+    if (SYM && k == KMAX) {
+        // full-size slice (nearly all of them): every operator load is issued before the first
+        // FMA needs one, instead of one row's worth per (data-dependent) branch
+        constexpr int TM = KMAX * (KMAX + 1) / 2;
+        double v[TM];
+#pragma unroll
+        for (int e = 0; e < TM; ++e) v[e] = __ldcs(vi + e * 32);
+#pragma unroll
+        for (int a = 0; a < KMAX; ++a)
+#pragma unroll
+            for (int b = 0; b <= a; ++b) {
+                const double w = v[a * (a + 1) / 2 + b];
+                y[a] = fma(w, rv[b], y[a]);
+                if (a != b) y[b] = fma(w, rv[a], y[b]);
+            }
+    } else if constexpr (SYM) {
 #pragma unroll
         for (int a = 0; a < KMAX; ++a) {
             if (a < k) {
