@@ -295,28 +295,31 @@ __global__ void k_symmetrize(double *E, int64_t n) {
 //   A_KK = Pk.  The three products are cuBLAS DGEMMs (build_coarse_t).
 constexpr int kGB = 32;
 
-// Pk = inverse of the b x b diagonal block: one warp, lane i owns row i of [A | I] in shared
-// memory (scalar Gauss-Jordan, no pivoting: the block is a Schur complement of an SPD matrix)
-__global__ void __launch_bounds__(32) k_gj_diag(const double *E, int64_t n, int64_t k0, int b, double *Pk, int *bad) {
+// Pk = inverse of the b x b diagonal block: one CTA, [A | I] in shared memory, scalar Gauss-Jordan
+// without pivoting (the block is a Schur complement of an SPD matrix); coalesced load / store
+__global__ void __launch_bounds__(256) k_gj_diag(const double *E, int64_t n, int64_t k0, int b, double *Pk, int *bad) {
     __shared__ double A[kGB][2 * kGB + 1];
-    const int i = threadIdx.x;
-    for (int j = 0; j < 2 * b; ++j)
-        A[i][j] = (i < b) ? (j < b ? E[(k0 + i) * n + k0 + j] : (j - b == i ? 1.0 : 0.0)) : 0.0;
-    __syncwarp();
+    __shared__ double colc[kGB];
+    const int tid = threadIdx.x, nb2 = 2 * b;
+    for (int t = tid; t < b * nb2; t += blockDim.x) {
+        const int i = t / nb2, j = t - i * nb2;
+        A[i][j] = j < b ? E[(k0 + i) * n + k0 + j] : (j - b == i ? 1.0 : 0.0);
+    }
+    __syncthreads();
     for (int c = 0; c < b; ++c) {
         const double piv = A[c][c];
-        if (i == 0 && !(piv > 0.0)) atomicExch(bad, 1);
-        const double f = (i < b && i != c) ? A[i][c] / piv : 0.0;
-        __syncwarp();
-        if (i < b && i != c)
-            for (int j = 0; j < 2 * b; ++j) A[i][j] -= f * A[c][j];
-        __syncwarp();
-        if (i == c)
-            for (int j = 0; j < 2 * b; ++j) A[c][j] /= piv;
-        __syncwarp();
+        if (tid == 0 && !(piv > 0.0)) atomicExch(bad, 1);
+        if (tid < b) colc[tid] = A[tid][c] / piv;
+        __syncthreads();
+        for (int t = tid; t < b * nb2; t += blockDim.x) {
+            const int i = t / nb2, j = t - i * nb2;
+            if (i != c) A[i][j] -= colc[i] * A[c][j];
+        }
+        __syncthreads();
+        for (int j = tid; j < nb2; j += blockDim.x) A[c][j] /= piv;
+        __syncthreads();
     }
-    if (i < b)
-        for (int j = 0; j < b; ++j) Pk[i * b + j] = A[i][b + j];
+    for (int t = tid; t < b * b; t += blockDim.x) Pk[t] = A[t / b][b + t % b];
 }
 
 // pivot columns A_IK = -X_I, A_KK = Pk
@@ -474,7 +477,7 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
     for (int64_t k0 = 0; k0 < C.nE; k0 += kGB) {
         const int b = (int)std::min<int64_t>(kGB, C.nE - k0);
         double *Ep = C.Einv.get();
-        k_gj_diag<<<1, 32, 0, s>>>(Ep, C.nE, k0, b, Pk.get(), bad.get());
+        k_gj_diag<<<1, 256, 0, s>>>(Ep, C.nE, k0, b, Pk.get(), bad.get());
         CR_CUDA(cudaMemcpyAsync(Yb.get(), Ep + k0 * C.nE, (size_t)b * C.nE * sizeof(double), cudaMemcpyDeviceToDevice, s));
         dgemm(s, b, n, b, 1.0, Pk.get(), b, Ep + k0, n, 0.0, X.get(), b);            // X^t = Pk^t E[:,K]^t
         dgemm(s, n, n, b, -1.0, Yb.get(), n, X.get(), b, 1.0, Ep, n);                  // E^t -= Y^t X^t
