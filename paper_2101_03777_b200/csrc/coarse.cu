@@ -350,7 +350,7 @@ __global__ void k_iota_u32(uint32_t *a, int64_t n) {
 }
 
 template <int D>
-static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const double *, double *)> &applyG,
+static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const double *, double *, int)> &applyG,
                            cudaStream_t s) {
     constexpr int NN = 1 << D, NV = NN * D * D;
     const cr_mesh_s *m = h->mesh;
@@ -453,7 +453,7 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
             for (int l = 0; l < D; ++l) {
                 k_coarse_colour<D><<<grid_for(nrows, T), T, 0, s>>>(V, nrows, colour, k, l, z.get());
                 CR_CHECK_LAUNCH();
-                applyG(z.get(), Y.get());
+                applyG(z.get(), Y.get(), colour);
                 k_coarse_restrict<D><<<(unsigned)C.nchunk, 256, 0, s>>>(V, Y.get(), C.part.get());
                 k_coarse_gather<D><<<grid_for(C.nE, T), T, 0, s>>>(V, C.part.get(), C.c.get());
                 CR_CHECK_LAUNCH();
@@ -493,7 +493,8 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
     C.built = H;
 }
 
-void build_coarse(cr_hybrid_s *h, int H, const std::function<void(const double *, double *)> &applyG, cudaStream_t s) {
+void build_coarse(cr_hybrid_s *h, int H, const std::function<void(const double *, double *, int)> &applyG,
+                  cudaStream_t s) {
     CR_REQUIRE(H >= 1 && H <= 64, CR_ERR_INVALID_ARG, "coarse grid intervals must be in [1, 64]");
     const int D = h->G.d;
     // at least ~4 faces per coarse unknown: a coarse grid finer than the mesh makes Z rank-deficient

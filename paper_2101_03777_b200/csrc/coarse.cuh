@@ -58,6 +58,22 @@ __device__ __forceinline__ int64_t coarse_node(const CoarseGrid &g, const int (&
     return node;
 }
 
+// does coarse cell ic have a corner node of colour `colour` (node indices mod 5, base-5 digits)?
+template <int D>
+__device__ __forceinline__ bool coarse_cell_active(const int (&ic)[D], int colour) {
+#pragma unroll
+    for (int n = 0; n < (1 << D); ++n) {
+        int col = 0, mul = 1;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            col += ((ic[i] + ((n >> i) & 1)) % 5) * mul;
+            mul *= 5;
+        }
+        if (col == colour) return true;
+    }
+    return false;
+}
+
 // (Z y) at a row: sum_n w_n sum_l a^(l) y[(node_n D + k) D + l]
 template <int D>
 __device__ __forceinline__ void coarse_prolong(const CoarseView &C, int64_t row, const double *y, double (&z)[D]) {

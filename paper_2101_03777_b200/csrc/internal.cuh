@@ -290,7 +290,9 @@ void build_afw(cr_hybrid_s *h, int mode, cudaStream_t s);
 // mf.cu
 void build_mf(cr_hybrid_s *h, cudaStream_t s);
 // coarse.cu
-void build_coarse(cr_hybrid_s *h, int H, const std::function<void(const double *, double *)> &applyG, cudaStream_t s);
+// applyG(z, Y, colour): Y = G z, z a colour sum of coarse columns (colour < 0: any z)
+void build_coarse(cr_hybrid_s *h, int H, const std::function<void(const double *, double *, int)> &applyG,
+                  cudaStream_t s);
 void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double *partials, unsigned *ticket,
                            cudaStream_t s);
 // shared: copy problem data into hybrid-owned buffers

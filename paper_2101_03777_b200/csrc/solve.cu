@@ -12,6 +12,8 @@
 //   BiCGStab  (nonsymmetric, NS): p,y | spmv+rhat.v | s,z | spmv+t.s,t.t | x,r update + rhat.r, r.r
 //   GMRES(m)  (nonsymmetric): Arnoldi with classical Gram-Schmidt twice, Givens on device
 // Stopping rule: TRUE relative residual ||S - G W|| / ||S|| <= rtol (reading 12).
+#include <cub/cub.cuh>
+
 #include <cmath>
 #include <cstddef>
 #include <cstring>
@@ -219,6 +221,40 @@ __global__ void __launch_bounds__(kT) k_mf_spmv(MfView M, const double *x, doubl
     GRID_STRIDE(t, M.ncells) acc[0] += mf_cell<D>(M, t, x, q, nown);
     if (REDUCE)
         reduce_and_finish<1>(acc, partials, &st->tickets[1], [&](double *t) { fin_or_store<1>(st, pqkind, t, 0.0, dist); });
+}
+
+// coarse setup: 32-cell slices with a face in a coarse cell that touches a node of `colour`
+template <int D>
+__global__ void k_mf_slice_flag(MfView M, CoarseView C, int colour, int64_t nslices, uint8_t *flag) {
+    constexpr int NF = D + 1;
+    for (int64_t sl = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); sl < nslices;
+         sl += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+        const int lane = threadIdx.x & 31;
+        bool act = false;
+#pragma unroll
+        for (int l = 0; l < NF; ++l) {
+            const int32_t row = M.ids[sl * (NF * 32) + l * 32 + lane];
+            if (row >= 0) {
+                int ic[D];
+                float xi[D];
+                coarse_locate<D>(C.g, C.fx + (int64_t)row * D, ic, xi);
+                act = act || coarse_cell_active<D>(ic, colour);
+            }
+        }
+        act = __any_sync(0xffffffffu, act);
+        if (lane == 0) flag[sl] = act ? 1 : 0;
+    }
+}
+
+// q += G_mf x over the listed slices only (coarse setup: x vanishes on every other cell)
+template <int D>
+__global__ void __launch_bounds__(kT) k_mf_spmv_slices(MfView M, const int32_t *slices, const int64_t *nact,
+                                                       const double *x, double *q, int64_t nown) {
+    const int64_t n = *nact * 32;
+    GRID_STRIDE(t, n) {
+        const int64_t tt = (int64_t)slices[t >> 5] * 32 + (t & 31);
+        mf_cell<D>(M, tt, x, q, nown);
+    }
 }
 
 // r = b - q, |r|^2 (FIN_RR)
@@ -1314,10 +1350,44 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         build_afw(h, AFW_SPD, s);
         trc.mark("patch preconditioner");
         const int H = o.coarse > 0 ? o.coarse : (D == 2 ? 16 : 8);
-        build_coarse(h, H, [&](const double *z, double *Y) {
+        // E = Z^t G Z needs G applied to colour sums of coarse columns; with the matrix-free G only
+        // the 32-cell slices touching the colour's support are applied (the rest of z is zero)
+        DevBuf<uint8_t> sflag;
+        DevBuf<int32_t> slist;
+        DevBuf<int64_t> snum;
+        DevBuf<uint8_t> stmp;
+        int last_colour = -1;
+        build_coarse(h, H, [&](const double *z, double *Y, int colour) {
             L.halo(s, const_cast<double *>(z));
-            if (L.mf) mf_apply<D, false>(L, s, z, Y, 0.0);
-            else spmv(h->G, z, Y, s);
+            if (L.mf && colour >= 0 && !L.dist) {
+                const int64_t nsl = h->mf.ncells / 32;
+                if (colour != last_colour) {
+                    if (sflag.n == 0) {
+                        sflag.alloc(nsl, s);
+                        slist.alloc(nsl, s);
+                        snum.alloc(1, s);
+                        size_t tb = 0;
+                        cub::CountingInputIterator<int32_t> it(0);
+                        CR_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, sflag.get(), slist.get(), snum.get(), nsl, s));
+                        stmp.alloc(tb, s);
+                    }
+                    k_mf_slice_flag<D><<<grid_for(nsl * 32, kT), kT, 0, s>>>(mf_view<D>(h), h->coarse.view(), colour, nsl,
+                                                                            sflag.get());
+                    CR_CHECK_LAUNCH();
+                    size_t tb = stmp.n;
+                    cub::CountingInputIterator<int32_t> it(0);
+                    CR_CUDA(cub::DeviceSelect::Flagged(stmp.get(), tb, it, sflag.get(), slist.get(), snum.get(), nsl, s));
+                    last_colour = colour;
+                }
+                CR_CUDA(cudaMemsetAsync(Y, 0, L.N * sizeof(double), s));
+                k_mf_spmv_slices<D><<<occ_grid(k_mf_spmv_slices<D>, kT, h->mf.ncells), kT, 0, s>>>(
+                    mf_view<D>(h), slist.get(), snum.get(), z, Y, L.nrows);
+                CR_CHECK_LAUNCH();
+            } else if (L.mf) {
+                mf_apply<D, false>(L, s, z, Y, 0.0);
+            } else {
+                spmv(h->G, z, Y, s);
+            }
         }, s);
         trc.mark("coarse space (E, E^-1)");
         if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
@@ -1628,7 +1698,7 @@ static void apply_precond_t(cr_hybrid_s *h, int method, const double *r, double 
             build_afw(h, AFW_SPD, s);
             // the coarse grid of the last two-level solve, else the default
             const int Hc = h->coarse.requested > 0 ? h->coarse.requested : (D == 2 ? 16 : 8);
-            build_coarse(h, Hc, [&](const double *zz, double *Y) { spmv(h->G, zz, Y, s); }, s);
+            build_coarse(h, Hc, [&](const double *zz, double *Y, int) { spmv(h->G, zz, Y, s); }, s);
             if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
             CR_CUDA(cudaMemsetAsync(w->st.get(), 0, sizeof(KState), s));
             coarse_restrict_solve(h, r, &w->st.get()->qc, w->partials.get(), &w->st.get()->tickets[4], s);
