@@ -214,7 +214,7 @@ __global__ void k_halo_pack(int64_t n, const int32_t *rows, const double *x, dou
 // ------------------------------------------------------------------ matrix-free G (mf.cuh)
 // q += G_mf x over this rank's cells (q pre-zeroed); REDUCE: p.q -> alpha (FIN_PQ)
 template <int D, bool REDUCE>
-__global__ void __launch_bounds__(kT) k_mf_spmv(MfView M, const double *x, double *q, int64_t nown, KState *st,
+__global__ void __launch_bounds__(kT, D == 2 ? 3 : 1) k_mf_spmv(MfView M, const double *x, double *q, int64_t nown, KState *st,
                                                 double *partials, int dist, int pqkind) {
     if (REDUCE && st->flag != FLAG_RUN) return;
     double acc[1] = {0.0};
@@ -576,7 +576,7 @@ enum { AFW_PCG_INIT = 0, AFW_PCG = 1, AFW_MINRES_INIT = 2, AFW_MINRES = 3, AFW_P
 
 // zs (per face slot) = patch contributions of M^{-1} r
 template <int D, int SLOTS, int KMAX, bool SYM, int WHAT>
-__global__ void __launch_bounds__(kT) k_afw_apply(AfwView A, const double *r, double *zs, double rtol, KState *st,
+__global__ void __launch_bounds__(kT, 4) k_afw_apply(AfwView A, const double *r, double *zs, double rtol, KState *st,
                                                   double *partials, int dist) {
     if (WHAT != AFW_PCG_INIT && WHAT != AFW_MINRES_INIT && WHAT != AFW_PCG2_INIT && st->flag != FLAG_RUN) return;
     double acc[1] = {0.0};
