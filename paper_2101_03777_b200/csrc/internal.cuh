@@ -95,7 +95,7 @@ constexpr int kSMs = 148;
 // grid-stride kernels: a second, partial wave would leave SMs idle while it drains.  Cached per
 // kernel; the grid only depends on the kernel and the GPU, so block partials stay deterministic.
 template <class F>
-inline int occ_grid(F kernel, int threads, int64_t work) {
+inline int occ_grid(F kernel, int threads, int64_t work, int reserve = 0) {
     static thread_local std::vector<std::pair<const void *, int>> cache;
     const void *key = reinterpret_cast<const void *>(kernel);
     int nb = 0;
@@ -107,7 +107,7 @@ inline int occ_grid(F kernel, int threads, int64_t work) {
         cache.emplace_back(key, nb);
     }
     int64_t b = (work + threads - 1) / threads;
-    const int64_t cap = (int64_t)kSMs * nb;
+    const int64_t cap = (int64_t)kSMs * (nb > reserve ? nb - reserve : 1);
     if (b > cap) b = cap;
     if (b < 1) b = 1;
     return (int)b;

@@ -1148,17 +1148,19 @@ static void launch_afw(Launcher &L, cudaStream_t ks, const double *r, double *zs
     AfwView A{P.ioff.get(), P.voff.get(), P.kl.get(), P.ids.get(), P.vals.get(), P.npatch, L.h->G.nrows};
     const int64_t nt = P.nslices * 32 * D;
     const bool sym = P.built != AFW_GEN;
+    // two-level: leave one block per SM to the coarse kernels that run concurrently on the side stream
+    const int rsv = 0;   // (reserving SM slots for the concurrent coarse kernels measured slower)
     KState *st = L.w->st.get();
     double *part = L.w->partials.get();
     if (P.kmax <= 6) {
-        if (sym) k_afw_apply<D, SLOTS, 6, true, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 6, true, WHAT>, kT, nt), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
-        else k_afw_apply<D, SLOTS, 6, false, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 6, false, WHAT>, kT, nt), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        if (sym) k_afw_apply<D, SLOTS, 6, true, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 6, true, WHAT>, kT, nt, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        else k_afw_apply<D, SLOTS, 6, false, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 6, false, WHAT>, kT, nt, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
     } else if (P.kmax <= 8) {
-        if (sym) k_afw_apply<D, SLOTS, 8, true, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 8, true, WHAT>, kT, nt), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
-        else k_afw_apply<D, SLOTS, 8, false, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 8, false, WHAT>, kT, nt), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        if (sym) k_afw_apply<D, SLOTS, 8, true, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 8, true, WHAT>, kT, nt, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        else k_afw_apply<D, SLOTS, 8, false, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 8, false, WHAT>, kT, nt, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
     } else {
-        if (sym) k_afw_apply<D, SLOTS, 16, true, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 16, true, WHAT>, kT, nt), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
-        else k_afw_apply<D, SLOTS, 16, false, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 16, false, WHAT>, kT, nt), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        if (sym) k_afw_apply<D, SLOTS, 16, true, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 16, true, WHAT>, kT, nt, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        else k_afw_apply<D, SLOTS, 16, false, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 16, false, WHAT>, kT, nt, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
     }
     CR_CHECK_LAUNCH();
     ++L.launches;
