@@ -120,6 +120,42 @@ __global__ void k_mf_partners(MeshView mv, const int32_t *list, int64_t ncell, i
     }
 }
 
+// Morton key of a cell centroid (21 bits per direction in 3D, 31 in 2D) inside the mesh bounding box
+__device__ __forceinline__ uint64_t spread2(uint64_t v) {   // 32 -> 64 bits, one zero between bits
+    v &= 0xffffffffull;
+    v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+    v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+    v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+    v = (v | (v << 2)) & 0x3333333333333333ull;
+    v = (v | (v << 1)) & 0x5555555555555555ull;
+    return v;
+}
+__device__ __forceinline__ uint64_t spread3(uint64_t v) {   // 21 -> 63 bits, two zeros between bits
+    v &= 0x1fffffull;
+    v = (v | (v << 32)) & 0x1f00000000ffffull;
+    v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+    v = (v | (v << 8)) & 0x100f00f00f00f00full;
+    v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+    v = (v | (v << 2)) & 0x1249249249249249ull;
+    return v;
+}
+template <int D>
+__global__ void k_mf_morton(const double *xK, const int32_t *list, int64_t n, const double *lo, const double *hi,
+                            uint64_t *key) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t K = list[t];
+        uint64_t k = 0;
+        for (int i = 0; i < D; ++i) {
+            const double w = hi[i] - lo[i];
+            const double u = w > 0 ? (xK[K * D + i] - lo[i]) / w : 0.0;
+            const double scale = D == 2 ? 2147483647.0 : 2097151.0;
+            const uint64_t q = (uint64_t)fmin(fmax(u * scale, 0.0), scale);
+            k |= (D == 2 ? spread2(q) : spread3(q)) << i;
+        }
+        key[t] = k;
+    }
+}
+
 template <int D>
 static void build_mf_t(cr_hybrid_s *h, cudaStream_t s) {
     using LY = MfLayout<D>;
@@ -147,6 +183,36 @@ static void build_mf_t(cr_hybrid_s *h, cudaStream_t s) {
     int64_t ncell = 0;
     CR_CUDA(cudaMemcpyAsync(&ncell, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CR_CUDA(cudaStreamSynchronize(s));
+    {
+        // cells in Morton order of their centroids: a 32-cell warp covers a compact block (4 x 4
+        // squares in 2D), so most of its faces are shared inside the warp (summed in registers)
+        // instead of needing an atomic from each side
+        DevBuf<double> lo, hi, comp;
+        lo.alloc(D, s); hi.alloc(D, s); comp.alloc(nc, s);
+        for (int i = 0; i < D; ++i) {
+            CR_CUDA(cudaMemcpy2DAsync(comp.get(), sizeof(double), m->xK.get() + i, D * sizeof(double), sizeof(double), nc,
+                                      cudaMemcpyDeviceToDevice, s));
+            size_t tr = 0;
+            CR_CUDA(cub::DeviceReduce::Min(nullptr, tr, comp.get(), lo.get() + i, (int)nc, s));
+            DevBuf<uint8_t> rt;
+            rt.alloc(tr, s);
+            CR_CUDA(cub::DeviceReduce::Min(rt.get(), tr, comp.get(), lo.get() + i, (int)nc, s));
+            CR_CUDA(cub::DeviceReduce::Max(rt.get(), tr, comp.get(), hi.get() + i, (int)nc, s));
+        }
+        DevBuf<uint64_t> key, key2;
+        DevBuf<int32_t> list2;
+        key.alloc(ncell, s); key2.alloc(ncell, s); list2.alloc(ncell, s);
+        k_mf_morton<D><<<grid_for(ncell, T), T, 0, s>>>(m->xK.get(), list.get(), ncell, lo.get(), hi.get(), key.get());
+        CR_CHECK_LAUNCH();
+        size_t ts = 0;
+        CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, ts, key.get(), key2.get(), list.get(), list2.get(), (int)ncell, 0,
+                                                D == 2 ? 64 : 63, s));
+        DevBuf<uint8_t> st;
+        st.alloc(ts, s);
+        CR_CUDA(cub::DeviceRadixSort::SortPairs(st.get(), ts, key.get(), key2.get(), list.get(), list2.get(), (int)ncell, 0,
+                                                D == 2 ? 64 : 63, s));
+        CR_CUDA(cudaMemcpyAsync(list.get(), list2.get(), ncell * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    }
     const int64_t nsl = (ncell + 31) / 32;
     M.ncells = nsl * 32;
     M.ids.alloc(nsl * 32 * LY::NF, s);
