@@ -170,7 +170,17 @@ enum { CR_PCG_JACOBI = 0, CR_PCG_BLOCKJACOBI = 1, CR_MINRES_ABSJACOBI = 2,
        /* two-level: the patch preconditioner plus the coarse correction Z (Z^t G Z)^{-1} Z^t,
         * Z_(j,k,l): W^(k) = a_sigma^(l) phi_j(x_sigma) on a uniform grid of `coarse` intervals
         * per direction; E = Z^t G Z assembled and inverted on the device.   */
-       CR_PCG_AFW2 = 7 };
+       CR_PCG_AFW2 = 7,
+       /* steady Stokes / NS step: flexible GMRES(restart) on the coupled system [[A, D^t],[D, 0]]
+        * (P:L253-306), right-preconditioned by the exact transient-Stokes inverse K_mu^{-1}
+        * (mass coefficient mu_inner, same nu and K0), applied through the hybrid method: cell
+        * right-hand sides -> S_mu -> CR_PCG_AFW2 on the matrix-free G_mu (to inner_rtol) ->
+        * recovery.  The W returned is the target's, formed from (U, P) by the local relation
+        * W_sigma = R_K - Ahat_K U_K + a_K P_K on the first cell of sigma; the stopping rule is
+        * the target's true ||S - G W|| / ||S|| <= rtol (assembled G).  iterations = outer
+        * iterations; inner_iterations = total inner PCG iterations; max_iter caps the outer
+        * ones (default 500); the initial W is ignored (x0 = 0).  Single rank.  DESIGN.md §7.1. */
+       CR_DC_FGMRES = 8 };
 typedef struct {
     int32_t method;       /* CR_* above                                                        */
     int32_t restart;      /* GMRES m (default 50)                                              */
@@ -179,6 +189,8 @@ typedef struct {
     int32_t check_every;  /* iterations per captured CUDA graph between host checks (def 64)   */
     int32_t matrix_free;  /* 0: assembled G; 1: matrix-free factored G (see above)             */
     int32_t coarse;       /* CR_PCG_AFW2: coarse intervals per direction (0: 16 in 2D, 8 in 3D) */
+    double mu_inner;      /* CR_DC_FGMRES: mass coefficient of the inner transient operator (0: 1) */
+    double inner_rtol;    /* CR_DC_FGMRES: inner PCG tolerance (0: 1e-11)                       */
 } cr_solver_opts;
 typedef struct {
     int64_t iterations;
@@ -189,6 +201,7 @@ typedef struct {
     double seconds;            /* device time of the solve (CUDA events)                        */
     int64_t spmv_calls;
     int64_t kernel_launches;   /* kernels launched by cr_solve                                   */
+    int64_t inner_iterations;  /* CR_DC_FGMRES: inner PCG iterations over all outer ones         */
 } cr_solve_report;
 cr_status cr_solve(cr_hybrid h, const cr_solver_opts *opts, double *W_d, cr_stream_t s,
                    cr_solve_report *rep);

@@ -34,10 +34,10 @@ STATUS = {0: "CR_OK", -1: "CR_ERR_INVALID_ARG", -2: "CR_ERR_CUDA", -3: "CR_ERR_O
 CR_STOKES, CR_NS_NEWTON_STEP = 0, 1
 CR_SHIFT_NONE, CR_SHIFT_MIS = 0, 1
 (CR_PCG_JACOBI, CR_PCG_BLOCKJACOBI, CR_MINRES_ABSJACOBI, CR_BICGSTAB_JACOBI, CR_GMRES_JACOBI,
- CR_PCG_AFW, CR_MINRES_AFW, CR_PCG_AFW2) = range(8)
+ CR_PCG_AFW, CR_MINRES_AFW, CR_PCG_AFW2, CR_DC_FGMRES) = range(9)
 METHODS = {"pcg": CR_PCG_JACOBI, "pcg_block": CR_PCG_BLOCKJACOBI, "minres": CR_MINRES_ABSJACOBI,
            "bicgstab": CR_BICGSTAB_JACOBI, "gmres": CR_GMRES_JACOBI, "pcg_afw": CR_PCG_AFW,
-           "minres_afw": CR_MINRES_AFW, "pcg_afw2": CR_PCG_AFW2}
+           "minres_afw": CR_MINRES_AFW, "pcg_afw2": CR_PCG_AFW2, "dc": CR_DC_FGMRES}
 
 
 class CrError(RuntimeError):
@@ -66,14 +66,14 @@ class Data(ctypes.Structure):
 class SolverOpts(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int32), ("restart", ctypes.c_int32), ("rtol", ctypes.c_double),
                 ("max_iter", ctypes.c_int64), ("check_every", ctypes.c_int32), ("matrix_free", ctypes.c_int32),
-                ("coarse", ctypes.c_int32)]
+                ("coarse", ctypes.c_int32), ("mu_inner", ctypes.c_double), ("inner_rtol", ctypes.c_double)]
 
 
 class SolveReport(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int64), ("rel_res_true", ctypes.c_double),
                 ("rel_res_recursive", ctypes.c_double), ("converged", ctypes.c_int32),
                 ("status", ctypes.c_int32), ("seconds", ctypes.c_double), ("spmv_calls", ctypes.c_int64),
-                ("kernel_launches", ctypes.c_int64)]
+                ("kernel_launches", ctypes.c_int64), ("inner_iterations", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -357,10 +357,15 @@ def partition_plan(dim: int, cell_faces, face_cells, face_dof, rank: int, nranks
 
 def cr_solve(hyb: Hybrid, W: torch.Tensor, method: str | int = "pcg", rtol: float = 1e-10,
              max_iter: int = 10**7, check_every: int = 64, restart: int = 50, matrix_free: int = 0, coarse: int = 0,
-             stream=None, raise_on_fail: bool = True) -> dict:
-    """Krylov solve of G W = S in place.  Returns the cr_solve_report as a dict."""
+             mu_inner: float = 0.0, inner_rtol: float = 0.0, stream=None, raise_on_fail: bool = True) -> dict:
+    """Krylov solve of G W = S in place.  Returns the cr_solve_report as a dict.
+    method "dc" (CR_DC_FGMRES): outer FGMRES on the coupled system preconditioned by the
+    transient hybrid solve (mu_inner, inner_rtol); max_iter then caps the outer iterations."""
     m = METHODS[method] if isinstance(method, str) else int(method)
-    opts = SolverOpts(m, restart, rtol, max_iter, check_every, int(matrix_free), int(coarse))
+    if m == CR_DC_FGMRES and max_iter == 10**7:
+        max_iter = 0
+    opts = SolverOpts(m, restart, rtol, max_iter, check_every, int(matrix_free), int(coarse), float(mu_inner),
+                      float(inner_rtol))
     rep = SolveReport()
     st = _lib.cr_solve(hyb._h, ctypes.byref(opts), _ptr(W, torch.float64), _stream(stream), ctypes.byref(rep))
     out = rep.as_dict()

@@ -255,7 +255,8 @@ cr_status cr_solve(cr_hybrid h, const cr_solver_opts *opts, double *W_d, cr_stre
     CR_API_BEGIN
     CR_REQUIRE(h && opts && W_d, CR_ERR_INVALID_ARG, "null argument");
     if (rep) std::memset(rep, 0, sizeof(*rep));
-    cr::solve(h, *opts, W_d, (cudaStream_t)s, rep);
+    if (opts->method == CR_DC_FGMRES) cr::solve_dc(h, *opts, W_d, (cudaStream_t)s, rep);
+    else cr::solve(h, *opts, W_d, (cudaStream_t)s, rep);
     CR_API_END
 }
 

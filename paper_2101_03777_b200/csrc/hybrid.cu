@@ -205,7 +205,8 @@ __device__ __forceinline__ void finish_row(const AsmOut &o, int64_t r, int slot,
 
 template <int D>
 __global__ void __launch_bounds__(128) k_assemble_stokes(MeshView mv, ProbView p, const int32_t *dof_face,
-                                                         int64_t nrows, int64_t row0, const int32_t *g2l, AsmOut o) {
+                                                         int64_t nrows, int64_t row0, const int32_t *g2l, AsmOut o,
+                                                         int sonly = 0) {
     constexpr int NF = D + 1;
     unsigned long long nb_local = 0;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
@@ -273,10 +274,15 @@ __global__ void __launch_bounds__(128) k_assemble_stokes(MeshView mv, ProbView p
                     for (int i = 0; i < D; ++i)
 #pragma unroll
                         for (int j = 0; j < D; ++j) diag[i][j] += b[i][j];
-                } else {
+                } else if (!sonly) {
                     write_block<D>(o, r, slot++, g2l ? g2l[c.dof[lq]] : (int32_t)c.dof[lq], b);
                 }
             }
+        }
+        if (sonly) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) o.S[r * D + i] = Sr[i];
+            continue;
         }
         finish_row<D>(o, r, slot, diag, Sr);
         nb_local += (unsigned long long)slot;
@@ -387,6 +393,8 @@ ProbView prob_view(const cr_hybrid_s *h) {
     p.uit = h->has_uit ? h->uit.get() : nullptr;
     p.pit = h->has_pit ? h->pit.get() : nullptr;
     p.E = h->prm.shift == CR_SHIFT_MIS ? h->E.get() : nullptr;
+    p.rcell = h->rcell.n ? h->rcell.get() : nullptr;
+    p.gcell = h->gcell.n ? h->gcell.get() : nullptr;
     return p;
 }
 
@@ -480,6 +488,31 @@ static void hybridise_t(cr_hybrid_s *h, const cr_mesh_s *m, cudaStream_t s) {
     CR_CUDA(cudaMemcpyAsync(&hnb, nb.get(), sizeof(hnb), cudaMemcpyDeviceToHost, s));
     CR_CUDA(cudaStreamSynchronize(s));
     G.nblocks = (int64_t)hnb;
+}
+
+// S of the same G for new cell right-hand sides (h->rcell / h->gcell): the Stokes assembly kernel with
+// its G writes disabled
+void hybrid_update_rhs(cr_hybrid_s *h, cudaStream_t s) {
+    const cr_mesh_s *m = h->mesh;
+    CR_REQUIRE(!h->is_ns, CR_ERR_INVALID_ARG, "hybrid_update_rhs: Stokes handles only");
+    const int64_t nrows = h->G.nrows;
+    const int64_t row0 = h->part.on ? h->part.row0 : 0;
+    const int32_t *g2l = h->part.on ? h->part.g2l.get() : nullptr;
+    DevBuf<int> err;
+    err.alloc(1, s);
+    err.zero(s);
+    DevBuf<unsigned long long> nb;
+    nb.alloc(1, s);
+    nb.zero(s);
+    AsmOut o{h->G.cols.get(), h->G.vals.get(), h->rowlen.get(), h->S.get(), h->dinv.get(), h->absdinv.get(),
+             h->bdinv.get(), nb.get(), err.get()};
+    MeshView mv = mesh_view(m);
+    ProbView p = prob_view(h);
+    if (m->dim == 2)
+        k_assemble_stokes<2><<<grid_for(nrows, 128, 16), 128, 0, s>>>(mv, p, m->dof_face.get(), nrows, row0, g2l, o, 1);
+    else
+        k_assemble_stokes<3><<<grid_for(nrows, 128, 16), 128, 0, s>>>(mv, p, m->dof_face.get(), nrows, row0, g2l, o, 1);
+    CR_CHECK_LAUNCH();
 }
 
 void hybridise(cr_hybrid_s *h, const cr_mesh_s *m, const cr_params &prm, const cr_data &data, cr_comm_s *comm,

@@ -235,6 +235,7 @@ struct cr_hybrid_s {
     // owned copies of the problem data (recovery needs them again)
     cr::DevBuf<double> fbar, dir, uit, pit;
     bool has_dir = false, has_uit = false, has_pit = false;
+    cr::DevBuf<double> rcell, gcell;   // explicit cell right-hand sides (dc.cu), empty unless set
     // shift
     cr::DevBuf<uint8_t> inM1;
     cr::DevBuf<double> lam, E;   // lam [nc], E [nc][d+1]
@@ -270,6 +271,10 @@ void build_mesh(cr_mesh_s *m, int dim, int64_t nv, const double *coords, int64_t
 // hybrid.cu
 void hybridise(cr_hybrid_s *h, const cr_mesh_s *m, const cr_params &prm, const cr_data &data, cr_comm_s *comm,
                cudaStream_t s);
+void hybrid_update_rhs(cr_hybrid_s *h, cudaStream_t s);   // recompute S only (same G)
+// dc.cu
+void solve_dc(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep);
+void coupled_spmv(const cr_coupled_s *c, const double *x, double *y, cudaStream_t s);
 // partition.cu
 void setup_part(cr_hybrid_s *h, const cr_mesh_s *m, cr_comm_s *comm, cudaStream_t s);
 void hybrid_export_csr(const cr_hybrid_s *h, int64_t *row_ptr, int32_t *cols, double *vals, double *S,

@@ -30,9 +30,12 @@ inline MeshView mesh_view(const cr_mesh_s *m) {
 }
 
 struct ProbView {
-    double mu, nu;
-    int k0, is_ns;
-    const double *fbar, *dir, *uit, *pit, *E;   // E [nc][d+1] or null
+    double mu = 0.0, nu = 0.0;
+    int k0 = 0, is_ns = 0;
+    const double *fbar = nullptr, *dir = nullptr, *uit = nullptr, *pit = nullptr, *E = nullptr;   // E [nc][d+1]
+    // explicit cell right-hand sides (coupled defect correction, dc.cu): R_K [nc][d+1][d], g_K [nc];
+    // when set they replace the force / Dirichlet terms of stokes_rhs
+    const double *rcell = nullptr, *gcell = nullptr;
 };
 
 template <int D>
@@ -92,6 +95,14 @@ template <int D>
 __device__ __forceinline__ void stokes_rhs(const Cell<D> &c, const ProbView &p, dd R[D + 1][D], dd &g) {
     constexpr int NF = D + 1;
     const int64_t K = c.K;
+    if (p.rcell) {
+#pragma unroll
+        for (int l = 0; l < NF; ++l)
+#pragma unroll
+            for (int i = 0; i < D; ++i) R[l][i] = dd_of(p.rcell[(K * NF + l) * D + i]);
+        g = dd_of(p.gcell[K]);
+        return;
+    }
     dd fdx[NF];
 #pragma unroll
     for (int l = 0; l < NF; ++l) {

@@ -183,6 +183,15 @@ def test_shifted_configs_full_size_assembly(idx):
     assert np.abs(Eg.cpu().numpy() - E).max() <= 1e-14 * np.abs(E).max()
     eG, eS = sampled_rows(mo, prm, data, E, hg, 150)
     assert eG <= 1e-12 and eS <= 1e-12, (eG, eS)
+    # the solve: coupled FGMRES preconditioned by the transient hybrid solve (CR_DC_FGMRES),
+    # stopped on the TARGET's true residual ||S - G W|| / ||S|| <= 1e-10 (G checked above)
+    W = torch.zeros(hg.n_rows, dtype=torch.float64, device=DEV)
+    rep = P.cr_solve(hg, W, "dc", rtol=cfg.rtol, coarse=32, mu_inner=1.0 if idx == 2 else 0.5)
+    assert rep["converged"] and rep["rel_res_true"] <= cfg.rtol, rep
+    assert rep["iterations"] <= 30, rep
+    U, Pp, diag = P.cr_recover(hg, W)
+    eP, eU = sampled_recovery(mo, prm, data, E, W.cpu().numpy(), U.cpu().numpy(), Pp.cpu().numpy(), 200)
+    assert eP <= 1e-11 and eU <= 1e-11, (eP, eU)
 
 
 # ------------------------------------------------------------------ configs[4]: 3D

@@ -239,6 +239,19 @@ MF_CASES = {   # the matrix-free factored operator (transient Stokes)
     "2d-dirichlet-n16-pcg-afw2-mf": (dict(dim=2, n=16, dirichlet=True), "pcg_afw2", 1e-12),
 }
 SOLVE_CASES["2d-jit-n24-pcg-afw2"] = (dict(dim=2, n=24), "pcg_afw2", 1e-12)
+# coupled defect correction (CR_DC_FGMRES): steady Stokes and NS steps, target residual 1e-11
+SOLVE_CASES.update({
+    "2d-steady-n16-dc": (dict(dim=2, n=16, mu=0.0, shift="mis", force="gaussian"), "dc", 1e-11),
+    "2d-steady-dirichlet-n12-dc": (dict(dim=2, n=12, mu=0.0, shift="mis", force="gaussian", dirichlet=True),
+                                   "dc", 1e-11),
+    "2d-steady-k0-interior-dc": (dict(dim=2, n=10, mu=0.0, shift="mis", force="gaussian", k0=57), "dc", 1e-11),
+    "3d-steady-n3-dc": (dict(dim=3, n=3, mu=0.0, shift="mis", force="gaussian"), "dc", 1e-11),
+    "2d-ns-nu001-n12-dc": (dict(dim=2, n=12, mu=0.0, nu=0.01, shift="mis", force="zero", ns=True, jitter=0.0),
+                           "dc", 1e-11),
+    "2d-ns-nu1-n8-dc": (dict(dim=2, n=8, mu=0.0, nu=1.0, shift="mis", force="zero", ns=True, jitter=0.0),
+                        "dc", 1e-11),
+    "2d-transient-n16-dc": (dict(dim=2, n=16, mu=1.0), "dc", 1e-11),
+})
 
 
 @pytest.mark.parametrize("name", list(SOLVE_CASES) + list(MF_CASES))
@@ -254,6 +267,10 @@ def test_solve_recover_parity(name):
     extra = dict(restart=128) if method == "gmres" else {}
     rep = P.cr_solve(hg, W, method, rtol=rtol, check_every=16, matrix_free=int(mf), **extra)
     assert rep["converged"] and rep["rel_res_true"] <= rtol, rep
+    if method == "dc":
+        # outer iterations: mesh-independent for Stokes; the coarse nu = 0.01
+        # NS mesh (cell Reynolds number ~ 8) needs more
+        assert 0 < rep["iterations"] <= (150 if "nu001" in name else 30) and rep["inner_iterations"] > 0, rep
     # the oracle recomputes the true residual of the GPU solution in binary128
     r = O.residual_f128(ho["G"], W.cpu().numpy(), ho["S"])
     assert np.linalg.norm(r) <= 1.5 * rtol * np.linalg.norm(ho["S"])
