@@ -71,6 +71,12 @@ class ClockSampler:
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's start-up (NVML init) stalls the driver for a few hundred ms: let it
+            # finish before the timed region opens, so only its cheap periodic queries overlap
+            t0 = time.time()
+            while len(self.lines) < 2 and time.time() - t0 < 10:
+                time.sleep(0.02)
+            self.lines.clear()
         except Exception:
             self.proc = None
         return self
@@ -184,6 +190,70 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
+# solver per config
+OTHER_SOLVERS = {2: dict(method="dc", coarse=32, mu_inner=1.0),
+                 3: dict(method="dc", coarse=32, mu_inner=0.5),
+                 4: dict(method="pcg_afw2", matrix_free=1, coarse=8)}
+
+
+def _ev(torch, stream):
+    e = torch.cuda.Event(enable_timing=True)
+    e.record(stream)
+    return e
+
+
+def stage_times(P, cfg, coords, cells, fbar, stream):
+    """One configs[1] step with CUDA events between the four C-ABI calls."""
+    import torch
+    torch.cuda.synchronize()
+    e = [_ev(torch, stream)]
+    mesh = P.cr_build_mesh(coords, cells)
+    e.append(_ev(torch, stream))
+    hyb = P.cr_hybridise(mesh, P.Problem(mu=cfg.mu, nu=cfg.nu, fbar=fbar))
+    e.append(_ev(torch, stream))
+    W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=coords.device)
+    rep = P.cr_solve(hyb, W, METHOD, rtol=cfg.rtol, check_every=64, matrix_free=MATRIX_FREE, coarse=COARSE)
+    e.append(_ev(torch, stream))
+    P.cr_recover(hyb, W)
+    e.append(_ev(torch, stream))
+    torch.cuda.synchronize()
+    t = [e[i].elapsed_time(e[i + 1]) * 1e-3 for i in range(4)]
+    return {"mesh_s": t[0], "hybridise_s": t[1], "solve_s": t[2], "recover_s": t[3],
+            "assembly_cells_per_s": mesh.nc / t[1], "mesh_cells_per_s": mesh.nc / t[0],
+            "recover_cells_per_s": mesh.nc / t[3], "iterations": rep["iterations"]}
+
+
+def other_config(P, ci, idx, dev, stream):
+    """Time-to-solution (mesh + hybridise + solve + recover, inputs in HBM) of configs[idx]."""
+    import torch
+    cfg = ci.CONFIGS[idx]
+    inp = ci.make_inputs(cfg)
+    tg = lambda a: torch.from_numpy(a).to(dev)
+    kw = {}
+    if cfg.shift == "mis":
+        kw.update(shift=P.CR_SHIFT_MIS, mis_seed=cfg.mis_seed)
+    if cfg.physics == "ns_step":
+        kw.update(physics=P.CR_NS_NEWTON_STEP, u_iter=tg(inp["u_iter"]))
+    prob = P.Problem(mu=cfg.mu, nu=cfg.nu, fbar=tg(inp["fbar"]), **kw)
+    coords, cells = tg(inp["coords"]), tg(inp["cells"])
+    sol = OTHER_SOLVERS[idx]
+    torch.cuda.synchronize()
+    a = _ev(torch, stream)
+    out = P.hybrid_method(coords, cells, prob, rtol=cfg.rtol, check_every=64, **sol)
+    b = _ev(torch, stream)
+    torch.cuda.synchronize()
+    rep = out["report"]
+    kind = {"stokes": "transient Stokes" if cfg.mu > 0 else "steady Stokes", "ns_step": "Navier-Stokes Newton step"}
+    r = {"workload": f"configs[{idx}] {cfg.dim}D {kind[cfg.physics]} n={cfg.n} (nu={cfg.nu})", "solver": sol,
+         "time_to_solution_s": a.elapsed_time(b) * 1e-3, "solve_s": rep["seconds"],
+         "iterations": rep["iterations"], "rel_res_true": rep["rel_res_true"],
+         "unknowns": out["hybrid"].n_rows, "cells": out["mesh"].nc}
+    if sol["method"] == "dc":
+        r["inner_iterations"] = rep["inner_iterations"]
+    del out
+    return r
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -193,6 +263,7 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override mesh size (debug only; not a bench value)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -354,6 +425,16 @@ def main():
         d2h = o2["U_host"].numel() * 8 + o2["P_host"].numel() * 8
         e2e = {"value": float(t2.item()), "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
+    # ---- stage times of one configs[1] step (assembly cells/s) and time-to-solution of the
+    # other configs (one run each, not part of the timed step; single GPU only)
+    stages, others = None, None
+    if world == 1 and not args.no_other_configs:
+        stages = stage_times(P, cfg, coords, cells, fbar, stream)
+        others = {}
+        for idx in (2, 3, 4):
+            others[f"configs[{idx}]"] = other_config(P, ci, idx, dev, stream)
+            torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s = oracle_sample()
@@ -371,7 +452,7 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "ms_steps_rank0": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args.n or cfg.n, world),
             "pcg": {"method": METHOD, "matrix_free": MATRIX_FREE, "coarse_intervals": COARSE,
@@ -390,6 +471,8 @@ def main():
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
             "e2e": e2e,
+            "stages_configs1": stages,
+            "other_configs": others,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
