@@ -40,6 +40,7 @@ CONFIG_IDX = 1
 METHOD = "pcg_afw2"  # patch additive Schwarz + coarse "stress x area" correction
 MATRIX_FREE = 1      # G applied from per-cell factors
 COARSE = 32          # coarse grid intervals per direction
+MAX_ITER = 20000     # a cap (the solve takes ~800): a regression fails loudly instead of running on
 # Jacobi-PCG iterations of configs[1] to a true 1e-10 residual, measured on B200 by this
 # bench (used only by --impl reference to extrapolate the oracle's per-iteration time).
 ITERS_CONFIG1_MEASURED = 162221   # Jacobi PCG, configs[1], B200 bench r01 (profiles/r01_bench_*.log)
@@ -212,7 +213,8 @@ def stage_times(P, cfg, coords, cells, fbar, stream):
     hyb = P.cr_hybridise(mesh, P.Problem(mu=cfg.mu, nu=cfg.nu, fbar=fbar))
     e.append(_ev(torch, stream))
     W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=coords.device)
-    rep = P.cr_solve(hyb, W, METHOD, rtol=cfg.rtol, check_every=64, matrix_free=MATRIX_FREE, coarse=COARSE)
+    rep = P.cr_solve(hyb, W, METHOD, rtol=cfg.rtol, check_every=64, matrix_free=MATRIX_FREE, coarse=COARSE,
+                     max_iter=MAX_ITER)
     e.append(_ev(torch, stream))
     P.cr_recover(hyb, W)
     e.append(_ev(torch, stream))
@@ -307,7 +309,8 @@ def main():
         mesh = P.cr_build_mesh(coords, cells)
         hyb = P.cr_hybridise(mesh, prob, comm=comm)
         W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=dev)
-        rep = P.cr_solve(hyb, W, METHOD, rtol=cfg.rtol, check_every=64, matrix_free=MATRIX_FREE, coarse=COARSE)
+        rep = P.cr_solve(hyb, W, METHOD, rtol=cfg.rtol, check_every=64, matrix_free=MATRIX_FREE, coarse=COARSE,
+                         max_iter=MAX_ITER)
         U, Pp, diag = P.cr_recover(hyb, W)
         return mesh, hyb, rep, U, Pp, diag
 
