@@ -194,7 +194,7 @@ def run_reference(args):
 # solver per config
 OTHER_SOLVERS = {2: dict(method="dc", coarse=32, mu_inner=1.0),
                  3: dict(method="dc", coarse=32, mu_inner=0.5),
-                 4: dict(method="pcg_afw2", matrix_free=1, coarse=8)}
+                 4: dict(method="pcg_afw2", matrix_free=1, coarse=16)}
 
 
 def _ev(torch, stream):

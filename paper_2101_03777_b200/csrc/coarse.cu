@@ -19,7 +19,11 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
+#include <cstdlib>
+#include <functional>
+#include <vector>
 
 #include "coarse.cuh"
 #include "internal.cuh"
@@ -349,6 +353,632 @@ __global__ void k_iota_u32(uint32_t *a, int64_t n) {
         a[i] = (uint32_t)i;
 }
 
+// ------------------------------------------------------------------ sparse direct coarse solve (ND)
+// E = Z^t G Z couples coarse nodes up to 2 apart in every direction (a fine cell straddling a
+// coarse grid line joins the supports of hats 2 apart), so E has a 5^D-node block stencil with
+// D^2 x D^2 blocks.  Stored structured: Es[((node * 5^D + nbr) * m + a) * m + b], m = D^2, nbr the
+// base-5 digits of (node' - node + 2).
+// Nested dissection of the (H+1)^D node grid: a box is split across its longest side by a
+// separator slab 2 nodes thick (no stencil coupling across it); boxes of <= kNdLeaf nodes per
+// side are leaf fronts.  Fronts in post-order (children first).  Multifrontal elimination with
+// explicit inverses (E SPD => every front's F_II is an SPD Schur complement):
+//   F = [[F_II, F_IB], [F_BI, F_BB]]  (original entries with a pivot end + children's updates)
+//   Finv = F_II^{-1},  W = F_BI Finv,  U = F_BB - W F_IB  (passed to the parent)
+// Solve E y = c:  forward (deepest level first)  b_I = c_I + children's u at I;  u = b_B - W b_I
+//                 backward (root first)          y_I = Finv b_I - W^t y_B
+// Every front's arithmetic is a fixed sequence (children summed in child order): deterministic.
+constexpr int kNdLeaf2 = 4, kNdLeaf3 = 3, kNdR = 2;
+
+struct HostFront {
+    std::vector<int32_t> I, B;   // nodes
+    int kid[2] = {-1, -1};
+    int depth = 0;
+};
+
+static void nd_plan(int H, int D, std::vector<HostFront> &F) {
+    const int n1 = H + 1, leaf = D == 2 ? kNdLeaf2 : kNdLeaf3;
+    auto nid = [&](const int *c) {
+        int64_t v = 0;
+        for (int i = D - 1; i >= 0; --i) v = v * n1 + c[i];
+        return (int32_t)v;
+    };
+    std::function<int(std::array<int, 3>, std::array<int, 3>, int)> rec = [&](std::array<int, 3> lo,
+                                                                             std::array<int, 3> hi, int depth) {
+        int ext[3] = {1, 1, 1}, ax = 0;
+        for (int i = 0; i < D; ++i) {
+            ext[i] = hi[i] - lo[i] + 1;
+            if (ext[i] > ext[ax]) ax = i;
+        }
+        HostFront f;
+        f.depth = depth;
+        std::array<int, 3> slo = lo, shi = hi;
+        if (ext[ax] > leaf) {
+            const int s0 = (lo[ax] + hi[ax] - kNdR + 1) / 2, s1 = s0 + kNdR - 1;
+            int k = 0;
+            std::array<int, 3> lo1 = lo, hi1 = hi, lo2 = lo, hi2 = hi;
+            hi1[ax] = s0 - 1;
+            lo2[ax] = s1 + 1;
+            if (hi1[ax] >= lo1[ax]) f.kid[k++] = rec(lo1, hi1, depth + 1);
+            if (hi2[ax] >= lo2[ax]) f.kid[k++] = rec(lo2, hi2, depth + 1);
+            slo[ax] = s0;
+            shi[ax] = s1;
+        }
+        int c[3];
+        for (c[2] = (D > 2 ? slo[2] : 0); c[2] <= (D > 2 ? shi[2] : 0); ++c[2])
+            for (c[1] = slo[1]; c[1] <= shi[1]; ++c[1])
+                for (c[0] = slo[0]; c[0] <= shi[0]; ++c[0]) f.I.push_back(nid(c));
+        std::sort(f.I.begin(), f.I.end());
+        F.push_back(std::move(f));
+        return (int)F.size() - 1;
+    };
+    F.clear();
+    rec({0, 0, 0}, {H, H, H}, 0);
+    // B sets: stencil neighbours of the pivots and the children's B, eliminated later
+    const int64_t nn = (int64_t)std::pow((double)n1, D);
+    std::vector<int32_t> pos(nn, -1);
+    for (int f = 0; f < (int)F.size(); ++f)
+        for (int32_t v : F[f].I) pos[v] = f;
+    for (int f = 0; f < (int)F.size(); ++f) {
+        std::vector<int32_t> b;
+        for (int k = 0; k < 2; ++k)
+            if (F[f].kid[k] >= 0) b.insert(b.end(), F[F[f].kid[k]].B.begin(), F[F[f].kid[k]].B.end());
+        for (int32_t v : F[f].I) {
+            int cv[3] = {0, 0, 0};
+            int64_t t = v;
+            for (int i = 0; i < D; ++i) { cv[i] = (int)(t % n1); t /= n1; }
+            const int span = 2 * kNdR + 1, nofs = D == 2 ? span * span : span * span * span;
+            for (int o = 0; o < nofs; ++o) {
+                int w[3], oo = o;
+                bool ok = true;
+                for (int i = 0; i < D; ++i) {
+                    w[i] = cv[i] + (oo % span) - kNdR;
+                    oo /= span;
+                    ok = ok && w[i] >= 0 && w[i] <= H;
+                }
+                if (ok && pos[nid(w)] > f) b.push_back(nid(w));
+            }
+        }
+        std::sort(b.begin(), b.end(), [&](int32_t x, int32_t y) { return pos[x] != pos[y] ? pos[x] < pos[y] : x < y; });
+        b.erase(std::unique(b.begin(), b.end()), b.end());
+        std::vector<int32_t> out;
+        for (int32_t v : b)
+            if (pos[v] != f) out.push_back(v);
+        F[f].B = std::move(out);
+    }
+}
+
+// structured E from the colour passes: E[(node(q'), nbr), comp(q'), (k, l)] = R[q']
+template <int D>
+__global__ void k_coarse_scatterEs(int64_t nE, int H, int colour, int k, int l, const double *R, double *Es) {
+    constexpr int M = D * D, NBR = D == 2 ? 25 : 125;
+    for (int64_t qp = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qp < nE; qp += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t node = qp / M;
+        int64_t t = node;
+        int cl = colour, nbr = 0, mul = 1;
+        bool ok = true;
+        for (int i = 0; i < D; ++i) {
+            const int ni = (int)(t % (H + 1));
+            t /= (H + 1);
+            const int ci = cl % 5;
+            cl /= 5;
+            int delta = ((ci - ni) % 5 + 5) % 5;
+            if (delta > 2) delta -= 5;
+            ok = ok && ni + delta >= 0 && ni + delta <= H;
+            nbr += (delta + 2) * mul;
+            mul *= 5;
+        }
+        if (!ok) continue;
+        Es[((node * NBR + nbr) * M + (qp - node * M)) * M + k * D + l] = R[qp];
+    }
+}
+
+// Es <- (Es + Es^t) / 2 (entry pairs (a, d, p, q) <-> (a + d, -d, q, p))
+template <int D>
+__global__ void k_es_symmetrize(int64_t nnode, int H, double *Es) {
+    constexpr int M = D * D, NBR = D == 2 ? 25 : 125;
+    const int64_t tot = nnode * NBR * M * M;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int q = (int)(t % M), p = (int)((t / M) % M);
+        const int nbr = (int)((t / (M * M)) % NBR);
+        const int64_t a = t / ((int64_t)M * M * NBR);
+        int64_t ta = a, b = 0, mul = 1;
+        int mnbr = 0, m5 = 1;
+        bool ok = true;
+        int nb = nbr;
+        for (int i = 0; i < D; ++i) {
+            const int ai = (int)(ta % (H + 1));
+            ta /= (H + 1);
+            const int d = nb % 5 - 2;
+            nb /= 5;
+            ok = ok && ai + d >= 0 && ai + d <= H;
+            b += (int64_t)(ai + d) * mul;
+            mul *= (H + 1);
+            mnbr += (2 - d) * m5;
+            m5 *= 5;
+        }
+        if (!ok || b < a || (b == a && q <= p)) continue;
+        const int64_t t2 = ((b * NBR + mnbr) * M + q) * M + p;
+        const double v = 0.5 * (Es[t] + Es[t2]);
+        Es[t] = v;
+        Es[t2] = v;
+    }
+}
+
+struct NdLevelDev {   // one depth of the factorisation
+    const int32_t *fronts;     // front ids
+    const int64_t *foff;       // prefix of n_pad^2 over the level (entries of F)
+    const int64_t *fbase;      // F offset of each front in the F pool
+    const int32_t *nIp, *nBp;  // padded sizes
+    int nf;
+};
+
+template <int D>
+__device__ __forceinline__ bool nd_stencil(int64_t a, int64_t b, int H, int &nbr) {
+    nbr = 0;
+    int m5 = 1;
+    for (int i = 0; i < D; ++i) {
+        const int ai = (int)(a % (H + 1)), bi = (int)(b % (H + 1));
+        a /= (H + 1);
+        b /= (H + 1);
+        const int d = bi - ai;
+        if (d < -2 || d > 2) return false;
+        nbr += (d + 2) * m5;
+        m5 *= 5;
+    }
+    return true;
+}
+
+// F of every front of a level (column-major, ld n_pad): original E entries with a pivot end,
+// identity on the padded pivots, 0 elsewhere
+template <int D>
+__global__ void k_nd_assemble(NdLevelDev L, const NdFrontDev *fr, const int32_t *nodes, const double *Es, int H,
+                              double *Fpool) {
+    constexpr int M = D * D, NBR = D == 2 ? 25 : 125;
+    const int64_t tot = L.foff[L.nf];
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = L.nf - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (L.foff[mid] <= t) lo = mid;
+            else hi = mid - 1;
+        }
+        const NdFrontDev F = fr[L.fronts[lo]];
+        const int nIp = L.nIp[lo], np = nIp + L.nBp[lo];
+        const int64_t e = t - L.foff[lo];
+        const int p = (int)(e % np), q = (int)(e / np);
+        auto decode = [&](int x, int64_t &node, int &comp, int &kind) {   // kind 0: I, 1: B, 2: pad I, 3: pad B
+            if (x < nIp) {
+                if (x < F.nI) { node = nodes[F.ioff + x / M]; comp = x % M; kind = 0; }
+                else kind = 2;
+            } else {
+                const int y = x - nIp;
+                if (y < F.nB) { node = nodes[F.boff + y / M]; comp = y % M; kind = 1; }
+                else kind = 3;
+            }
+        };
+        int64_t np_ = 0, nq = 0;
+        int cp = 0, cq = 0, kp = 0, kq = 0;
+        decode(p, np_, cp, kp);
+        decode(q, nq, cq, kq);
+        double v = 0.0;
+        int nbr;
+        if (kp <= 1 && kq <= 1 && (kp == 0 || kq == 0) && nd_stencil<D>(np_, nq, H, nbr))
+            v = Es[((np_ * NBR + nbr) * M + cp) * M + cq];
+        else if (kp == 2 && p == q)
+            v = 1.0;
+        Fpool[L.fbase[lo] + e] = v;
+    }
+}
+
+// F_f[map(k), map(l)] += U_child[k, l] for child `which` of every front of the level
+__global__ void k_nd_extend(NdLevelDev L, NdLevelDev Lc, const NdFrontDev *fr, const int32_t *map,
+                            const int32_t *child_slot, int which, double *Fpool) {
+    // child_slot[f] = index of front f within the child level arrays (fronts of depth d+1)
+    for (int i = blockIdx.y; i < L.nf; i += gridDim.y) {
+        const NdFrontDev F = fr[L.fronts[i]];
+        const int kid = which == 0 ? F.kid0 : F.kid1;
+        if (kid < 0) continue;
+        const NdFrontDev K = fr[kid];
+        const int ci = child_slot[kid];
+        const int npc = Lc.nIp[ci] + Lc.nBp[ci], nIpc = Lc.nIp[ci];
+        const int np = L.nIp[i] + L.nBp[i], nIp = L.nIp[i];
+        const double *U = Fpool + Lc.fbase[ci] + nIpc + (int64_t)nIpc * npc;
+        double *Fp = Fpool + L.fbase[i];
+        const int64_t tot = (int64_t)K.nB * K.nB;
+        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+            const int k = (int)(t % K.nB), l = (int)(t / K.nB);
+            int pk = map[K.map + k], pl = map[K.map + l];
+            pk = pk < F.nI ? pk : nIp + (pk - F.nI);
+            pl = pl < F.nI ? pl : nIp + (pl - F.nI);
+            Fp[pk + (int64_t)pl * np] += U[k + (int64_t)l * npc];
+        }
+    }
+}
+
+// copy the pivot block F_II (ld n_pad) into Finv (ld nIp)
+__global__ void k_nd_copy_pivots(const double *Fp, int np, int nIp, double *Fi) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)nIp * nIp; t += (int64_t)gridDim.x * blockDim.x)
+        Fi[t] = Fp[(t % nIp) + (t / nIp) * (int64_t)np];
+}
+
+__global__ void k_nd_transpose(const NdFrontDev *fr, const int64_t *pre, int nf, const double *W, double *Wt) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < pre[nf]; t += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nf - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pre[mid] <= t) lo = mid;
+            else hi = mid - 1;
+        }
+        const NdFrontDev F = fr[lo];
+        const int64_t e = t - pre[lo];
+        const int i = (int)(e % F.nI), b = (int)(e / F.nI);
+        Wt[F.wt + e] = W[F.w + b + (int64_t)i * F.ldW];
+    }
+}
+
+struct NdSolveView {
+    const NdFrontDev *fr;
+    const int32_t *nodes, *map;
+    const double *finv, *w, *wt;
+    double *bi, *u;
+    int m;
+};
+
+// forward elimination of one level: block = (front, 32 B rows), a warp per row over W^t
+__global__ void __launch_bounds__(256) k_nd_fwd(NdSolveView V, const int2 *items, const double *c) {
+    extern __shared__ double sm[];
+    const int2 it = items[blockIdx.x];
+    const NdFrontDev F = V.fr[it.x];
+    const int m = V.m, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *bI = sm, *lB = sm + F.nI;
+    for (int i = threadIdx.x; i < F.nI; i += blockDim.x) bI[i] = c[(int64_t)V.nodes[F.ioff + i / m] * m + i % m];
+    for (int b = threadIdx.x; b < F.nB; b += blockDim.x) lB[b] = 0.0;
+    __syncthreads();
+    for (int o = 0; o < 2; ++o) {
+        const int kid = o == 0 ? F.kid0 : F.kid1;
+        if (kid < 0) continue;
+        const NdFrontDev K = V.fr[kid];
+        for (int k = threadIdx.x; k < K.nB; k += blockDim.x) {
+            const int pos = V.map[K.map + k];
+            const double v = V.u[K.u + k];
+            if (pos < F.nI) bI[pos] += v;
+            else lB[pos - F.nI] += v;
+        }
+        __syncthreads();
+    }
+    if (it.y == 0)
+        for (int i = threadIdx.x; i < F.nI; i += blockDim.x) V.bi[F.bi + i] = bI[i];
+    for (int rr = 0; rr < 4; ++rr) {
+        const int b = it.y + warp * 4 + rr;
+        if (b >= F.nB) break;
+        const double *wb = V.wt + F.wt + (int64_t)b * F.nI;
+        double a = 0.0;
+        for (int i = lane; i < F.nI; i += 32) a = fma(wb[i], bI[i], a);
+        a = warp_sum(a);
+        if (lane == 0) V.u[F.u + b] = lB[b] - a;
+    }
+}
+
+// back substitution of one level: block = (front, 32 I rows), a warp per row
+__global__ void __launch_bounds__(256) k_nd_bwd(NdSolveView V, const int2 *items, double *y) {
+    extern __shared__ double sm[];
+    const int2 it = items[blockIdx.x];
+    const NdFrontDev F = V.fr[it.x];
+    const int m = V.m, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *bI = sm, *xB = sm + F.nI;
+    for (int i = threadIdx.x; i < F.nI; i += blockDim.x) bI[i] = V.bi[F.bi + i];
+    for (int b = threadIdx.x; b < F.nB; b += blockDim.x) xB[b] = y[(int64_t)V.nodes[F.boff + b / m] * m + b % m];
+    __syncthreads();
+    for (int rr = 0; rr < 4; ++rr) {
+        const int i = it.y + warp * 4 + rr;
+        if (i >= F.nI) break;
+        const double *fi = V.finv + F.finv + (int64_t)i * F.ldFi;
+        const double *wi = V.w + F.w + (int64_t)i * F.ldW;
+        double a = 0.0, bsum = 0.0;
+        for (int j = lane; j < F.nI; j += 32) a = fma(fi[j], bI[j], a);
+        for (int b = lane; b < F.nB; b += 32) bsum = fma(wi[b], xB[b], bsum);
+        a = warp_sum(a - bsum);
+        if (lane == 0) y[(int64_t)V.nodes[F.ioff + i / m] * m + i % m] = a;
+    }
+}
+
+// q = c^t y -> *qout
+__global__ void __launch_bounds__(256) k_nd_dot(int64_t n, const double *c, const double *y, double *qout,
+                                                double *partials, unsigned *ticket) {
+    double acc[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        acc[0] = fma(c[i], y[i], acc[0]);
+    reduce_and_finish<1>(acc, partials, ticket, [&](double *t) { *qout = t[0]; });
+}
+
+static void gj_invert(double *A, int64_t n, cudaStream_t s);   // below (blocked Gauss-Jordan, SPD)
+
+struct BlasBatched {
+    int (*GetrfB)(void *, int, double *const[], int, int *, int *, int) = nullptr;
+    int (*GetriB)(void *, int, const double *const[], int, const int *, double *const[], int, int *, int) = nullptr;
+    int (*GemmB)(void *, int, int, int, int, int, const double *, const double *const[], int, const double *const[], int,
+                 const double *, double *const[], int, int) = nullptr;
+};
+static BlasBatched &blas_batched() {
+    static thread_local BlasBatched b = [] {
+        BlasBatched x;
+        Blas &bl = blas();
+        if (!bl.h) return x;
+        x.GetrfB = (decltype(x.GetrfB))dlsym(bl.h, "cublasDgetrfBatched");
+        x.GetriB = (decltype(x.GetriB))dlsym(bl.h, "cublasDgetriBatched");
+        x.GemmB = (decltype(x.GemmB))dlsym(bl.h, "cublasDgemmBatched");
+        return x;
+    }();
+    return b;
+}
+
+template <class T>
+static void upload(DevBuf<T> &d, const std::vector<T> &h, cudaStream_t s) {
+    d.alloc(h.size(), s);
+    if (!h.empty()) CR_CUDA(cudaMemcpyAsync(d.get(), h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+template <int D>
+static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
+    constexpr int M = D * D;
+    CoarseNd &N = C.nd;
+    std::vector<HostFront> F;
+    nd_plan(H, D, F);
+    const int nf = (int)F.size();
+    int maxd = 0;
+    for (auto &f : F) maxd = std::max(maxd, f.depth);
+    std::vector<std::vector<int>> lev(maxd + 1);
+    for (int f = 0; f < nf; ++f) lev[F[f].depth].push_back(f);
+    std::vector<int> parent(nf, -1), slot(nf, 0);
+    for (int f = 0; f < nf; ++f)
+        for (int k = 0; k < 2; ++k)
+            if (F[f].kid[k] >= 0) parent[F[f].kid[k]] = f;
+    // padded sizes: levels with many small fronts are factorised by batched cuBLAS calls
+    std::vector<int> nIp(nf), nBp(nf);
+    std::vector<char> batched(maxd + 1, 0);
+    for (int d = 0; d <= maxd; ++d) {
+        int mi = 0, mb = 0;
+        for (int f : lev[d]) { mi = std::max(mi, (int)F[f].I.size() * M); mb = std::max(mb, (int)F[f].B.size() * M); }
+        batched[d] = lev[d].size() >= 4 && mi <= 256;
+        for (size_t k = 0; k < lev[d].size(); ++k) {
+            const int f = lev[d][k];
+            slot[f] = (int)k;
+            nIp[f] = batched[d] ? mi : (int)F[f].I.size() * M;
+            nBp[f] = batched[d] ? mb : (int)F[f].B.size() * M;
+        }
+    }
+    std::vector<NdFrontDev> fr(nf);
+    std::vector<int32_t> nodes, map;
+    int64_t ofi = 0, ow = 0, owt = 0, obi = 0, ou = 0, fpool = 0, maxn = 0, bytes = 0;
+    std::vector<int64_t> fbase(nf);
+    for (int f = 0; f < nf; ++f) {
+        NdFrontDev &x = fr[f];
+        x.ioff = (int64_t)nodes.size();
+        nodes.insert(nodes.end(), F[f].I.begin(), F[f].I.end());
+        x.boff = (int64_t)nodes.size();
+        nodes.insert(nodes.end(), F[f].B.begin(), F[f].B.end());
+        x.nI = (int32_t)F[f].I.size() * M;
+        x.nB = (int32_t)F[f].B.size() * M;
+        x.kid0 = F[f].kid[0];
+        x.kid1 = F[f].kid[1];
+        x.ldFi = nIp[f];
+        x.ldW = std::max(nBp[f], 1);
+        x.finv = ofi; ofi += (int64_t)nIp[f] * nIp[f];
+        x.w = ow; ow += (int64_t)nBp[f] * nIp[f];
+        x.wt = owt; owt += (int64_t)x.nB * x.nI;
+        x.bi = obi; obi += x.nI;
+        x.u = ou; ou += x.nB;
+        fbase[f] = fpool;
+        fpool += (int64_t)(nIp[f] + nBp[f]) * (nIp[f] + nBp[f]);
+        maxn = std::max<int64_t>(maxn, x.nI + x.nB);
+        bytes += 8 * ((int64_t)x.nI * x.nI + 2 * (int64_t)x.nB * x.nI);
+        // this front's B unknowns -> local unknowns of the parent
+        x.map = (int64_t)map.size();
+        if (parent[f] >= 0) {
+            const HostFront &P = F[parent[f]];
+            for (int32_t v : F[f].B) {
+                int pos;
+                auto it = std::lower_bound(P.I.begin(), P.I.end(), v);
+                if (it != P.I.end() && *it == v) {
+                    pos = (int)(it - P.I.begin());
+                } else {
+                    auto jt = std::find(P.B.begin(), P.B.end(), v);
+                    CR_REQUIRE(jt != P.B.end(), CR_ERR_INVALID_ARG, "coarse ND plan: child boundary node missing in parent");
+                    pos = (int)P.I.size() + (int)(jt - P.B.begin());
+                }
+                for (int c = 0; c < M; ++c) map.push_back(pos * M + c);
+            }
+        }
+    }
+    upload(N.fr, fr, s);
+    upload(N.nodes, nodes, s);
+    upload(N.map, map, s);
+    N.finv.alloc(std::max<int64_t>(ofi, 1), s);
+    N.w.alloc(std::max<int64_t>(ow, 1), s);
+    N.w.zero(s);
+    N.wt.alloc(std::max<int64_t>(owt, 1), s);
+    N.bi.alloc(std::max<int64_t>(obi, 1), s);
+    N.u.alloc(std::max<int64_t>(ou, 1), s);
+    N.m = M;
+    N.maxdepth = maxd;
+    N.nfront = nf;
+    N.smem = maxn * (int64_t)sizeof(double);
+    N.bytes = bytes;
+    CR_REQUIRE(N.smem <= 227 * 1024, CR_ERR_INVALID_ARG, "coarse ND front too large for shared memory");
+    if (N.smem > 48 * 1024) {
+        CR_CUDA(cudaFuncSetAttribute(k_nd_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)N.smem));
+        CR_CUDA(cudaFuncSetAttribute(k_nd_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)N.smem));
+    }
+    // work items
+    N.fwd.clear(); N.bwd.clear(); N.nfwd.assign(maxd + 1, 0); N.nbwd.assign(maxd + 1, 0);
+    N.fwd.resize(maxd + 1); N.bwd.resize(maxd + 1);
+    for (int d = 0; d <= maxd; ++d) {
+        std::vector<int2> a, b;
+        for (int f : lev[d]) {
+            for (int r = 0; r < std::max(fr[f].nB, 1); r += 32) a.push_back(make_int2(f, r));
+            for (int r = 0; r < fr[f].nI; r += 32) b.push_back(make_int2(f, r));
+        }
+        upload(N.fwd[d], a, s);
+        upload(N.bwd[d], b, s);
+        N.nfwd[d] = (int)a.size();
+        N.nbwd[d] = (int)b.size();
+    }
+    // numeric factorisation, deepest level first
+    DevBuf<double> Fp;
+    Fp.alloc(std::max<int64_t>(fpool, 1), s);
+    std::vector<DevBuf<int32_t>> lfronts(maxd + 2), lnIp(maxd + 2), lnBp(maxd + 2);
+    std::vector<DevBuf<int64_t>> lfoff(maxd + 2), lfbase(maxd + 2);
+    std::vector<NdLevelDev> LV(maxd + 2);
+    std::vector<int32_t> hslot(slot.begin(), slot.end());
+    DevBuf<int32_t> dslot;
+    upload(dslot, hslot, s);
+    BlasBatched &bb = blas_batched();
+    Blas &bl = blas();
+    CR_REQUIRE(bl.handle && bb.GemmB && bb.GetrfB && bb.GetriB, CR_ERR_CUDA, "cuBLAS batched routines unavailable");
+    const int T = 256;
+    for (int d = maxd; d >= 0; --d) {
+        const auto &L = lev[d];
+        std::vector<int32_t> hf(L.begin(), L.end()), hi(L.size()), hb(L.size());
+        std::vector<int64_t> hoff(L.size() + 1, 0), hbase(L.size());
+        for (size_t k = 0; k < L.size(); ++k) {
+            const int f = L[k];
+            hi[k] = nIp[f];
+            hb[k] = nBp[f];
+            const int64_t np = nIp[f] + nBp[f];
+            hoff[k + 1] = hoff[k] + np * np;
+            hbase[k] = fbase[f];
+        }
+        upload(lfronts[d], hf, s); upload(lnIp[d], hi, s); upload(lnBp[d], hb, s);
+        upload(lfoff[d], hoff, s); upload(lfbase[d], hbase, s);
+        LV[d] = NdLevelDev{lfronts[d].get(), lfoff[d].get(), lfbase[d].get(), lnIp[d].get(), lnBp[d].get(), (int)L.size()};
+        k_nd_assemble<D><<<grid_for(hoff.back(), T, 16), T, 0, s>>>(LV[d], N.fr.get(), N.nodes.get(), Es, H, Fp.get());
+        CR_CHECK_LAUNCH();
+        if (d < maxd) {
+            int64_t mxb = 1;
+            for (int f : L)
+                for (int k = 0; k < 2; ++k)
+                    if (F[f].kid[k] >= 0) mxb = std::max<int64_t>(mxb, (int64_t)fr[F[f].kid[k]].nB * fr[F[f].kid[k]].nB);
+            dim3 g((unsigned)std::min<int64_t>((mxb + T - 1) / T, 4096), (unsigned)std::min<size_t>(L.size(), 65535));
+            for (int which = 0; which < 2; ++which) {
+                k_nd_extend<<<g, T, 0, s>>>(LV[d], LV[d + 1], N.fr.get(), N.map.get(), dslot.get(), which, Fp.get());
+                CR_CHECK_LAUNCH();
+            }
+        }
+        const double one = 1.0, zero = 0.0, mone = -1.0;
+        bl.SetStream(bl.handle, s);
+        if (batched[d]) {
+            const int nb = (int)L.size(), ni = nIp[L[0]], nbp = nBp[L[0]], np = ni + nbp;
+            std::vector<double *> pA(nb), pFi(nb), pFB(nb), pW(nb), pFIB(nb), pFBB(nb);
+            for (int k = 0; k < nb; ++k) {
+                const int f = L[k];
+                double *base = Fp.get() + fbase[f];
+                pA[k] = base;
+                pFi[k] = N.finv.get() + fr[f].finv;
+                pFB[k] = base + ni;
+                pW[k] = N.w.get() + fr[f].w;
+                pFIB[k] = base + (int64_t)ni * np;
+                pFBB[k] = base + ni + (int64_t)ni * np;
+            }
+            DevBuf<double *> dA, dFi, dFB, dW, dFIB, dFBB;
+            upload(dA, pA, s); upload(dFi, pFi, s); upload(dFB, pFB, s);
+            upload(dW, pW, s); upload(dFIB, pFIB, s); upload(dFBB, pFBB, s);
+            DevBuf<int> piv, info;
+            piv.alloc((size_t)ni * nb, s);
+            info.alloc(nb, s);
+            info.zero(s);
+            CR_REQUIRE(bb.GetrfB(bl.handle, ni, dA.get(), np, piv.get(), info.get(), nb) == 0, CR_ERR_CUDA, "cublasDgetrfBatched failed");
+            CR_REQUIRE(bb.GetriB(bl.handle, ni, dA.get(), np, piv.get(), dFi.get(), ni, info.get(), nb) == 0, CR_ERR_CUDA,
+                       "cublasDgetriBatched failed");
+            std::vector<int> hinfo(nb);
+            CR_CUDA(cudaMemcpyAsync(hinfo.data(), info.get(), nb * sizeof(int), cudaMemcpyDeviceToHost, s));
+            CR_CUDA(cudaStreamSynchronize(s));
+            for (int v : hinfo) CR_REQUIRE(v == 0, CR_ERR_SINGULAR_LOCAL, "coarse ND front is singular");
+            if (nbp > 0) {
+                CR_REQUIRE(bb.GemmB(bl.handle, 0, 0, nbp, ni, ni, &one, dFB.get(), np, dFi.get(), ni, &zero, dW.get(), nbp, nb) == 0,
+                           CR_ERR_CUDA, "cublasDgemmBatched failed");
+                CR_REQUIRE(bb.GemmB(bl.handle, 0, 0, nbp, nbp, ni, &mone, dW.get(), nbp, dFIB.get(), np, &one, dFBB.get(), np, nb) == 0,
+                           CR_ERR_CUDA, "cublasDgemmBatched failed");
+            }
+            CR_CUDA(cudaStreamSynchronize(s));   // the pointer arrays are freed at scope exit
+        } else {
+            for (int f : L) {
+                const int ni = nIp[f], nbp = nBp[f], np = ni + nbp;
+                double *base = Fp.get() + fbase[f];
+                double *Fi = N.finv.get() + fr[f].finv;
+                k_nd_copy_pivots<<<grid_for((int64_t)ni * ni, T, 16), T, 0, s>>>(base, np, ni, Fi);
+                CR_CHECK_LAUNCH();
+                gj_invert(Fi, ni, s);
+                if (nbp > 0) {
+                    dgemm(s, nbp, ni, ni, 1.0, base + ni, np, Fi, ni, 0.0, N.w.get() + fr[f].w, nbp);
+                    dgemm(s, nbp, nbp, ni, -1.0, N.w.get() + fr[f].w, nbp, base + (int64_t)ni * np, np, 1.0,
+                          base + ni + (int64_t)ni * np, np);
+                }
+            }
+        }
+    }
+    // W^t (nI x nB, ld nI) for the forward pass: a warp per B row then reads contiguously
+    {
+        std::vector<int64_t> pre(nf + 1, 0);
+        for (int f = 0; f < nf; ++f) pre[f + 1] = pre[f] + (int64_t)fr[f].nB * fr[f].nI;
+        DevBuf<int64_t> dpre;
+        upload(dpre, pre, s);
+        if (pre[nf] > 0) {
+            k_nd_transpose<<<grid_for(pre[nf], T, 16), T, 0, s>>>(N.fr.get(), dpre.get(), nf, N.w.get(), N.wt.get());
+            CR_CHECK_LAUNCH();
+        }
+        CR_CUDA(cudaStreamSynchronize(s));
+    }
+    N.on = true;
+}
+
+// y = E^{-1} c by the ND fronts, q = c^t y
+static void nd_solve(const CoarseOp &C, const double *c, double *y, double *qout, double *partials, unsigned *ticket,
+                     cudaStream_t s) {
+    const CoarseNd &N = C.nd;
+    NdSolveView V{N.fr.get(), N.nodes.get(), N.map.get(), N.finv.get(), N.w.get(), N.wt.get(),
+                  const_cast<double *>(N.bi.get()), const_cast<double *>(N.u.get()), N.m};
+    for (int d = N.maxdepth; d >= 0; --d) {
+        k_nd_fwd<<<N.nfwd[d], 256, N.smem, s>>>(V, N.fwd[d].get(), c);
+        CR_CHECK_LAUNCH();
+    }
+    for (int d = 0; d <= N.maxdepth; ++d) {
+        k_nd_bwd<<<N.nbwd[d], 256, N.smem, s>>>(V, N.bwd[d].get(), y);
+        CR_CHECK_LAUNCH();
+    }
+    k_nd_dot<<<occ_grid(k_nd_dot, 256, C.nE), 256, 0, s>>>(C.nE, c, y, qout, partials, ticket);
+    CR_CHECK_LAUNCH();
+}
+
+
+// blocked Gauss-Jordan inversion in place of an SPD n x n matrix (row- or column-major: a
+// row-major M is the column-major M^t for cuBLAS):
+//   Y = A[K,:];  X = A[:,K] Pk;  A -= X Y;  A[K,:] = Pk Y;  A[:,K] = -X, A[K,K] = Pk
+static void gj_invert(double *A, int64_t n64, cudaStream_t s) {
+    const int T = 256;
+    DevBuf<double> Pk, X, Yb;
+    Pk.alloc(kGB * kGB, s);
+    X.alloc(n64 * kGB, s);
+    Yb.alloc(n64 * kGB, s);
+    DevBuf<int> bad;
+    bad.alloc(1, s);
+    bad.zero(s);
+    const int n = (int)n64;
+    for (int64_t k0 = 0; k0 < n64; k0 += kGB) {
+        const int b = (int)std::min<int64_t>(kGB, n64 - k0);
+        k_gj_diag<<<1, 256, 0, s>>>(A, n64, k0, b, Pk.get(), bad.get());
+        CR_CUDA(cudaMemcpyAsync(Yb.get(), A + k0 * n64, (size_t)b * n64 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        dgemm(s, b, n, b, 1.0, Pk.get(), b, A + k0, n, 0.0, X.get(), b);            // X^t = Pk^t A[:,K]^t
+        dgemm(s, n, n, b, -1.0, Yb.get(), n, X.get(), b, 1.0, A, n);                 // A^t -= Y^t X^t
+        dgemm(s, n, b, b, 1.0, Yb.get(), n, Pk.get(), b, 0.0, A + k0 * n64, n);     // A[K,:]^t = Y^t Pk^t
+        k_gj_cols<<<grid_for(n64 * b, T), T, 0, s>>>(A, n64, k0, b, Pk.get(), X.get());
+    }
+    CR_CHECK_LAUNCH();
+    int hb = 0;
+    CR_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    CR_CUDA(cudaStreamSynchronize(s));
+    CR_REQUIRE(hb == 0, CR_ERR_SINGULAR_LOCAL, "coarse matrix Z^t G Z is not positive definite");
+}
+
 template <int D>
 static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const double *, double *, int)> &applyG,
                            cudaStream_t s) {
@@ -437,8 +1067,20 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
     C.c.alloc(C.nE, s);
     C.y.alloc(C.nE, s);
     C.gpart.alloc((size_t)kSMs * 32, s);
-    C.Einv.alloc(C.nE * C.nE, s);
-    C.Einv.zero(s);
+    // dense E^{-1} (one bandwidth-bound GEMV per iteration) while it is at most 8000^2 doubles,
+    // the ND sparse direct solve beyond (its ~2 log2(H) dependent levels cost latency, its bytes
+    // grow only like nE log nE).  CR_COARSE_DENSE=1 / CR_COARSE_ND=1 force one (tests).
+    const bool dense = std::getenv("CR_COARSE_DENSE") ? true : std::getenv("CR_COARSE_ND") ? false : C.nE <= 8000;
+    C.nd = CoarseNd();
+    constexpr int NBR = D == 2 ? 25 : 125;
+    DevBuf<double> Es;
+    if (dense) {
+        C.Einv.alloc(C.nE * C.nE, s);
+        C.Einv.zero(s);
+    } else {
+        Es.alloc((size_t)nnode * NBR * D * D * D * D, s);
+        Es.zero(s);
+    }
     // E = Z^t G Z by colours
     CoarseView V = C.view();
     DevBuf<double> z, Y;
@@ -458,44 +1100,30 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
                 k_coarse_gather<D><<<grid_for(C.nE, T), T, 0, s>>>(V, C.part.get(), C.c.get());
                 CR_CHECK_LAUNCH();
                 if (h->part.on) h->comm->impl->allreduce(C.c.get(), (int)C.nE, false, s);
-                k_coarse_scatterE<D><<<grid_for(C.nE, T), T, 0, s>>>(C.nE, H, colour, k, l, C.c.get(), C.Einv.get());
+                if (dense)
+                    k_coarse_scatterE<D><<<grid_for(C.nE, T), T, 0, s>>>(C.nE, H, colour, k, l, C.c.get(), C.Einv.get());
+                else
+                    k_coarse_scatterEs<D><<<grid_for(C.nE, T), T, 0, s>>>(C.nE, H, colour, k, l, C.c.get(), Es.get());
                 CR_CHECK_LAUNCH();
             }
     tr.mark("coarse: E = Z^t G Z");
-    k_symmetrize<<<grid_for(C.nE * C.nE, T, 64), T, 0, s>>>(C.Einv.get(), C.nE);
-    CR_CHECK_LAUNCH();
-    // blocked Gauss-Jordan on the row-major E (a row-major M is the column-major M^t for cuBLAS):
-    //   Y = E[K,:];  X = E[:,K] Pk;  E -= X Y;  E[K,:] = Pk Y;  E[:,K] = -X, E[K,K] = Pk
-    DevBuf<double> Pk, X, Yb;
-    Pk.alloc(kGB * kGB, s);
-    X.alloc(C.nE * kGB, s);
-    Yb.alloc(C.nE * kGB, s);
-    DevBuf<int> bad;
-    bad.alloc(1, s);
-    bad.zero(s);
-    const int n = (int)C.nE;
-    for (int64_t k0 = 0; k0 < C.nE; k0 += kGB) {
-        const int b = (int)std::min<int64_t>(kGB, C.nE - k0);
-        double *Ep = C.Einv.get();
-        k_gj_diag<<<1, 256, 0, s>>>(Ep, C.nE, k0, b, Pk.get(), bad.get());
-        CR_CUDA(cudaMemcpyAsync(Yb.get(), Ep + k0 * C.nE, (size_t)b * C.nE * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        dgemm(s, b, n, b, 1.0, Pk.get(), b, Ep + k0, n, 0.0, X.get(), b);            // X^t = Pk^t E[:,K]^t
-        dgemm(s, n, n, b, -1.0, Yb.get(), n, X.get(), b, 1.0, Ep, n);                  // E^t -= Y^t X^t
-        dgemm(s, n, b, b, 1.0, Yb.get(), n, Pk.get(), b, 0.0, Ep + k0 * C.nE, n);     // E[K,:]^t = Y^t Pk^t
-        k_gj_cols<<<grid_for(C.nE * b, T), T, 0, s>>>(Ep, C.nE, k0, b, Pk.get(), X.get());
+    if (dense) {
+        k_symmetrize<<<grid_for(C.nE * C.nE, T, 64), T, 0, s>>>(C.Einv.get(), C.nE);
+        CR_CHECK_LAUNCH();
+        gj_invert(C.Einv.get(), C.nE, s);
+        tr.mark("coarse: E^-1 (Gauss-Jordan)");
+    } else {
+        k_es_symmetrize<D><<<grid_for((int64_t)nnode * NBR * D * D * D * D, T, 16), T, 0, s>>>(nnode, H, Es.get());
+        CR_CHECK_LAUNCH();
+        nd_setup<D>(C, Es.get(), H, s);
+        tr.mark("coarse: E factorised (nested dissection)");
     }
-    CR_CHECK_LAUNCH();
-    int hb = 0;
-    CR_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-    CR_CUDA(cudaStreamSynchronize(s));
-    tr.mark("coarse: E^-1 (Gauss-Jordan)");
-    CR_REQUIRE(hb == 0, CR_ERR_SINGULAR_LOCAL, "coarse matrix Z^t G Z is not positive definite");
     C.built = H;
 }
 
 void build_coarse(cr_hybrid_s *h, int H, const std::function<void(const double *, double *, int)> &applyG,
                   cudaStream_t s) {
-    CR_REQUIRE(H >= 1 && H <= 64, CR_ERR_INVALID_ARG, "coarse grid intervals must be in [1, 64]");
+    CR_REQUIRE(H >= 1 && H <= 256, CR_ERR_INVALID_ARG, "coarse grid intervals must be in [1, 256]");
     const int D = h->G.d;
     // at least ~4 faces per coarse unknown: a coarse grid finer than the mesh makes Z rank-deficient
     const double nglob = (double)(h->part.on ? h->part.nglobal : h->G.nrows);
@@ -530,6 +1158,10 @@ void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double
     }
     CR_CHECK_LAUNCH();
     if (h->part.on) h->comm->impl->allreduce(C.c.get(), (int)C.nE, false, s);
+    if (C.nd.on) {
+        nd_solve(C, C.c.get(), C.y.get(), qout, partials, ticket, s);
+        return;
+    }
     k_coarse_gemv<<<occ_grid(k_coarse_gemv, 128, C.nE * 128), 128, 0, s>>>(C.Einv.get(), C.nE, C.c.get(), C.y.get(),
                                                                            qout, partials, ticket);
     CR_CHECK_LAUNCH();

@@ -202,6 +202,29 @@ struct AfwPrec {
 };
 enum { AFW_SPD = 0, AFW_ABS = 1, AFW_GEN = 2 };
 
+// sparse direct coarse solve (coarse.cu, "ND"): nested dissection of the coarse node grid into
+// fronts (separator slabs 2 nodes thick: Z^t G Z couples nodes up to 2 apart), multifrontal
+// elimination with explicit front inverses.  Per front f (unknowns I = its pivots, B = the
+// ancestors' unknowns it couples to): Finv = F_II^{-1}, W = F_BI Finv (column-major, ld ldW).
+struct NdFrontDev {
+    int64_t ioff, boff;       // into nodes[]: I nodes, B nodes
+    int64_t finv, w, wt, bi, u;   // into the pools (wt: W^t, nI x nB, ld nI)
+    int64_t map;              // into map[]: this front's B unknown -> parent local unknown
+    int32_t nI, nB;           // unknowns
+    int32_t kid0, kid1;       // child fronts (-1: none)
+    int32_t ldFi, ldW;        // leading dimensions of Finv (>= nI) and W (>= nB)
+};
+struct CoarseNd {
+    bool on = false;
+    int m = 0, maxdepth = 0;
+    int64_t nfront = 0, smem = 0, bytes = 0;   // dynamic shared bytes of the solve; Finv + W bytes
+    cr::DevBuf<NdFrontDev> fr;
+    cr::DevBuf<int32_t> nodes, map;
+    cr::DevBuf<double> finv, w, wt, bi, u;
+    std::vector<cr::DevBuf<int2>> fwd, bwd;    // per depth: (front, first row) work items
+    std::vector<int> nfwd, nbwd;
+};
+
 // two-level coarse correction (coarse.cu)
 struct CoarseOp {
     int built = 0;               // H it was built for (0 = not built)
@@ -213,6 +236,7 @@ struct CoarseOp {
     cr::DevBuf<int64_t> chunk_start, cell_chunk;
     cr::DevBuf<double> part, c, y, Einv;
     cr::DevBuf<double> gpart;    // block partials of the coarse GEMV (its own: it runs concurrently)
+    CoarseNd nd;                 // sparse direct solve (default); Einv (dense inverse) when off
     cr::CoarseView view() const {
         return cr::CoarseView{g, fx.get(), fa.get(), perm.get(), chunk_start.get(), cell_chunk.get(), nE};
     }

@@ -208,7 +208,7 @@ def test_config4_3d_full_size():
     eG, eS = sampled_rows(mo, prm, data, E, hg, 100)
     assert eG <= 1e-12 and eS <= 1e-12, (eG, eS)
     W = torch.zeros(hg.n_rows, dtype=torch.float64, device=DEV)
-    rep = P.cr_solve(hg, W, "pcg_afw2", rtol=cfg.rtol, check_every=64, matrix_free=1, coarse=8)
+    rep = P.cr_solve(hg, W, "pcg_afw2", rtol=cfg.rtol, check_every=64, matrix_free=1, coarse=16)   # ND coarse solve
     assert rep["converged"] and rep["rel_res_true"] <= cfg.rtol
     U, Pp, diag = P.cr_recover(hg, W)
     eP, eU = sampled_recovery(mo, prm, data, E, W.cpu().numpy(), U.cpu().numpy(), Pp.cpu().numpy(), 200)
