@@ -616,78 +616,123 @@ __global__ void k_nd_transpose(const NdFrontDev *fr, const int64_t *pre, int nf,
     }
 }
 
-struct NdSolveView {
-    const NdFrontDev *fr;
-    const int32_t *nodes, *map;
-    const double *finv, *w, *wt;
-    double *bi, *u;
-    int m;
+
+// software grid barrier (all CTAs of the launch are co-resident: grid <= one wave).  Polls with
+// gpu-scope acquire loads (a volatile load is a system-scope strong load: far slower).
+__device__ __forceinline__ unsigned nd_ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void nd_grid_barrier(unsigned *bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = nd_ld_acquire(bar + 1);
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (nd_ld_acquire(bar + 1) == g) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// lane's share of sum_i a[i] x[i] (i = lane, lane + 32, ...): 4 independent loads in flight
+__device__ __forceinline__ double nd_dot_lane(const double *__restrict__ a, const double *x, int n, int lane) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int i = lane;
+    for (; i + 96 < n; i += 128) {
+        s0 = fma(a[i], __ldcg(x + i), s0);
+        s1 = fma(a[i + 32], __ldcg(x + i + 32), s1);
+        s2 = fma(a[i + 64], __ldcg(x + i + 64), s2);
+        s3 = fma(a[i + 96], __ldcg(x + i + 96), s3);
+    }
+    for (; i < n; i += 32) s0 = fma(a[i], __ldcg(x + i), s0);
+    return (s0 + s1) + (s2 + s3);
+}
+// the same with x gathered: sum_i a[i] x[idx[i]]
+__device__ __forceinline__ double nd_dot_lane_g(const double *__restrict__ a, const double *x, const int32_t *idx, int n,
+                                                int lane) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int i = lane;
+    for (; i + 96 < n; i += 128) {
+        const int j0 = idx[i], j1 = idx[i + 32], j2 = idx[i + 64], j3 = idx[i + 96];
+        s0 = fma(a[i], __ldcg(x + j0), s0);
+        s1 = fma(a[i + 32], __ldcg(x + j1), s1);
+        s2 = fma(a[i + 64], __ldcg(x + j2), s2);
+        s3 = fma(a[i + 96], __ldcg(x + j3), s3);
+    }
+    for (; i < n; i += 32) s0 = fma(a[i], __ldcg(x + idx[i]), s0);
+    return (s0 + s1) + (s2 + s3);
+}
+
+constexpr int kNdMaxLev = 48;
+struct NdSched {
+    int nlev;
+    int aoff[kNdMaxLev + 1];   // forward level L (depth maxd - L): local rhs assembly entries
+    int boff[kNdMaxLev + 1];   //                                   B rows
+    int coff[kNdMaxLev + 1];   // backward depth L: I rows
 };
 
-// forward elimination of one level: block = (front, 32 B rows), a warp per row over W^t
-__global__ void __launch_bounds__(256) k_nd_fwd(NdSolveView V, const int2 *items, const double *c) {
-    extern __shared__ double sm[];
-    const int2 it = items[blockIdx.x];
-    const NdFrontDev F = V.fr[it.x];
-    const int m = V.m, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double *bI = sm, *lB = sm + F.nI;
-    for (int i = threadIdx.x; i < F.nI; i += blockDim.x) bI[i] = c[(int64_t)V.nodes[F.ioff + i / m] * m + i % m];
-    for (int b = threadIdx.x; b < F.nB; b += blockDim.x) lB[b] = 0.0;
-    __syncthreads();
-    for (int o = 0; o < 2; ++o) {
-        const int kid = o == 0 ? F.kid0 : F.kid1;
-        if (kid < 0) continue;
-        const NdFrontDev K = V.fr[kid];
-        for (int k = threadIdx.x; k < K.nB; k += blockDim.x) {
-            const int pos = V.map[K.map + k];
-            const double v = V.u[K.u + k];
-            if (pos < F.nI) bI[pos] += v;
-            else lB[pos - F.nI] += v;
+struct NdSolveView {
+    const NdFrontDev *fr;
+    const int2 *inv;
+    const int32_t *uidx;
+    const double *finv, *w, *wt;
+    double *bi, *lb, *u;
+    const int2 *la, *lbr, *lc;
+};
+
+// The whole solve E y = c in one persistent launch.  Per forward level: (A) every local
+// unknown of the level's fronts: b = c (pivots) + child 0's u + child 1's u (fixed order);
+// (B) a warp per B row: u = b_B - W b_I.  Per backward level: (C) a warp per pivot row:
+// y_I = Finv b_I - W^t y_B.  Levels and phases are separated by grid barriers; data written
+// by other CTAs is read through L2 (__ldcg).  Then q = c^t y.
+__global__ void __launch_bounds__(256) k_nd_solve(NdSolveView V, NdSched S, const double *c, double *y, unsigned *bar,
+                                                  int64_t nE, double *qout, double *partials, unsigned *ticket) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+    const int64_t gw = gt >> 5, nw = gs >> 5;
+    for (int L = 0; L < S.nlev; ++L) {
+        for (int64_t k = S.aoff[L] + gt; k < S.aoff[L + 1]; k += gs) {
+            const int2 e = V.la[k];
+            const NdFrontDev F = V.fr[e.x];
+            const int2 ch = V.inv[F.inv + e.y];
+            double v = e.y < F.nI ? c[V.uidx[F.uoff + e.y]] : 0.0;
+            if (ch.x >= 0) v += __ldcg(V.u + ch.x);
+            if (ch.y >= 0) v += __ldcg(V.u + ch.y);
+            if (e.y < F.nI) V.bi[F.bi + e.y] = v;
+            else V.lb[F.lb + e.y - F.nI] = v;
         }
-        __syncthreads();
+        nd_grid_barrier(bar);
+        if (S.boff[L + 1] > S.boff[L]) {
+            for (int64_t k = S.boff[L] + gw; k < S.boff[L + 1]; k += nw) {
+                const int2 e = V.lbr[k];
+                const NdFrontDev F = V.fr[e.x];
+                const double a = warp_sum(nd_dot_lane(V.wt + F.wt + (int64_t)e.y * F.nI, V.bi + F.bi, F.nI, lane));
+                if (lane == 0) V.u[F.u + e.y] = __ldcg(V.lb + F.lb + e.y) - a;
+            }
+            nd_grid_barrier(bar);
+        }
     }
-    if (it.y == 0)
-        for (int i = threadIdx.x; i < F.nI; i += blockDim.x) V.bi[F.bi + i] = bI[i];
-    for (int rr = 0; rr < 4; ++rr) {
-        const int b = it.y + warp * 4 + rr;
-        if (b >= F.nB) break;
-        const double *wb = V.wt + F.wt + (int64_t)b * F.nI;
-        double a = 0.0;
-        for (int i = lane; i < F.nI; i += 32) a = fma(wb[i], bI[i], a);
-        a = warp_sum(a);
-        if (lane == 0) V.u[F.u + b] = lB[b] - a;
+    for (int L = 0; L < S.nlev; ++L) {
+        for (int64_t k = S.coff[L] + gw; k < S.coff[L + 1]; k += nw) {
+            const int2 e = V.lc[k];
+            const NdFrontDev F = V.fr[e.x];
+            const double pa = nd_dot_lane(V.finv + F.finv + (int64_t)e.y * F.ldFi, V.bi + F.bi, F.nI, lane);
+            const double pb = nd_dot_lane_g(V.w + F.w + (int64_t)e.y * F.ldW, y, V.uidx + F.uoff + F.nI, F.nB, lane);
+            const double a = warp_sum(pa - pb);
+            if (lane == 0) y[V.uidx[F.uoff + e.y]] = a;
+        }
+        nd_grid_barrier(bar);
     }
-}
-
-// back substitution of one level: block = (front, 32 I rows), a warp per row
-__global__ void __launch_bounds__(256) k_nd_bwd(NdSolveView V, const int2 *items, double *y) {
-    extern __shared__ double sm[];
-    const int2 it = items[blockIdx.x];
-    const NdFrontDev F = V.fr[it.x];
-    const int m = V.m, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double *bI = sm, *xB = sm + F.nI;
-    for (int i = threadIdx.x; i < F.nI; i += blockDim.x) bI[i] = V.bi[F.bi + i];
-    for (int b = threadIdx.x; b < F.nB; b += blockDim.x) xB[b] = y[(int64_t)V.nodes[F.boff + b / m] * m + b % m];
-    __syncthreads();
-    for (int rr = 0; rr < 4; ++rr) {
-        const int i = it.y + warp * 4 + rr;
-        if (i >= F.nI) break;
-        const double *fi = V.finv + F.finv + (int64_t)i * F.ldFi;
-        const double *wi = V.w + F.w + (int64_t)i * F.ldW;
-        double a = 0.0, bsum = 0.0;
-        for (int j = lane; j < F.nI; j += 32) a = fma(fi[j], bI[j], a);
-        for (int b = lane; b < F.nB; b += 32) bsum = fma(wi[b], xB[b], bsum);
-        a = warp_sum(a - bsum);
-        if (lane == 0) y[(int64_t)V.nodes[F.ioff + i / m] * m + i % m] = a;
-    }
-}
-
-// q = c^t y -> *qout
-__global__ void __launch_bounds__(256) k_nd_dot(int64_t n, const double *c, const double *y, double *qout,
-                                                double *partials, unsigned *ticket) {
     double acc[1] = {0.0};
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        acc[0] = fma(c[i], y[i], acc[0]);
+    for (int64_t i = gt; i < nE; i += gs) acc[0] = fma(c[i], __ldcg(y + i), acc[0]);
     reduce_and_finish<1>(acc, partials, ticket, [&](double *t) { *qout = t[0]; });
 }
 
@@ -749,7 +794,8 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
     }
     std::vector<NdFrontDev> fr(nf);
     std::vector<int32_t> nodes, map;
-    int64_t ofi = 0, ow = 0, owt = 0, obi = 0, ou = 0, fpool = 0, maxn = 0, bytes = 0;
+    int64_t ofi = 0, ow = 0, owt = 0, obi = 0, ou = 0, olb = 0, oinv = 0, fpool = 0, maxn = 0, bytes = 0;
+    std::vector<int32_t> uidx;
     std::vector<int64_t> fbase(nf);
     for (int f = 0; f < nf; ++f) {
         NdFrontDev &x = fr[f];
@@ -768,6 +814,13 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
         x.wt = owt; owt += (int64_t)x.nB * x.nI;
         x.bi = obi; obi += x.nI;
         x.u = ou; ou += x.nB;
+        x.lb = olb; olb += x.nB;
+        x.inv = oinv; oinv += x.nI + x.nB;
+        x.uoff = (int64_t)uidx.size();
+        for (int32_t v : F[f].I)
+            for (int cc = 0; cc < M; ++cc) uidx.push_back(v * M + cc);
+        for (int32_t v : F[f].B)
+            for (int cc = 0; cc < M; ++cc) uidx.push_back(v * M + cc);
         fbase[f] = fpool;
         fpool += (int64_t)(nIp[f] + nBp[f]) * (nIp[f] + nBp[f]);
         maxn = std::max<int64_t>(maxn, x.nI + x.nB);
@@ -790,9 +843,24 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
             }
         }
     }
+    // children's u entries landing on each local unknown of their parent (absolute u indices)
+    std::vector<int2> inv(oinv, make_int2(-1, -1));
+    for (int f = 0; f < nf; ++f)
+        for (int k = 0; k < 2; ++k) {
+            const int kid = F[f].kid[k];
+            if (kid < 0) continue;
+            for (int q = 0; q < fr[kid].nB; ++q) {
+                const int pos = map[fr[kid].map + q];
+                int2 &e = inv[fr[f].inv + pos];
+                (k == 0 ? e.x : e.y) = (int)(fr[kid].u + q);
+            }
+        }
     upload(N.fr, fr, s);
     upload(N.nodes, nodes, s);
     upload(N.map, map, s);
+    upload(N.inv, inv, s);
+    upload(N.uidx, uidx, s);
+    N.lb.alloc(std::max<int64_t>(olb, 1), s);
     N.finv.alloc(std::max<int64_t>(ofi, 1), s);
     N.w.alloc(std::max<int64_t>(ow, 1), s);
     N.w.zero(s);
@@ -802,26 +870,35 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
     N.m = M;
     N.maxdepth = maxd;
     N.nfront = nf;
-    N.smem = maxn * (int64_t)sizeof(double);
     N.bytes = bytes;
-    CR_REQUIRE(N.smem <= 227 * 1024, CR_ERR_INVALID_ARG, "coarse ND front too large for shared memory");
-    if (N.smem > 48 * 1024) {
-        CR_CUDA(cudaFuncSetAttribute(k_nd_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)N.smem));
-        CR_CUDA(cudaFuncSetAttribute(k_nd_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)N.smem));
-    }
-    // work items
-    N.fwd.clear(); N.bwd.clear(); N.nfwd.assign(maxd + 1, 0); N.nbwd.assign(maxd + 1, 0);
-    N.fwd.resize(maxd + 1); N.bwd.resize(maxd + 1);
-    for (int d = 0; d <= maxd; ++d) {
-        std::vector<int2> a, b;
-        for (int f : lev[d]) {
-            for (int r = 0; r < std::max(fr[f].nB, 1); r += 32) a.push_back(make_int2(f, r));
-            for (int r = 0; r < fr[f].nI; r += 32) b.push_back(make_int2(f, r));
+    // work lists: forward by level deepest first (A: local unknowns, B: B rows), backward root
+    // first (C: pivot rows)
+    CR_REQUIRE(maxd + 1 <= kNdMaxLev, CR_ERR_INVALID_ARG, "coarse ND tree too deep");
+    {
+        std::vector<int2> la, lbr, lc;
+        N.aoff.assign(maxd + 2, 0);
+        N.boff.assign(maxd + 2, 0);
+        N.coff.assign(maxd + 2, 0);
+        for (int L = 0; L <= maxd; ++L) {
+            for (int f : lev[maxd - L]) {
+                for (int p = 0; p < fr[f].nI + fr[f].nB; ++p) la.push_back(make_int2(f, p));
+                for (int b = 0; b < fr[f].nB; ++b) lbr.push_back(make_int2(f, b));
+            }
+            for (int f : lev[L])
+                for (int i = 0; i < fr[f].nI; ++i) lc.push_back(make_int2(f, i));
+            N.aoff[L + 1] = (int)la.size();
+            N.boff[L + 1] = (int)lbr.size();
+            N.coff[L + 1] = (int)lc.size();
         }
-        upload(N.fwd[d], a, s);
-        upload(N.bwd[d], b, s);
-        N.nfwd[d] = (int)a.size();
-        N.nbwd[d] = (int)b.size();
+        upload(N.la, la, s);
+        upload(N.lbr, lbr, s);
+        upload(N.lc, lc, s);
+        N.bar.alloc(2, s);
+        N.bar.zero(s);
+        int occ = 0;
+        CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_nd_solve, 256, 0));
+        CR_REQUIRE(occ >= 1, CR_ERR_INVALID_ARG, "coarse ND solve kernel does not fit on an SM");
+        N.grid = kSMs * std::min(occ, 8);   // more resident warps: the phases are latency-bound
     }
     // numeric factorisation, deepest level first
     DevBuf<double> Fp;
@@ -935,17 +1012,17 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
 static void nd_solve(const CoarseOp &C, const double *c, double *y, double *qout, double *partials, unsigned *ticket,
                      cudaStream_t s) {
     const CoarseNd &N = C.nd;
-    NdSolveView V{N.fr.get(), N.nodes.get(), N.map.get(), N.finv.get(), N.w.get(), N.wt.get(),
-                  const_cast<double *>(N.bi.get()), const_cast<double *>(N.u.get()), N.m};
-    for (int d = N.maxdepth; d >= 0; --d) {
-        k_nd_fwd<<<N.nfwd[d], 256, N.smem, s>>>(V, N.fwd[d].get(), c);
-        CR_CHECK_LAUNCH();
+    NdSolveView V{N.fr.get(), N.inv.get(), N.uidx.get(), N.finv.get(), N.w.get(), N.wt.get(),
+                  const_cast<double *>(N.bi.get()), const_cast<double *>(N.lb.get()), const_cast<double *>(N.u.get()),
+                  N.la.get(), N.lbr.get(), N.lc.get()};
+    NdSched S;
+    S.nlev = N.maxdepth + 1;
+    for (int L = 0; L <= S.nlev; ++L) {
+        S.aoff[L] = N.aoff[L];
+        S.boff[L] = N.boff[L];
+        S.coff[L] = N.coff[L];
     }
-    for (int d = 0; d <= N.maxdepth; ++d) {
-        k_nd_bwd<<<N.nbwd[d], 256, N.smem, s>>>(V, N.bwd[d].get(), y);
-        CR_CHECK_LAUNCH();
-    }
-    k_nd_dot<<<occ_grid(k_nd_dot, 256, C.nE), 256, 0, s>>>(C.nE, c, y, qout, partials, ticket);
+    k_nd_solve<<<N.grid, 256, 0, s>>>(V, S, c, y, const_cast<unsigned *>(N.bar.get()), C.nE, qout, partials, ticket);
     CR_CHECK_LAUNCH();
 }
 

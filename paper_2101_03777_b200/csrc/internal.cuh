@@ -209,6 +209,7 @@ enum { AFW_SPD = 0, AFW_ABS = 1, AFW_GEN = 2 };
 struct NdFrontDev {
     int64_t ioff, boff;       // into nodes[]: I nodes, B nodes
     int64_t finv, w, wt, bi, u;   // into the pools (wt: W^t, nI x nB, ld nI)
+    int64_t lb, inv, uoff;        // local B rhs; children's u index per local unknown; global unknowns
     int64_t map;              // into map[]: this front's B unknown -> parent local unknown
     int32_t nI, nB;           // unknowns
     int32_t kid0, kid1;       // child fronts (-1: none)
@@ -217,12 +218,17 @@ struct NdFrontDev {
 struct CoarseNd {
     bool on = false;
     int m = 0, maxdepth = 0;
-    int64_t nfront = 0, smem = 0, bytes = 0;   // dynamic shared bytes of the solve; Finv + W bytes
+    int64_t nfront = 0, bytes = 0;   // fronts; bytes one solve reads (Finv + 2 W)
     cr::DevBuf<NdFrontDev> fr;
     cr::DevBuf<int32_t> nodes, map;
     cr::DevBuf<double> finv, w, wt, bi, u;
-    std::vector<cr::DevBuf<int2>> fwd, bwd;    // per depth: (front, first row) work items
-    std::vector<int> nfwd, nbwd;
+    cr::DevBuf<double> lb;                     // forward: local right-hand side on B
+    cr::DevBuf<int2> inv;                      // per front local unknown: u index of child 0 / 1 (-1)
+    cr::DevBuf<int32_t> uidx;                  // per front: global unknown of each local unknown
+    cr::DevBuf<int2> la, lbr, lc;              // (front, local index) work lists by level
+    std::vector<int> aoff, boff, coff;         // level offsets into la / lbr / lc
+    cr::DevBuf<unsigned> bar;                  // grid barrier of the persistent solve kernel
+    int grid = 0;
 };
 
 // two-level coarse correction (coarse.cu)
