@@ -148,6 +148,21 @@ cr_status cr_spmv(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s);
  * unpartitioned handles): G = sum_K H_K C_K[I (x) Shat_K^{-1} - u_K u_K^t]C_K H_K^t, u = w/sqrt(B)
  * (P:L508-517); x_d, y_d [n_rows], must not alias.  Asynchronous after the first build.    */
 cr_status cr_spmv_mf(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s);
+/* ------------------------------------------------------------------ time stepping
+ * Backward Euler for transient Stokes keeps G (and its preconditioners) from step to step:
+ * only S changes ("all the linear systems have the same matrix").
+ * cr_transient_rhs: per-cell right-hand sides of the step U^n -> U^{n+1}:
+ *   R_K(l) = data terms of the handle (force P:L298-301, Dirichlet fold)
+ *            + mu |K|/(d+1) U^n_{sigma(l)}   (lumped mass; interior faces)
+ *   g_K    = data term.
+ *   U_prev_d [nf_int][dim] (global numbering), R_d [nc][dim+1][dim], g_d [nc].  Asynchronous.
+ * cr_hybrid_set_cell_rhs: replace the handle's right-hand side by explicit R_K, g_K (any split
+ *   with sum_K H_K R_K = the momentum right-hand side is admissible) and recompute S
+ *   with the same G; R_d = g_d = NULL restores the data-derived S.  Transient / steady Stokes
+ *   handles (not NS).  Asynchronous.                                                          */
+cr_status cr_transient_rhs(cr_hybrid h, const double *U_prev_d, double *R_d, double *g_d, cr_stream_t s);
+cr_status cr_hybrid_set_cell_rhs(cr_hybrid h, const double *R_d, const double *g_d, cr_stream_t s);
+
 /* matrix-free operator statistics (0 if not built): cells (padded to 32) and device bytes     */
 cr_status cr_hybrid_mf_info(cr_hybrid h, int64_t *ncells, int64_t *bytes);
 void cr_destroy_hybrid(cr_hybrid h);

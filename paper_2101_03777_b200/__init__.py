@@ -105,6 +105,8 @@ _sig = {
     "cr_partition_plan": [_i32, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp],
     "cr_apply_precond": [_vp, _i32, _vp, _vp, _vp],
     "cr_hybrid_precond_info": [_vp, _P(_i64), _P(_i32), _P(_i64), _P(_i64)],
+    "cr_transient_rhs": [_vp, _vp, _vp, _vp, _vp],
+    "cr_hybrid_set_cell_rhs": [_vp, _vp, _vp, _vp],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -272,6 +274,21 @@ class Hybrid:
                                            ctypes.byref(nby)))
         return dict(npatch=npatch.value, kmax=kmax.value, nfallback=nfb.value, bytes=nby.value)
 
+    def transient_rhs(self, U_prev: torch.Tensor, stream=None):
+        """Cell right-hand sides (R [nc, d+1, d], g [nc]) of the backward-Euler step from U_prev
+        [nf_int, d] (lumped mass P:L129)."""
+        m = self.mesh
+        dev = U_prev.device
+        R = torch.empty((m.nc, m.dim + 1, m.dim), dtype=torch.float64, device=dev)
+        g = torch.empty(m.nc, dtype=torch.float64, device=dev)
+        _check(_lib.cr_transient_rhs(self._h, _ptr(U_prev, torch.float64), _ptr(R), _ptr(g), _stream(stream)))
+        return R, g
+
+    def set_cell_rhs(self, R: torch.Tensor | None = None, g: torch.Tensor | None = None, stream=None):
+        """S of the same G for explicit cell right-hand sides (None: the data-derived S)."""
+        _check(_lib.cr_hybrid_set_cell_rhs(self._h, None if R is None else _ptr(R, torch.float64),
+                                           None if g is None else _ptr(g, torch.float64), _stream(stream)))
+
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
             _lib.cr_destroy_hybrid(self._h)
@@ -430,6 +447,31 @@ def hybrid_method(coords: torch.Tensor, cells: torch.Tensor, prob: Problem, meth
     rep = cr_solve(hyb, W, method, rtol, stream=stream, **solve_kw)
     U, P, diag = cr_recover(hyb, W, stream)
     return dict(mesh=mesh, hybrid=hyb, W=W, U=U, P=P, diag=diag, report=rep)
+
+
+def time_march(coords: torch.Tensor, cells: torch.Tensor, prob: Problem, nsteps: int, U0: torch.Tensor | None = None,
+               method: str = "pcg_afw2", rtol: float = 1e-10, warm_start: bool = True, stream=None,
+               **solve_kw) -> dict:
+    """Backward Euler for transient Stokes (mu = 1/dt) with the hybrid method: G, its
+    patch / coarse preconditioners and matrix-free factors are built once and reused by every
+    step; per step only S (cr_transient_rhs + cr_hybrid_set_cell_rhs), the solve
+    (warm-started from the previous W) and the recovery run."""
+    mesh = cr_build_mesh(coords, cells, stream)
+    hyb = cr_hybridise(mesh, prob, stream)
+    dev = coords.device
+    U = torch.zeros((mesh.nf_int, mesh.dim), dtype=torch.float64, device=dev) if U0 is None else U0
+    W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=dev)
+    Us, Ps, reps = [], [], []
+    for _ in range(nsteps):
+        R, g = hyb.transient_rhs(U, stream)
+        hyb.set_cell_rhs(R, g, stream)
+        if not warm_start:
+            W.zero_()
+        reps.append(cr_solve(hyb, W, method, rtol, stream=stream, **solve_kw))
+        U, P, _ = cr_recover(hyb, W, stream)
+        Us.append(U)
+        Ps.append(P)
+    return dict(mesh=mesh, hybrid=hyb, U=Us, P=Ps, reports=reps)
 
 
 def hybrid_method_host(coords, cells, fbar, mu: float, nu: float, method: str = "pcg", rtol: float = 1e-10,

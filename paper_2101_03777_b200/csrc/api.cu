@@ -235,6 +235,33 @@ cr_status cr_spmv_mf(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s)
     CR_API_END
 }
 
+cr_status cr_hybrid_set_cell_rhs(cr_hybrid h, const double *R_d, const double *g_d, cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(h && ((R_d == nullptr) == (g_d == nullptr)), CR_ERR_INVALID_ARG, "R_d and g_d: both or neither");
+    CR_REQUIRE(!h->is_ns, CR_ERR_INVALID_ARG, "explicit cell right-hand sides: Stokes handles only");
+    cudaStream_t st = (cudaStream_t)s;
+    const cr_mesh_s *m = h->mesh;
+    if (!R_d) {
+        h->rcell.release();
+        h->gcell.release();
+    } else {
+        const size_t nr = (size_t)m->nc * (m->dim + 1) * m->dim;
+        if (h->rcell.n != nr) h->rcell.alloc(nr, st);
+        if (h->gcell.n != (size_t)m->nc) h->gcell.alloc(m->nc, st);
+        CR_CUDA(cudaMemcpyAsync(h->rcell.get(), R_d, nr * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        CR_CUDA(cudaMemcpyAsync(h->gcell.get(), g_d, m->nc * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    cr::hybrid_update_rhs(h, st);
+    CR_API_END
+}
+
+cr_status cr_transient_rhs(cr_hybrid h, const double *U_prev_d, double *R_d, double *g_d, cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(h && U_prev_d && R_d && g_d, CR_ERR_INVALID_ARG, "null argument");
+    cr::transient_rhs(h, U_prev_d, R_d, g_d, (cudaStream_t)s);
+    CR_API_END
+}
+
 cr_status cr_hybrid_mf_info(cr_hybrid h, int64_t *ncells, int64_t *bytes) {
     CR_API_BEGIN
     CR_REQUIRE(h, CR_ERR_INVALID_ARG, "null handle");

@@ -490,6 +490,44 @@ static void hybridise_t(cr_hybrid_s *h, const cr_mesh_s *m, cudaStream_t s) {
     G.nblocks = (int64_t)hnb;
 }
 
+// backward-Euler step right-hand side per cell (mu = 1/dt; lumped mass |K|/(d+1) per local
+// face): R_K(l) = data terms (force, Dirichlet fold) + mu |K|/(d+1) U^n_sigma(l),
+// g_K = data term.  Rounded once from double-double.
+template <int D>
+__global__ void __launch_bounds__(128) k_transient_rhs(MeshView mv, ProbView p, int64_t nc, const double *Uprev,
+                                                       double *Rout, double *gout) {
+    constexpr int NF = D + 1;
+    for (int64_t K = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; K < nc; K += (int64_t)gridDim.x * blockDim.x) {
+        Cell<D> c;
+        load_cell<D>(mv, K, c);
+        dd R[NF][D], g;
+        stokes_rhs<D>(c, p, R, g);
+        const dd mK = two_prod(p.mu, c.vol) / (double)NF;
+#pragma unroll
+        for (int l = 0; l < NF; ++l)
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                dd v = R[l][i];
+                if (c.dof[l] >= 0) v = v + mK * Uprev[(int64_t)c.dof[l] * D + i];
+                Rout[(K * NF + l) * D + i] = dd_round(v);
+            }
+        gout[K] = dd_round(g);
+    }
+}
+
+void transient_rhs(const cr_hybrid_s *h, const double *Uprev, double *R, double *g, cudaStream_t s) {
+    const cr_mesh_s *m = h->mesh;
+    CR_REQUIRE(!h->is_ns, CR_ERR_INVALID_ARG, "transient right-hand side: Stokes handles only");
+    ProbView p = prob_view(h);
+    p.rcell = p.gcell = nullptr;   // the data-derived terms
+    MeshView mv = mesh_view(m);
+    if (m->dim == 2)
+        k_transient_rhs<2><<<grid_for(m->nc, 128, 16), 128, 0, s>>>(mv, p, m->nc, Uprev, R, g);
+    else
+        k_transient_rhs<3><<<grid_for(m->nc, 128, 16), 128, 0, s>>>(mv, p, m->nc, Uprev, R, g);
+    CR_CHECK_LAUNCH();
+}
+
 // S of the same G for new cell right-hand sides (h->rcell / h->gcell): the Stokes assembly kernel with
 // its G writes disabled
 void hybrid_update_rhs(cr_hybrid_s *h, cudaStream_t s) {

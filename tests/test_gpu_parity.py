@@ -497,3 +497,45 @@ def test_nccl_single_rank_partitioned_path():
     assert out["report"]["iterations"] == ref["report"]["iterations"]
     assert relL2(out["U"].cpu().numpy(), ref["U"].cpu().numpy()) <= 1e-12
     assert relL2(out["P"].cpu().numpy(), ref["P"].cpu().numpy()) <= 1e-10
+
+
+# ------------------------------------------------------------------ time stepping
+@pytest.mark.parametrize("dim,n,nsteps", [(2, 16, 3), (3, 3, 2)])
+def test_time_march_matches_oracle(dim, n, nsteps):
+    """Backward Euler with the same G every step (cr_transient_rhs + cr_hybrid_set_cell_rhs,
+    warm-started two-level PCG) against the oracle's per-step refined direct solves."""
+    coords, cells, prm, data, prob = make_case(dim=dim, n=n, force="gaussian", seed=5)
+    mo = O.build_mesh(coords, cells)
+    U0 = np.random.default_rng(6).normal(size=(mo.nf_int, dim))
+    Uo, Po = O.backward_euler(mo, prm, data, nsteps, U0=U0)
+    out = P.time_march(tg(coords), tg(cells), prob, nsteps, U0=tg(U0), method="pcg_afw2", rtol=1e-12,
+                       matrix_free=1, check_every=16)
+    for k in range(nsteps):
+        assert relL2(out["U"][k].cpu().numpy(), Uo[k]) <= 1e-8, k
+        assert relL2(out["P"][k].cpu().numpy(), Po[k]) <= 1e-8, k
+        assert out["reports"][k]["converged"]
+    # restoring the data-derived right-hand side gives back the original S
+    hg = out["hybrid"]
+    S1 = hg.export_csr()[3].clone()
+    R, g = hg.transient_rhs(torch.zeros((mo.nf_int, dim), dtype=torch.float64, device=DEV))
+    hg.set_cell_rhs(R, g)          # mu M 0 = 0: the same S from explicit cell terms
+    S2 = hg.export_csr()[3].clone()
+    hg.set_cell_rhs()
+    S3 = hg.export_csr()[3]
+    ho = O.hybridise(mo, prm, data)
+    assert np.abs(S2.cpu().numpy() - ho["S"]).max() <= 1e-12 * np.abs(ho["S"]).max()
+    assert np.abs(S3.cpu().numpy() - ho["S"]).max() <= 1e-12 * np.abs(ho["S"]).max()
+    assert S1.shape == S3.shape
+
+
+def test_time_march_warm_start_cuts_iterations():
+    """Later steps start from the previous W: fewer iterations than a cold start."""
+    coords, cells, prm, data, prob = make_case(dim=2, n=48, force="gaussian", seed=7)
+    kw = dict(method="pcg_afw2", rtol=1e-12, matrix_free=1, check_every=8)
+    warm = P.time_march(tg(coords), tg(cells), prob, 4, **kw)
+    cold = P.time_march(tg(coords), tg(cells), prob, 4, warm_start=False, **kw)
+    wi = [r["iterations"] for r in warm["reports"]]
+    ci_ = [r["iterations"] for r in cold["reports"]]
+    assert sum(wi[1:]) < sum(ci_[1:]), (wi, ci_)
+    for a, b in zip(warm["U"], cold["U"]):
+        assert relL2(a.cpu().numpy(), b.cpu().numpy()) <= 1e-8
