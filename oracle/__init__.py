@@ -14,6 +14,7 @@ Layout
   krylov.py    C-6  direct solve + refinement, CPU Krylov      (§4)
   post.py      C-8  error norms, zero-mean pressure
   timestep.py  backward-Euler steps with one coupled matrix
+  newton.py    Newton's method for steady Navier-Stokes
   cell_f128.c  per-cell algebra in binary128 (libquadmath)
 
 Every function cites the PAPER.md lines it follows ("P:Lnnn").
@@ -56,8 +57,9 @@ from .scheme import (Params, Data, cell_arrays, local_blocks, mis_priority, shif
 from .krylov import (residual_f128, direct_refined, pcg, minres, bicgstab, gmres)  # noqa: E402
 from .post import zero_mean, errors  # noqa: E402
 from .timestep import lumped_mass, backward_euler  # noqa: E402
+from .newton import cell_face_values, newton_ns  # noqa: E402
 
 __all__ = ["build", "lib", "Mesh", "build_mesh", "Params", "Data", "cell_arrays",
            "local_blocks", "mis_priority", "shift_E", "assemble_coupled", "hybridise",
            "recover", "hybrid_pipeline", "eliminate_cells", "recover_cells", "residual_f128", "direct_refined", "pcg",
-           "minres", "bicgstab", "gmres", "zero_mean", "errors", "lumped_mass", "backward_euler"]
+           "minres", "bicgstab", "gmres", "zero_mean", "errors", "lumped_mass", "backward_euler", "cell_face_values", "newton_ns"]
