@@ -271,6 +271,26 @@ def time_stepping(P, cfg, coords, cells, fbar, stream, nsteps=5):
             "note": "step 1 includes the preconditioner / coarse-space setup; later steps reuse them"}
 
 
+def newton_cavity(P, ci, dev, stream, n=256, nu=0.01, tol=5e-7):
+    """Steady lid-driven cavity (Re = 1/nu) by Newton's method (tolerance of P:L783-799
+    Table 7), each step through the hybrid path (NS step + CR_DC_FGMRES)."""
+    import torch
+    coords, cells = ci.square_mesh(n, 0.0, 4)
+    wall = ci.lid_dirichlet_2d(coords, cells)
+    tg = lambda a: torch.from_numpy(a).to(dev)
+    f = torch.zeros((cells.shape[0], 2), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    a = _ev(torch, stream)
+    out = P.newton_ns(tg(coords), tg(cells), nu, f, tg(wall), tol=tol, mis_seed=44, coarse=32, mu_inner=0.5,
+                      inner_rtol=1e-7)
+    b = _ev(torch, stream)
+    torch.cuda.synchronize()
+    return {"workload": f"2D lid-driven cavity n={n} Re={1 / nu:g}, Newton to ||dU|| <= {tol:g} ||U||",
+            "newton_steps": len(out["history"]), "history": out["history"], "total_s": a.elapsed_time(b) * 1e-3,
+            "outer_iterations": [r["iterations"] for r in out["reports"]],
+            "inner_iterations": [r["inner_iterations"] for r in out["reports"]]}
+
+
 def other_config(P, ci, idx, dev, stream):
     """Time-to-solution (mesh + hybridise + solve + recover, inputs in HBM) of configs[idx]."""
     import torch
@@ -484,10 +504,11 @@ def main():
 
     # ---- stage times of one configs[1] step (assembly cells/s) and time-to-solution of the
     # other configs (one run each, not part of the timed step; single GPU only)
-    stages, others, tstep = None, None, None
+    stages, others, tstep, newton = None, None, None, None
     if world == 1 and not args.no_other_configs:
         stages = stage_times(P, cfg, coords, cells, fbar, stream)
         tstep = time_stepping(P, cfg, coords, cells, fbar, stream)
+        newton = newton_cavity(P, ci, dev, stream)
         others = {}
         for idx in (2, 3, 4):
             others[f"configs[{idx}]"] = other_config(P, ci, idx, dev, stream)
@@ -532,6 +553,7 @@ def main():
             "stages_configs1": stages,
             "other_configs": others,
             "time_stepping_configs1": tstep,
+            "newton_cavity": newton,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -241,6 +241,13 @@ cr_status cr_hybrid_precond_info(cr_hybrid h, int64_t *npatch, int32_t *kmax, in
 cr_status cr_recover(cr_hybrid h, const double *W_d, double *U_d, double *P_d, double *diag_d,
                      cr_stream_t s);
 
+/* Per (cell, local face) values of a face field (the Newton iterate layout of cr_data.u_iter_d,
+ * P:L302): out_d[K][l] = U_d[face_dof(sigma)] on interior faces, bnd_d[K][l] (wall / lid values;
+ * NULL = 0) on boundary faces.  U_d [nf_int][dim], bnd_d / out_d [nc][dim+1][dim].  Newton's
+ * method for steady Navier-Stokes iterates cr_hybridise(u_iter = this, p_iter = P^k)
+ * -> cr_solve -> cr_recover (increments dU, dP).  Asynchronous.                               */
+cr_status cr_cell_face_values(cr_mesh m, const double *U_d, const double *bnd_d, double *out_d, cr_stream_t s);
+
 /* ------------------------------------------------------------------ multi-GPU
  * One process per GPU.  Rank q of P owns the contiguous block rows [floor(q F/P), floor((q+1)F/P))
  * of G (F = nf_int, lexicographic face order = slabs); every rank builds the whole mesh, assembles

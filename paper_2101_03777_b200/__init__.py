@@ -107,6 +107,7 @@ _sig = {
     "cr_hybrid_precond_info": [_vp, _P(_i64), _P(_i32), _P(_i64), _P(_i64)],
     "cr_transient_rhs": [_vp, _vp, _vp, _vp, _vp],
     "cr_hybrid_set_cell_rhs": [_vp, _vp, _vp, _vp],
+    "cr_cell_face_values": [_vp, _vp, _vp, _vp, _vp],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -472,6 +473,44 @@ def time_march(coords: torch.Tensor, cells: torch.Tensor, prob: Problem, nsteps:
         Us.append(U)
         Ps.append(P)
     return dict(mesh=mesh, hybrid=hyb, U=Us, P=Ps, reports=reps)
+
+
+def cell_face_values(mesh: "Mesh", U: torch.Tensor, bnd: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """[nc, d+1, d]: U on interior faces, bnd (wall values, or 0) on boundary faces."""
+    out = torch.empty((mesh.nc, mesh.dim + 1, mesh.dim), dtype=torch.float64, device=U.device)
+    _check(_lib.cr_cell_face_values(mesh._h, _ptr(U, torch.float64), _ptr(bnd, torch.float64), _ptr(out),
+                                    _stream(stream)))
+    return out
+
+
+def newton_ns(coords: torch.Tensor, cells: torch.Tensor, nu: float, fbar: torch.Tensor, wall: torch.Tensor | None,
+              max_newton: int = 30, tol: float = 5e-7, mis_seed: int = 0, method: str = "dc", rtol: float = 1e-10,
+              stream=None, **solve_kw) -> dict:
+    """Newton's method for steady Navier-Stokes from U^0 = 0, P^0 = 0: each
+    step hybridises the linearised problem at (U^k, P^k) (MIS shift), solves it (default: coupled
+    FGMRES preconditioned by the transient hybrid solve) and recovers the increments; stops when
+    ||dU|| <= tol ||U^{k+1}||."""
+    mesh = cr_build_mesh(coords, cells, stream)
+    dev = coords.device
+    U = torch.zeros((mesh.nf_int, mesh.dim), dtype=torch.float64, device=dev)
+    Pk = torch.zeros(mesh.nc, dtype=torch.float64, device=dev)
+    hist, reps = [], []
+    for _ in range(max_newton):
+        uit = cell_face_values(mesh, U, wall, stream)
+        prob = Problem(mu=0.0, nu=nu, fbar=fbar, physics=CR_NS_NEWTON_STEP, shift=CR_SHIFT_MIS, mis_seed=mis_seed,
+                       u_iter=uit, p_iter=Pk)
+        hyb = cr_hybridise(mesh, prob, stream)
+        W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=dev)
+        reps.append(cr_solve(hyb, W, method, rtol, stream=stream, **solve_kw))
+        dU, dP, _ = cr_recover(hyb, W, stream)
+        U = U + dU
+        Pk = Pk + dP
+        rel = float(torch.linalg.norm(dU) / torch.clamp(torch.linalg.norm(U), min=1e-300))
+        hist.append(rel)
+        del hyb
+        if rel <= tol:
+            break
+    return dict(mesh=mesh, U=U, P=Pk, history=hist, reports=reps)
 
 
 def hybrid_method_host(coords, cells, fbar, mu: float, nu: float, method: str = "pcg", rtol: float = 1e-10,

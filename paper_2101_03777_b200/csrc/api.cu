@@ -307,6 +307,13 @@ cr_status cr_hybrid_precond_info(cr_hybrid h, int64_t *npatch, int32_t *kmax, in
     CR_API_END
 }
 
+cr_status cr_cell_face_values(cr_mesh m, const double *U_d, const double *bnd_d, double *out_d, cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(m && U_d && out_d, CR_ERR_INVALID_ARG, "null argument");
+    cr::cell_face_values(m, U_d, bnd_d, out_d, (cudaStream_t)s);
+    CR_API_END
+}
+
 cr_status cr_recover(cr_hybrid h, const double *W_d, double *U_d, double *P_d, double *diag_d, cr_stream_t s) {
     CR_API_BEGIN
     CR_REQUIRE(h && W_d && U_d && P_d, CR_ERR_INVALID_ARG, "null argument");

@@ -303,6 +303,7 @@ void hybridise(cr_hybrid_s *h, const cr_mesh_s *m, const cr_params &prm, const c
                cudaStream_t s);
 void hybrid_update_rhs(cr_hybrid_s *h, cudaStream_t s);   // recompute S only (same G)
 void transient_rhs(const cr_hybrid_s *h, const double *Uprev, double *R, double *g, cudaStream_t s);
+void cell_face_values(const cr_mesh_s *m, const double *U, const double *bnd, double *out, cudaStream_t s);
 // dc.cu
 void solve_dc(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep);
 void coupled_spmv(const cr_coupled_s *c, const double *x, double *y, cudaStream_t s);

@@ -123,6 +123,28 @@ __global__ void k_cell_divergence(MeshView mv, const double *dir, int64_t nc, co
     if ((threadIdx.x & 31) == 0) atomic_max_nonneg(diag, mx);
 }
 
+// per (cell, local face) values of a face field: U on interior faces, bnd (or 0) on boundary faces
+template <int D>
+__global__ void k_cell_face_values(const int32_t *cell_faces, const int32_t *face_dof, int64_t nc, const double *U,
+                                   const double *bnd, double *out) {
+    constexpr int NF = D + 1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nc * NF; t += (int64_t)gridDim.x * blockDim.x) {
+        const int dof = face_dof[cell_faces[t]];
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+            out[t * D + i] = dof >= 0 ? U[(int64_t)dof * D + i] : (bnd ? bnd[t * D + i] : 0.0);
+    }
+}
+
+void cell_face_values(const cr_mesh_s *m, const double *U, const double *bnd, double *out, cudaStream_t s) {
+    const int64_t n = m->nc * (m->dim + 1);
+    if (m->dim == 2)
+        k_cell_face_values<2><<<grid_for(n, 256), 256, 0, s>>>(m->cell_faces.get(), m->face_dof.get(), m->nc, U, bnd, out);
+    else
+        k_cell_face_values<3><<<grid_for(n, 256), 256, 0, s>>>(m->cell_faces.get(), m->face_dof.get(), m->nc, U, bnd, out);
+    CR_CHECK_LAUNCH();
+}
+
 void recover(const cr_hybrid_s *h, const double *W, double *U, double *P, double *diag, cudaStream_t s) {
     const cr_mesh_s *m = h->mesh;
     const int D = m->dim;

@@ -539,3 +539,19 @@ def test_time_march_warm_start_cuts_iterations():
     assert sum(wi[1:]) < sum(ci_[1:]), (wi, ci_)
     for a, b in zip(warm["U"], cold["U"]):
         assert relL2(a.cpu().numpy(), b.cpu().numpy()) <= 1e-8
+
+
+# ------------------------------------------------------------------ Newton for steady NS
+@pytest.mark.parametrize("n,nu", [(8, 0.1), (12, 0.01)])
+def test_newton_ns_matches_oracle(n, nu):
+    """Lid-driven cavity: Newton steps through cr_cell_face_values + cr_hybridise (NS step, MIS
+    shift) + CR_DC_FGMRES + cr_recover, against the oracle's Newton with refined direct solves."""
+    coords, cells = ci.square_mesh(n, 0.0, 4)
+    mo = O.build_mesh(coords, cells)
+    wall = ci.lid_dirichlet_2d(coords, cells)
+    f = np.zeros((mo.nc, 2))
+    Uo, Po, ho = O.newton_ns(mo, O.Params(mu=0.0, nu=nu, physics="ns_step"), f, wall, tol=1e-10)
+    out = P.newton_ns(tg(coords), tg(cells), nu, tg(f), tg(wall), tol=1e-10, mis_seed=11, rtol=1e-12)
+    assert abs(len(out["history"]) - len(ho)) <= 1, (out["history"], ho)
+    assert relL2(out["U"].cpu().numpy(), Uo) <= 1e-8
+    assert relL2(out["P"].cpu().numpy(), Po) <= 1e-8
