@@ -95,12 +95,13 @@ __global__ void k_coarse_faces(const int32_t *dof_face, int64_t row0, int64_t nr
 // per thread (independent loads in flight); warp shuffles then shared memory reduce the block
 // (fixed trees: deterministic).
 template <int D>
-__global__ void __launch_bounds__(256) k_coarse_restrict(CoarseView C, const double *r, double *part) {
+__global__ void __launch_bounds__(256) k_coarse_restrict(CoarseView C, const double *r, double *part,
+                                                         const int32_t *list = nullptr) {
     constexpr int NN = 1 << D, DD = D * D, NV = NN * DD;
     constexpr int TPR = 1;                           // threads per row
     constexpr int NA = NV;                           // accumulators per thread
     constexpr int SL = 256 / TPR, U = 4;
-    const int64_t ch = blockIdx.x;
+    const int64_t ch = list ? (int64_t)list[blockIdx.x] : (int64_t)blockIdx.x;   // list: a subset of chunks
     const int64_t b = C.chunk_start[ch], e = C.chunk_start[ch + 1];
     const int slot = threadIdx.x / TPR;
     double acc[NA];
@@ -255,6 +256,35 @@ __global__ void k_coarse_colour(CoarseView C, int64_t nrows, int colour, int k, 
             if (col == colour) s += w[n];
         }
         for (int i = 0; i < D; ++i) z[r * D + i] = (i == k) ? s * (double)C.fa[r * D + l] : 0.0;
+    }
+}
+
+// the colour column sum of one (k, l) written only on the rows of the listed chunks (the coarse cells
+// of the colour's supports; every other row of z stays 0), or those rows cleared
+template <int D>
+__global__ void __launch_bounds__(256) k_coarse_colour_chunks(CoarseView C, const int32_t *list, int colour, int k,
+                                                              int l, int clear, double *z) {
+    constexpr int NN = 1 << D;
+    const int64_t ch = list[blockIdx.x];
+    for (int64_t t = C.chunk_start[ch] + threadIdx.x; t < C.chunk_start[ch + 1]; t += blockDim.x) {
+        const int64_t r = C.perm[t];
+        double s = 0.0;
+        if (!clear) {
+            int ic[D];
+            float xi[D];
+            coarse_locate<D>(C.g, C.fx + r * D, ic, xi);
+            double w[NN];
+            coarse_weights<D>(C.g, C.fx + r * D, w);
+            for (int n = 0; n < NN; ++n) {
+                int col = 0, mul = 1;
+                for (int i = 0; i < D; ++i) {
+                    col += ((ic[i] + ((n >> i) & 1)) % 5) * mul;
+                    mul *= 5;
+                }
+                if (col == colour) s += w[n];
+            }
+        }
+        for (int i = 0; i < D; ++i) z[r * D + i] = (i == k && !clear) ? s * (double)C.fa[r * D + l] : 0.0;
     }
 }
 
@@ -1167,15 +1197,71 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
     z.zero(s);
     int ncol = 1;
     for (int i = 0; i < D; ++i) ncol *= 5;
+    // Single rank: per colour, z is written only on the chunks of the coarse cells of its supports
+    // (cell index = colour digit - 1 or colour digit, mod 5, in every direction: (2/5)^D of the
+    // rows), G z is nonzero only one fine cell around them, so the restriction runs over the
+    // chunks of cells at digit - 2 .. digit + 1 ((4/5)^D), and z and Y are cleared on those rows
+    // afterwards instead of being rewritten / memset whole.  (Needs fine cells smaller than coarse
+    // cells: the H clamp above.)
+    const bool restricted = !h->part.on;
+    std::vector<int32_t> lsup, lact;
+    std::vector<int64_t> osup(ncol + 1, 0), oact(ncol + 1, 0);
+    DevBuf<int32_t> dsup, dact;
+    if (restricted) {
+        std::vector<int64_t> hcc(ncc + 1);
+        CR_CUDA(cudaMemcpyAsync(hcc.data(), C.cell_chunk.get(), (ncc + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CR_CUDA(cudaStreamSynchronize(s));
+        for (int colour = 0; colour < ncol; ++colour) {
+            for (int64_t cell = 0; cell < ncc; ++cell) {
+                int64_t t = cell;
+                int cl = colour;
+                bool sup = true, act = true;
+                for (int i = 0; i < D; ++i) {
+                    const int x = (int)(t % H);
+                    t /= H;
+                    const int dgt = cl % 5;
+                    cl /= 5;
+                    const int dm = ((x - dgt) % 5 + 5) % 5;   // x - digit mod 5
+                    sup = sup && (dm == 0 || dm == 4);
+                    act = act && dm != 2;
+                }
+                for (int64_t ch = hcc[cell]; ch < hcc[cell + 1]; ++ch) {
+                    if (sup) lsup.push_back((int32_t)ch);
+                    if (act) lact.push_back((int32_t)ch);
+                }
+            }
+            osup[colour + 1] = (int64_t)lsup.size();
+            oact[colour + 1] = (int64_t)lact.size();
+        }
+        upload(dsup, lsup, s);
+        upload(dact, lact, s);
+        Y.zero(s);
+    }
     for (int colour = 0; colour < ncol; ++colour)
         for (int k = 0; k < D; ++k)
             for (int l = 0; l < D; ++l) {
-                k_coarse_colour<D><<<grid_for(nrows, T), T, 0, s>>>(V, nrows, colour, k, l, z.get());
+                const unsigned nsup = (unsigned)(osup[colour + 1] - osup[colour]);
+                const unsigned nact = (unsigned)(oact[colour + 1] - oact[colour]);
+                if (restricted) {
+                    if (nsup) k_coarse_colour_chunks<D><<<nsup, 256, 0, s>>>(V, dsup.get() + osup[colour], colour, k, l, 0, z.get());
+                } else {
+                    k_coarse_colour<D><<<grid_for(nrows, T), T, 0, s>>>(V, nrows, colour, k, l, z.get());
+                }
                 CR_CHECK_LAUNCH();
-                applyG(z.get(), Y.get(), colour);
-                k_coarse_restrict<D><<<(unsigned)C.nchunk, 256, 0, s>>>(V, Y.get(), C.part.get());
+                applyG(z.get(), Y.get(), restricted ? colour : -1 - colour);
+                if (restricted) {
+                    C.part.zero(s);
+                    if (nact) k_coarse_restrict<D><<<nact, 256, 0, s>>>(V, Y.get(), C.part.get(), dact.get() + oact[colour]);
+                } else {
+                    k_coarse_restrict<D><<<(unsigned)C.nchunk, 256, 0, s>>>(V, Y.get(), C.part.get());
+                }
                 k_coarse_gather<D><<<grid_for(C.nE, T), T, 0, s>>>(V, C.part.get(), C.c.get());
                 CR_CHECK_LAUNCH();
+                if (restricted) {
+                    if (nsup) k_coarse_colour_chunks<D><<<nsup, 256, 0, s>>>(V, dsup.get() + osup[colour], colour, k, l, 1, z.get());
+                    if (nact) k_coarse_colour_chunks<D><<<nact, 256, 0, s>>>(V, dact.get() + oact[colour], colour, k, l, 1, Y.get());
+                    CR_CHECK_LAUNCH();
+                }
                 if (h->part.on) h->comm->impl->allreduce(C.c.get(), (int)C.nE, false, s);
                 if (dense)
                     k_coarse_scatterE<D><<<grid_for(C.nE, T), T, 0, s>>>(C.nE, H, colour, k, l, C.c.get(), C.Einv.get());

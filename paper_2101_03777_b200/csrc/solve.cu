@@ -1381,7 +1381,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                     CR_CUDA(cub::DeviceSelect::Flagged(stmp.get(), tb, it, sflag.get(), slist.get(), snum.get(), nsl, s));
                     last_colour = colour;
                 }
-                CR_CUDA(cudaMemsetAsync(Y, 0, L.N * sizeof(double), s));
+                // Y arrives zero (build_coarse clears the rows it touched after each pass)
                 k_mf_spmv_slices<D><<<occ_grid(k_mf_spmv_slices<D>, kT, h->mf.ncells), kT, 0, s>>>(
                     mf_view<D>(h), slist.get(), snum.get(), z, Y, L.nrows);
                 CR_CHECK_LAUNCH();
