@@ -457,10 +457,17 @@ def main():
                 "frac": bytes_ / sec / 1e9 / peak, "traffic": traffic_, "peak_source": peak_src,
                 "algorithmic_bytes": bytes_, "launch_s": sec}
 
+    prec_traffic = None   # ncu --set full DRAM bytes of k_afw_apply (the zsum's slot read-back is not in it)
+    afile = os.path.join(ROOT, "profiles", "afw_dram_bytes.json")
+    if os.path.exists(afile) and mesh.dim == 2:
+        try:
+            prec_traffic = json.load(open(afile)).get("dram_bytes_per_launch")
+        except Exception:
+            prec_traffic = None
     prec2_bytes = prec_bytes + coarse_bytes
     kernels = {
         "mf": roof("k_mf_spmv (matrix-free factored G x, per-cell factors, the in-solve G apply)", mf_bytes, mf_s),
-        "precond": roof("k_afw_apply + k_afw_zsum (patch additive Schwarz z = M^-1 r)", prec_bytes, prec_s),
+        "precond": roof("k_afw_apply + k_afw_zsum (patch additive Schwarz z = M^-1 r)", prec_bytes, prec_s, prec_traffic),
         "precond_two_level": roof("coarse restrict + gather + E^-1 GEMV + patch apply + combine (z = M2^-1 r)",
                                   prec2_bytes, prec2_s),
         "spmv": roof("k_spmv (assembled sliced block-ELL G x, same row code as the assembled PCG SpMV)",
