@@ -285,6 +285,16 @@ cr_status cr_partition_plan(int32_t dim, int64_t nf_int, const int32_t *cell_fac
                             int64_t *row_range, int64_t *recv_counts, int64_t *send_counts,
                             int32_t *ghosts, int32_t *send_rows);
 
+/* The nested-dissection plan of the coarse solve (host only, no GPU; coarse.cu)
+ * for an (H+1)^dim node grid: fronts in post-order (children before parents), each with its
+ * depth, child fronts kids [nf][2] (-1 none), pivot nodes I and boundary nodes B (the
+ * later-eliminated nodes its subtree couples to through the 5^dim-node stencil of Z^t G Z), the
+ * lists concatenated in front order (node = x + (H+1) (y + (H+1) z)).  Call once with the array
+ * arguments NULL to size them.                                                                */
+cr_status cr_coarse_nd_plan(int32_t H, int32_t dim, int64_t *nfront, int32_t *maxdepth, int64_t *total_I,
+                            int64_t *total_B, int32_t *depth, int32_t *kids, int32_t *nI, int32_t *nB,
+                            int32_t *I_nodes, int32_t *B_nodes);
+
 const char *cr_last_error(void);
 const char *cr_version(void);
 

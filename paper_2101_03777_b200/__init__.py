@@ -108,6 +108,7 @@ _sig = {
     "cr_transient_rhs": [_vp, _vp, _vp, _vp, _vp],
     "cr_hybrid_set_cell_rhs": [_vp, _vp, _vp, _vp],
     "cr_cell_face_values": [_vp, _vp, _vp, _vp, _vp],
+    "cr_coarse_nd_plan": [_i32, _i32, _P(_i64), _P(_i32), _P(_i64), _P(_i64), _vp, _vp, _vp, _vp, _vp, _vp],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -511,6 +512,25 @@ def newton_ns(coords: torch.Tensor, cells: torch.Tensor, nu: float, fbar: torch.
         if rel <= tol:
             break
     return dict(mesh=mesh, U=U, P=Pk, history=hist, reports=reps)
+
+
+def coarse_nd_plan(H: int, dim: int) -> dict:
+    """The host nested-dissection plan of the coarse solve (no GPU): per front depth, kids, I and B
+    node lists (numpy)."""
+    import numpy as np
+    nf, md, ti, tb = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.cr_coarse_nd_plan(H, dim, ctypes.byref(nf), ctypes.byref(md), ctypes.byref(ti), ctypes.byref(tb),
+                                  None, None, None, None, None, None))
+    n = nf.value
+    depth, kids = np.zeros(n, np.int32), np.zeros(2 * n, np.int32)
+    nI, nB = np.zeros(n, np.int32), np.zeros(n, np.int32)
+    In, Bn = np.zeros(max(ti.value, 1), np.int32), np.zeros(max(tb.value, 1), np.int32)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    _check(_lib.cr_coarse_nd_plan(H, dim, ctypes.byref(nf), ctypes.byref(md), ctypes.byref(ti), ctypes.byref(tb),
+                                  p(depth), p(kids), p(nI), p(nB), p(In), p(Bn)))
+    oi, ob = np.concatenate([[0], np.cumsum(nI)]), np.concatenate([[0], np.cumsum(nB)])
+    return dict(maxdepth=md.value, depth=depth, kids=kids.reshape(n, 2),
+                I=[In[oi[f]:oi[f + 1]] for f in range(n)], B=[Bn[ob[f]:ob[f + 1]] for f in range(n)])
 
 
 def hybrid_method_host(coords, cells, fbar, mu: float, nu: float, method: str = "pcg", rtol: float = 1e-10,

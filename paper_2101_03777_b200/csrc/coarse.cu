@@ -1331,3 +1331,40 @@ void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double
 }
 
 }  // namespace cr
+
+// ------------------------------------------------------------------ host-only plan export (tests)
+extern "C" cr_status cr_coarse_nd_plan(int32_t H, int32_t dim, int64_t *nfront, int32_t *maxdepth, int64_t *total_I,
+                                       int64_t *total_B, int32_t *depth, int32_t *kids, int32_t *nI, int32_t *nB,
+                                       int32_t *I_nodes, int32_t *B_nodes) {
+    try {
+        CR_REQUIRE(dim == 2 || dim == 3, CR_ERR_INVALID_ARG, "dim must be 2 or 3");
+        CR_REQUIRE(H >= 1 && H <= 256, CR_ERR_INVALID_ARG, "H must be in [1, 256]");
+        CR_REQUIRE(nfront && maxdepth && total_I && total_B, CR_ERR_INVALID_ARG, "null argument");
+        std::vector<cr::HostFront> F;
+        cr::nd_plan(H, dim, F);
+        int64_t ti = 0, tb = 0;
+        int md = 0;
+        for (size_t f = 0; f < F.size(); ++f) {
+            if (depth) depth[f] = F[f].depth;
+            if (kids) { kids[2 * f] = F[f].kid[0]; kids[2 * f + 1] = F[f].kid[1]; }
+            if (nI) nI[f] = (int32_t)F[f].I.size();
+            if (nB) nB[f] = (int32_t)F[f].B.size();
+            if (I_nodes) std::copy(F[f].I.begin(), F[f].I.end(), I_nodes + ti);
+            if (B_nodes) std::copy(F[f].B.begin(), F[f].B.end(), B_nodes + tb);
+            ti += (int64_t)F[f].I.size();
+            tb += (int64_t)F[f].B.size();
+            md = std::max(md, F[f].depth);
+        }
+        *nfront = (int64_t)F.size();
+        *maxdepth = md;
+        *total_I = ti;
+        *total_B = tb;
+        return CR_OK;
+    } catch (const cr::Error &e) {
+        cr::set_last_error(e.what());
+        return e.code;
+    } catch (const std::exception &e) {
+        cr::set_last_error(e.what());
+        return CR_ERR_INVALID_ARG;
+    }
+}
