@@ -365,6 +365,75 @@ __global__ void k_gj_cols(double *E, int64_t n, int64_t k0, int b, const double 
     }
 }
 
+// 3D restriction of one chunk with 9 accumulators per lane (the 72 of one thread per row need 227
+// registers: one CTA per SM, latency-bound).  Each lane loads the data of 4 rows (4 x 32 rows per
+// warp in flight); the products are then formed by corner: lane L owns corner L % 8 and, by warp
+// shuffles, takes the rows 4k + L / 8 (k = 0..7) of every 32-row batch.  Fixed shuffle / shared
+// memory trees: deterministic.
+__global__ void __launch_bounds__(256, 2) k_coarse_restrict3(CoarseView C, const double *r, double *part,
+                                                          const int32_t *list = nullptr) {
+    constexpr int D = 3, DD = 9, NV = 72, U = 4;
+    const int64_t ch = list ? (int64_t)list[blockIdx.x] : (int64_t)blockIdx.x;
+    const int64_t b = C.chunk_start[ch], e = C.chunk_start[ch + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int corner = lane & 7, rsub = lane >> 3;
+    double acc[DD];
+#pragma unroll
+    for (int v = 0; v < DD; ++v) acc[v] = 0.0;
+    for (int64_t t0 = b + warp * 32 + lane; t0 - lane < e; t0 += (int64_t)8 * 32 * U) {
+        float xi[U][D], av[U][D];
+        double rv[U][D];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t t = t0 + (int64_t)u * 8 * 32;
+            const int64_t row = t < e ? (int64_t)C.perm[t] : -1;
+            float xv[D];
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                xv[i] = row >= 0 ? C.fx[row * D + i] : 0.f;
+                av[u][i] = row >= 0 ? C.fa[row * D + i] : 0.f;
+                rv[u][i] = row >= 0 ? r[row * D + i] : 0.0;
+            }
+            int ic[D];
+            coarse_locate<D>(C.g, xv, ic, xi[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int src = 4 * k + rsub;   // row of this batch handled now by this lane's corner
+                float x0 = __shfl_sync(0xffffffffu, xi[u][0], src), x1 = __shfl_sync(0xffffffffu, xi[u][1], src),
+                      x2 = __shfl_sync(0xffffffffu, xi[u][2], src);
+                float a0 = __shfl_sync(0xffffffffu, av[u][0], src), a1 = __shfl_sync(0xffffffffu, av[u][1], src),
+                      a2 = __shfl_sync(0xffffffffu, av[u][2], src);
+                double r0 = __shfl_sync(0xffffffffu, rv[u][0], src), r1 = __shfl_sync(0xffffffffu, rv[u][1], src),
+                       r2 = __shfl_sync(0xffffffffu, rv[u][2], src);
+                const double wn = ((corner & 1) ? (double)x0 : 1.0 - (double)x0) *
+                                  ((corner & 2) ? (double)x1 : 1.0 - (double)x1) *
+                                  ((corner & 4) ? (double)x2 : 1.0 - (double)x2);
+                const double ar[DD] = {(double)a0 * r0, (double)a1 * r0, (double)a2 * r0,
+                                       (double)a0 * r1, (double)a1 * r1, (double)a2 * r1,
+                                       (double)a0 * r2, (double)a1 * r2, (double)a2 * r2};
+#pragma unroll
+                for (int v = 0; v < DD; ++v) acc[v] = fma(wn, ar[v], acc[v]);
+            }
+    }
+    __shared__ double sh[8][NV];
+#pragma unroll
+    for (int v = 0; v < DD; ++v) {
+        double x = acc[v];
+        x += __shfl_xor_sync(0xffffffffu, x, 16);
+        x += __shfl_xor_sync(0xffffffffu, x, 8);
+        if (lane < 8) sh[warp][lane * DD + v] = x;   // lane = corner
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < NV; v += blockDim.x) {
+        double x = 0.0;
+        for (int w = 0; w < 8; ++w) x += sh[w][v];
+        part[ch * NV + v] = x;
+    }
+}
+
 // first sorted position with coarse cell >= c (c = 0..ncc)
 __global__ void k_cell_starts(const uint32_t *cc_sorted, int64_t n, int64_t ncc, int64_t *cstart) {
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= ncc; c += (int64_t)gridDim.x * blockDim.x) {
@@ -1251,9 +1320,13 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
                 applyG(z.get(), Y.get(), restricted ? colour : -1 - colour);
                 if (restricted) {
                     C.part.zero(s);
-                    if (nact) k_coarse_restrict<D><<<nact, 256, 0, s>>>(V, Y.get(), C.part.get(), dact.get() + oact[colour]);
+                    if (nact) {
+                        if (D == 3) k_coarse_restrict3<<<nact, 256, 0, s>>>(V, Y.get(), C.part.get(), dact.get() + oact[colour]);
+                        else k_coarse_restrict<D><<<nact, 256, 0, s>>>(V, Y.get(), C.part.get(), dact.get() + oact[colour]);
+                    }
                 } else {
-                    k_coarse_restrict<D><<<(unsigned)C.nchunk, 256, 0, s>>>(V, Y.get(), C.part.get());
+                    if (D == 3) k_coarse_restrict3<<<(unsigned)C.nchunk, 256, 0, s>>>(V, Y.get(), C.part.get());
+                    else k_coarse_restrict<D><<<(unsigned)C.nchunk, 256, 0, s>>>(V, Y.get(), C.part.get());
                 }
                 k_coarse_gather<D><<<grid_for(C.nE, T), T, 0, s>>>(V, C.part.get(), C.c.get());
                 CR_CHECK_LAUNCH();
@@ -1316,7 +1389,7 @@ void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double
         k_coarse_restrict<2><<<(unsigned)C.nchunk, 256, 0, s>>>(V, r, C.part.get());
         k_coarse_gather<2><<<grid_for(C.nE, T), T, 0, s>>>(V, C.part.get(), C.c.get());
     } else {
-        k_coarse_restrict<3><<<(unsigned)C.nchunk, 256, 0, s>>>(V, r, C.part.get());
+        k_coarse_restrict3<<<(unsigned)C.nchunk, 256, 0, s>>>(V, r, C.part.get());
         k_coarse_gather<3><<<grid_for(C.nE, T), T, 0, s>>>(V, C.part.get(), C.c.get());
     }
     CR_CHECK_LAUNCH();

@@ -214,7 +214,7 @@ __global__ void k_halo_pack(int64_t n, const int32_t *rows, const double *x, dou
 // ------------------------------------------------------------------ matrix-free G (mf.cuh)
 // q += G_mf x over this rank's cells (q pre-zeroed); REDUCE: p.q -> alpha (FIN_PQ)
 template <int D, bool REDUCE>
-__global__ void __launch_bounds__(kT, D == 2 ? 3 : 1) k_mf_spmv(MfView M, const double *x, double *q, int64_t nown, KState *st,
+__global__ void __launch_bounds__(kT, D == 2 ? 3 : 2) k_mf_spmv(MfView M, const double *x, double *q, int64_t nown, KState *st,
                                                 double *partials, int dist, int pqkind) {
     if (REDUCE && st->flag != FLAG_RUN) return;
     double acc[1] = {0.0};
@@ -248,7 +248,7 @@ __global__ void k_mf_slice_flag(MfView M, CoarseView C, int colour, int64_t nsli
 
 // q += G_mf x over the listed slices only (coarse setup: x vanishes on every other cell)
 template <int D>
-__global__ void __launch_bounds__(kT) k_mf_spmv_slices(MfView M, const int32_t *slices, const int64_t *nact,
+__global__ void __launch_bounds__(kT, D == 2 ? 3 : 2) k_mf_spmv_slices(MfView M, const int32_t *slices, const int64_t *nact,
                                                        const double *x, double *q, int64_t nown) {
     const int64_t n = *nact * 32;
     GRID_STRIDE(t, n) {
