@@ -1155,6 +1155,70 @@ static void gj_invert(double *A, int64_t n64, cudaStream_t s) {
     CR_REQUIRE(hb == 0, CR_ERR_SINGULAR_LOCAL, "coarse matrix Z^t G Z is not positive definite");
 }
 
+// Dense SPD inverse by cuSOLVER (dlopen'ed libcusolver.so.11): Cholesky potrf + potri on the lower
+// triangle, then the upper triangle mirrored.  ~3x fewer flops than Gauss-Jordan and LAPACK-size
+// panels (the coarse setup is part of every solve); Gauss-Jordan is the fallback when the library
+// is missing.  A non-positive pivot (info > 0) throws CR_ERR_SINGULAR_LOCAL (build_coarse halves H).
+struct Lapack {
+    void *h = nullptr, *handle = nullptr;
+    int (*Create)(void **) = nullptr;
+    int (*SetStream)(void *, cudaStream_t) = nullptr;
+    int (*PotrfBS)(void *, int, int, double *, int, int *) = nullptr;
+    int (*Potrf)(void *, int, int, double *, int, double *, int, int *) = nullptr;
+    int (*PotriBS)(void *, int, int, double *, int, int *) = nullptr;
+    int (*Potri)(void *, int, int, double *, int, double *, int, int *) = nullptr;
+};
+static Lapack &lapack() {
+    static thread_local Lapack L = [] {
+        Lapack x;
+        x.h = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL);
+        if (!x.h) return x;
+        x.Create = (decltype(x.Create))dlsym(x.h, "cusolverDnCreate");
+        x.SetStream = (decltype(x.SetStream))dlsym(x.h, "cusolverDnSetStream");
+        x.PotrfBS = (decltype(x.PotrfBS))dlsym(x.h, "cusolverDnDpotrf_bufferSize");
+        x.Potrf = (decltype(x.Potrf))dlsym(x.h, "cusolverDnDpotrf");
+        x.PotriBS = (decltype(x.PotriBS))dlsym(x.h, "cusolverDnDpotri_bufferSize");
+        x.Potri = (decltype(x.Potri))dlsym(x.h, "cusolverDnDpotri");
+        if (!(x.Create && x.SetStream && x.PotrfBS && x.Potrf && x.PotriBS && x.Potri) || x.Create(&x.handle) != 0)
+            x.handle = nullptr;
+        return x;
+    }();
+    return L;
+}
+
+__global__ void k_mirror_lower(double *A, int64_t n) {   // column-major: A(j, i) = A(i, j), i > j
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / n, i = t - j * n;
+        if (i > j) A[j + i * n] = A[i + j * n];
+    }
+}
+
+static void spd_invert(double *A, int64_t n64, cudaStream_t s) {
+    Lapack &L = lapack();
+    if (!L.handle) {
+        gj_invert(A, n64, s);
+        return;
+    }
+    const int n = (int)n64, lower = 0;
+    L.SetStream(L.handle, s);
+    int lw1 = 0, lw2 = 0;
+    CR_REQUIRE(L.PotrfBS(L.handle, lower, n, A, n, &lw1) == 0 && L.PotriBS(L.handle, lower, n, A, n, &lw2) == 0,
+               CR_ERR_CUDA, "cusolverDn buffer size query failed");
+    DevBuf<double> work;
+    work.alloc(std::max(std::max(lw1, lw2), 1), s);
+    DevBuf<int> info;
+    info.alloc(2, s);
+    info.zero(s);
+    CR_REQUIRE(L.Potrf(L.handle, lower, n, A, n, work.get(), lw1, info.get()) == 0, CR_ERR_CUDA, "cusolverDnDpotrf failed");
+    CR_REQUIRE(L.Potri(L.handle, lower, n, A, n, work.get(), lw2, info.get() + 1) == 0, CR_ERR_CUDA, "cusolverDnDpotri failed");
+    k_mirror_lower<<<grid_for(n64 * n64, 256, 16), 256, 0, s>>>(A, n64);
+    CR_CHECK_LAUNCH();
+    int hi[2] = {0, 0};
+    CR_CUDA(cudaMemcpyAsync(hi, info.get(), 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CR_CUDA(cudaStreamSynchronize(s));
+    CR_REQUIRE(hi[0] == 0 && hi[1] == 0, CR_ERR_SINGULAR_LOCAL, "coarse matrix is not positive definite (potrf/potri)");
+}
+
 template <int D>
 static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const double *, double *, int)> &applyG,
                            cudaStream_t s) {
@@ -1346,8 +1410,8 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
     if (dense) {
         k_symmetrize<<<grid_for(C.nE * C.nE, T, 64), T, 0, s>>>(C.Einv.get(), C.nE);
         CR_CHECK_LAUNCH();
-        gj_invert(C.Einv.get(), C.nE, s);
-        tr.mark("coarse: E^-1 (Gauss-Jordan)");
+        spd_invert(C.Einv.get(), C.nE, s);
+        tr.mark("coarse: E^-1 (Cholesky potrf + potri)");
     } else {
         k_es_symmetrize<D><<<grid_for((int64_t)nnode * NBR * D * D * D * D, T, 16), T, 0, s>>>(nnode, H, Es.get());
         CR_CHECK_LAUNCH();
