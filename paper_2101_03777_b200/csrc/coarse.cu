@@ -836,6 +836,7 @@ __global__ void __launch_bounds__(256) k_nd_solve(NdSolveView V, NdSched S, cons
 }
 
 static void gj_invert(double *A, int64_t n, cudaStream_t s);   // below (blocked Gauss-Jordan, SPD)
+static void spd_invert(double *A, int64_t n, cudaStream_t s);  // below (cuSOLVER Cholesky, GJ fallback)
 
 struct BlasBatched {
     int (*GetrfB)(void *, int, double *const[], int, int *, int *, int) = nullptr;
@@ -1083,7 +1084,7 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
                 double *Fi = N.finv.get() + fr[f].finv;
                 k_nd_copy_pivots<<<grid_for((int64_t)ni * ni, T, 16), T, 0, s>>>(base, np, ni, Fi);
                 CR_CHECK_LAUNCH();
-                gj_invert(Fi, ni, s);
+                spd_invert(Fi, ni, s);
                 if (nbp > 0) {
                     dgemm(s, nbp, ni, ni, 1.0, base + ni, np, Fi, ni, 0.0, N.w.get() + fr[f].w, nbp);
                     dgemm(s, nbp, nbp, ni, -1.0, N.w.get() + fr[f].w, nbp, base + (int64_t)ni * np, np, 1.0,
