@@ -295,6 +295,16 @@ cr_status cr_coarse_nd_plan(int32_t H, int32_t dim, int64_t *nfront, int32_t *ma
                             int64_t *total_B, int32_t *depth, int32_t *kids, int32_t *nI, int32_t *nB,
                             int32_t *I_nodes, int32_t *B_nodes);
 
+/* Sparse direct solve A x = b of a canonical CSR system (int64 row_ptr [n+1], int32 cols, f64
+ * vals: the layout of cr_hybrid_export_csr / cr_coupled_export_csr) on the device with cuSOLVER
+ * (plain library factorisation): method 0 = sparse Cholesky (SPD: the transient hybrid G,
+ * P:L535), 1 = sparse QR (the indefinite coupled matrix); reorder 0 none, 1 symrcm,
+ * 2 symamd, 3 metis.  The paper's direct-solver comparison (Table 4).  Synchronises
+ * `s`; *singularity (may be NULL) = -1 or the first singular pivot (then CR_ERR_SINGULAR_LOCAL). */
+cr_status cr_sparse_direct_solve(int64_t n, int64_t nnz, const int64_t *row_ptr_d, const int32_t *cols_d,
+                                 const double *vals_d, const double *b_d, double *x_d, int32_t method,
+                                 int32_t reorder, cr_stream_t s, int32_t *singularity);
+
 const char *cr_last_error(void);
 const char *cr_version(void);
 

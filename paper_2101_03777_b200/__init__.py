@@ -109,6 +109,7 @@ _sig = {
     "cr_hybrid_set_cell_rhs": [_vp, _vp, _vp, _vp],
     "cr_cell_face_values": [_vp, _vp, _vp, _vp, _vp],
     "cr_coarse_nd_plan": [_i32, _i32, _P(_i64), _P(_i32), _P(_i64), _P(_i64), _vp, _vp, _vp, _vp, _vp, _vp],
+    "cr_sparse_direct_solve": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _P(_i32)],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -512,6 +513,17 @@ def newton_ns(coords: torch.Tensor, cells: torch.Tensor, nu: float, fbar: torch.
         if rel <= tol:
             break
     return dict(mesh=mesh, U=U, P=Pk, history=hist, reports=reps)
+
+
+def sparse_direct_solve(rp: torch.Tensor, ci: torch.Tensor, v: torch.Tensor, b: torch.Tensor, method: str = "chol",
+                        reorder: int = 3, stream=None) -> torch.Tensor:
+    """x = A^{-1} b for a canonical CSR (as exported) by cuSOLVER sparse Cholesky ("chol") or QR ("qr")."""
+    x = torch.empty_like(b)
+    sing = ctypes.c_int32()
+    _check(_lib.cr_sparse_direct_solve(rp.numel() - 1, ci.numel(), _ptr(rp, torch.int64), _ptr(ci, torch.int32),
+                                       _ptr(v, torch.float64), _ptr(b, torch.float64), _ptr(x, torch.float64),
+                                       0 if method == "chol" else 1, reorder, _stream(stream), ctypes.byref(sing)))
+    return x
 
 
 def coarse_nd_plan(H: int, dim: int) -> dict:

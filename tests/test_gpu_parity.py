@@ -555,3 +555,25 @@ def test_newton_ns_matches_oracle(n, nu):
     assert abs(len(out["history"]) - len(ho)) <= 1, (out["history"], ho)
     assert relL2(out["U"].cpu().numpy(), Uo) <= 1e-8
     assert relL2(out["P"].cpu().numpy(), Po) <= 1e-8
+
+
+# ------------------------------------------------------------------ direct solvers
+@pytest.mark.parametrize("n", [2, 3])
+def test_sparse_direct_hybrid_and_coupled(n):
+    """Table 4's comparison on the GPU: sparse Cholesky of the hybrid G and sparse QR of the coupled
+    matrix both give the oracle's (U, P) on a 3D Kuhn mesh (transient, dt = 5e-4)."""
+    coords, cells, prm, data, prob = make_case(dim=3, n=n, mu=2000.0)
+    mo = O.build_mesh(coords, cells)
+    ho = O.hybrid_pipeline(mo, prm, data)
+    mg = P.cr_build_mesh(tg(coords), tg(cells))
+    hg = P.cr_hybridise(mg, prob)
+    rp, ci_, v, S = hg.export_csr()
+    W = P.sparse_direct_solve(rp, ci_, v, S, "chol")
+    U, Pp, _ = P.cr_recover(hg, W)
+    assert relL2(U.cpu().numpy(), ho["U"]) <= 1e-8 and relL2(Pp.cpu().numpy(), ho["P"]) <= 1e-8
+    cg = P.cr_assemble_coupled(mg, prob)
+    rp2, ci2, v2, rhs = cg.export_csr()
+    x = P.sparse_direct_solve(rp2, ci2, v2, rhs, "qr").cpu().numpy()
+    nU = 3 * mo.nf_int
+    assert relL2(x[:nU].reshape(-1, 3), ho["U"]) <= 1e-8
+    assert relL2(np.insert(x[nU:], 0, 0.0), ho["P"]) <= 1e-8
