@@ -555,6 +555,11 @@ def hybrid_method_host(coords, cells, fbar, mu: float, nu: float, method: str = 
     f = fbar.to(dev, non_blocking=True)
     prob = Problem(mu=mu, nu=nu, fbar=f, **kw)
     out = hybrid_method(c, k, prob, method, rtol, stream, comm, matrix_free=matrix_free, coarse=coarse)
-    out["U_host"] = out["U"].to("cpu")
-    out["P_host"] = out["P"].to("cpu")
+    # results land in pinned host buffers (page-locked: full-speed device -> host copies)
+    Uh = torch.empty(out["U"].shape, dtype=out["U"].dtype, pin_memory=True)
+    Ph = torch.empty(out["P"].shape, dtype=out["P"].dtype, pin_memory=True)
+    Uh.copy_(out["U"], non_blocking=True)
+    Ph.copy_(out["P"], non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    out["U_host"], out["P_host"] = Uh, Ph
     return out
