@@ -1745,20 +1745,30 @@ void spmv_part(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s) {
     else spmv_part_t<3>(h, x, y, s);
 }
 
-// y = G_mf x (matrix-free factored operator) on an unpartitioned handle
+// y = G_mf x (matrix-free factored operator); on a partitioned handle x holds the owned rows and
+// the ghosts come by the halo exchange (a collective: every rank calls it)
 template <int D>
 static void spmv_mf_t(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s) {
     ensure_work(h, s);
     build_mf(h, s);
-    Launcher L{h, h->work, s};
+    SolverWork *w = h->work;
+    Launcher L{h, w, s};
     L.D = D;
     L.nrows = h->G.nrows;
-    L.N = h->work->N;
-    mf_apply<D, false>(L, s, x, y, 0.0);
+    L.N = w->N;
+    const double *xin = x;
+    if (h->part.on) {
+        L.dist = 1;
+        L.comm = h->comm->impl;
+        double *xt = w->t.get();
+        CR_CUDA(cudaMemcpyAsync(xt, x, w->N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        L.halo(s, xt);
+        xin = xt;
+    }
+    mf_apply<D, false>(L, s, xin, y, 0.0);
 }
 
 void spmv_mf(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s) {
-    CR_REQUIRE(!h->part.on, CR_ERR_INVALID_ARG, "cr_spmv_mf: unpartitioned handles only");
     if (h->G.d == 2) spmv_mf_t<2>(h, x, y, s);
     else spmv_mf_t<3>(h, x, y, s);
 }

@@ -443,6 +443,7 @@ def test_partitioned_loopback(dim, n, nranks, method):
     ho = O.hybrid_pipeline(mo, prm, data)
     grp = P.LoopbackGroup(nranks)
     res, errs = [None] * nranks, []
+    xglob = np.random.default_rng(12).normal(size=mo.nf_int * mo.dim)
 
     def run(rank):
         try:
@@ -454,8 +455,14 @@ def test_partitioned_loopback(dim, n, nranks, method):
                 out = P.hybrid_method(c, k, prob, method[:-3] if mf else method, rtol=1e-12, stream=st, comm=comm,
                                       check_every=16, matrix_free=int(mf))
                 rp, cols, vals, S = out["hybrid"].export_csr(st)
+                inf = out["hybrid"].partition_info()
+                ymf = None
+                if mf:   # cr_spmv_mf on a partitioned handle: halo exchange inside (collective)
+                    xl = tg(xglob[inf["row0"] * mo.dim:inf["row1"] * mo.dim])
+                    ymf = torch.empty_like(xl)
+                    out["hybrid"].spmv_mf(xl, ymf, st)
                 st.synchronize()
-                res[rank] = dict(out=out, info=out["hybrid"].partition_info(), rp=rp.cpu().numpy(),
+                res[rank] = dict(out=out, info=inf, ymf=None if ymf is None else ymf.cpu().numpy(), rp=rp.cpu().numpy(),
                                  cols=cols.cpu().numpy(), vals=vals.cpu().numpy(), S=S.cpu().numpy(),
                                  U=out["U"].cpu().numpy(), P=out["P"].cpu().numpy())
         except Exception as e:   # pragma: no cover
@@ -483,6 +490,9 @@ def test_partitioned_loopback(dim, n, nranks, method):
         assert relL2(r["U"], ho["U"]) <= 1e-8 and relL2(r["P"], ho["P"]) <= 1e-8
         assert np.array_equal(r["U"], res[0]["U"]) and np.array_equal(r["P"], res[0]["P"])
         assert r["out"]["report"]["converged"]
+        if r["ymf"] is not None:
+            yref = (Go @ xglob)[r0 * d:r1 * d]
+            assert np.abs(r["ymf"] - yref).max() <= 1e-11 * np.abs(Go).max() * np.abs(xglob).max()
     assert rows_seen == mo.nf_int
 
 
