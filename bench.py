@@ -39,7 +39,7 @@ METRIC = "hybridised-system PCG time-to-solution; SpMV GB/s as % of B200 HBM pea
 CONFIG_IDX = 1
 METHOD = "pcg_afw2"  # patch additive Schwarz + coarse "stress x area" correction
 MATRIX_FREE = 1      # G applied from per-cell factors
-COARSE = 32          # coarse grid intervals per direction
+COARSE = 32          # coarse grid intervals per direction (dense E^-1; H = 64 uses the flat ND solve)
 MAX_ITER = 20000     # a cap (the solve takes ~800): a regression fails loudly instead of running on
 # Jacobi-PCG iterations of configs[1] to a true 1e-10 residual, measured on B200 by this
 # bench (used only by --impl reference to extrapolate the oracle's per-iteration time).
@@ -482,8 +482,8 @@ def main():
     # PCG-two-level iteration: G apply + update (x,p,r,q read; x,r write) + patch apply + coarse
     # (restriction reads r and the fp32 row basis, E^-1 once) + p update (+ basis again)
     g_bytes = mf_bytes if MATRIX_FREE else spmv_bytes
-    nE = 4 * (COARSE + 1) ** 2 if mesh.dim == 2 else 9 * (COARSE + 1) ** 3
-    coarse_bytes = N8 + 8 * N + 8 * nE * nE + 8 * N     # r, (x, a) fp32, E^-1, (x, a) again
+    cinfo = hyb.coarse_info()
+    coarse_bytes = N8 + 8 * N + cinfo["solve_bytes"] + 8 * N   # r, (x, a) fp32, E^-1 or ND fronts, (x, a) again
     iter_bytes = g_bytes + 6 * N8 + (pinfo["bytes"] + N8 + slots * N8) + coarse_bytes + (slots * N8 + 2 * N8)
     iter_gbs = iter_bytes * rep["iterations"] / rep["seconds"] / 1e9 if rep["seconds"] > 0 else None
 
@@ -503,7 +503,7 @@ def main():
     kernels = {
         "mf": roof("k_mf_spmv (matrix-free factored G x, per-cell factors, the in-solve G apply)", mf_bytes, mf_s),
         "precond": roof("k_afw_apply + k_afw_zsum (patch additive Schwarz z = M^-1 r)", prec_bytes, prec_s, prec_traffic),
-        "precond_two_level": roof("coarse restrict + gather + E^-1 GEMV + patch apply + combine (z = M2^-1 r)",
+        "precond_two_level": roof("coarse restrict + gather + E^-1 solve (nested dissection) + patch apply + combine (z = M2^-1 r)",
                                   prec2_bytes, prec2_s),
         "spmv": roof("k_spmv (assembled sliced block-ELL G x, same row code as the assembled PCG SpMV)",
                      spmv_bytes, spmv_s, traffic),
@@ -573,15 +573,14 @@ def main():
 
     launches = rep["kernel_launches"] + 25     # mesh (sort/scan/geometry ~15), hybridise 1, recover 3, copies
     launches += 12   # patch build (pairs, sort, scans, setup)
-    nE_ = 4 * (COARSE + 1) ** 2 if ndim == 2 else 9 * (COARSE + 1) ** 3
-    launches += (5 ** ndim) * ndim ** 2 * 5 + 5 * ((nE_ + 31) // 32) + 10   # coarse E assembly + inversion
+    launches += (5 ** ndim) * ndim ** 2 * 8 + 200   # coarse E assembly (colour passes) + ND factorisation
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "ms_steps_rank0": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args.n or cfg.n, world),
-            "pcg": {"method": METHOD, "matrix_free": MATRIX_FREE, "coarse_intervals": COARSE,
+            "pcg": {"method": METHOD, "matrix_free": MATRIX_FREE, "coarse_intervals": COARSE, "coarse": cinfo,
                     "iterations": rep["iterations"],
                     "rel_res_true": rep["rel_res_true"], "solve_s": rep["seconds"],
                     "ms_per_iter": rep["seconds"] / max(rep["iterations"], 1) * 1e3,

@@ -163,6 +163,11 @@ cr_status cr_spmv_mf(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s)
 cr_status cr_transient_rhs(cr_hybrid h, const double *U_prev_d, double *R_d, double *g_d, cr_stream_t s);
 cr_status cr_hybrid_set_cell_rhs(cr_hybrid h, const double *R_d, const double *g_d, cr_stream_t s);
 
+/* two-level coarse space of the handle (0 if not built): intervals H, coarse unknowns nE, nd = 1
+ * for the nested-dissection solve (0: dense E^{-1}), bytes one coarse solve reads (E^{-1} or the
+ * fronts' Finv + 2 W).  Any pointer may be NULL.                                              */
+cr_status cr_hybrid_coarse_info(cr_hybrid h, int32_t *H, int64_t *nE, int32_t *nd, int64_t *solve_bytes);
+
 /* matrix-free operator statistics (0 if not built): cells (padded to 32) and device bytes     */
 cr_status cr_hybrid_mf_info(cr_hybrid h, int64_t *ncells, int64_t *bytes);
 void cr_destroy_hybrid(cr_hybrid h);
@@ -286,12 +291,13 @@ cr_status cr_partition_plan(int32_t dim, int64_t nf_int, const int32_t *cell_fac
                             int32_t *ghosts, int32_t *send_rows);
 
 /* The nested-dissection plan of the coarse solve (host only, no GPU; coarse.cu)
- * for an (H+1)^dim node grid: fronts in post-order (children before parents), each with its
- * depth, child fronts kids [nf][2] (-1 none), pivot nodes I and boundary nodes B (the
- * later-eliminated nodes its subtree couples to through the 5^dim-node stencil of Z^t G Z), the
- * lists concatenated in front order (node = x + (H+1) (y + (H+1) z)).  Call once with the array
- * arguments NULL to size them.                                                                */
-cr_status cr_coarse_nd_plan(int32_t H, int32_t dim, int64_t *nfront, int32_t *maxdepth, int64_t *total_I,
+ * for an (H+1)^dim node grid: box = 0 recursive bisection, box > 0 the flat two-level plan
+ * (separator slabs after every `box` nodes form the root, the boxes are its children).  Fronts
+ * in post-order (children before parents), each with its depth, its parent (in `kids` [nf]; -1
+ * for the root), pivot nodes I and boundary nodes B (the later-eliminated nodes its subtree
+ * couples to through the 5^dim-node stencil of Z^t G Z), the lists concatenated in front order
+ * (node = x + (H+1) (y + (H+1) z)).  Call once with the array arguments NULL to size them.     */
+cr_status cr_coarse_nd_plan(int32_t H, int32_t dim, int32_t box, int64_t *nfront, int32_t *maxdepth, int64_t *total_I,
                             int64_t *total_B, int32_t *depth, int32_t *kids, int32_t *nI, int32_t *nB,
                             int32_t *I_nodes, int32_t *B_nodes);
 

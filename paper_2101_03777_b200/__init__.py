@@ -108,8 +108,9 @@ _sig = {
     "cr_transient_rhs": [_vp, _vp, _vp, _vp, _vp],
     "cr_hybrid_set_cell_rhs": [_vp, _vp, _vp, _vp],
     "cr_cell_face_values": [_vp, _vp, _vp, _vp, _vp],
-    "cr_coarse_nd_plan": [_i32, _i32, _P(_i64), _P(_i32), _P(_i64), _P(_i64), _vp, _vp, _vp, _vp, _vp, _vp],
+    "cr_coarse_nd_plan": [_i32, _i32, _i32, _P(_i64), _P(_i32), _P(_i64), _P(_i64), _vp, _vp, _vp, _vp, _vp, _vp],
     "cr_sparse_direct_solve": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _P(_i32)],
+    "cr_hybrid_coarse_info": [_vp, _P(_i32), _P(_i64), _P(_i32), _P(_i64)],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -270,6 +271,11 @@ class Hybrid:
         m = METHODS[method] if isinstance(method, str) else int(method)
         _check(_lib.cr_apply_precond(self._h, m, _ptr(r, torch.float64), _ptr(z, torch.float64), _stream(stream)))
         return z
+
+    def coarse_info(self) -> dict:
+        H, nE, nd, nb = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64()
+        _check(_lib.cr_hybrid_coarse_info(self._h, ctypes.byref(H), ctypes.byref(nE), ctypes.byref(nd), ctypes.byref(nb)))
+        return dict(H=H.value, nE=nE.value, nested_dissection=bool(nd.value), solve_bytes=nb.value)
 
     def precond_info(self) -> dict:
         npatch, kmax, nfb, nby = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
@@ -526,22 +532,22 @@ def sparse_direct_solve(rp: torch.Tensor, ci: torch.Tensor, v: torch.Tensor, b: 
     return x
 
 
-def coarse_nd_plan(H: int, dim: int) -> dict:
-    """The host nested-dissection plan of the coarse solve (no GPU): per front depth, kids, I and B
-    node lists (numpy)."""
+def coarse_nd_plan(H: int, dim: int, box: int = 0) -> dict:
+    """The host nested-dissection plan of the coarse solve (no GPU): per front depth, parent, I and
+    B node lists (numpy).  box > 0: the flat two-level plan."""
     import numpy as np
     nf, md, ti, tb = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
-    _check(_lib.cr_coarse_nd_plan(H, dim, ctypes.byref(nf), ctypes.byref(md), ctypes.byref(ti), ctypes.byref(tb),
-                                  None, None, None, None, None, None))
+    _check(_lib.cr_coarse_nd_plan(H, dim, box, ctypes.byref(nf), ctypes.byref(md), ctypes.byref(ti),
+                                  ctypes.byref(tb), None, None, None, None, None, None))
     n = nf.value
-    depth, kids = np.zeros(n, np.int32), np.zeros(2 * n, np.int32)
+    depth, kids = np.zeros(n, np.int32), np.full(n, -1, np.int32)
     nI, nB = np.zeros(n, np.int32), np.zeros(n, np.int32)
     In, Bn = np.zeros(max(ti.value, 1), np.int32), np.zeros(max(tb.value, 1), np.int32)
     p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
-    _check(_lib.cr_coarse_nd_plan(H, dim, ctypes.byref(nf), ctypes.byref(md), ctypes.byref(ti), ctypes.byref(tb),
-                                  p(depth), p(kids), p(nI), p(nB), p(In), p(Bn)))
+    _check(_lib.cr_coarse_nd_plan(H, dim, box, ctypes.byref(nf), ctypes.byref(md), ctypes.byref(ti),
+                                  ctypes.byref(tb), p(depth), p(kids), p(nI), p(nB), p(In), p(Bn)))
     oi, ob = np.concatenate([[0], np.cumsum(nI)]), np.concatenate([[0], np.cumsum(nB)])
-    return dict(maxdepth=md.value, depth=depth, kids=kids.reshape(n, 2),
+    return dict(maxdepth=md.value, depth=depth, parent=kids,
                 I=[In[oi[f]:oi[f + 1]] for f in range(n)], B=[Bn[ob[f]:ob[f + 1]] for f in range(n)])
 
 

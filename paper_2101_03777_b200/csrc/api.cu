@@ -262,6 +262,17 @@ cr_status cr_transient_rhs(cr_hybrid h, const double *U_prev_d, double *R_d, dou
     CR_API_END
 }
 
+cr_status cr_hybrid_coarse_info(cr_hybrid h, int32_t *H, int64_t *nE, int32_t *nd, int64_t *solve_bytes) {
+    CR_API_BEGIN
+    CR_REQUIRE(h, CR_ERR_INVALID_ARG, "null handle");
+    const auto &C = h->coarse;
+    if (H) *H = C.built;
+    if (nE) *nE = C.built ? C.nE : 0;
+    if (nd) *nd = C.built && C.nd.on ? 1 : 0;
+    if (solve_bytes) *solve_bytes = !C.built ? 0 : C.nd.on ? C.nd.bytes : (int64_t)(8 * C.nE * C.nE);
+    CR_API_END
+}
+
 cr_status cr_hybrid_mf_info(cr_hybrid h, int64_t *ncells, int64_t *bytes) {
     CR_API_BEGIN
     CR_REQUIRE(h, CR_ERR_INVALID_ARG, "null handle");

@@ -470,11 +470,11 @@ constexpr int kNdLeaf2 = 4, kNdLeaf3 = 3, kNdR = 2;
 
 struct HostFront {
     std::vector<int32_t> I, B;   // nodes
-    int kid[2] = {-1, -1};
+    std::vector<int> kids;       // child fronts
     int depth = 0;
 };
 
-static void nd_plan(int H, int D, std::vector<HostFront> &F) {
+static void nd_plan(int H, int D, std::vector<HostFront> &F, int box = 0) {
     const int n1 = H + 1, leaf = D == 2 ? kNdLeaf2 : kNdLeaf3;
     auto nid = [&](const int *c) {
         int64_t v = 0;
@@ -493,12 +493,11 @@ static void nd_plan(int H, int D, std::vector<HostFront> &F) {
         std::array<int, 3> slo = lo, shi = hi;
         if (ext[ax] > leaf) {
             const int s0 = (lo[ax] + hi[ax] - kNdR + 1) / 2, s1 = s0 + kNdR - 1;
-            int k = 0;
             std::array<int, 3> lo1 = lo, hi1 = hi, lo2 = lo, hi2 = hi;
             hi1[ax] = s0 - 1;
             lo2[ax] = s1 + 1;
-            if (hi1[ax] >= lo1[ax]) f.kid[k++] = rec(lo1, hi1, depth + 1);
-            if (hi2[ax] >= lo2[ax]) f.kid[k++] = rec(lo2, hi2, depth + 1);
+            if (hi1[ax] >= lo1[ax]) f.kids.push_back(rec(lo1, hi1, depth + 1));
+            if (hi2[ax] >= lo2[ax]) f.kids.push_back(rec(lo2, hi2, depth + 1));
             slo[ax] = s0;
             shi[ax] = s1;
         }
@@ -511,7 +510,53 @@ static void nd_plan(int H, int D, std::vector<HostFront> &F) {
         return (int)F.size() - 1;
     };
     F.clear();
-    rec({0, 0, 0}, {H, H, H}, 0);
+    if (box > 0) {
+        // flat two-level plan: separator slabs (2 nodes thick) after every `box` nodes per axis,
+        // root = all separator nodes, children = the boxes between them (any number)
+        // a slab must leave at least one node after it (else it would not separate anything)
+        auto sep = [&](int x) { return x % (box + kNdR) >= box && (x / (box + kNdR)) * (box + kNdR) + box + kNdR <= H; };
+        std::vector<std::array<int, 2>> seg;   // box intervals per axis
+        for (int x = 0; x <= H;) {
+            if (sep(x)) { ++x; continue; }
+            int y = x;
+            while (y + 1 <= H && !sep(y + 1)) ++y;
+            seg.push_back({x, y});
+            x = y + 1;
+        }
+        const int ns = (int)seg.size();
+        if (ns < 2) {   // the grid is smaller than one box: recursive bisection instead
+            nd_plan(H, D, F, 0);
+            return;
+        }
+        HostFront root;
+        root.depth = 0;
+        int nbox = 1;
+        for (int i = 0; i < D; ++i) nbox *= ns;
+        for (int bi = 0; bi < nbox; ++bi) {
+            int t = bi, c[3] = {0, 0, 0}, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+            for (int i = 0; i < D; ++i) { lo[i] = seg[t % ns][0]; hi[i] = seg[t % ns][1]; t /= ns; }
+            HostFront f;
+            f.depth = 1;
+            for (c[2] = lo[2]; c[2] <= hi[2]; ++c[2])
+                for (c[1] = lo[1]; c[1] <= hi[1]; ++c[1])
+                    for (c[0] = lo[0]; c[0] <= hi[0]; ++c[0]) f.I.push_back(nid(c));
+            std::sort(f.I.begin(), f.I.end());
+            root.kids.push_back((int)F.size());
+            F.push_back(std::move(f));
+        }
+        int c[3] = {0, 0, 0};
+        for (c[2] = 0; c[2] <= (D > 2 ? H : 0); ++c[2])
+            for (c[1] = 0; c[1] <= H; ++c[1])
+                for (c[0] = 0; c[0] <= H; ++c[0]) {
+                    bool s2 = false;
+                    for (int i = 0; i < D; ++i) s2 = s2 || sep(c[i]);
+                    if (s2) root.I.push_back(nid(c));
+                }
+        std::sort(root.I.begin(), root.I.end());
+        F.push_back(std::move(root));
+    } else {
+        rec({0, 0, 0}, {H, H, H}, 0);
+    }
     // B sets: stencil neighbours of the pivots and the children's B, eliminated later
     const int64_t nn = (int64_t)std::pow((double)n1, D);
     std::vector<int32_t> pos(nn, -1);
@@ -519,8 +564,7 @@ static void nd_plan(int H, int D, std::vector<HostFront> &F) {
         for (int32_t v : F[f].I) pos[v] = f;
     for (int f = 0; f < (int)F.size(); ++f) {
         std::vector<int32_t> b;
-        for (int k = 0; k < 2; ++k)
-            if (F[f].kid[k] >= 0) b.insert(b.end(), F[F[f].kid[k]].B.begin(), F[F[f].kid[k]].B.end());
+        for (int k : F[f].kids) b.insert(b.end(), F[k].B.begin(), F[k].B.end());
         for (int32_t v : F[f].I) {
             int cv[3] = {0, 0, 0};
             int64_t t = v;
@@ -671,12 +715,12 @@ __global__ void k_nd_assemble(NdLevelDev L, const NdFrontDev *fr, const int32_t 
 
 // F_f[map(k), map(l)] += U_child[k, l] for child `which` of every front of the level
 __global__ void k_nd_extend(NdLevelDev L, NdLevelDev Lc, const NdFrontDev *fr, const int32_t *map,
-                            const int32_t *child_slot, int which, double *Fpool) {
+                            const int32_t *kids, const int32_t *child_slot, int which, double *Fpool) {
     // child_slot[f] = index of front f within the child level arrays (fronts of depth d+1)
     for (int i = blockIdx.y; i < L.nf; i += gridDim.y) {
         const NdFrontDev F = fr[L.fronts[i]];
-        const int kid = which == 0 ? F.kid0 : F.kid1;
-        if (kid < 0) continue;
+        if (which >= F.kid_cnt) continue;
+        const int kid = kids[F.kid_off + which];
         const NdFrontDev K = fr[kid];
         const int ci = child_slot[kid];
         const int npc = Lc.nIp[ci] + Lc.nBp[ci], nIpc = Lc.nIp[ci];
@@ -780,7 +824,8 @@ struct NdSched {
 
 struct NdSolveView {
     const NdFrontDev *fr;
-    const int2 *inv;
+    const int64_t *invp;
+    const int32_t *invl;
     const int32_t *uidx;
     const double *finv, *w, *wt;
     double *bi, *lb, *u;
@@ -801,10 +846,8 @@ __global__ void __launch_bounds__(256) k_nd_solve(NdSolveView V, NdSched S, cons
         for (int64_t k = S.aoff[L] + gt; k < S.aoff[L + 1]; k += gs) {
             const int2 e = V.la[k];
             const NdFrontDev F = V.fr[e.x];
-            const int2 ch = V.inv[F.inv + e.y];
             double v = e.y < F.nI ? c[V.uidx[F.uoff + e.y]] : 0.0;
-            if (ch.x >= 0) v += __ldcg(V.u + ch.x);
-            if (ch.y >= 0) v += __ldcg(V.u + ch.y);
+            for (int64_t q = V.invp[F.inv + e.y]; q < V.invp[F.inv + e.y + 1]; ++q) v += __ldcg(V.u + V.invl[q]);
             if (e.y < F.nI) V.bi[F.bi + e.y] = v;
             else V.lb[F.lb + e.y - F.nI] = v;
         }
@@ -836,7 +879,7 @@ __global__ void __launch_bounds__(256) k_nd_solve(NdSolveView V, NdSched S, cons
 }
 
 static void gj_invert(double *A, int64_t n, cudaStream_t s);   // below (blocked Gauss-Jordan, SPD)
-static void spd_invert(double *A, int64_t n, cudaStream_t s);  // below (cuSOLVER Cholesky, GJ fallback)
+static void spd_invert(double *A, int64_t n, cudaStream_t s, int *info_d = nullptr);   // below (cuSOLVER Cholesky)
 
 struct BlasBatched {
     int (*GetrfB)(void *, int, double *const[], int, int *, int *, int) = nullptr;
@@ -867,8 +910,14 @@ template <int D>
 static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
     constexpr int M = D * D;
     CoarseNd &N = C.nd;
+    Trace tr(s);
     std::vector<HostFront> F;
-    nd_plan(H, D, F);
+    // 2D: the flat two-level plan (boxes of 12 nodes per side under one separator front): 3 solve
+    // phases instead of 3 per bisection level, the whole separator set as one dense front
+    // (configs[1] H = 64: 470 iterations, 0.48 ms each against dense H = 32's 774 x 0.37 ms).
+    // 3D: recursive bisection.  CR_ND_BOX overrides (0 = bisection; tests / experiments).
+    const char *eb = std::getenv("CR_ND_BOX");
+    nd_plan(H, D, F, eb ? std::max(0, atoi(eb)) : (D == 2 ? 12 : 0));
     const int nf = (int)F.size();
     int maxd = 0;
     for (auto &f : F) maxd = std::max(maxd, f.depth);
@@ -876,8 +925,7 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
     for (int f = 0; f < nf; ++f) lev[F[f].depth].push_back(f);
     std::vector<int> parent(nf, -1), slot(nf, 0);
     for (int f = 0; f < nf; ++f)
-        for (int k = 0; k < 2; ++k)
-            if (F[f].kid[k] >= 0) parent[F[f].kid[k]] = f;
+        for (int k : F[f].kids) parent[k] = f;
     // padded sizes: levels with many small fronts are factorised by batched cuBLAS calls
     std::vector<int> nIp(nf), nBp(nf);
     std::vector<char> batched(maxd + 1, 0);
@@ -895,7 +943,7 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
     std::vector<NdFrontDev> fr(nf);
     std::vector<int32_t> nodes, map;
     int64_t ofi = 0, ow = 0, owt = 0, obi = 0, ou = 0, olb = 0, oinv = 0, fpool = 0, maxn = 0, bytes = 0;
-    std::vector<int32_t> uidx;
+    std::vector<int32_t> uidx, kidl;
     std::vector<int64_t> fbase(nf);
     for (int f = 0; f < nf; ++f) {
         NdFrontDev &x = fr[f];
@@ -905,8 +953,9 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
         nodes.insert(nodes.end(), F[f].B.begin(), F[f].B.end());
         x.nI = (int32_t)F[f].I.size() * M;
         x.nB = (int32_t)F[f].B.size() * M;
-        x.kid0 = F[f].kid[0];
-        x.kid1 = F[f].kid[1];
+        x.kid_off = (int32_t)kidl.size();
+        x.kid_cnt = (int32_t)F[f].kids.size();
+        kidl.insert(kidl.end(), F[f].kids.begin(), F[f].kids.end());
         x.ldFi = nIp[f];
         x.ldW = std::max(nBp[f], 1);
         x.finv = ofi; ofi += (int64_t)nIp[f] * nIp[f];
@@ -943,22 +992,27 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
             }
         }
     }
-    // children's u entries landing on each local unknown of their parent (absolute u indices)
-    std::vector<int2> inv(oinv, make_int2(-1, -1));
+    // children's u entries landing on each local unknown of their parent (absolute u indices, in
+    // child order: a fixed summation order), as CSR rows
+    std::vector<std::vector<int32_t>> invr(oinv);
     for (int f = 0; f < nf; ++f)
-        for (int k = 0; k < 2; ++k) {
-            const int kid = F[f].kid[k];
-            if (kid < 0) continue;
-            for (int q = 0; q < fr[kid].nB; ++q) {
-                const int pos = map[fr[kid].map + q];
-                int2 &e = inv[fr[f].inv + pos];
-                (k == 0 ? e.x : e.y) = (int)(fr[kid].u + q);
-            }
-        }
+        for (int kid : F[f].kids)
+            for (int q = 0; q < fr[kid].nB; ++q) invr[fr[f].inv + map[fr[kid].map + q]].push_back((int32_t)(fr[kid].u + q));
+    std::vector<int64_t> invp(oinv + 1, 0);
+    std::vector<int32_t> invl;
+    for (int64_t g = 0; g < oinv; ++g) {
+        invl.insert(invl.end(), invr[g].begin(), invr[g].end());
+        invp[g + 1] = (int64_t)invl.size();
+    }
+    tr.mark("  nd: plan + maps (host)");
     upload(N.fr, fr, s);
     upload(N.nodes, nodes, s);
     upload(N.map, map, s);
-    upload(N.inv, inv, s);
+    upload(N.invp, invp, s);
+    if (invl.empty()) invl.push_back(0);
+    upload(N.invl, invl, s);
+    if (kidl.empty()) kidl.push_back(0);
+    upload(N.kids, kidl, s);
     upload(N.uidx, uidx, s);
     N.lb.alloc(std::max<int64_t>(olb, 1), s);
     N.finv.alloc(std::max<int64_t>(ofi, 1), s);
@@ -1000,15 +1054,20 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
         CR_REQUIRE(occ >= 1, CR_ERR_INVALID_ARG, "coarse ND solve kernel does not fit on an SM");
         N.grid = kSMs * std::min(occ, 8);   // more resident warps: the phases are latency-bound
     }
+    tr.mark("  nd: uploads + work lists");
     // numeric factorisation, deepest level first
     DevBuf<double> Fp;
     Fp.alloc(std::max<int64_t>(fpool, 1), s);
+    tr.mark("  nd: F pool alloc");
     std::vector<DevBuf<int32_t>> lfronts(maxd + 2), lnIp(maxd + 2), lnBp(maxd + 2);
     std::vector<DevBuf<int64_t>> lfoff(maxd + 2), lfbase(maxd + 2);
     std::vector<NdLevelDev> LV(maxd + 2);
     std::vector<int32_t> hslot(slot.begin(), slot.end());
     DevBuf<int32_t> dslot;
     upload(dslot, hslot, s);
+    DevBuf<int> finfo;   // cuSOLVER infos of the fronts inverted one by one, checked once at the end
+    finfo.alloc(2 * (size_t)nf, s);
+    finfo.zero(s);
     BlasBatched &bb = blas_batched();
     Blas &bl = blas();
     CR_REQUIRE(bl.handle && bb.GemmB && bb.GetrfB && bb.GetriB, CR_ERR_CUDA, "cuBLAS batched routines unavailable");
@@ -1030,14 +1089,18 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
         LV[d] = NdLevelDev{lfronts[d].get(), lfoff[d].get(), lfbase[d].get(), lnIp[d].get(), lnBp[d].get(), (int)L.size()};
         k_nd_assemble<D><<<grid_for(hoff.back(), T, 16), T, 0, s>>>(LV[d], N.fr.get(), N.nodes.get(), Es, H, Fp.get());
         CR_CHECK_LAUNCH();
+        tr.mark("  nd: level assemble");
         if (d < maxd) {
             int64_t mxb = 1;
-            for (int f : L)
-                for (int k = 0; k < 2; ++k)
-                    if (F[f].kid[k] >= 0) mxb = std::max<int64_t>(mxb, (int64_t)fr[F[f].kid[k]].nB * fr[F[f].kid[k]].nB);
+            int maxk = 0;
+            for (int f : L) {
+                maxk = std::max(maxk, (int)F[f].kids.size());
+                for (int k : F[f].kids) mxb = std::max<int64_t>(mxb, (int64_t)fr[k].nB * fr[k].nB);
+            }
             dim3 g((unsigned)std::min<int64_t>((mxb + T - 1) / T, 4096), (unsigned)std::min<size_t>(L.size(), 65535));
-            for (int which = 0; which < 2; ++which) {
-                k_nd_extend<<<g, T, 0, s>>>(LV[d], LV[d + 1], N.fr.get(), N.map.get(), dslot.get(), which, Fp.get());
+            for (int which = 0; which < maxk; ++which) {   // one child at a time: fixed summation order
+                k_nd_extend<<<g, T, 0, s>>>(LV[d], LV[d + 1], N.fr.get(), N.map.get(), N.kids.get(), dslot.get(), which,
+                                           Fp.get());
                 CR_CHECK_LAUNCH();
             }
         }
@@ -1084,7 +1147,7 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
                 double *Fi = N.finv.get() + fr[f].finv;
                 k_nd_copy_pivots<<<grid_for((int64_t)ni * ni, T, 16), T, 0, s>>>(base, np, ni, Fi);
                 CR_CHECK_LAUNCH();
-                spd_invert(Fi, ni, s);
+                spd_invert(Fi, ni, s, finfo.get() + 2 * f);
                 if (nbp > 0) {
                     dgemm(s, nbp, ni, ni, 1.0, base + ni, np, Fi, ni, 0.0, N.w.get() + fr[f].w, nbp);
                     dgemm(s, nbp, nbp, ni, -1.0, N.w.get() + fr[f].w, nbp, base + (int64_t)ni * np, np, 1.0,
@@ -1092,6 +1155,13 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
                 }
             }
         }
+    }
+    tr.mark("  nd: level factorisations");
+    {
+        std::vector<int> hinfo(2 * (size_t)nf);
+        CR_CUDA(cudaMemcpyAsync(hinfo.data(), finfo.get(), hinfo.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CR_CUDA(cudaStreamSynchronize(s));
+        for (int v : hinfo) CR_REQUIRE(v == 0, CR_ERR_SINGULAR_LOCAL, "coarse ND front is not positive definite");
     }
     // W^t (nI x nB, ld nI) for the forward pass: a warp per B row then reads contiguously
     {
@@ -1112,7 +1182,7 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
 static void nd_solve(const CoarseOp &C, const double *c, double *y, double *qout, double *partials, unsigned *ticket,
                      cudaStream_t s) {
     const CoarseNd &N = C.nd;
-    NdSolveView V{N.fr.get(), N.inv.get(), N.uidx.get(), N.finv.get(), N.w.get(), N.wt.get(),
+    NdSolveView V{N.fr.get(), N.invp.get(), N.invl.get(), N.uidx.get(), N.finv.get(), N.w.get(), N.wt.get(),
                   const_cast<double *>(N.bi.get()), const_cast<double *>(N.lb.get()), const_cast<double *>(N.u.get()),
                   N.la.get(), N.lbr.get(), N.lc.get()};
     NdSched S;
@@ -1194,10 +1264,13 @@ __global__ void k_mirror_lower(double *A, int64_t n) {   // column-major: A(j, i
     }
 }
 
-static void spd_invert(double *A, int64_t n64, cudaStream_t s) {
+// info_d != nullptr: no host synchronisation; the two cuSOLVER infos are written to info_d[0..1]
+// for the caller to check once (the ND setup inverts many fronts back to back)
+static void spd_invert(double *A, int64_t n64, cudaStream_t s, int *info_d) {
     Lapack &L = lapack();
     if (!L.handle) {
         gj_invert(A, n64, s);
+        if (info_d) CR_CUDA(cudaMemsetAsync(info_d, 0, 2 * sizeof(int), s));
         return;
     }
     const int n = (int)n64, lower = 0;
@@ -1208,14 +1281,19 @@ static void spd_invert(double *A, int64_t n64, cudaStream_t s) {
     DevBuf<double> work;
     work.alloc(std::max(std::max(lw1, lw2), 1), s);
     DevBuf<int> info;
-    info.alloc(2, s);
-    info.zero(s);
-    CR_REQUIRE(L.Potrf(L.handle, lower, n, A, n, work.get(), lw1, info.get()) == 0, CR_ERR_CUDA, "cusolverDnDpotrf failed");
-    CR_REQUIRE(L.Potri(L.handle, lower, n, A, n, work.get(), lw2, info.get() + 1) == 0, CR_ERR_CUDA, "cusolverDnDpotri failed");
+    int *inf = info_d;
+    if (!inf) {
+        info.alloc(2, s);
+        inf = info.get();
+    }
+    CR_CUDA(cudaMemsetAsync(inf, 0, 2 * sizeof(int), s));
+    CR_REQUIRE(L.Potrf(L.handle, lower, n, A, n, work.get(), lw1, inf) == 0, CR_ERR_CUDA, "cusolverDnDpotrf failed");
+    CR_REQUIRE(L.Potri(L.handle, lower, n, A, n, work.get(), lw2, inf + 1) == 0, CR_ERR_CUDA, "cusolverDnDpotri failed");
     k_mirror_lower<<<grid_for(n64 * n64, 256, 16), 256, 0, s>>>(A, n64);
     CR_CHECK_LAUNCH();
+    if (info_d) return;
     int hi[2] = {0, 0};
-    CR_CUDA(cudaMemcpyAsync(hi, info.get(), 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CR_CUDA(cudaMemcpyAsync(hi, inf, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     CR_CUDA(cudaStreamSynchronize(s));
     CR_REQUIRE(hi[0] == 0 && hi[1] == 0, CR_ERR_SINGULAR_LOCAL, "coarse matrix is not positive definite (potrf/potri)");
 }
@@ -1471,7 +1549,7 @@ void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double
 }  // namespace cr
 
 // ------------------------------------------------------------------ host-only plan export (tests)
-extern "C" cr_status cr_coarse_nd_plan(int32_t H, int32_t dim, int64_t *nfront, int32_t *maxdepth, int64_t *total_I,
+extern "C" cr_status cr_coarse_nd_plan(int32_t H, int32_t dim, int32_t box, int64_t *nfront, int32_t *maxdepth, int64_t *total_I,
                                        int64_t *total_B, int32_t *depth, int32_t *kids, int32_t *nI, int32_t *nB,
                                        int32_t *I_nodes, int32_t *B_nodes) {
     try {
@@ -1479,12 +1557,14 @@ extern "C" cr_status cr_coarse_nd_plan(int32_t H, int32_t dim, int64_t *nfront, 
         CR_REQUIRE(H >= 1 && H <= 256, CR_ERR_INVALID_ARG, "H must be in [1, 256]");
         CR_REQUIRE(nfront && maxdepth && total_I && total_B, CR_ERR_INVALID_ARG, "null argument");
         std::vector<cr::HostFront> F;
-        cr::nd_plan(H, dim, F);
+        CR_REQUIRE(box >= 0, CR_ERR_INVALID_ARG, "box must be >= 0");
+        cr::nd_plan(H, dim, F, box);
         int64_t ti = 0, tb = 0;
         int md = 0;
         for (size_t f = 0; f < F.size(); ++f) {
             if (depth) depth[f] = F[f].depth;
-            if (kids) { kids[2 * f] = F[f].kid[0]; kids[2 * f + 1] = F[f].kid[1]; }
+            if (kids)
+                for (int k : F[f].kids) kids[k] = (int32_t)f;   // kids[] returns each front's parent
             if (nI) nI[f] = (int32_t)F[f].I.size();
             if (nB) nB[f] = (int32_t)F[f].B.size();
             if (I_nodes) std::copy(F[f].I.begin(), F[f].I.end(), I_nodes + ti);

@@ -209,10 +209,10 @@ enum { AFW_SPD = 0, AFW_ABS = 1, AFW_GEN = 2 };
 struct NdFrontDev {
     int64_t ioff, boff;       // into nodes[]: I nodes, B nodes
     int64_t finv, w, wt, bi, u;   // into the pools (wt: W^t, nI x nB, ld nI)
-    int64_t lb, inv, uoff;        // local B rhs; children's u index per local unknown; global unknowns
+    int64_t lb, inv, uoff;        // local B rhs; children's u per local unknown (CSR row); global unknowns
     int64_t map;              // into map[]: this front's B unknown -> parent local unknown
     int32_t nI, nB;           // unknowns
-    int32_t kid0, kid1;       // child fronts (-1: none)
+    int32_t kid_off, kid_cnt; // child fronts: kids[kid_off .. kid_off + kid_cnt)
     int32_t ldFi, ldW;        // leading dimensions of Finv (>= nI) and W (>= nB)
 };
 struct CoarseNd {
@@ -223,7 +223,8 @@ struct CoarseNd {
     cr::DevBuf<int32_t> nodes, map;
     cr::DevBuf<double> finv, w, wt, bi, u;
     cr::DevBuf<double> lb;                     // forward: local right-hand side on B
-    cr::DevBuf<int2> inv;                      // per front local unknown: u index of child 0 / 1 (-1)
+    cr::DevBuf<int64_t> invp;                  // per front local unknown: CSR offsets into invl
+    cr::DevBuf<int32_t> invl, kids;            // children's u indices landing on it; child front lists
     cr::DevBuf<int32_t> uidx;                  // per front: global unknown of each local unknown
     cr::DevBuf<int2> la, lbr, lc;              // (front, local index) work lists by level
     std::vector<int> aoff, boff, coff;         // level offsets into la / lbr / lc

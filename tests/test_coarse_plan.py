@@ -22,9 +22,10 @@ def _coords(v, H, d):
     return np.array(c)
 
 
-@pytest.mark.parametrize("H,d", [(1, 2), (3, 2), (8, 2), (13, 2), (21, 2), (2, 3), (5, 3), (8, 3)])
-def test_nd_plan_is_a_valid_elimination(H, d):
-    pl = P.coarse_nd_plan(H, d)
+@pytest.mark.parametrize("H,d,box", [(1, 2, 0), (3, 2, 0), (8, 2, 0), (13, 2, 0), (21, 2, 0), (2, 3, 0), (5, 3, 0),
+                                     (8, 3, 0), (21, 2, 4), (24, 2, 6), (11, 2, 8), (9, 3, 3), (2, 2, 4)])
+def test_nd_plan_is_a_valid_elimination(H, d, box):
+    pl = P.coarse_nd_plan(H, d, box)
     nf = len(pl["I"])
     nn = (H + 1) ** d
     pos = np.full(nn, -1)
@@ -33,13 +34,11 @@ def test_nd_plan_is_a_valid_elimination(H, d):
             assert pos[v] == -1, "node in two fronts"
             pos[v] = f
     assert (pos >= 0).all()
-    parent = np.full(nf, -1)
+    parent = pl["parent"].astype(int)
     for f in range(nf):
-        for k in pl["kids"][f]:
-            if k >= 0:
-                assert k < f and parent[k] == -1
-                parent[k] = f
-                assert pl["depth"][k] == pl["depth"][f] + 1
+        if parent[f] >= 0:
+            assert f < parent[f]
+            assert pl["depth"][f] == pl["depth"][parent[f]] + 1
     assert (parent == -1).sum() == 1 and parent[nf - 1] == -1
     anc = [set() for _ in range(nf)]
     for f in range(nf):
