@@ -878,6 +878,48 @@ __global__ void __launch_bounds__(256) k_nd_solve(NdSolveView V, NdSched S, cons
     reduce_and_finish<1>(acc, partials, ticket, [&](double *t) { *qout = t[0]; });
 }
 
+// One phase of one level as its own launch (shallow trees: the flat plan has 2 levels, so 5 short
+// launches replace the persistent kernel and its spin barriers).  kind 0: A, 1: B, 2: C.
+__global__ void __launch_bounds__(256) k_nd_phase(NdSolveView V, int kind, int64_t k0, int64_t k1, const double *c,
+                                                  double *y) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+    if (kind == 0) {
+        for (int64_t k = k0 + gt; k < k1; k += gs) {
+            const int2 e = V.la[k];
+            const NdFrontDev F = V.fr[e.x];
+            double v = e.y < F.nI ? c[V.uidx[F.uoff + e.y]] : 0.0;
+            for (int64_t q = V.invp[F.inv + e.y]; q < V.invp[F.inv + e.y + 1]; ++q) v += V.u[V.invl[q]];
+            if (e.y < F.nI) V.bi[F.bi + e.y] = v;
+            else V.lb[F.lb + e.y - F.nI] = v;
+        }
+        return;
+    }
+    for (int64_t k = k0 + (gt >> 5); k < k1; k += gs >> 5) {
+        if (kind == 1) {
+            const int2 e = V.lbr[k];
+            const NdFrontDev F = V.fr[e.x];
+            const double a = warp_sum(nd_dot_lane(V.wt + F.wt + (int64_t)e.y * F.nI, V.bi + F.bi, F.nI, lane));
+            if (lane == 0) V.u[F.u + e.y] = V.lb[F.lb + e.y] - a;
+        } else {
+            const int2 e = V.lc[k];
+            const NdFrontDev F = V.fr[e.x];
+            const double pa = nd_dot_lane(V.finv + F.finv + (int64_t)e.y * F.ldFi, V.bi + F.bi, F.nI, lane);
+            const double pb = nd_dot_lane_g(V.w + F.w + (int64_t)e.y * F.ldW, y, V.uidx + F.uoff + F.nI, F.nB, lane);
+            const double a = warp_sum(pa - pb);
+            if (lane == 0) y[V.uidx[F.uoff + e.y]] = a;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_nd_cdot(int64_t n, const double *c, const double *y, double *qout,
+                                                 double *partials, unsigned *ticket) {
+    double acc[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        acc[0] = fma(c[i], y[i], acc[0]);
+    reduce_and_finish<1>(acc, partials, ticket, [&](double *t) { *qout = t[0]; });
+}
+
 static void gj_invert(double *A, int64_t n, cudaStream_t s);   // below (blocked Gauss-Jordan, SPD)
 static void spd_invert(double *A, int64_t n, cudaStream_t s, int *info_d = nullptr);   // below (cuSOLVER Cholesky)
 
@@ -1192,7 +1234,25 @@ static void nd_solve(const CoarseOp &C, const double *c, double *y, double *qout
         S.boff[L] = N.boff[L];
         S.coff[L] = N.coff[L];
     }
-    k_nd_solve<<<N.grid, 256, 0, s>>>(V, S, c, y, const_cast<unsigned *>(N.bar.get()), C.nE, qout, partials, ticket);
+    static const char *ep = std::getenv("CR_ND_PERSIST");
+    const bool persistent = ep ? atoi(ep) != 0 : N.maxdepth > 1;
+    if (persistent) {
+        k_nd_solve<<<N.grid, 256, 0, s>>>(V, S, c, y, const_cast<unsigned *>(N.bar.get()), C.nE, qout, partials, ticket);
+        CR_CHECK_LAUNCH();
+        return;
+    }
+    auto launch = [&](int kind, int64_t k0, int64_t k1) {
+        if (k1 <= k0) return;
+        const int64_t work = kind == 0 ? (k1 - k0) : (k1 - k0) * 32;
+        k_nd_phase<<<grid_for(work, 256, 8), 256, 0, s>>>(V, kind, k0, k1, c, y);
+        CR_CHECK_LAUNCH();
+    };
+    for (int L = 0; L < S.nlev; ++L) {
+        launch(0, S.aoff[L], S.aoff[L + 1]);
+        launch(1, S.boff[L], S.boff[L + 1]);
+    }
+    for (int L = 0; L < S.nlev; ++L) launch(2, S.coff[L], S.coff[L + 1]);
+    k_nd_cdot<<<occ_grid(k_nd_cdot, 256, C.nE), 256, 0, s>>>(C.nE, c, y, qout, partials, ticket);
     CR_CHECK_LAUNCH();
 }
 
