@@ -39,7 +39,7 @@ METRIC = "hybridised-system PCG time-to-solution; SpMV GB/s as % of B200 HBM pea
 CONFIG_IDX = 1
 METHOD = "pcg_afw2"  # patch additive Schwarz + coarse "stress x area" correction
 MATRIX_FREE = 1      # G applied from per-cell factors
-COARSE = 32          # coarse grid intervals per direction (dense E^-1; H = 64 uses the flat ND solve)
+COARSE = 64          # coarse grid intervals per direction (flat nested-dissection coarse solve)
 MAX_ITER = 20000     # a cap (the solve takes ~800): a regression fails loudly instead of running on
 # Jacobi-PCG iterations of configs[1] to a true 1e-10 residual, measured on B200 by this
 # bench (used only by --impl reference to extrapolate the oracle's per-iteration time).
@@ -222,8 +222,8 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- our arm
 # solver per config
-OTHER_SOLVERS = {2: dict(method="dc", coarse=32, mu_inner=1.0),
-                 3: dict(method="dc", coarse=32, mu_inner=0.5, inner_rtol=1e-7),
+OTHER_SOLVERS = {2: dict(method="dc", coarse=64, mu_inner=1.0),
+                 3: dict(method="dc", coarse=64, mu_inner=0.5, inner_rtol=1e-7),
                  4: dict(method="pcg_afw2", matrix_free=1, coarse=16)}
 
 

@@ -208,7 +208,7 @@ typedef struct {
     int64_t max_iter;     /* total Krylov iterations cap                                       */
     int32_t check_every;  /* iterations per captured CUDA graph between host checks (def 64)   */
     int32_t matrix_free;  /* 0: assembled G; 1: matrix-free factored G (see above)             */
-    int32_t coarse;       /* CR_PCG_AFW2: coarse intervals per direction (0: 32 in 2D, 16 in 3D; <= 256);
+    int32_t coarse;       /* CR_PCG_AFW2: coarse intervals per direction (0: 64 in 2D, 16 in 3D; <= 256);
                            * E^{-1} dense up to 8000 unknowns, else nested-dissection fronts  */
     double mu_inner;      /* CR_DC_FGMRES: mass coefficient of the inner transient operator (0: 1) */
     double inner_rtol;    /* CR_DC_FGMRES: inner PCG tolerance (0: 1e-11)                       */

@@ -43,6 +43,21 @@ static void keep_pool() {
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        // reserve physical memory for the pool once (CR_POOL_RESERVE_GB, default 16): growing the
+        // pool mid-solve (mapping new memory after a burst of frees of mixed sizes) stalled the
+        // first allocation after a two-level solve for up to 0.5 s
+        const char *e = std::getenv("CR_POOL_RESERVE_GB");
+        const double gb = e ? atof(e) : 16.0;
+        size_t fr = 0, tot = 0;
+        if (gb > 0 && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+            const size_t want = std::min((size_t)(gb * 1073741824.0), fr / 2);
+            void *p = nullptr;
+            if (want > 0 && cudaMallocAsync(&p, want, 0) == cudaSuccess) {
+                cudaFreeAsync(p, 0);
+                cudaStreamSynchronize(0);
+            }
+            cudaGetLastError();
+        }
     }
     done_dev = dev;
 }

@@ -267,6 +267,7 @@ struct cr_hybrid_s {
     cr::DevBuf<double> fbar, dir, uit, pit;
     bool has_dir = false, has_uit = false, has_pit = false;
     cr::DevBuf<double> rcell, gcell;   // explicit cell right-hand sides (dc.cu), empty unless set
+    cr::DevBuf<double> uhat;           // recovery scratch: per-cell copies of U
     // shift
     cr::DevBuf<uint8_t> inM1;
     cr::DevBuf<double> lam, E;   // lam [nc], E [nc][d+1]

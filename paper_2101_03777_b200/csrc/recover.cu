@@ -163,8 +163,9 @@ void recover(const cr_hybrid_s *h, const double *W, double *U, double *P, double
     const int64_t nc = m->nc, nrows = m->nf_int;
     MeshView mv = mesh_view(m);
     ProbView p = prob_view(h);
-    DevBuf<double> Uhat;
-    Uhat.alloc(nc * (D + 1) * D, s);
+    // the per-cell copies live in the handle (allocated once: no pool traffic per recovery)
+    DevBuf<double> &Uhat = const_cast<cr_hybrid_s *>(h)->uhat;
+    if (Uhat.n != (size_t)(nc * (D + 1) * D)) Uhat.alloc(nc * (D + 1) * D, s);
     DevBuf<int> err;
     err.alloc(1, s);
     err.zero(s);

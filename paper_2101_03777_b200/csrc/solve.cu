@@ -1351,7 +1351,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         constexpr int SLOTS = D == 2 ? 2 : 3;
         build_afw(h, AFW_SPD, s);
         trc.mark("patch preconditioner");
-        const int H = o.coarse > 0 ? o.coarse : (D == 2 ? 32 : 16);
+        const int H = o.coarse > 0 ? o.coarse : (D == 2 ? 64 : 16);
         // E = Z^t G Z needs G applied to colour sums of coarse columns; with the matrix-free G only
         // the 32-cell slices touching the colour's support are applied (the rest of z is zero)
         DevBuf<uint8_t> sflag;
@@ -1699,7 +1699,7 @@ static void apply_precond_t(cr_hybrid_s *h, int method, const double *r, double 
         case CR_PCG_AFW2: {
             build_afw(h, AFW_SPD, s);
             // the coarse grid of the last two-level solve, else the default
-            const int Hc = h->coarse.requested > 0 ? h->coarse.requested : (D == 2 ? 32 : 16);
+            const int Hc = h->coarse.requested > 0 ? h->coarse.requested : (D == 2 ? 64 : 16);
             build_coarse(h, Hc, [&](const double *zz, double *Y, int) { spmv(h->G, zz, Y, s); }, s);
             if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
             CR_CUDA(cudaMemsetAsync(w->st.get(), 0, sizeof(KState), s));
