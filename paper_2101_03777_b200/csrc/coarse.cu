@@ -999,7 +999,7 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
     for (int d = 0; d <= maxd; ++d) {
         int mi = 0, mb = 0;
         for (int f : lev[d]) { mi = std::max(mi, (int)F[f].I.size() * M); mb = std::max(mb, (int)F[f].B.size() * M); }
-        batched[d] = lev[d].size() >= 4 && mi <= 256;
+        batched[d] = lev[d].size() >= 4 && mi <= 640;
         for (size_t k = 0; k < lev[d].size(); ++k) {
             const int f = lev[d][k];
             slot[f] = (int)k;
