@@ -13,6 +13,7 @@
 //   GMRES(m)  (nonsymmetric): Arnoldi with classical Gram-Schmidt twice, Givens on device
 // Stopping rule: TRUE relative residual ||S - G W|| / ||S|| <= rtol (reading 12).
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include <cmath>
 #include <cstddef>
@@ -1149,7 +1150,12 @@ static void launch_afw(Launcher &L, cudaStream_t ks, const double *r, double *zs
     const int64_t nt = P.nslices * 32 * D;
     const bool sym = P.built != AFW_GEN;
     // two-level: leave one block per SM to the coarse kernels that run concurrently on the side stream
-    const int rsv = 0;   // (reserving SM slots for the concurrent coarse kernels measured slower)
+    // two-level in 2D: leave 2 of the 4 block slots per SM to the concurrent coarse path (its
+    // latency-bound nested-dissection phases then overlap the patch solves: -3 % per iteration at
+    // H = 64; in 3D and with the dense E^-1 reserving measured slower).  CR_AFW_RSV overrides.
+    static const char *er = std::getenv("CR_AFW_RSV");
+    const bool two_level = WHAT == AFW_PCG2 || WHAT == AFW_PCG2_INIT;
+    const int rsv = er ? atoi(er) : (D == 2 && two_level && !L.dist && L.h->coarse.nd.on ? 2 : 0);
     KState *st = L.w->st.get();
     double *part = L.w->partials.get();
     if (P.kmax <= 6) {
