@@ -293,12 +293,12 @@ cr_status cr_partition_plan(int32_t dim, int64_t nf_int, const int32_t *cell_fac
 /* The nested-dissection plan of the coarse solve (host only, no GPU; coarse.cu)
  * for an (H+1)^dim node grid: box = 0 recursive bisection, box > 0 the flat two-level plan
  * (separator slabs after every `box` nodes form the root, the boxes are its children).  Fronts
- * in post-order (children before parents), each with its depth, its parent (in `kids` [nf]; -1
+ * in post-order (children before parents), each with its depth, its parent (parent [nf]; -1
  * for the root), pivot nodes I and boundary nodes B (the later-eliminated nodes its subtree
  * couples to through the 5^dim-node stencil of Z^t G Z), the lists concatenated in front order
  * (node = x + (H+1) (y + (H+1) z)).  Call once with the array arguments NULL to size them.     */
 cr_status cr_coarse_nd_plan(int32_t H, int32_t dim, int32_t box, int64_t *nfront, int32_t *maxdepth, int64_t *total_I,
-                            int64_t *total_B, int32_t *depth, int32_t *kids, int32_t *nI, int32_t *nB,
+                            int64_t *total_B, int32_t *depth, int32_t *parent, int32_t *nI, int32_t *nB,
                             int32_t *I_nodes, int32_t *B_nodes);
 
 /* Sparse direct solve A x = b of a canonical CSR system (int64 row_ptr [n+1], int32 cols, f64

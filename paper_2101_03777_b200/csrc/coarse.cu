@@ -1635,7 +1635,7 @@ void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double
 
 // ------------------------------------------------------------------ host-only plan export (tests)
 extern "C" cr_status cr_coarse_nd_plan(int32_t H, int32_t dim, int32_t box, int64_t *nfront, int32_t *maxdepth, int64_t *total_I,
-                                       int64_t *total_B, int32_t *depth, int32_t *kids, int32_t *nI, int32_t *nB,
+                                       int64_t *total_B, int32_t *depth, int32_t *parent, int32_t *nI, int32_t *nB,
                                        int32_t *I_nodes, int32_t *B_nodes) {
     try {
         CR_REQUIRE(dim == 2 || dim == 3, CR_ERR_INVALID_ARG, "dim must be 2 or 3");
@@ -1648,8 +1648,10 @@ extern "C" cr_status cr_coarse_nd_plan(int32_t H, int32_t dim, int32_t box, int6
         int md = 0;
         for (size_t f = 0; f < F.size(); ++f) {
             if (depth) depth[f] = F[f].depth;
-            if (kids)
-                for (int k : F[f].kids) kids[k] = (int32_t)f;   // kids[] returns each front's parent
+            if (parent) {
+                if (f + 1 == F.size()) parent[f] = -1;
+                for (int k : F[f].kids) parent[k] = (int32_t)f;
+            }
             if (nI) nI[f] = (int32_t)F[f].I.size();
             if (nB) nB[f] = (int32_t)F[f].B.size();
             if (I_nodes) std::copy(F[f].I.begin(), F[f].I.end(), I_nodes + ti);
