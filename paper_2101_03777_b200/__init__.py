@@ -551,19 +551,32 @@ def coarse_nd_plan(H: int, dim: int, box: int = 0) -> dict:
                 I=[In[oi[f]:oi[f + 1]] for f in range(n)], B=[Bn[ob[f]:ob[f + 1]] for f in range(n)])
 
 
+_PINNED = {}
+
+
+def _pinned(shape, dtype, slot):
+    key = (shape, dtype, slot)
+    t = _PINNED.get(key)
+    if t is None:
+        t = _PINNED[key] = torch.empty(shape, dtype=dtype, pin_memory=True)
+    return t
+
+
 def hybrid_method_host(coords, cells, fbar, mu: float, nu: float, method: str = "pcg", rtol: float = 1e-10,
                        stream=None, comm: Comm | None = None, matrix_free: int = 0, coarse: int = 0, **kw) -> dict:
     """End-to-end entry point from HOST buffers: pinned host -> device copies, the hybrid
-    method on the device, and U, P copied back to host (the `e2e` path of bench.py)."""
+    method on the device, and U, P copied back to host (the `e2e` path of bench.py).  U_host and
+    P_host are pinned buffers reused by the next call with the same sizes."""
     dev = torch.device("cuda")
     c = coords.to(dev, non_blocking=True)
     k = cells.to(dev, non_blocking=True)
     f = fbar.to(dev, non_blocking=True)
     prob = Problem(mu=mu, nu=nu, fbar=f, **kw)
     out = hybrid_method(c, k, prob, method, rtol, stream, comm, matrix_free=matrix_free, coarse=coarse)
-    # results land in pinned host buffers (page-locked: full-speed device -> host copies)
-    Uh = torch.empty(out["U"].shape, dtype=out["U"].dtype, pin_memory=True)
-    Ph = torch.empty(out["P"].shape, dtype=out["P"].dtype, pin_memory=True)
+    # results land in pinned host buffers (page-locked: full-speed device -> host copies), kept per
+    # shape and reused by the next call (page-locking 100 MB costs tens of ms): copy them to keep them
+    Uh = _pinned(tuple(out["U"].shape), out["U"].dtype, 0)
+    Ph = _pinned(tuple(out["P"].shape), out["P"].dtype, 1)
     Uh.copy_(out["U"], non_blocking=True)
     Ph.copy_(out["P"], non_blocking=True)
     torch.cuda.current_stream().synchronize()
