@@ -90,19 +90,39 @@ __global__ void k_coarse_faces(const int32_t *dof_face, int64_t row0, int64_t nr
     }
 }
 
+// row r is "interior" to its coarse cell when every face of its two cells lies in that cell: G z
+// then vanishes on r for any z supported outside the cell (setup restrictions skip such rows)
+template <int D>
+__global__ void k_coarse_interior(const int32_t *dof_face, const int32_t *face_cells, const int32_t *cell_faces,
+                                  const int32_t *face_dof, int64_t nrows, const uint32_t *cc, uint32_t *key) {
+    constexpr int NF = D + 1;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = dof_face[r];
+        bool inter = true;
+        for (int side = 0; side < 2; ++side) {
+            const int64_t K = face_cells[2 * f + side];
+            for (int l = 0; l < NF; ++l) {
+                const int d = face_dof[cell_faces[K * NF + l]];
+                if (d >= 0 && cc[d] != cc[r]) inter = false;
+            }
+        }
+        key[r] = cc[r] * 2u + (inter ? 1u : 0u);
+    }
+}
+
 // partial restriction of one chunk: the 2^D nodes of its coarse cell x D^2 tensor components.
 // One thread per row with all 2^D D^2 accumulators (16 in 2D, 72 in 3D); rows are read 4 at a time
 // per thread (independent loads in flight); warp shuffles then shared memory reduce the block
 // (fixed trees: deterministic).
 template <int D>
 __global__ void __launch_bounds__(256) k_coarse_restrict(CoarseView C, const double *r, double *part,
-                                                         const int32_t *list = nullptr) {
+                                                         const int32_t *list = nullptr, const int64_t *ends = nullptr) {
     constexpr int NN = 1 << D, DD = D * D, NV = NN * DD;
     constexpr int TPR = 1;                           // threads per row
     constexpr int NA = NV;                           // accumulators per thread
     constexpr int SL = 256 / TPR, U = 4;
     const int64_t ch = list ? (int64_t)list[blockIdx.x] : (int64_t)blockIdx.x;   // list: a subset of chunks
-    const int64_t b = C.chunk_start[ch], e = C.chunk_start[ch + 1];
+    const int64_t b = C.chunk_start[ch], e = ends ? ends[blockIdx.x] : C.chunk_start[ch + 1];
     const int slot = threadIdx.x / TPR;
     double acc[NA];
 #pragma unroll
@@ -263,10 +283,11 @@ __global__ void k_coarse_colour(CoarseView C, int64_t nrows, int colour, int k, 
 // of the colour's supports; every other row of z stays 0), or those rows cleared
 template <int D>
 __global__ void __launch_bounds__(256) k_coarse_colour_chunks(CoarseView C, const int32_t *list, int colour, int k,
-                                                              int l, int clear, double *z) {
+                                                              int l, int clear, double *z, const int64_t *ends = nullptr) {
     constexpr int NN = 1 << D;
     const int64_t ch = list[blockIdx.x];
-    for (int64_t t = C.chunk_start[ch] + threadIdx.x; t < C.chunk_start[ch + 1]; t += blockDim.x) {
+    const int64_t end = ends ? ends[blockIdx.x] : C.chunk_start[ch + 1];
+    for (int64_t t = C.chunk_start[ch] + threadIdx.x; t < end; t += blockDim.x) {
         const int64_t r = C.perm[t];
         double s = 0.0;
         if (!clear) {
@@ -371,10 +392,10 @@ __global__ void k_gj_cols(double *E, int64_t n, int64_t k0, int b, const double 
 // shuffles, takes the rows 4k + L / 8 (k = 0..7) of every 32-row batch.  Fixed shuffle / shared
 // memory trees: deterministic.
 __global__ void __launch_bounds__(256, 2) k_coarse_restrict3(CoarseView C, const double *r, double *part,
-                                                          const int32_t *list = nullptr) {
+                                                          const int32_t *list = nullptr, const int64_t *ends = nullptr) {
     constexpr int D = 3, DD = 9, NV = 72, U = 4;
     const int64_t ch = list ? (int64_t)list[blockIdx.x] : (int64_t)blockIdx.x;
-    const int64_t b = C.chunk_start[ch], e = C.chunk_start[ch + 1];
+    const int64_t b = C.chunk_start[ch], e = ends ? ends[blockIdx.x] : C.chunk_start[ch + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int corner = lane & 7, rsub = lane >> 3;
     double acc[DD];
@@ -435,12 +456,14 @@ __global__ void __launch_bounds__(256, 2) k_coarse_restrict3(CoarseView C, const
 }
 
 // first sorted position with coarse cell >= c (c = 0..ncc)
-__global__ void k_cell_starts(const uint32_t *cc_sorted, int64_t n, int64_t ncc, int64_t *cstart) {
+__global__ void k_cell_starts(const uint32_t *cc_sorted, int64_t n, int64_t ncc, int64_t *cstart, int mult = 1,
+                              int add = 0) {
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= ncc; c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t key = c * mult + add;
         int64_t lo = 0, hi = n;
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
-            if ((int64_t)cc_sorted[mid] < c) lo = mid + 1;
+            if ((int64_t)cc_sorted[mid] < key) lo = mid + 1;
             else hi = mid;
         }
         cstart[c] = lo;
@@ -1433,11 +1456,24 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
                                                        m->cell_faces.get(), m->a.get(), m->xs.get(), C.g, C.fx.get(),
                                                        C.fa.get(), cc.get());
     CR_CHECK_LAUNCH();
+    // sort key: coarse cell x 2 + interior bit (single rank), so each cell's rows that G can couple
+    // to a neighbouring cell come first
+    const bool layered = !h->part.on;
+    std::vector<int64_t> cbnd(ncc + 1, 0);   // per cell: first interior row (sorted position)
     {
+        DevBuf<uint32_t> key;
+        if (layered) {
+            key.alloc(nrows, s);
+            k_coarse_interior<D><<<grid_for(nrows, T), T, 0, s>>>(m->dof_face.get(), m->face_cells.get(),
+                                                                  m->cell_faces.get(), m->face_dof.get(), nrows, cc.get(),
+                                                                  key.get());
+            CR_CHECK_LAUNCH();
+            CR_CUDA(cudaMemcpyAsync(cc.get(), key.get(), nrows * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        }
         k_iota_u32<<<grid_for(nrows, T), T, 0, s>>>(idx.get(), nrows);
         CR_CHECK_LAUNCH();
         int bits = 1;
-        while (((int64_t)1 << bits) < ncc) ++bits;
+        while (((int64_t)1 << bits) < ncc * (layered ? 2 : 1)) ++bits;
         size_t tb = 0;
         CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, cc.get(), cc2.get(), idx.get(),
                                                 reinterpret_cast<uint32_t *>(C.perm.get()), (int)nrows, 0, bits, s));
@@ -1448,11 +1484,20 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
         // rows of each coarse cell (device), chunks of <= kCH rows (host: a few thousand entries)
         DevBuf<int64_t> cs;
         cs.alloc(ncc + 1, s);
-        k_cell_starts<<<grid_for(ncc + 1, T), T, 0, s>>>(cc2.get(), nrows, ncc, cs.get());
+        k_cell_starts<<<grid_for(ncc + 1, T), T, 0, s>>>(cc2.get(), nrows, ncc, cs.get(), layered ? 2 : 1, 0);
         CR_CHECK_LAUNCH();
         std::vector<int64_t> cstart(ncc + 1);
         CR_CUDA(cudaMemcpyAsync(cstart.data(), cs.get(), (ncc + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         CR_CUDA(cudaStreamSynchronize(s));
+        if (layered) {
+            k_cell_starts<<<grid_for(ncc + 1, T), T, 0, s>>>(cc2.get(), nrows, ncc, cs.get(), 2, 1);
+            CR_CHECK_LAUNCH();
+            CR_CUDA(cudaMemcpyAsync(cbnd.data(), cs.get(), (ncc + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            CR_CUDA(cudaStreamSynchronize(s));
+        } else {
+            cbnd = std::vector<int64_t>(cstart.begin() + 1, cstart.end());   // every row "boundary"
+            cbnd.push_back(nrows);
+        }
         std::vector<int64_t> chunk_start, cell_chunk(ncc + 1, 0);
         for (int64_t c = 0; c < ncc; ++c) {
             cell_chunk[c] = (int64_t)chunk_start.size();
@@ -1502,11 +1547,13 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
     // cells: the H clamp above.)
     const bool restricted = !h->part.on;
     std::vector<int32_t> lsup, lact;
-    std::vector<int64_t> osup(ncol + 1, 0), oact(ncol + 1, 0);
+    std::vector<int64_t> osup(ncol + 1, 0), oact(ncol + 1, 0), lend;
     DevBuf<int32_t> dsup, dact;
+    DevBuf<int64_t> dend;
     if (restricted) {
-        std::vector<int64_t> hcc(ncc + 1);
+        std::vector<int64_t> hcc(ncc + 1), hcs(C.nchunk + 1);
         CR_CUDA(cudaMemcpyAsync(hcc.data(), C.cell_chunk.get(), (ncc + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CR_CUDA(cudaMemcpyAsync(hcs.data(), C.chunk_start.get(), (C.nchunk + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         CR_CUDA(cudaStreamSynchronize(s));
         for (int colour = 0; colour < ncol; ++colour) {
             for (int64_t cell = 0; cell < ncc; ++cell) {
@@ -1524,7 +1571,13 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
                 }
                 for (int64_t ch = hcc[cell]; ch < hcc[cell + 1]; ++ch) {
                     if (sup) lsup.push_back((int32_t)ch);
-                    if (act) lact.push_back((int32_t)ch);
+                    if (sup) {   // the colour's supports: every row
+                        lact.push_back((int32_t)ch);
+                        lend.push_back(hcs[ch + 1]);
+                    } else if (act && hcs[ch] < cbnd[cell]) {   // ring cells: rows G couples outside the cell
+                        lact.push_back((int32_t)ch);
+                        lend.push_back(std::min(hcs[ch + 1], cbnd[cell]));
+                    }
                 }
             }
             osup[colour + 1] = (int64_t)lsup.size();
@@ -1532,6 +1585,7 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
         }
         upload(dsup, lsup, s);
         upload(dact, lact, s);
+        upload(dend, lend, s);
         Y.zero(s);
     }
     for (int colour = 0; colour < ncol; ++colour)
@@ -1549,8 +1603,12 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
                 if (restricted) {
                     C.part.zero(s);
                     if (nact) {
-                        if (D == 3) k_coarse_restrict3<<<nact, 256, 0, s>>>(V, Y.get(), C.part.get(), dact.get() + oact[colour]);
-                        else k_coarse_restrict<D><<<nact, 256, 0, s>>>(V, Y.get(), C.part.get(), dact.get() + oact[colour]);
+                        if (D == 3)
+                            k_coarse_restrict3<<<nact, 256, 0, s>>>(V, Y.get(), C.part.get(), dact.get() + oact[colour],
+                                                                    dend.get() + oact[colour]);
+                        else
+                            k_coarse_restrict<D><<<nact, 256, 0, s>>>(V, Y.get(), C.part.get(), dact.get() + oact[colour],
+                                                                      dend.get() + oact[colour]);
                     }
                 } else {
                     if (D == 3) k_coarse_restrict3<<<(unsigned)C.nchunk, 256, 0, s>>>(V, Y.get(), C.part.get());
@@ -1560,7 +1618,9 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
                 CR_CHECK_LAUNCH();
                 if (restricted) {
                     if (nsup) k_coarse_colour_chunks<D><<<nsup, 256, 0, s>>>(V, dsup.get() + osup[colour], colour, k, l, 1, z.get());
-                    if (nact) k_coarse_colour_chunks<D><<<nact, 256, 0, s>>>(V, dact.get() + oact[colour], colour, k, l, 1, Y.get());
+                    if (nact)
+                        k_coarse_colour_chunks<D><<<nact, 256, 0, s>>>(V, dact.get() + oact[colour], colour, k, l, 1, Y.get(),
+                                                                       dend.get() + oact[colour]);
                     CR_CHECK_LAUNCH();
                 }
                 if (h->part.on) h->comm->impl->allreduce(C.c.get(), (int)C.nE, false, s);
