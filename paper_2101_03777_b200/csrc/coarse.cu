@@ -972,6 +972,8 @@ static void gj_invert(double *A, int64_t n, cudaStream_t s);   // below (blocked
 static void spd_invert(double *A, int64_t n, cudaStream_t s, int *info_d = nullptr);   // below (cuSOLVER Cholesky)
 
 struct BlasBatched {
+    int (*TrsmB)(void *, int, int, int, int, int, int, const double *, const double *const[], int, double *const[], int,
+                 int) = nullptr;
     int (*GetrfB)(void *, int, double *const[], int, int *, int *, int) = nullptr;
     int (*GetriB)(void *, int, const double *const[], int, const int *, double *const[], int, int *, int) = nullptr;
     int (*GemmB)(void *, int, int, int, int, int, const double *, const double *const[], int, const double *const[], int,
@@ -983,6 +985,7 @@ static BlasBatched &blas_batched() {
         Blas &bl = blas();
         if (!bl.h) return x;
         x.GetrfB = (decltype(x.GetrfB))dlsym(bl.h, "cublasDgetrfBatched");
+        x.TrsmB = (decltype(x.TrsmB))dlsym(bl.h, "cublasDtrsmBatched");
         x.GetriB = (decltype(x.GetriB))dlsym(bl.h, "cublasDgetriBatched");
         x.GemmB = (decltype(x.GemmB))dlsym(bl.h, "cublasDgemmBatched");
         return x;
@@ -994,6 +997,38 @@ template <class T>
 static void upload(DevBuf<T> &d, const std::vector<T> &h, cudaStream_t s) {
     d.alloc(h.size(), s);
     if (!h.empty()) CR_CUDA(cudaMemcpyAsync(d.get(), h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+struct Lapack;
+static Lapack &lapack();
+static bool lapack_potrf_batched(int n, int lda, int nb, double **A, int *info, cudaStream_t s);
+
+__global__ void k_identity_batched(double *const *X, int n, int nb) {
+    const int64_t tot = (int64_t)n * n * nb;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int b = (int)(t / ((int64_t)n * n));
+        const int64_t e = t - (int64_t)b * n * n;
+        X[b][e] = (e % n) == (e / n) ? 1.0 : 0.0;
+    }
+}
+
+// Finv = A^{-1} for a batch of SPD pivot blocks (in place factor of A, ld lda; Finv ld n):
+// Cholesky (cusolverDnDpotrfBatched), X = I, L X = I, L^t X' = X (two cublasDtrsmBatched).
+// Returns false when a routine is unavailable (the caller then uses batched LU + inverse).
+static bool nd_batched_cholesky_inverse(int n, int lda, int nb, double **dA, double **dX, const std::vector<double *> &,
+                                        int *info, cudaStream_t s) {
+    BlasBatched &bb = blas_batched();
+    Blas &bl = blas();
+    if (!bb.TrsmB || !bl.handle) return false;
+    if (!lapack_potrf_batched(n, lda, nb, dA, info, s)) return false;
+    k_identity_batched<<<grid_for((int64_t)n * n * nb, 256, 16), 256, 0, s>>>(dX, n, nb);
+    CR_CHECK_LAUNCH();
+    bl.SetStream(bl.handle, s);
+    const double one = 1.0;
+    // column-major: side left (0), lower (0), no-trans (0) / trans (1), non-unit diagonal (0)
+    CR_REQUIRE(bb.TrsmB(bl.handle, 0, 0, 0, 0, n, n, &one, dA, lda, dX, n, nb) == 0, CR_ERR_CUDA, "cublasDtrsmBatched failed");
+    CR_REQUIRE(bb.TrsmB(bl.handle, 0, 0, 1, 0, n, n, &one, dA, lda, dX, n, nb) == 0, CR_ERR_CUDA, "cublasDtrsmBatched failed");
+    return true;
 }
 
 template <int D>
@@ -1216,9 +1251,12 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
             piv.alloc((size_t)ni * nb, s);
             info.alloc(nb, s);
             info.zero(s);
-            CR_REQUIRE(bb.GetrfB(bl.handle, ni, dA.get(), np, piv.get(), info.get(), nb) == 0, CR_ERR_CUDA, "cublasDgetrfBatched failed");
-            CR_REQUIRE(bb.GetriB(bl.handle, ni, dA.get(), np, piv.get(), dFi.get(), ni, info.get(), nb) == 0, CR_ERR_CUDA,
-                       "cublasDgetriBatched failed");
+            if (!nd_batched_cholesky_inverse(ni, np, nb, dA.get(), dFi.get(), pFi, info.get(), s)) {
+                CR_REQUIRE(bb.GetrfB(bl.handle, ni, dA.get(), np, piv.get(), info.get(), nb) == 0, CR_ERR_CUDA,
+                           "cublasDgetrfBatched failed");
+                CR_REQUIRE(bb.GetriB(bl.handle, ni, dA.get(), np, piv.get(), dFi.get(), ni, info.get(), nb) == 0, CR_ERR_CUDA,
+                           "cublasDgetriBatched failed");
+            }
             std::vector<int> hinfo(nb);
             CR_CUDA(cudaMemcpyAsync(hinfo.data(), info.get(), nb * sizeof(int), cudaMemcpyDeviceToHost, s));
             CR_CUDA(cudaStreamSynchronize(s));
@@ -1346,6 +1384,7 @@ struct Lapack {
     int (*Potrf)(void *, int, int, double *, int, double *, int, int *) = nullptr;
     int (*PotriBS)(void *, int, int, double *, int, int *) = nullptr;
     int (*Potri)(void *, int, int, double *, int, double *, int, int *) = nullptr;
+    int (*PotrfB)(void *, int, int, double *[], int, int *, int) = nullptr;
 };
 static Lapack &lapack() {
     static thread_local Lapack L = [] {
@@ -1358,6 +1397,7 @@ static Lapack &lapack() {
         x.Potrf = (decltype(x.Potrf))dlsym(x.h, "cusolverDnDpotrf");
         x.PotriBS = (decltype(x.PotriBS))dlsym(x.h, "cusolverDnDpotri_bufferSize");
         x.Potri = (decltype(x.Potri))dlsym(x.h, "cusolverDnDpotri");
+        x.PotrfB = (decltype(x.PotrfB))dlsym(x.h, "cusolverDnDpotrfBatched");
         if (!(x.Create && x.SetStream && x.PotrfBS && x.Potrf && x.PotriBS && x.Potri) || x.Create(&x.handle) != 0)
             x.handle = nullptr;
         return x;
@@ -1404,6 +1444,14 @@ static void spd_invert(double *A, int64_t n64, cudaStream_t s, int *info_d) {
     CR_CUDA(cudaMemcpyAsync(hi, inf, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     CR_CUDA(cudaStreamSynchronize(s));
     CR_REQUIRE(hi[0] == 0 && hi[1] == 0, CR_ERR_SINGULAR_LOCAL, "coarse matrix is not positive definite (potrf/potri)");
+}
+
+static bool lapack_potrf_batched(int n, int lda, int nb, double **A, int *info, cudaStream_t s) {
+    Lapack &L = lapack();
+    if (!L.handle || !L.PotrfB) return false;
+    L.SetStream(L.handle, s);
+    CR_REQUIRE(L.PotrfB(L.handle, 0, n, A, lda, info, nb) == 0, CR_ERR_CUDA, "cusolverDnDpotrfBatched failed");
+    return true;
 }
 
 template <int D>
