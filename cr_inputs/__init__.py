@@ -68,12 +68,16 @@ def normal01(seed: int, stream: int, index) -> np.ndarray:
 
 # ----------------------------------------------------------------------------- meshes
 
-def square_mesh(n: int, jitter: float = 0.0, seed: int = 0):
-    """Unit square, n x n squares, each split along the lower-left -> upper-right
-    diagonal into two triangles (SPEC.md L38 layout).
+def square_mesh(n: int, jitter: float = 0.0, seed: int = 0, flip_seed: int | None = None):
+    """Unit square, n x n squares, each split along a diagonal into two triangles.
 
-    vertex (i, j) -> j*(n+1)+i ; square (i, j) -> cells 2(jn+i) = {(i,j),(i+1,j),(i+1,j+1)}
-    and 2(jn+i)+1 = {(i,j),(i+1,j+1),(i,j+1)}.
+    vertex (i, j) -> j*(n+1)+i ; square (i, j) -> cells 2(jn+i) and 2(jn+i)+1.
+    Default (``flip_seed`` None, SPEC.md L38 layout): every square is split along its
+    lower-left -> upper-right diagonal: {(i,j),(i+1,j),(i+1,j+1)}, {(i,j),(i+1,j+1),(i,j+1)}.
+    ``flip_seed`` given: each square independently (counter-based coin of stream 21) takes
+    the other diagonal, {(i,j),(i+1,j),(i,j+1)}, {(i+1,j),(i+1,j+1),(i,j+1)} — an
+    unstructured-topology stand-in for the paper's Mesh1 family: interior vertex
+    valences then range over 4..8 instead of a fixed 6.
     ``jitter`` is the amplitude relative to h: interior vertices move by independent
     U(-jitter*h, jitter*h) per coordinate (BASELINE.json configs[2] "up to 0.2h").
     Returns coords [nv,2] f64, cells [nc,3] i32.
@@ -99,35 +103,62 @@ def square_mesh(n: int, jitter: float = 0.0, seed: int = 0):
     cells = np.empty((2 * n * n, 3), dtype=np.int32)
     cells[0::2] = np.stack([v00, v10, v11], axis=1)
     cells[1::2] = np.stack([v00, v11, v01], axis=1)
+    if flip_seed is not None:
+        flip = uniform01(flip_seed, 21, np.arange(n * n, dtype=np.uint64)) < 0.5
+        cells[0::2][flip] = np.stack([v00, v10, v01], axis=1)[flip]
+        cells[1::2][flip] = np.stack([v10, v11, v01], axis=1)[flip]
     return coords, cells
 
 
 _PERMS3 = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]
 
 
-def cube_mesh(n: int):
-    """Unit cube, n^3 cubes, each split into the 6 Kuhn tetrahedra sharing the main
+def cube_mesh(n: int, flip_seed: int | None = None, jitter: float = 0.0, seed: int = 0):
+    """Unit cube, n^3 cubes, each split into the 6 Kuhn tetrahedra sharing a main
     diagonal ("splitting in 6 tetrahedra each cube").
 
     vertex (i,j,k) -> (k(n+1)+j)(n+1)+i ; cube (i,j,k) -> tets 6(kn^2+jn+i)+p for the
     axis permutations p in lexicographic order; tet vertices: corner, corner+e_p0,
-    corner+e_p0+e_p1, corner+e_p0+e_p1+e_p2.
+    corner+e_p0+e_p1, corner+e_p0+e_p1+e_p2 (corner = the cube's lowest vertex).
+    ``flip_seed`` given: the Kuhn split of cube (i,j,k) is mirrored in x iff bx[i], in y iff
+    by[j], in z iff bz[k] (counter-based coins, streams 31..33) — i.e. it runs along one of
+    the 4 main diagonals.  The triangulation a cube induces on a square face depends only
+    on the mirror bits of the two axes spanning that face, which the neighbour across the
+    face shares, so the mesh stays conforming while edge valences vary (an unstructured
+    stand-in, as in ``square_mesh``).  ``jitter``: interior vertices move by independent
+    U(-jitter*h, jitter*h) per coordinate (seed ``seed``, streams 0..2).
     """
     h = 1.0 / n
     k, j, i = np.meshgrid(np.arange(n + 1), np.arange(n + 1), np.arange(n + 1), indexing="ij")
     coords = np.stack([i.ravel() * h, j.ravel() * h, k.ravel() * h], axis=1).astype(np.float64)
     for c, g in enumerate((i, j, k)):
         coords[g.ravel() == n, c] = 1.0
+    if jitter > 0.0:
+        vid = np.arange((n + 1) ** 3, dtype=np.uint64)
+        interior = np.ones(vid.shape, dtype=bool)
+        for g in (i, j, k):
+            interior &= (g.ravel() > 0) & (g.ravel() < n)
+        for c in range(3):
+            dx = (2.0 * uniform01(seed, c, vid) - 1.0) * (jitter * h)
+            coords[interior, c] += dx[interior]
     ck, cj, ci = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
     ci = ci.ravel(); cj = cj.ravel(); ck = ck.ravel()
     stride = (1, n + 1, (n + 1) ** 2)
-    corner = (ck * (n + 1) + cj) * (n + 1) + ci
+    if flip_seed is None:
+        mir = [np.zeros(ci.shape, dtype=np.int64)] * 3
+    else:
+        line = np.arange(n, dtype=np.uint64)
+        mir = [(uniform01(flip_seed, 31 + a, line) < 0.5).astype(np.int64)[g]
+               for a, g in enumerate((ci, cj, ck))]
+    # start corner of the (possibly mirrored) diagonal; steps of -1 along mirrored axes
+    corner = ((ck + mir[2]) * (n + 1) + (cj + mir[1])) * (n + 1) + (ci + mir[0])
+    step = [stride[a] * (1 - 2 * mir[a]) for a in range(3)]
     cells = np.empty((6 * n ** 3, 4), dtype=np.int32)
     for p, perm in enumerate(_PERMS3):
         v0 = corner
-        v1 = v0 + stride[perm[0]]
-        v2 = v1 + stride[perm[1]]
-        v3 = v2 + stride[perm[2]]
+        v1 = v0 + step[perm[0]]
+        v2 = v1 + step[perm[1]]
+        v3 = v2 + step[perm[2]]
         cells[p::6] = np.stack([v0, v1, v2, v3], axis=1)
     return coords, cells
 

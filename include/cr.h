@@ -129,7 +129,9 @@ void cr_destroy_coupled(cr_coupled c);
  * Ahat_K^{-1}, w = Ahat^{-1} D_K, B_K = D_K^t w, G_K and S_K in double-double,
  * written straight into a sliced block-ELL G (d x d blocks, width 2d+1) — no atomics, no
  * staging.  shift = MIS runs the M1/M2 construction first (hashed-priority Luby rounds that
- * reproduce the sequential greedy MIS exactly).  `comm` must be NULL (1 GPU).
+ * reproduce the sequential greedy MIS exactly).  `comm`: NULL (or a single-rank communicator
+ * without an id) = the whole G on this GPU; a multi-rank communicator = this rank's block rows
+ * only (see "multi-GPU" below; the communicator must outlive the handle).
  * Synchronises `s`.  Errors: NO_INTERIOR_FACE, SINGULAR_LOCAL, INVALID_ARG, OOM, CUDA.   */
 cr_status cr_hybridise(cr_mesh m, const cr_params *prm, const cr_data *data, cr_comm comm,
                        cr_stream_t s, cr_hybrid *out);
@@ -212,6 +214,13 @@ typedef struct {
                            * E^{-1} dense up to 8000 unknowns, else nested-dissection fronts  */
     double mu_inner;      /* CR_DC_FGMRES: mass coefficient of the inner transient operator (0: 1) */
     double inner_rtol;    /* CR_DC_FGMRES: inner PCG tolerance (0: 1e-11)                       */
+    int32_t refine_dd;    /* 1: parity mode (PCG methods, one GPU): after the fp64 solve, iterative
+                           * refinement W += G^{-1}(S - G W) with the residual S - G W evaluated in
+                           * double-double (the operator the solve used: assembled G, or the
+                           * factored G_K of every cell, summed in dd) until that residual is
+                           * <= rtol (at most 8 rounds; rel_res_true is then the dd residual).
+                           * Reaches below the fp64 residual floor of the recursive iteration. */
+    int32_t reserved;
 } cr_solver_opts;
 typedef struct {
     int64_t iterations;
@@ -222,7 +231,16 @@ typedef struct {
     double seconds;            /* device time of the solve (CUDA events)                        */
     int64_t spmv_calls;
     int64_t kernel_launches;   /* kernels launched by cr_solve                                   */
-    int64_t inner_iterations;  /* CR_DC_FGMRES: inner PCG iterations over all outer ones         */
+    int64_t inner_iterations;  /* CR_DC_FGMRES: inner PCG iterations over all outer ones;
+                                  refine_dd: PCG iterations of the refinement rounds             */
+    double kappa_lanczos_est;  /* PCG methods: lambda_max / lambda_min of the preconditioned G,
+                                  estimated from the Lanczos tridiagonal of the first <= 1024 CG
+                                  coefficients (alpha_k, beta_k); 0 for other methods            */
+    double lambda_min_est, lambda_max_est;
+    double bytes_moved;        /* algorithmic HBM bytes of the iterations (per-iteration bytes of
+                                  the method's kernels x iterations)               */
+    int32_t refine_rounds;     /* refine_dd: refinement rounds run                               */
+    int32_t reserved;
 } cr_solve_report;
 cr_status cr_solve(cr_hybrid h, const cr_solver_opts *opts, double *W_d, cr_stream_t s,
                    cr_solve_report *rep);
@@ -245,6 +263,14 @@ cr_status cr_hybrid_precond_info(cr_hybrid h, int64_t *npatch, int32_t *kmax, in
  * and max_K |sum_{sigma in F_K} a_{K,sigma} . U_sigma| (boundary faces at their Dirichlet value). */
 cr_status cr_recover(cr_hybrid h, const double *W_d, double *U_d, double *P_d, double *diag_d,
                      cr_stream_t s);
+
+/* ------------------------------------------------------------------ Newton update
+ * U_d[i] += dU_d[i] (i < nU), P_d[k] += dP_d[k] (k < nP) on the device, and returns on the host
+ * norms_h[0] = ||dU||_2, norms_h[1] = ||U + dU||_2 (fixed-order reductions: deterministic);
+ * Newton's method stops when norms_h[0] <= tol * norms_h[1] (tol = 5e-7).
+ * U_d / dU_d [nU], P_d / dP_d [nP] (dP_d may be NULL: P unchanged).  Synchronises `s`.       */
+cr_status cr_newton_update(int64_t nU, double *U_d, const double *dU_d, int64_t nP, double *P_d,
+                           const double *dP_d, double *norms_h, cr_stream_t s);
 
 /* Per (cell, local face) values of a face field (the Newton iterate layout of cr_data.u_iter_d,
  * P:L302): out_d[K][l] = U_d[face_dof(sigma)] on interior faces, bnd_d[K][l] (wall / lid values;
@@ -310,6 +336,34 @@ cr_status cr_coarse_nd_plan(int32_t H, int32_t dim, int32_t box, int64_t *nfront
 cr_status cr_sparse_direct_solve(int64_t n, int64_t nnz, const int64_t *row_ptr_d, const int32_t *cols_d,
                                  const double *vals_d, const double *b_d, double *x_d, int32_t method,
                                  int32_t reorder, cr_stream_t s, int32_t *singularity);
+
+/* ------------------------------------------------------------------ the whole method from HOST buffers
+ * The paper's "hybrid method" end to end for a caller whose data lives in host
+ * memory: coords_h [nv][dim], cells_h [nc][dim+1], fbar_h [nc][dim] (and, when non-NULL,
+ * dirichlet_h [nc][dim+1][dim]) are copied to the device on `s` (pinned host memory makes the
+ * copies asynchronous DMA; pageable memory works, staged by the driver), then cr_build_mesh ->
+ * cr_hybridise -> cr_solve -> cr_recover run on the device, and U_h [nf_int][dim] and P_h [nc]
+ * (caller-owned HOST buffers; size nf_int from the mesh — pass sizes_h [2] = {nf_int*dim, nc}
+ * capacities) receive the result.  The handles and device buffers live only for the call.
+ * mesh_info (may be NULL) receives the mesh counts; rep the solve report.  Synchronises `s`.
+ * Errors: those of the four calls; INVALID_ARG when a capacity is too small.               */
+cr_status cr_hybrid_method_host(int32_t dim, int64_t nv, const double *coords_h, int64_t nc,
+                                const int32_t *cells_h, const cr_params *prm, const double *fbar_h,
+                                const double *dirichlet_h, const cr_solver_opts *opts, double *U_h,
+                                double *P_h, const int64_t *sizes_h, cr_mesh_info_t *mesh_info,
+                                cr_solve_report *rep, cr_stream_t s);
+
+/* ------------------------------------------------------------------ memory and accounting
+ * All device memory of the handles comes from the library's OWN stream-ordered pool on the
+ * current device (cudaMemPoolCreate; the device's default pool is never modified).  The pool
+ * keeps freed memory mapped for re-use by the next call (release threshold UINT64_MAX).
+ * cr_pool_reserve: map `bytes` into the pool now (opt-in; avoids mapping new memory in the
+ * middle of a later solve).  cr_pool_trim: return all but `keep_bytes` of the unused memory.
+ * cr_kernel_launches: kernels this process launched from libcr so far (direct launches plus
+ * the kernel nodes of every replayed solver graph; CUB, cuBLAS and cuSOLVER launches excluded). */
+cr_status cr_pool_reserve(int64_t bytes, cr_stream_t s);
+cr_status cr_pool_trim(int64_t keep_bytes);
+int64_t cr_kernel_launches(void);
 
 const char *cr_last_error(void);
 const char *cr_version(void);

@@ -66,14 +66,18 @@ class Data(ctypes.Structure):
 class SolverOpts(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int32), ("restart", ctypes.c_int32), ("rtol", ctypes.c_double),
                 ("max_iter", ctypes.c_int64), ("check_every", ctypes.c_int32), ("matrix_free", ctypes.c_int32),
-                ("coarse", ctypes.c_int32), ("mu_inner", ctypes.c_double), ("inner_rtol", ctypes.c_double)]
+                ("coarse", ctypes.c_int32), ("mu_inner", ctypes.c_double), ("inner_rtol", ctypes.c_double),
+                ("refine_dd", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class SolveReport(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int64), ("rel_res_true", ctypes.c_double),
                 ("rel_res_recursive", ctypes.c_double), ("converged", ctypes.c_int32),
                 ("status", ctypes.c_int32), ("seconds", ctypes.c_double), ("spmv_calls", ctypes.c_int64),
-                ("kernel_launches", ctypes.c_int64), ("inner_iterations", ctypes.c_int64)]
+                ("kernel_launches", ctypes.c_int64), ("inner_iterations", ctypes.c_int64),
+                ("kappa_lanczos_est", ctypes.c_double), ("lambda_min_est", ctypes.c_double),
+                ("lambda_max_est", ctypes.c_double), ("bytes_moved", ctypes.c_double),
+                ("refine_rounds", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -111,6 +115,11 @@ _sig = {
     "cr_coarse_nd_plan": [_i32, _i32, _i32, _P(_i64), _P(_i32), _P(_i64), _P(_i64), _vp, _vp, _vp, _vp, _vp, _vp],
     "cr_sparse_direct_solve": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _P(_i32)],
     "cr_hybrid_coarse_info": [_vp, _P(_i32), _P(_i64), _P(_i32), _P(_i64)],
+    "cr_newton_update": [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp],
+    "cr_hybrid_method_host": [_i32, _i64, _vp, _i64, _vp, _P(Params), _vp, _vp, _P(SolverOpts), _vp, _vp, _vp,
+                              _P(MeshInfo), _P(SolveReport), _vp],
+    "cr_pool_reserve": [_i64, _vp],
+    "cr_pool_trim": [_i64],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -121,9 +130,12 @@ for _name in ("cr_destroy_mesh", "cr_destroy_coupled", "cr_destroy_hybrid", "cr_
     getattr(_lib, _name).restype = None
 _lib.cr_last_error.restype = ctypes.c_char_p
 _lib.cr_version.restype = ctypes.c_char_p
+_lib.cr_kernel_launches.restype = ctypes.c_int64
+_lib.cr_kernel_launches.argtypes = []
 
 ABI_SYMBOLS = sorted(list(_sig) + ["cr_destroy_mesh", "cr_destroy_coupled", "cr_destroy_hybrid",
-                                   "cr_comm_destroy", "cr_loopback_destroy", "cr_last_error", "cr_version"])
+                                   "cr_comm_destroy", "cr_loopback_destroy", "cr_last_error", "cr_version",
+                                   "cr_kernel_launches"])
 
 
 def _check(status: int, report=None):
@@ -151,6 +163,21 @@ def _ptr(t: torch.Tensor | None, dtype=None):
 
 def version() -> str:
     return _lib.cr_version().decode()
+
+
+def kernel_launches() -> int:
+    """Kernels libcr launched in this process so far (cr_kernel_launches)."""
+    return int(_lib.cr_kernel_launches())
+
+
+def pool_reserve(nbytes: int, stream=None):
+    """Map nbytes into libcr's own memory pool now (cr_pool_reserve; opt-in)."""
+    _check(_lib.cr_pool_reserve(int(nbytes), _stream(stream)))
+
+
+def pool_trim(keep_bytes: int = 0):
+    """Return unused pool memory beyond keep_bytes to the device (cr_pool_trim)."""
+    _check(_lib.cr_pool_trim(int(keep_bytes)))
 
 
 # ------------------------------------------------------------------ handles
@@ -381,17 +408,23 @@ def partition_plan(dim: int, cell_faces, face_cells, face_dof, rank: int, nranks
     return dict(row0=int(rr[0]), row1=int(rr[1]), recv_counts=rc, send_counts=sc, ghosts=gh, send_rows=sr)
 
 
-def cr_solve(hyb: Hybrid, W: torch.Tensor, method: str | int = "pcg", rtol: float = 1e-10,
-             max_iter: int = 10**7, check_every: int = 64, restart: int = 50, matrix_free: int = 0, coarse: int = 0,
-             mu_inner: float = 0.0, inner_rtol: float = 0.0, stream=None, raise_on_fail: bool = True) -> dict:
-    """Krylov solve of G W = S in place (P:L549).  Returns the cr_solve_report as a dict.
-    method "dc" (CR_DC_FGMRES): outer FGMRES on the coupled system preconditioned by the
-    transient hybrid solve (mu_inner, inner_rtol); max_iter then caps the outer iterations."""
+def _opts(method, rtol, max_iter, check_every, restart, matrix_free, coarse, mu_inner, inner_rtol, refine_dd):
     m = METHODS[method] if isinstance(method, str) else int(method)
     if m == CR_DC_FGMRES and max_iter == 10**7:
         max_iter = 0
-    opts = SolverOpts(m, restart, rtol, max_iter, check_every, int(matrix_free), int(coarse), float(mu_inner),
-                      float(inner_rtol))
+    return SolverOpts(m, restart, rtol, max_iter, check_every, int(matrix_free), int(coarse), float(mu_inner),
+                      float(inner_rtol), int(refine_dd), 0)
+
+
+def cr_solve(hyb: Hybrid, W: torch.Tensor, method: str | int = "pcg", rtol: float = 1e-10,
+             max_iter: int = 10**7, check_every: int = 64, restart: int = 50, matrix_free: int = 0, coarse: int = 0,
+             mu_inner: float = 0.0, inner_rtol: float = 0.0, refine_dd: int = 0, stream=None,
+             raise_on_fail: bool = True) -> dict:
+    """Krylov solve of G W = S in place (P:L549).  Returns the cr_solve_report as a dict.
+    method "dc" (CR_DC_FGMRES): outer FGMRES on the coupled system preconditioned by the
+    transient hybrid solve (mu_inner, inner_rtol); max_iter then caps the outer iterations.
+    refine_dd = 1: double-double residual + iterative refinement (parity mode, PCG methods)."""
+    opts = _opts(method, rtol, max_iter, check_every, restart, matrix_free, coarse, mu_inner, inner_rtol, refine_dd)
     rep = SolveReport()
     st = _lib.cr_solve(hyb._h, ctypes.byref(opts), _ptr(W, torch.float64), _stream(stream), ctypes.byref(rep))
     out = rep.as_dict()
@@ -511,14 +544,23 @@ def newton_ns(coords: torch.Tensor, cells: torch.Tensor, nu: float, fbar: torch.
         W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=dev)
         reps.append(cr_solve(hyb, W, method, rtol, stream=stream, **solve_kw))
         dU, dP, _ = cr_recover(hyb, W, stream)
-        U = U + dU
-        Pk = Pk + dP
-        rel = float(torch.linalg.norm(dU) / torch.clamp(torch.linalg.norm(U), min=1e-300))
+        du, un = newton_update(U, dU, Pk, dP, stream)
+        rel = du / max(un, 1e-300)
         hist.append(rel)
         del hyb
         if rel <= tol:
             break
     return dict(mesh=mesh, U=U, P=Pk, history=hist, reports=reps)
+
+
+def newton_update(U: torch.Tensor, dU: torch.Tensor, P: torch.Tensor | None = None, dP: torch.Tensor | None = None,
+                  stream=None):
+    """U += dU, P += dP in place on the device (cr_newton_update); returns (||dU||, ||U_new||)."""
+    norms = (ctypes.c_double * 2)()
+    _check(_lib.cr_newton_update(U.numel(), _ptr(U, torch.float64), _ptr(dU, torch.float64),
+                                 0 if P is None else P.numel(), _ptr(P, torch.float64), _ptr(dP, torch.float64),
+                                 ctypes.cast(norms, ctypes.c_void_p), _stream(stream)))
+    return norms[0], norms[1]
 
 
 def sparse_direct_solve(rp: torch.Tensor, ci: torch.Tensor, v: torch.Tensor, b: torch.Tensor, method: str = "chol",
@@ -551,34 +593,50 @@ def coarse_nd_plan(H: int, dim: int, box: int = 0) -> dict:
                 I=[In[oi[f]:oi[f + 1]] for f in range(n)], B=[Bn[ob[f]:ob[f + 1]] for f in range(n)])
 
 
-_PINNED = {}
-
-
-def _pinned(shape, dtype, slot):
-    key = (shape, dtype, slot)
-    t = _PINNED.get(key)
-    if t is None:
-        t = _PINNED[key] = torch.empty(shape, dtype=dtype, pin_memory=True)
-    return t
+def _hptr(a, dtype):
+    """Host pointer of a contiguous CPU tensor / numpy array of the given torch dtype."""
+    import numpy as np
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda:
+            raise ValueError("host buffers expected (cr_hybrid_method_host copies them to the device)")
+        if a.dtype != dtype or not a.is_contiguous():
+            raise TypeError(f"expected a contiguous {dtype} CPU tensor")
+        return ctypes.c_void_p(a.data_ptr())
+    npd = {torch.float64: np.float64, torch.int32: np.int32}[dtype]
+    if not isinstance(a, np.ndarray) or a.dtype != npd or not a.flags.c_contiguous:
+        raise TypeError(f"expected a C-contiguous {npd.__name__} array")
+    return a.ctypes.data_as(ctypes.c_void_p)
 
 
 def hybrid_method_host(coords, cells, fbar, mu: float, nu: float, method: str = "pcg", rtol: float = 1e-10,
-                       stream=None, comm: Comm | None = None, matrix_free: int = 0, coarse: int = 0, **kw) -> dict:
-    """End-to-end entry point from HOST buffers: pinned host -> device copies, the hybrid
-    method on the device, and U, P copied back to host (the `e2e` path of bench.py).  U_host and
-    P_host are pinned buffers reused by the next call with the same sizes."""
-    dev = torch.device("cuda")
-    c = coords.to(dev, non_blocking=True)
-    k = cells.to(dev, non_blocking=True)
-    f = fbar.to(dev, non_blocking=True)
-    prob = Problem(mu=mu, nu=nu, fbar=f, **kw)
-    out = hybrid_method(c, k, prob, method, rtol, stream, comm, matrix_free=matrix_free, coarse=coarse)
-    # results land in pinned host buffers (page-locked: full-speed device -> host copies), kept per
-    # shape and reused by the next call (page-locking 100 MB costs tens of ms): copy them to keep them
-    Uh = _pinned(tuple(out["U"].shape), out["U"].dtype, 0)
-    Ph = _pinned(tuple(out["P"].shape), out["P"].dtype, 1)
-    Uh.copy_(out["U"], non_blocking=True)
-    Ph.copy_(out["P"], non_blocking=True)
-    torch.cuda.current_stream().synchronize()
-    out["U_host"], out["P_host"] = Uh, Ph
-    return out
+                       stream=None, dirichlet=None, out: tuple | None = None, matrix_free: int = 0, coarse: int = 0,
+                       max_iter: int = 10**7, check_every: int = 64, restart: int = 50, mu_inner: float = 0.0,
+                       inner_rtol: float = 0.0, refine_dd: int = 0, gauge_cell: int = 0, **prob_kw) -> dict:
+    """The hybrid method end to end from HOST buffers through the C ABI (cr_hybrid_method_host):
+    host -> device copies, mesh, hybridisation, solve, recovery and device -> host copies of U and
+    P, all on `stream` (synchronised before returning).  coords [nv, d] f64, cells [nc, d+1] i32,
+    fbar [nc, d] f64 (CPU tensors or numpy; pinned memory makes the copies asynchronous DMA).
+    out = (U_h, P_h): caller-owned host buffers with capacity >= d * nf_int and >= nc (default:
+    fresh pinned tensors, owned by the caller).  Returns U_host [nf_int, d], P_host [nc] (views of
+    out), the solve report and the mesh counts."""
+    d = int(coords.shape[1])
+    nv, nc = int(coords.shape[0]), int(cells.shape[0])
+    if out is None:
+        cap = (d + 1) * nc // 2 + (d + 1) * nc % 2   # nf_int <= (d+1) nc / 2
+        out = (torch.empty(cap * d, dtype=torch.float64, pin_memory=True),
+               torch.empty(nc, dtype=torch.float64, pin_memory=True))
+    Uh, Ph = out
+    sizes = (ctypes.c_int64 * 2)(Uh.numel(), Ph.numel())
+    prob = Problem(mu=mu, nu=nu, fbar=None, gauge_cell=gauge_cell, **prob_kw)
+    prm = prob.params()
+    opts = _opts(method, rtol, max_iter, check_every, restart, matrix_free, coarse, mu_inner, inner_rtol, refine_dd)
+    info, rep = MeshInfo(), SolveReport()
+    _check(_lib.cr_hybrid_method_host(d, nv, _hptr(coords, torch.float64), nc, _hptr(cells, torch.int32),
+                                      ctypes.byref(prm), _hptr(fbar, torch.float64),
+                                      None if dirichlet is None else _hptr(dirichlet, torch.float64),
+                                      ctypes.byref(opts), _hptr(Uh, torch.float64), _hptr(Ph, torch.float64),
+                                      ctypes.cast(sizes, ctypes.c_void_p), ctypes.byref(info), ctypes.byref(rep),
+                                      _stream(stream)), rep.as_dict())
+    nU = int(info.n_unknowns)
+    return dict(U_host=Uh[:nU].view(-1, d), P_host=Ph[:nc], report=rep.as_dict(), nf_int=int(info.nf_int),
+                nf=int(info.nf), n_unknowns=nU)

@@ -1,12 +1,15 @@
 // C ABI entry points of libcr (include/cr.h).  Every entry point converts exceptions into a
 // cr_status and a thread-local message; no C++ exception crosses the ABI.
 #include <cstring>
+#include <memory>
 #include <string>
 
 #include "internal.cuh"
 
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
+#include <mutex>
 
 namespace cr {
 static thread_local std::string g_last_error;
@@ -32,35 +35,56 @@ void Trace::mark(const char *what) {
 }
 }  // namespace cr
 
-// Keep freed stream-ordered memory in the device's default pool (no trim to the OS at every
-// synchronisation): repeated solves re-use their buffers without remapping.
-static void keep_pool() {
+namespace cr {
+// ------------------------------------------------------------------ memory pool, SM count, launch counter
+static std::mutex g_dev_mu;
+static cudaMemPool_t g_pool[64] = {};
+static int g_sms[64] = {};
+static std::atomic<long long> g_launches{0};
+thread_local bool g_capturing = false;
+
+static int cur_dev() {
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return;
-    static thread_local int done_dev = -1;
-    if (done_dev == dev) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        // reserve physical memory for the pool once (CR_POOL_RESERVE_GB, default 16): growing the
-        // pool mid-solve (mapping new memory after a burst of frees of mixed sizes) stalled the
-        // first allocation after a two-level solve for up to 0.5 s
-        const char *e = std::getenv("CR_POOL_RESERVE_GB");
-        const double gb = e ? atof(e) : 16.0;
-        size_t fr = 0, tot = 0;
-        if (gb > 0 && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
-            const size_t want = std::min((size_t)(gb * 1073741824.0), fr / 2);
-            void *p = nullptr;
-            if (want > 0 && cudaMallocAsync(&p, want, 0) == cudaSuccess) {
-                cudaFreeAsync(p, 0);
-                cudaStreamSynchronize(0);
-            }
-            cudaGetLastError();
-        }
-    }
-    done_dev = dev;
+    CR_CUDA(cudaGetDevice(&dev));
+    CR_REQUIRE(dev >= 0 && dev < 64, CR_ERR_INVALID_ARG, "device index out of range");
+    return dev;
 }
+
+cudaMemPool_t lib_pool() {
+    const int dev = cur_dev();
+    if (g_pool[dev]) return g_pool[dev];
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (!g_pool[dev]) {
+        cudaMemPoolProps pp{};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.handleTypes = cudaMemHandleTypeNone;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = dev;
+        cudaMemPool_t pool;
+        CR_CUDA(cudaMemPoolCreate(&pool, &pp));
+        // memory freed by one call stays mapped for the next (no trim at synchronisations):
+        // repeated solves re-use their buffers without remapping.  cr_pool_trim returns it.
+        uint64_t thr = UINT64_MAX;
+        CR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        g_pool[dev] = pool;
+    }
+    return g_pool[dev];
+}
+
+int num_sms() {
+    const int dev = cur_dev();
+    if (!g_sms[dev]) {
+        int n = 0;
+        CR_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+        g_sms[dev] = n > 0 ? n : 1;
+    }
+    return g_sms[dev];
+}
+
+void count_launches(int64_t n) {
+    if (!g_capturing) g_launches.fetch_add(n, std::memory_order_relaxed);
+}
+}  // namespace cr
 
 cr_hybrid_s::~cr_hybrid_s() { cr::free_solver_work(work); }
 
@@ -84,14 +108,34 @@ cr_hybrid_s::~cr_hybrid_s() { cr::free_solver_work(work); }
 extern "C" {
 
 const char *cr_last_error(void) { return cr::g_last_error.c_str(); }
-const char *cr_version(void) { return "libcr 0.1 (sm_100a, fp64, double-double local elimination)"; }
+const char *cr_version(void) { return "libcr 0.2 (sm_100a, fp64, double-double local elimination)"; }
+
+int64_t cr_kernel_launches(void) { return (int64_t)cr::g_launches.load(); }
+
+cr_status cr_pool_reserve(int64_t bytes, cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(bytes >= 0, CR_ERR_INVALID_ARG, "bytes < 0");
+    if (bytes > 0) {
+        void *p = nullptr;
+        CR_CUDA(cudaMallocFromPoolAsync(&p, (size_t)bytes, cr::lib_pool(), (cudaStream_t)s));
+        CR_CUDA(cudaFreeAsync(p, (cudaStream_t)s));
+        CR_CUDA(cudaStreamSynchronize((cudaStream_t)s));
+    }
+    CR_API_END
+}
+
+cr_status cr_pool_trim(int64_t keep_bytes) {
+    CR_API_BEGIN
+    CR_REQUIRE(keep_bytes >= 0, CR_ERR_INVALID_ARG, "keep_bytes < 0");
+    CR_CUDA(cudaMemPoolTrimTo(cr::lib_pool(), (size_t)keep_bytes));
+    CR_API_END
+}
 
 cr_status cr_build_mesh(int32_t dim, int64_t nv, const double *coords_d, int64_t nc, const int32_t *cells_d,
                         cr_stream_t s, cr_mesh *out) {
     CR_API_BEGIN
     CR_REQUIRE(out, CR_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
-    keep_pool();
     cr_mesh_s *m = new cr_mesh_s();
     try {
         cr::build_mesh(m, dim, nv, coords_d, nc, cells_d, (cudaStream_t)s);
@@ -344,6 +388,68 @@ cr_status cr_recover(cr_hybrid h, const double *W_d, double *U_d, double *P_d, d
     CR_API_BEGIN
     CR_REQUIRE(h && W_d && U_d && P_d, CR_ERR_INVALID_ARG, "null argument");
     cr::recover(h, W_d, U_d, P_d, diag_d, (cudaStream_t)s);
+    CR_API_END
+}
+
+cr_status cr_newton_update(int64_t nU, double *U_d, const double *dU_d, int64_t nP, double *P_d, const double *dP_d,
+                           double *norms_h, cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(nU >= 0 && nP >= 0 && U_d && dU_d && norms_h && (!dP_d || P_d), CR_ERR_INVALID_ARG, "bad arguments");
+    cr::newton_update(nU, U_d, dU_d, nP, P_d, dP_d, norms_h, (cudaStream_t)s);
+    CR_API_END
+}
+
+cr_status cr_hybrid_method_host(int32_t dim, int64_t nv, const double *coords_h, int64_t nc, const int32_t *cells_h,
+                                const cr_params *prm, const double *fbar_h, const double *dirichlet_h,
+                                const cr_solver_opts *opts, double *U_h, double *P_h, const int64_t *sizes_h,
+                                cr_mesh_info_t *mesh_info, cr_solve_report *rep, cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(coords_h && cells_h && prm && fbar_h && opts && U_h && P_h && sizes_h, CR_ERR_INVALID_ARG,
+               "null argument");
+    CR_REQUIRE((dim == 2 || dim == 3) && nv > 0 && nc > 0, CR_ERR_INVALID_ARG, "bad mesh sizes");
+    if (rep) std::memset(rep, 0, sizeof(*rep));
+    cudaStream_t st = (cudaStream_t)s;
+    // host -> device (DMA straight from pinned buffers; the driver stages pageable ones)
+    cr::DevBuf<double> coords, fbar, dir;
+    cr::DevBuf<int32_t> cells;
+    coords.alloc((size_t)nv * dim, st);
+    cells.alloc((size_t)nc * (dim + 1), st);
+    fbar.alloc((size_t)nc * dim, st);
+    CR_CUDA(cudaMemcpyAsync(coords.get(), coords_h, (size_t)nv * dim * sizeof(double), cudaMemcpyHostToDevice, st));
+    CR_CUDA(cudaMemcpyAsync(cells.get(), cells_h, (size_t)nc * (dim + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CR_CUDA(cudaMemcpyAsync(fbar.get(), fbar_h, (size_t)nc * dim * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (dirichlet_h) {
+        dir.alloc((size_t)nc * (dim + 1) * dim, st);
+        CR_CUDA(cudaMemcpyAsync(dir.get(), dirichlet_h, (size_t)nc * (dim + 1) * dim * sizeof(double),
+                                cudaMemcpyHostToDevice, st));
+    }
+    std::unique_ptr<cr_mesh_s> m(new cr_mesh_s());
+    cr::build_mesh(m.get(), dim, nv, coords.get(), nc, cells.get(), st);
+    const int64_t nU = (int64_t)dim * m->nf_int;
+    CR_REQUIRE(sizes_h[0] >= nU && sizes_h[1] >= nc, CR_ERR_INVALID_ARG, "U_h / P_h capacity too small");
+    if (mesh_info) {
+        mesh_info->dim = dim;
+        mesh_info->nv = nv;
+        mesh_info->nc = nc;
+        mesh_info->nf = m->nf;
+        mesh_info->nf_int = m->nf_int;
+        mesh_info->n_unknowns = nU;
+    }
+    const cr_data data{fbar.get(), dirichlet_h ? dir.get() : nullptr, nullptr, nullptr};
+    std::unique_ptr<cr_hybrid_s> h(new cr_hybrid_s());
+    cr::hybridise(h.get(), m.get(), *prm, data, nullptr, st);
+    cr::DevBuf<double> W, U, P;
+    W.alloc(nU, st);
+    W.zero(st);
+    U.alloc(nU, st);
+    P.alloc(nc, st);
+    if (opts->method == CR_DC_FGMRES) cr::solve_dc(h.get(), *opts, W.get(), st, rep);
+    else cr::solve(h.get(), *opts, W.get(), st, rep);
+    cr::recover(h.get(), W.get(), U.get(), P.get(), nullptr, st);
+    // device -> host
+    CR_CUDA(cudaMemcpyAsync(U_h, U.get(), nU * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CR_CUDA(cudaMemcpyAsync(P_h, P.get(), nc * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CR_CUDA(cudaStreamSynchronize(st));
     CR_API_END
 }
 

@@ -1174,10 +1174,13 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
         upload(N.lc, lc, s);
         N.bar.alloc(2, s);
         N.bar.zero(s);
-        int occ = 0;
+        int occ = 0, dev = 0, coop = 0;
         CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_nd_solve, 256, 0));
-        CR_REQUIRE(occ >= 1, CR_ERR_INVALID_ARG, "coarse ND solve kernel does not fit on an SM");
-        N.grid = kSMs * std::min(occ, 8);   // more resident warps: the phases are latency-bound
+        CR_CUDA(cudaGetDevice(&dev));
+        CR_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+        // one co-resident wave (more resident warps: the phases are latency-bound); 0 = no
+        // persistent kernel (per-phase launches)
+        N.grid = (coop && occ >= 1) ? num_sms() * std::min(occ, 8) : 0;
     }
     tr.mark("  nd: uploads + work lists");
     // numeric factorisation, deepest level first
@@ -1321,9 +1324,23 @@ static void nd_solve(const CoarseOp &C, const double *c, double *y, double *qout
         S.coff[L] = N.coff[L];
     }
     static const char *ep = std::getenv("CR_ND_PERSIST");
-    const bool persistent = ep ? atoi(ep) != 0 : N.maxdepth > 1;
+    const bool persistent = (ep ? atoi(ep) != 0 : N.maxdepth > 1) && N.grid > 0;
     if (persistent) {
-        k_nd_solve<<<N.grid, 256, 0, s>>>(V, S, c, y, const_cast<unsigned *>(N.bar.get()), C.nE, qout, partials, ticket);
+        // cooperative launch: the runtime guarantees that all N.grid CTAs are co-resident (the
+        // software grid barrier needs it), or fails the launch — then the per-phase launches
+        // below take over.  N.grid = SMs x occupancy of this device (0 when cooperative launches
+        // are unsupported).
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(N.grid);
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CR_CUDA(cudaLaunchKernelEx(&cfg, k_nd_solve, V, S, c, y, const_cast<unsigned *>(N.bar.get()), C.nE, qout,
+                                   partials, ticket));
         CR_CHECK_LAUNCH();
         return;
     }
@@ -1563,7 +1580,7 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
     C.part.alloc(std::max<int64_t>(C.nchunk, 1) * NV, s);
     C.c.alloc(C.nE, s);
     C.y.alloc(C.nE, s);
-    C.gpart.alloc((size_t)kSMs * 32, s);
+    C.gpart.alloc((size_t)num_sms() * 32, s);
     // dense E^{-1} (one bandwidth-bound GEMV per iteration) while it is at most 8000^2 doubles,
     // the ND sparse direct solve beyond (its ~2 log2(H) dependent levels cost latency, its bytes
     // grow only like nE log nE).  CR_COARSE_DENSE=1 / CR_COARSE_ND=1 force one (tests).

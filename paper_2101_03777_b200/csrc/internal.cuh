@@ -30,7 +30,7 @@ void set_last_error(const std::string &m);
         }                                                                                  \
     } while (0)
 
-#define CR_CHECK_LAUNCH() CR_CUDA(cudaGetLastError())
+#define CR_CHECK_LAUNCH() do { ::cr::count_launches(1); CR_CUDA(cudaGetLastError()); } while (0)
 
 #define CR_REQUIRE(cond, code, msg)                     \
     do {                                                \
@@ -47,6 +47,17 @@ struct SyncFreeScope {
     SyncFreeScope() { cudaDeviceSynchronize(); g_sync_free = true; }
     ~SyncFreeScope() { g_sync_free = false; }
 };
+
+// the library's own stream-ordered memory pool on the current device (api.cu): created on first
+// use with a release threshold of UINT64_MAX, so memory freed by one call is re-used by the next
+// without remapping; the device's DEFAULT pool (and the host application's) is never touched.
+cudaMemPool_t lib_pool();
+// SMs of the current device (cached per device): grids are sized from it, never from a constant
+int num_sms();
+// kernels launched by the library on this process (cr_kernel_launches): direct launches are
+// counted in CR_CHECK_LAUNCH, kernels replayed inside the solvers' CUDA graphs by the solver
+void count_launches(int64_t n);
+extern thread_local bool g_capturing;   // inside a solver graph capture: launches not counted
 
 template <class T>
 struct DevBuf {
@@ -67,7 +78,7 @@ struct DevBuf {
         n = count;
         s_ = s;
         if (count == 0) return;
-        CR_CUDA(cudaMallocAsync((void **)&p, count * sizeof(T) + 16, s));
+        CR_CUDA(cudaMallocFromPoolAsync((void **)&p, count * sizeof(T) + 16, lib_pool(), s));
     }
     void zero(cudaStream_t s) { if (n) CR_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
     void fill_bytes(int v, cudaStream_t s) { if (n) CR_CUDA(cudaMemsetAsync(p, v, n * sizeof(T), s)); }
@@ -88,8 +99,8 @@ enum DevErr : int {
     DE_SINGULAR = 5, DE_BZERO = 6
 };
 
-// grid sizing: B200 has 148 SMs; streaming kernels use a fixed grid (deterministic partials)
-constexpr int kSMs = 148;
+// grid sizing: streaming kernels use a fixed grid per device (deterministic partials), a
+// multiple of the device's SM count (148 on B200)
 
 // Grid of exactly one wave of resident blocks (occupancy of `kernel` at `threads` per block) for
 // grid-stride kernels: a second, partial wave would leave SMs idle while it drains.  Cached per
@@ -107,14 +118,14 @@ inline int occ_grid(F kernel, int threads, int64_t work, int reserve = 0) {
         cache.emplace_back(key, nb);
     }
     int64_t b = (work + threads - 1) / threads;
-    const int64_t cap = (int64_t)kSMs * (nb > reserve ? nb - reserve : 1);
+    const int64_t cap = (int64_t)num_sms() * (nb > reserve ? nb - reserve : 1);
     if (b > cap) b = cap;
     if (b < 1) b = 1;
     return (int)b;
 }
 inline int grid_for(int64_t work, int threads, int max_blocks_per_sm = 8) {
     int64_t b = (work + threads - 1) / threads;
-    int64_t cap = (int64_t)kSMs * max_blocks_per_sm;
+    int64_t cap = (int64_t)num_sms() * max_blocks_per_sm;
     if (b > cap) b = cap;
     if (b < 1) b = 1;
     return (int)b;
@@ -257,6 +268,7 @@ struct MfOp {
     cr::DevBuf<uint8_t> sg;
     cr::DevBuf<double> v;
     cr::DevBuf<uint8_t> nb;      // in-warp face partners (mf.cuh)
+    cr::DevBuf<int32_t> slot;    // [nc] slot t of cell K (-1: not stored on this rank)
 };
 
 struct cr_hybrid_s {
@@ -318,8 +330,16 @@ void assemble_coupled(cr_coupled_s *c, const cr_mesh_s *m, const cr_params &prm,
 void spmv(const BlockEll &G, const double *x, double *y, cudaStream_t s);
 // recover.cu
 void recover(const cr_hybrid_s *h, const double *W, double *U, double *P, double *diag, cudaStream_t s);
+void newton_update(int64_t nU, double *U, const double *dU, int64_t nP, double *P, const double *dP, double *norms,
+                   cudaStream_t s);
 // solve.cu
 void solve(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep);
+// one solve of G W = rhs (rhs NULL: S) with the fp64 solvers (solve.cu)
+void solve_rhs(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep,
+               const double *rhs);
+// refine.cu: r = S - G W with G W summed in double-double (the assembled G, or the matrix-free
+// factors when `mf`); returns ||r||_2 and ||S||_2 (host)
+void residual_dd(cr_hybrid_s *h, bool mf, const double *W, double *r, double *rnorm, double *snorm, cudaStream_t s);
 void free_solver_work(SolverWork *w);
 void apply_precond(cr_hybrid_s *h, int method, const double *r, double *z, cudaStream_t s);
 void spmv_part(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s);

@@ -226,7 +226,7 @@ static void build_mf_t(cr_hybrid_s *h, cudaStream_t s) {
                                                                M.sg.get(), M.v.get(), err.get());
     CR_CHECK_LAUNCH();
     // in-warp face partners
-    DevBuf<int32_t> slot;
+    DevBuf<int32_t> &slot = M.slot;   // kept: the dd residual (refine.cu) finds a cell's factors by it
     slot.alloc(nc, s);
     slot.fill_bytes(0xFF, s);
     k_mf_slot<<<grid_for(ncell, T), T, 0, s>>>(list.get(), ncell, slot.get());

@@ -4,6 +4,7 @@
 //   K16b face kernel : U_sigma = copy of face_cells[sigma][0]; max |Uhat_K - Uhat_L|
 //   K16c cell kernel : max_K |sum_{sigma in F_K} a_{K,sigma} . U_sigma| (Dirichlet values on
 //                      boundary faces) — the discrete divergence of the assembled U
+#include <vector>
 #include "local.cuh"
 #include "spmv.cuh"
 
@@ -194,6 +195,55 @@ void recover(const cr_hybrid_s *h, const double *W, double *U, double *P, double
     CR_CUDA(cudaMemcpyAsync(&he, err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     CR_CUDA(cudaStreamSynchronize(s));
     CR_REQUIRE(he == DE_OK, CR_ERR_SINGULAR_LOCAL, "local elimination failed during recovery");
+}
+
+// Newton update: U += dU, P += dP, per-block partials of |dU|^2 and |U + dU|^2
+__global__ void __launch_bounds__(256) k_newton_update(int64_t nU, double *U, const double *dU, int64_t nP, double *P,
+                                                       const double *dP, double *part) {
+    __shared__ double s0[256], s1[256];
+    double a = 0.0, b = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nU; i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = dU[i], u = U[i] + d;
+        U[i] = u;
+        a = fma(d, d, a);
+        b = fma(u, u, b);
+    }
+    if (dP)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nP; i += (int64_t)gridDim.x * blockDim.x)
+            P[i] += dP[i];
+    s0[threadIdx.x] = a;
+    s1[threadIdx.x] = b;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            s0[threadIdx.x] += s0[threadIdx.x + o];
+            s1[threadIdx.x] += s1[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = s0[0];
+        part[2 * blockIdx.x + 1] = s1[0];
+    }
+}
+
+void newton_update(int64_t nU, double *U, const double *dU, int64_t nP, double *P, const double *dP, double *norms,
+                   cudaStream_t s) {
+    const int G = num_sms() * 4;
+    DevBuf<double> part;
+    part.alloc(2 * G, s);
+    k_newton_update<<<G, 256, 0, s>>>(nU, U, dU, nP, P, dP, part.get());
+    CR_CHECK_LAUNCH();
+    std::vector<double> h(2 * G);
+    CR_CUDA(cudaMemcpyAsync(h.data(), part.get(), 2 * G * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CR_CUDA(cudaStreamSynchronize(s));
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < G; ++k) {   // fixed order: deterministic
+        a += h[2 * k];
+        b += h[2 * k + 1];
+    }
+    norms[0] = sqrt(a);
+    norms[1] = sqrt(b);
 }
 
 }  // namespace cr

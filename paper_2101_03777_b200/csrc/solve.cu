@@ -28,6 +28,7 @@ namespace cr {
 
 enum { FLAG_RUN = 0, FLAG_CONV = 1, FLAG_BREAK = 2 };
 constexpr int kMaxRestart = 128;
+constexpr int kLanczos = 1024;   // CG coefficients kept for the kappa estimate (cr_solve_report)
 
 struct KState {
     // ---- header: read back by the host after every graph replay
@@ -49,6 +50,9 @@ struct KState {
     // ---- GMRES arrays (device only)
     double H[(kMaxRestart + 1) * kMaxRestart];
     double cs[kMaxRestart], sn[kMaxRestart], g[kMaxRestart + 1], h[kMaxRestart + 1], y[kMaxRestart];
+    // PCG: (rho_k, p_k^t G p_k) of iteration k < kLanczos -> alpha_k = rho_k / pq_k,
+    // beta_k = rho_{k+1} / rho_k: the Lanczos tridiagonal of the preconditioned G
+    double lz[2 * kLanczos];
 };
 constexpr size_t kStateHeader = offsetof(KState, H);
 
@@ -63,6 +67,7 @@ struct SolverWork {
     KState *hst = nullptr;      // pinned
     cudaGraphExec_t graph = nullptr;
     int graph_key = -1;
+    int64_t graph_kernels = 0;  // kernel nodes of `graph` (launch accounting)
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     cudaStream_t cap = nullptr;   // private capture stream
     cudaStream_t side = nullptr;  // two-level: the coarse path runs here, concurrently with the patches
@@ -131,6 +136,7 @@ __device__ __forceinline__ void apply_fin(KState *st, int kind, const double *t,
             st->flag = (t[1] <= st->tol2) ? FLAG_CONV : FLAG_RUN;
             break;
         case FIN_PQ:         // t = p.q
+            if (st->iters < kLanczos) { st->lz[2 * st->iters] = st->rho; st->lz[2 * st->iters + 1] = t[0]; }
             st->pq = t[0];
             if (!(t[0] > 0.0)) st->flag = FLAG_BREAK;
             else st->alpha = st->rho / t[0];
@@ -178,6 +184,7 @@ __device__ __forceinline__ void apply_fin(KState *st, int kind, const double *t,
         case FIN_AFW2_QF: st->qf = t[0]; break;
         case FIN_PQ2:
             st->rho = st->qf + st->qc;
+            if (st->iters < kLanczos) { st->lz[2 * st->iters] = st->rho; st->lz[2 * st->iters + 1] = t[0]; }
             st->pq = t[0];
             if (!(t[0] > 0.0)) st->flag = FLAG_BREAK;
             else st->alpha = st->rho / t[0];
@@ -1045,7 +1052,7 @@ static void ensure_work(cr_hybrid_s *h, cudaStream_t s) {
         b->alloc(Nalloc, s);
         b->zero(s);
     }
-    w->partials.alloc((size_t)kSMs * 16 * (kMaxRestart + 1), s);
+    w->partials.alloc((size_t)num_sms() * 16 * (kMaxRestart + 1), s);
     w->st.alloc(1, s);
     w->st.zero(s);
     CR_CUDA(cudaMallocHost((void **)&w->hst, sizeof(KState)));
@@ -1194,24 +1201,132 @@ static void graph_loop(Launcher &L, cudaStream_t &ks, int key, int k, Body body,
         ks = w->cap;
         CR_CUDA(cudaStreamBeginCapture(w->cap, cudaStreamCaptureModeThreadLocal));
         int64_t l0 = L.launches, s0 = L.spmvs;
-        for (int i = 0; i < k; ++i) body(i);
+        g_capturing = true;   // captured launches are counted when the graph replays
+        try {
+            for (int i = 0; i < k; ++i) body(i);
+        } catch (...) {
+            g_capturing = false;
+            cudaGraph_t junk;
+            cudaStreamEndCapture(w->cap, &junk);
+            if (junk) cudaGraphDestroy(junk);
+            throw;
+        }
+        g_capturing = false;
         L.launches = l0;
         L.spmvs = s0;
         CR_CUDA(cudaStreamEndCapture(w->cap, &g));
         ks = L.s;
+        size_t nn = 0;
+        CR_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        if (nn) CR_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+        w->graph_kernels = 0;
+        for (auto nd : nodes) {
+            cudaGraphNodeType ty;
+            CR_CUDA(cudaGraphNodeGetType(nd, &ty));
+            if (ty == cudaGraphNodeTypeKernel) ++w->graph_kernels;
+        }
         CR_CUDA(cudaGraphInstantiate(&w->graph, g, 0));
         CR_CUDA(cudaGraphDestroy(g));
         w->graph_key = key;
     }
     while (true) {
         CR_CUDA(cudaGraphLaunch(w->graph, L.s));
+        count_launches(w->graph_kernels);
         read_state(w, L.s);
         if (done()) break;
     }
 }
 
+// extreme eigenvalues of the symmetric tridiagonal T (diag a, off-diagonal b) by bisection on
+// the Sturm count (host; m <= kLanczos)
+static double tri_eig(const std::vector<double> &a, const std::vector<double> &b, int k) {
+    const int m = (int)a.size();
+    double lo = INFINITY, hi = -INFINITY;
+    for (int i = 0; i < m; ++i) {   // Gershgorin bounds
+        const double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i + 1 < m ? fabs(b[i]) : 0.0);
+        lo = fmin(lo, a[i] - r);
+        hi = fmax(hi, a[i] + r);
+    }
+    auto count_below = [&](double x) {   // eigenvalues < x
+        int c = 0;
+        double q = a[0] - x;
+        if (q < 0) ++c;
+        for (int i = 1; i < m; ++i) {
+            const double qq = q != 0.0 ? q : 1e-300;
+            q = a[i] - x - b[i - 1] * b[i - 1] / qq;
+            if (q < 0) ++c;
+        }
+        return c;
+    };
+    for (int it = 0; it < 200; ++it) {   // k-th smallest eigenvalue (0-based)
+        const double mid = 0.5 * (lo + hi);
+        if (count_below(mid) > k) hi = mid;
+        else lo = mid;
+        if (hi - lo <= 1e-14 * fmax(fabs(lo), fabs(hi))) break;
+    }
+    return 0.5 * (lo + hi);
+}
+
+// kappa of the preconditioned G from the CG coefficients: T_kk = 1/alpha_k + beta_{k-1}/alpha_{k-1},
+// T_{k,k+1} = sqrt(beta_k)/alpha_k (the Lanczos matrix CG builds implicitly)
+static void lanczos_kappa(SolverWork *w, cudaStream_t s, int64_t iters, cr_solve_report *rep) {
+    const int m = (int)std::min<int64_t>(iters, kLanczos) - 1;
+    if (m < 2) return;
+    std::vector<double> lz(2 * (m + 1));
+    CR_CUDA(cudaMemcpyAsync(lz.data(), reinterpret_cast<const char *>(w->st.get()) + offsetof(KState, lz),
+                            lz.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CR_CUDA(cudaStreamSynchronize(s));
+    std::vector<double> a(m), b(m > 0 ? m - 1 : 0);
+    double alpha_prev = 0.0, beta_prev = 0.0;
+    for (int k = 0; k < m; ++k) {
+        const double rho = lz[2 * k], pq = lz[2 * k + 1], rho1 = lz[2 * (k + 1)];
+        if (!(rho > 0 && pq > 0 && rho1 > 0)) return;
+        const double alpha = rho / pq, beta = rho1 / rho;
+        a[k] = 1.0 / alpha + (k > 0 ? beta_prev / alpha_prev : 0.0);
+        if (k + 1 < m) b[k] = sqrt(beta) / alpha;
+        alpha_prev = alpha;
+        beta_prev = beta;
+    }
+    const double lmin = tri_eig(a, b, 0), lmax = tri_eig(a, b, m - 1);
+    rep->lambda_min_est = lmin;
+    rep->lambda_max_est = lmax;
+    rep->kappa_lanczos_est = lmin > 0 ? lmax / lmin : 0.0;
+}
+
+// algorithmic HBM bytes of one iteration of `o.method`:
+// G apply (assembled: values + block cols + x + y; matrix-free: cell factors + x + q), the
+// vector updates, and the preconditioner's operator and vectors
+static double iter_bytes(const cr_hybrid_s *h, const cr_solver_opts &o) {
+    const double N8 = 8.0 * (double)h->G.nrows * h->G.d;
+    const int d = h->G.d, slots = d == 2 ? 2 : 3;
+    const double nnz = (double)h->G.nblocks * d * d;
+    const double g_asm = 8.0 * nnz + 4.0 * (double)h->G.nblocks + 2 * N8;
+    const double g_mf = h->mf.built ? (double)(h->mf.v.n * sizeof(double) + h->mf.ids.n * sizeof(int32_t) + h->mf.sg.n +
+                                               h->mf.nb.n) + 2 * N8
+                                    : g_asm;
+    const double g = o.matrix_free ? g_mf : g_asm;
+    const double afw = h->afw.built >= 0 ? (double)(h->afw.vals.n * sizeof(double) + h->afw.ids.n * sizeof(int32_t) +
+                                                    h->afw.kl.n + 2 * h->afw.ioff.n * sizeof(int64_t))
+                                         : 0.0;
+    switch (o.method) {
+        case CR_PCG_JACOBI: return g + 7 * N8;                 // x, r, p, q, dinv read; x, r write (+ p rewrite)
+        case CR_PCG_BLOCKJACOBI: return g + 6 * N8 + N8 * d;   // + inverse diagonal blocks
+        case CR_PCG_AFW: return g + 6 * N8 + (afw + N8 + slots * N8) + (slots * N8 + 2 * N8);
+        case CR_PCG_AFW2: {
+            const double coarse = 2 * N8 + (double)(h->coarse.nd.on ? h->coarse.nd.bytes : 8 * h->coarse.nE * h->coarse.nE);
+            return g + 6 * N8 + (afw + N8 + slots * N8) + coarse + (slots * N8 + 2 * N8 + N8);
+        }
+        case CR_MINRES_ABSJACOBI: return g + 10 * N8;
+        case CR_MINRES_AFW: return g + 10 * N8 + afw + 2 * slots * N8;
+        case CR_BICGSTAB_JACOBI: return 2 * g + 12 * N8;
+        default: return 0.0;
+    }
+}
+
 template <int D>
-static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep) {
+static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep,
+                    const double *rhs) {
     ensure_work(h, s);
     SolverWork *w = h->work;
     Launcher L{h, w, s};
@@ -1238,7 +1353,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     kk = (kk + 1) & ~1;   // even: MINRES buffer rotation has period 2
     double *x = w->x.get();
     CR_CUDA(cudaMemcpyAsync(x, W, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    CR_CUDA(cudaMemcpyAsync(w->b.get(), h->S.get(), N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CR_CUDA(cudaMemcpyAsync(w->b.get(), rhs ? rhs : h->S.get(), N * sizeof(double), cudaMemcpyDeviceToDevice, s));
     CR_CUDA(cudaMemsetAsync(w->st.get(), 0, sizeof(KState), s));
     CR_CUDA(cudaEventRecord(w->e0, s));
     double *part = w->partials.get();
@@ -1663,6 +1778,11 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         rep->seconds = ms * 1e-3;
         rep->spmv_calls = L.spmvs;
         rep->kernel_launches = L.launches;
+        rep->inner_iterations = 0;
+        rep->kappa_lanczos_est = rep->lambda_min_est = rep->lambda_max_est = 0.0;
+        rep->refine_rounds = 0;
+        rep->bytes_moved = iter_bytes(h, o) * (double)w->hst->iters;
+        if (pcg_family && w->hst->iters > 1) lanczos_kappa(w, s, w->hst->iters, rep);
     }
     if (status != CR_OK) throw Error(status, "solver did not converge (see report)");
 }
@@ -1784,9 +1904,10 @@ void apply_precond(cr_hybrid_s *h, int method, const double *r, double *z, cudaS
     else apply_precond_t<3>(h, method, r, z, s);
 }
 
-void solve(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep) {
-    if (h->G.d == 2) solve_t<2>(h, o, W, s, rep);
-    else solve_t<3>(h, o, W, s, rep);
+void solve_rhs(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep,
+               const double *rhs) {
+    if (h->G.d == 2) solve_t<2>(h, o, W, s, rep, rhs);
+    else solve_t<3>(h, o, W, s, rep, rhs);
 }
 
 }  // namespace cr
