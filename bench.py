@@ -2,24 +2,23 @@
 """Benchmark of the hybrid method's hot path on B200 (BASELINE.json metric:
 "hybridised-system PCG time-to-solution; SpMV GB/s as % of B200 HBM peak").
 
-Workload (one "step"): BASELINE.json configs[1] — 2D transient Stokes, unit square,
-1024 x 1024 squares split into 2,097,152 triangles, interior vertices jittered by up to
-0.2h (seed 2), mu = nu = 1, manufactured fp64 force — run through the whole hot path:
-cr_build_mesh -> cr_hybridise -> cr_solve (PCG to a TRUE relative residual of 1e-10, with
-the two-level preconditioner (patch additive Schwarz + a coarse "stress x area vector" space)
-and the matrix-free factored G)
--> cr_recover, inputs resident in HBM.  value = seconds per step (time to solution, lower is better).
-The same step with Jacobi PCG (the north star's baseline solver) is timed once and reported
-under "pcg_jacobi".
+Headline workload (one "step"): BASELINE.json configs[4] — the largest single-GPU config:
+3D transient Stokes, unit cube, 128^3 cubes x 6 Kuhn tetrahedra (12,582,912 cells, 75,202,560
+face unknowns), mu = nu = 1, manufactured fp64 force — through the whole hot path:
+cr_build_mesh -> cr_hybridise -> cr_solve (PCG to a TRUE relative residual of 1e-10 with the
+two-level preconditioner (edge-patch additive Schwarz + coarse "stress x area" space, nested-
+dissection coarse solve) on the matrix-free factored G) -> cr_recover,
+inputs resident in HBM.  value = seconds per step (time to solution, lower is better).
+`--config 1` times configs[1] (2D n = 1024) instead; configs[1..3], time stepping, Newton and
+the Table 4 analogue are reported inside the same line (`other_configs`).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 4|1]
 
 For N > 1 (torchrun, one rank per GPU) the SAME problem is partitioned: each rank owns a slab
 of face rows of G, exchanges SpMV ghosts with its neighbours (NCCL send/recv) and allreduces
-the Krylov dot products (strong scaling); timed on the device, max over
-ranks.
---impl reference times the CPU oracle (oracle/, numpy/scipy + binary128 C) on the host
-cores on a bounded sample of the same workload and extrapolates per unit.
+the Krylov dot products (strong scaling); timed on the device, max over ranks.
+--impl reference times the CPU oracle (oracle/, numpy/scipy + binary128 C) on the host cores on
+a bounded sample of the same workload family and extrapolates per unit.
 """
 from __future__ import annotations
 
@@ -36,14 +35,20 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "hybridised-system PCG time-to-solution; SpMV GB/s as % of B200 HBM peak"
-CONFIG_IDX = 1
-METHOD = "pcg_afw2"  # patch additive Schwarz + coarse "stress x area" correction
-MATRIX_FREE = 1      # G applied from per-cell factors
-COARSE = 64          # coarse grid intervals per direction (flat nested-dissection coarse solve)
-MAX_ITER = 20000     # a cap (the solve takes ~800): a regression fails loudly instead of running on
-# Jacobi-PCG iterations of configs[1] to a true 1e-10 residual, measured on B200 by this
-# bench (used only by --impl reference to extrapolate the oracle's per-iteration time).
-ITERS_CONFIG1_MEASURED = 162221   # Jacobi PCG, configs[1], B200 bench r01 (profiles/r01_bench_*.log)
+HEADLINE = 4         # BASELINE.json configs[4]: the largest config that fits one GPU
+# The solver bench.py times, per config (tests/test_gpu_bench_parity.py runs exactly these):
+# two-level PCG (patch additive Schwarz + coarse "stress x area" space)
+# on the matrix-free factored G (§5.2); coarse = intervals per direction of the coarse grid.
+# rtol: the TRUE relative residual; 2D needs 1e-11 for relL2(P) <= 1e-8 against the coupled
+# solution (2.5e-8 at 1e-10, 3.9e-9 at 1e-11 on n = 256; DESIGN.md §2 reading 13), 3D meets it
+# at the north star's 1e-10.
+SOLVERS = {1: dict(method="pcg_afw2", matrix_free=1, coarse=64, rtol=1e-11),
+           4: dict(method="pcg_afw2", matrix_free=1, coarse=16, rtol=1e-10)}
+MAX_ITER = 20000     # a cap (the solves take ~500): a regression fails loudly instead of running on
+# Jacobi-PCG iterations to a true 1e-10 residual, measured on the B200 (the oracle's own solver;
+# used to extrapolate the CPU oracle's time): configs[1] by the r01 driver run (BENCH_r01.json
+# pcg_jacobi), configs[4] by `python bench.py --jacobi` (profiles/r02_jacobi_configs4.log).
+JACOBI_ITERS = {1: 161758, 4: None}
 
 
 def measured_peaks():
@@ -146,13 +151,18 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle arm
-def oracle_sample(n_sample: int = 256, iters: int = 200):
-    """Time the oracle, as it stands, on a bounded sample of the configs[1] family (same
-    generator, jitter, mu, nu; n = n_sample) and return per-unit costs."""
+# bounded samples of each config family the oracle times (mesh size n_sample, PCG iterations)
+ORACLE_SAMPLE = {1: (256, 200), 4: (12, 200)}
+
+
+def oracle_sample(cfg_idx: int):
+    """Time the oracle, as it stands, on a bounded sample of the configs[cfg_idx] family (same
+    generator, jitter, mu, nu; smaller n) and return per-unit costs."""
     import numpy as np
     import cr_inputs as ci
     import oracle as O
-    cfg = ci.CONFIGS[CONFIG_IDX]
+    n_sample, iters = ORACLE_SAMPLE[cfg_idx]
+    cfg = ci.CONFIGS[cfg_idx]
     inp = ci.make_inputs(cfg, n=n_sample)
     t0 = time.perf_counter()
     m = O.build_mesh(inp["coords"], inp["cells"])
@@ -165,7 +175,7 @@ def oracle_sample(n_sample: int = 256, iters: int = 200):
     O.recover(m, prm, data, h["E"], np.zeros(len(h["S"])))
     t4 = time.perf_counter()
     return dict(nc=m.nc, nnz=h["G"].nnz, mesh_s=t1 - t0, hyb_s=t2 - t1, iter_s=(t3 - t2) / rep["iterations"],
-                rec_s=t4 - t3, iters=rep["iterations"], n=n_sample)
+                rec_s=t4 - t3, iters=rep["iterations"], n=n_sample, dim=m.dim)
 
 
 def oracle_extrapolate(s: dict, nc_full: int, nnz_full: int, iters_full: int) -> float:
@@ -173,47 +183,68 @@ def oracle_extrapolate(s: dict, nc_full: int, nnz_full: int, iters_full: int) ->
     return (s["mesh_s"] + s["hyb_s"] + s["rec_s"]) * f + s["iter_s"] * (nnz_full / s["nnz"]) * iters_full
 
 
-def workload_config(n, world):
-    """The `config` object of both arms (identical by construction; closed-form sizes of the
-    structured n x n triangulation)."""
-    nc, nnz, nb, N = full_sizes(n)
-    return {"workload": "configs[1] 2D transient Stokes n=%d jittered 0.2h, two-level-preconditioned PCG to "
-                        "true 1e-10" % n,
+def full_sizes(cfg_idx):
+    """Closed-form sizes of the structured meshes: cells, nnz(G), blocks, unknowns."""
+    import cr_inputs as ci
+    n = ci.CONFIGS[cfg_idx].n
+    if ci.CONFIGS[cfg_idx].dim == 2:
+        nc, nf_int = 2 * n * n, 3 * n * n - 2 * n
+        nb = nf_int + 12 * (n - 1) ** 2 + 8 * (n - 1)
+        return nc, 4 * nb, nb, 2 * nf_int
+    nc, nf_int = 6 * n ** 3, 12 * n ** 3 - 6 * n * n
+    nb = nf_int + 72 * n * (n - 1) ** 2 + 72 * n * (n - 1) + 12 * n
+    return nc, 9 * nb, nb, 3 * nf_int
+
+
+def jacobi_iters(cfg_idx):
+    """Jacobi-PCG iteration count of the config (measured on the B200; see JACOBI_ITERS).  For
+    configs[4] without a measurement: the SURVEY A.5 fit (n^1.35 from n <= 32), labelled."""
+    it = JACOBI_ITERS.get(cfg_idx)
+    if it:
+        return it, "measured on the B200"
+    return 70000, "SURVEY A.5 fit (not measured)"
+
+
+def workload_config(cfg_idx, world):
+    """The `config` object of both arms (identical by construction)."""
+    import cr_inputs as ci
+    cfg = ci.CONFIGS[cfg_idx]
+    nc, nnz, nb, N = full_sizes(cfg_idx)
+    sol = SOLVERS[cfg_idx]
+    if cfg.dim == 2:
+        what = f"configs[1] 2D transient Stokes n={cfg.n} jittered 0.2h (triangles)"
+    else:
+        what = f"configs[4] 3D transient Stokes n={cfg.n} Kuhn cubes (6 tetrahedra each)"
+    return {"workload": what + f", two-level-preconditioned PCG on the matrix-free G to true {sol['rtol']:g}",
             "cells": nc, "unknowns": N, "nnz_G": nnz, "blocks_G": nb,
             "parallelism": (f"face rows partitioned over {world} GPUs (NCCL halo send/recv + allreduce)"
                             if world > 1 else "1 GPU"),
-            "l2": "working set > L2 (G = %.2f GB per SpMV) and a 256 MB L2 flush before each step" % (8 * nnz / 1e9)}
-
-
-def full_sizes(n=1024):
-    nc = 2 * n * n
-    nf_int = 3 * n * n - 2 * n
-    nb = nf_int + 12 * (n - 1) ** 2 + 8 * (n - 1)
-    return nc, 4 * nb, nb, 2 * nf_int
+            "l2": "working set > L2 (G = %.2f GB assembled; per-iteration streams > 1 GB) and a 256 MB L2 flush "
+                  "before each step" % (8 * nnz / 1e9)}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    nc, nnz, nb, N = full_sizes()
-    iters_full = ITERS_CONFIG1_MEASURED or 170000
-    vals = []
-    samples = []
+    cfg_idx = args.config
+    nc, nnz, nb, N = full_sizes(cfg_idx)
+    iters_full, src = jacobi_iters(cfg_idx)
+    vals, samples = [], []
     for i in range(args.warmup + args.steps):
-        s = oracle_sample()
+        s = oracle_sample(cfg_idx)
         if i >= args.warmup:
             vals.append(oracle_extrapolate(s, nc, nnz, iters_full))
             samples.append(s)
     v = statistics.mean(vals)
     s = samples[-1]
-    sample_desc = (f"oracle on configs[1]-family mesh n={s['n']} ({s['nc']} cells): mesh+hybridise+recover "
-                   f"timed in full, PCG timed over {s['iters']} iterations; extrapolated per cell and per "
-                   f"nnz x {iters_full} iterations (B200-measured count) to n=1024")
+    sample_desc = (f"oracle on the configs[{cfg_idx}] family at n={s['n']} ({s['nc']} cells): mesh+hybridise+recover "
+                   f"timed in full, Jacobi PCG (the oracle's solver) timed over {s['iters']} iterations; extrapolated "
+                   f"per cell and per nnz x {iters_full} iterations ({src}) to the full workload")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(1024, args.gpus),
+            "config": workload_config(cfg_idx, args.gpus),
             "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "oracle", "sample": sample_desc},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -221,10 +252,9 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
-# solver per config
+# solvers of the configs without a transient hybrid system
 OTHER_SOLVERS = {2: dict(method="dc", coarse=64, mu_inner=1.0),
-                 3: dict(method="dc", coarse=64, mu_inner=0.5, inner_rtol=1e-7),
-                 4: dict(method="pcg_afw2", matrix_free=1, coarse=16)}
+                 3: dict(method="dc", coarse=64, mu_inner=0.5, inner_rtol=1e-7)}
 
 
 def _ev(torch, stream):
@@ -233,9 +263,18 @@ def _ev(torch, stream):
     return e
 
 
-def stage_times(P, cfg, coords, cells, fbar, stream):
-    """One configs[1] step with CUDA events between the four C-ABI calls."""
+def _solver(cfg_idx):
+    sol = dict(SOLVERS[cfg_idx])
+    rtol = sol.pop("rtol")
+    return sol, rtol
+
+
+def stage_times(P, cfg_idx, coords, cells, fbar, stream):
+    """One step with CUDA events between the four C-ABI calls."""
     import torch
+    import cr_inputs as ci
+    cfg = ci.CONFIGS[cfg_idx]
+    sol, rtol = _solver(cfg_idx)
     torch.cuda.synchronize()
     e = [_ev(torch, stream)]
     mesh = P.cr_build_mesh(coords, cells)
@@ -243,8 +282,7 @@ def stage_times(P, cfg, coords, cells, fbar, stream):
     hyb = P.cr_hybridise(mesh, P.Problem(mu=cfg.mu, nu=cfg.nu, fbar=fbar))
     e.append(_ev(torch, stream))
     W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=coords.device)
-    rep = P.cr_solve(hyb, W, METHOD, rtol=cfg.rtol, check_every=64, matrix_free=MATRIX_FREE, coarse=COARSE,
-                     max_iter=MAX_ITER)
+    rep = P.cr_solve(hyb, W, rtol=rtol, check_every=64, max_iter=MAX_ITER, **sol)
     e.append(_ev(torch, stream))
     P.cr_recover(hyb, W)
     e.append(_ev(torch, stream))
@@ -259,10 +297,11 @@ def time_stepping(P, cfg, coords, cells, fbar, stream, nsteps=5):
     """configs[1] as nsteps backward-Euler steps (mu = 1/dt) with G and its preconditioners built
     once: per-step iterations (warm start) and solve times."""
     import torch
+    sol, rtol = _solver(1)
     torch.cuda.synchronize()
     a = _ev(torch, stream)
-    out = P.time_march(coords, cells, P.Problem(mu=cfg.mu, nu=cfg.nu, fbar=fbar), nsteps, method=METHOD,
-                       rtol=cfg.rtol, matrix_free=MATRIX_FREE, coarse=COARSE, check_every=64, max_iter=MAX_ITER)
+    out = P.time_march(coords, cells, P.Problem(mu=cfg.mu, nu=cfg.nu, fbar=fbar), nsteps, rtol=rtol, check_every=64,
+                       max_iter=MAX_ITER, **sol)
     b = _ev(torch, stream)
     torch.cuda.synchronize()
     reps = out["reports"]
@@ -339,16 +378,19 @@ def other_config(P, ci, idx, dev, stream):
         kw.update(physics=P.CR_NS_NEWTON_STEP, u_iter=tg(inp["u_iter"]))
     prob = P.Problem(mu=cfg.mu, nu=cfg.nu, fbar=tg(inp["fbar"]), **kw)
     coords, cells = tg(inp["coords"]), tg(inp["cells"])
-    sol = OTHER_SOLVERS[idx]
+    if idx in SOLVERS:
+        sol, rtol = _solver(idx)
+    else:
+        sol, rtol = OTHER_SOLVERS[idx], cfg.rtol
     torch.cuda.synchronize()
     a = _ev(torch, stream)
-    out = P.hybrid_method(coords, cells, prob, rtol=cfg.rtol, check_every=64, **sol)
+    out = P.hybrid_method(coords, cells, prob, rtol=rtol, check_every=64, **sol)
     b = _ev(torch, stream)
     torch.cuda.synchronize()
     rep = out["report"]
     kind = {"stokes": "transient Stokes" if cfg.mu > 0 else "steady Stokes", "ns_step": "Navier-Stokes Newton step"}
     r = {"workload": f"configs[{idx}] {cfg.dim}D {kind[cfg.physics]} n={cfg.n} (nu={cfg.nu})", "solver": sol,
-         "time_to_solution_s": a.elapsed_time(b) * 1e-3, "solve_s": rep["seconds"],
+         "rtol": rtol, "time_to_solution_s": a.elapsed_time(b) * 1e-3, "solve_s": rep["seconds"],
          "iterations": rep["iterations"], "rel_res_true": rep["rel_res_true"],
          "unknowns": out["hybrid"].n_rows, "cells": out["mesh"].nc}
     if sol["method"] == "dc":
@@ -357,13 +399,78 @@ def other_config(P, ci, idx, dev, stream):
     return r
 
 
+def kernel_rooflines(P, torch, hyb, mesh, rep, stream, dev, peak, peak_src, cfg_idx):
+    """Per-kernel algorithmic GB/s of the iteration's kernels, each re-launched standalone on the
+    bench's stream and timed with CUDA events (the in-solve launches replay inside CUDA graphs).
+    The dominant kernel is the one with the largest share of the iteration (every kernel below
+    launches once per iteration, so share = its time / the sum)."""
+    N, nnz, nb = hyb.n_rows, hyb.nnz, hyb.nblocks
+    N8 = 8 * N
+    pinfo, minfo, cinfo = hyb.precond_info(), hyb.mf_info(), hyb.coarse_info()
+    slots = 2 if mesh.dim == 2 else 3
+
+    def time_launch(fn, nrep=20):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(nrep):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / nrep * 1e-3
+
+    x = torch.randn(N, dtype=torch.float64, device=dev)
+    y = torch.empty_like(x)
+    mf_s = time_launch(lambda: hyb.spmv_mf(x, y))
+    mf_bytes = minfo["bytes"] + N8 + N8                   # per-cell factors + x once + q once
+    prec_s = time_launch(lambda: hyb.apply_precond("pcg_afw", x, y))
+    # patch operator + r read + slot contributions written, then read back and z written
+    prec_bytes = pinfo["bytes"] + N8 + slots * N8 + slots * N8 + N8
+    prec2_s = time_launch(lambda: hyb.apply_precond(SOLVERS[cfg_idx]["method"], x, y))
+    coarse_bytes = N8 + 8 * N + cinfo["solve_bytes"] + 8 * N   # r, (x, a) fp32, E^-1 or ND fronts, (x, a) again
+    prec2_bytes = prec_bytes + coarse_bytes
+    spmv_s = time_launch(lambda: hyb.spmv(x, y))
+    spmv_bytes = 8 * nnz + 4 * nb + N8 + N8               # SURVEY §8(d): values + block cols + x once + y
+
+    def traffic(tag):
+        f = os.path.join(ROOT, "profiles", f"r02_dram_bytes_{tag}.json")
+        try:
+            return json.load(open(f)).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+
+    def roof(kernel, bytes_, sec, tr=None):
+        return {"kernel": kernel, "bound": "hbm", "achieved": bytes_ / sec / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": bytes_ / sec / 1e9 / peak, "traffic": tr, "peak_source": peak_src,
+                "algorithmic_bytes": bytes_, "launch_s": sec}
+
+    tag = f"c{cfg_idx}"
+    kernels = {
+        "mf": roof("k_mf_spmv (matrix-free factored G x, per-cell factors: the in-solve G apply)", mf_bytes, mf_s,
+                   traffic(tag + "_mf")),
+        "precond": roof("k_afw_apply + k_afw_zsum (patch additive Schwarz z = M^-1 r)", prec_bytes, prec_s,
+                        traffic(tag + "_afw")),
+        "precond_two_level": roof("coarse restrict + gather + E^-1 (nested dissection) + patch apply + combine "
+                                  "(z = M2^-1 r)", prec2_bytes, prec2_s),
+        "spmv_assembled": roof("k_spmv (assembled sliced block-ELL G x; not used by the bench's solve)", spmv_bytes,
+                               spmv_s, traffic(tag + "_spmv")),
+    }
+    it_s = (rep["seconds"] - rep["setup_seconds"]) / max(rep["iterations"], 1)
+    shares = {"mf": mf_s / it_s, "precond_two_level": prec2_s / it_s}
+    dominant = "precond" if prec_s >= mf_s else "mf"
+    return kernels, dominant, shares
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=HEADLINE, choices=sorted(SOLVERS))
     ap.add_argument("--n", type=int, default=None, help="override mesh size (debug only; not a bench value)")
+    ap.add_argument("--jacobi", action="store_true", help="also solve the headline config with Jacobi PCG (minutes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true")
@@ -396,7 +503,9 @@ def main():
         if world > 1:
             dist.barrier()
 
-    cfg = ci.CONFIGS[CONFIG_IDX]
+    cfg_idx = args.config
+    cfg = ci.CONFIGS[cfg_idx]
+    sol, rtol = _solver(cfg_idx)
     inp = ci.make_inputs(cfg, n=args.n)
     coords_h = torch.from_numpy(inp["coords"]).pin_memory()
     cells_h = torch.from_numpy(inp["cells"]).pin_memory()
@@ -410,8 +519,7 @@ def main():
         mesh = P.cr_build_mesh(coords, cells)
         hyb = P.cr_hybridise(mesh, prob, comm=comm)
         W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=dev)
-        rep = P.cr_solve(hyb, W, METHOD, rtol=cfg.rtol, check_every=64, matrix_free=MATRIX_FREE, coarse=COARSE,
-                         max_iter=MAX_ITER)
+        rep = P.cr_solve(hyb, W, rtol=rtol, check_every=64, max_iter=MAX_ITER, **sol)
         U, Pp, diag = P.cr_recover(hyb, W)
         return mesh, hyb, rep, U, Pp, diag
 
@@ -423,6 +531,7 @@ def main():
     reps = []
     barrier()
     torch.cuda.synchronize()
+    l0 = P.kernel_launches()
     with ClockSampler(local_rank) as clk:
         for k in range(args.steps):
             flush.zero_()
@@ -433,6 +542,7 @@ def main():
             out = new   # the previous step's handles are released after its end event
             del new
         torch.cuda.synchronize()
+    launches = P.kernel_launches() - l0
     barrier()
     ms = [a.elapsed_time(b) for a, b in evs]
     ms_per_step = sum(ms) / len(ms)
@@ -441,95 +551,48 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item())
     mesh, hyb, rep = out[0], out[1], reps[-1]
-    N, nnz, nb = hyb.n_rows, hyb.nnz, hyb.nblocks
+    nnz, nb, nrows = hyb.nnz, hyb.nblocks, hyb.n_rows
 
-    # ---- per-kernel rooflines: each kernel of the PCG step re-launched standalone on the same
-    # stream and timed with CUDA events (the in-solve launches live inside a CUDA graph)
     peak, peak_src = measured_peaks()
-    N8 = 8 * N
-    pinfo = hyb.precond_info()
-    slots = 2 if mesh.dim == 2 else 3
+    kernels, dominant, shares = kernel_rooflines(P, torch, hyb, mesh, rep, stream, dev, peak, peak_src, cfg_idx)
+    cinfo, pinfo, minfo = hyb.coarse_info(), hyb.precond_info(), hyb.mf_info()
+    iter_s = rep["seconds"] - rep["setup_seconds"]
+    iter_gbs = rep["bytes_moved"] / iter_s / 1e9 if iter_s > 0 else None
 
-    def time_launch(fn, nrep=50):
-        for _ in range(5):
-            fn()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(nrep):
-            fn()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / nrep * 1e-3
+    # the north star's baseline solver (Jacobi PCG) on the same G: to solution with --jacobi, else
+    # a sample of 2,000 iterations for its time per iteration
+    jac = None
+    if world == 1:
+        Wj = torch.zeros(nrows, dtype=torch.float64, device=dev)
+        if args.jacobi:
+            rj = P.cr_solve(hyb, Wj, "pcg", rtol=rtol, check_every=256, raise_on_fail=False)
+            jac = {"iterations": rj["iterations"], "rel_res_true": rj["rel_res_true"], "solve_s": rj["seconds"],
+                   "converged": bool(rj["converged"]), "kappa_lanczos_est": rj["kappa_lanczos_est"]}
+        else:
+            rj = P.cr_solve(hyb, Wj, "pcg", rtol=rtol, check_every=256, max_iter=2000, raise_on_fail=False)
+            jac = {"sampled_iterations": rj["iterations"], "ms_per_iter": rj["seconds"] / max(rj["iterations"], 1) * 1e3,
+                   "iter_gbs": rj["bytes_moved"] / (rj["seconds"] - rj["setup_seconds"]) / 1e9 if rj["seconds"] > 0 else None,
+                   "kappa_lanczos_est_partial": rj["kappa_lanczos_est"],
+                   "iterations_to_1e-10": jacobi_iters(cfg_idx)[0], "iterations_source": jacobi_iters(cfg_idx)[1]}
+        del Wj
 
-    x = torch.randn(N, dtype=torch.float64, device=dev)
-    y = torch.empty_like(x)
-    spmv_s = time_launch(lambda: hyb.spmv(x, y))
-    spmv_bytes = 8 * nnz + 4 * nb + N8 + N8          # values + block cols + x once + y
-    mf_s = time_launch(lambda: hyb.spmv_mf(x, y))
-    minfo = hyb.mf_info()
-    mf_bytes = minfo["bytes"] + N8 + N8              # per-cell factors + x once + q once
-    prec_s = time_launch(lambda: hyb.apply_precond("pcg_afw", x, y))
-    prec2_s = time_launch(lambda: hyb.apply_precond(METHOD, x, y))
-    # patch operator + r read + slot contributions written, then read back and z written
-    prec_bytes = pinfo["bytes"] + N8 + slots * N8 + slots * N8 + N8
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "spmv_dram_bytes.json")
-    if os.path.exists(tfile):
-        try:
-            traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    # PCG-two-level iteration: G apply + update (x,p,r,q read; x,r write) + patch apply + coarse
-    # (restriction reads r and the fp32 row basis, E^-1 once) + p update (+ basis again)
-    g_bytes = mf_bytes if MATRIX_FREE else spmv_bytes
-    cinfo = hyb.coarse_info()
-    coarse_bytes = N8 + 8 * N + cinfo["solve_bytes"] + 8 * N   # r, (x, a) fp32, E^-1 or ND fronts, (x, a) again
-    iter_bytes = g_bytes + 6 * N8 + (pinfo["bytes"] + N8 + slots * N8) + coarse_bytes + (slots * N8 + 2 * N8)
-    iter_gbs = iter_bytes * rep["iterations"] / rep["seconds"] / 1e9 if rep["seconds"] > 0 else None
-
-    def roof(kernel, bytes_, sec, traffic_=None):
-        return {"kernel": kernel, "bound": "hbm", "achieved": bytes_ / sec / 1e9, "peak": peak, "unit": "GB/s",
-                "frac": bytes_ / sec / 1e9 / peak, "traffic": traffic_, "peak_source": peak_src,
-                "algorithmic_bytes": bytes_, "launch_s": sec}
-
-    prec_traffic = None   # ncu --set full DRAM bytes of k_afw_apply (the zsum's slot read-back is not in it)
-    afile = os.path.join(ROOT, "profiles", "afw_dram_bytes.json")
-    if os.path.exists(afile) and mesh.dim == 2:
-        try:
-            prec_traffic = json.load(open(afile)).get("dram_bytes_per_launch")
-        except Exception:
-            prec_traffic = None
-    prec2_bytes = prec_bytes + coarse_bytes
-    kernels = {
-        "mf": roof("k_mf_spmv (matrix-free factored G x, per-cell factors, the in-solve G apply)", mf_bytes, mf_s),
-        "precond": roof("k_afw_apply + k_afw_zsum (patch additive Schwarz z = M^-1 r)", prec_bytes, prec_s, prec_traffic),
-        "precond_two_level": roof("coarse restrict + gather + E^-1 solve (nested dissection) + patch apply + combine (z = M2^-1 r)",
-                                  prec2_bytes, prec2_s),
-        "spmv": roof("k_spmv (assembled sliced block-ELL G x, same row code as the assembled PCG SpMV)",
-                     spmv_bytes, spmv_s, traffic),
-    }
-    dominant = "mf" if mf_s >= prec_s else "precond"
-
-    # ---- one-level patch PCG (assembled G), and the north star's baseline solver (Jacobi PCG)
-    Wa = torch.zeros(N, dtype=torch.float64, device=dev)
-    repa = P.cr_solve(hyb, Wa, "pcg_afw", rtol=cfg.rtol, check_every=64, matrix_free=0)
-    Wj = torch.zeros(N, dtype=torch.float64, device=dev)
-    repj = P.cr_solve(hyb, Wj, "pcg", rtol=cfg.rtol, check_every=64)
-
-    # ---- e2e through the public API from HOST buffers (pinned host -> device -> host)
-    # (the handles of the timed steps are released first, as a caller's next solve would)
+    # ---- e2e through the C ABI from HOST buffers (cr_hybrid_method_host: pinned host -> device,
+    # the whole method, device -> host of U and P), caller-owned pinned result buffers
     nc_full, ndim = mesh.nc, mesh.dim
-    del out, hyb, mesh, Wa, Wj, x, y
+    nf_int = mesh.nf_int
+    del out, hyb, mesh
     e2e = None
-    if not args.no_e2e:
-        def e2e_step():
-            return P.hybrid_method_host(coords_h, cells_h, fbar_h, cfg.mu, cfg.nu, METHOD, cfg.rtol, comm=comm,
-                                        matrix_free=MATRIX_FREE, coarse=COARSE)
+    if not args.no_e2e and world == 1:
+        Uh = torch.empty(nf_int * ndim, dtype=torch.float64, pin_memory=True)
+        Ph = torch.empty(nc_full, dtype=torch.float64, pin_memory=True)
 
-        o2 = e2e_step()   # warm-up
-        del o2
+        def e2e_step():
+            return P.hybrid_method_host(coords_h, cells_h, fbar_h, cfg.mu, cfg.nu, rtol=rtol, out=(Uh, Ph),
+                                        stream=stream, max_iter=MAX_ITER, **sol)
+
+        e2e_step()   # warm-up
         e2e_ms = []
-        for _ in range(args.steps):   # K steps, each with its own host -> device -> host copies
+        for _ in range(min(args.steps, 5)):   # each with its own host -> device -> host copies
             torch.cuda.synchronize()
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -538,65 +601,63 @@ def main():
             b.record(stream)
             torch.cuda.synchronize()
             e2e_ms.append(a.elapsed_time(b))
-            o2 = res   # the previous step's handles are released outside the timed region
-            del res
-        e2e_s = sum(e2e_ms) / len(e2e_ms) * 1e-3
-        t2 = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
         h2d = coords_h.numel() * 8 + cells_h.numel() * 4 + fbar_h.numel() * 8
-        d2h = o2["U_host"].numel() * 8 + o2["P_host"].numel() * 8
-        e2e = {"value": float(t2.item()), "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+        d2h = res["U_host"].numel() * 8 + res["P_host"].numel() * 8
+        e2e = {"value": sum(e2e_ms) / len(e2e_ms) * 1e-3, "unit": "s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": len(e2e_ms), "api": "cr_hybrid_method_host (C ABI)"}
 
-    # ---- stage times of one configs[1] step (assembly cells/s) and time-to-solution of the
-    # other configs (one run each, not part of the timed step; single GPU only)
+    # ---- stage times of one step and time-to-solution of the other configs (single GPU only)
     stages, others, tstep, newton, table4 = None, None, None, None, None
     if world == 1 and not args.no_other_configs:
-        stages = stage_times(P, cfg, coords, cells, fbar, stream)
-        tstep = time_stepping(P, cfg, coords, cells, fbar, stream)
-        newton = newton_cavity(P, ci, dev, stream)
-        table4 = direct_table4(P, ci, dev, stream)
+        stages = stage_times(P, cfg_idx, coords, cells, fbar, stream)
+        del coords, cells, fbar
+        torch.cuda.empty_cache()
         others = {}
-        for idx in (2, 3, 4):
+        for idx in (1, 2, 3, 4):
+            if idx == cfg_idx:
+                continue
             others[f"configs[{idx}]"] = other_config(P, ci, idx, dev, stream)
             torch.cuda.empty_cache()
+        c1 = ci.CONFIGS[1]
+        i1 = ci.make_inputs(c1)
+        tg = lambda a: torch.from_numpy(a).to(dev)
+        tstep = time_stepping(P, c1, tg(i1["coords"]), tg(i1["cells"]), tg(i1["fbar"]), stream)
+        newton = newton_cavity(P, ci, dev, stream)
+        table4 = direct_table4(P, ci, dev, stream)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        s = oracle_sample()
-        v = oracle_extrapolate(s, nc_full, nnz, repj["iterations"])
+        s = oracle_sample(cfg_idx)
+        it_full, src = jacobi_iters(cfg_idx)
+        v = oracle_extrapolate(s, nc_full, nnz, it_full)
         cpu = {"value": v, "unit": "s", "cores": 1, "kind": "oracle",
-               "sample": (f"oracle on configs[1]-family mesh n={s['n']} ({s['nc']} cells): mesh+hybridise+recover "
-                          f"timed in full ({s['mesh_s'] + s['hyb_s'] + s['rec_s']:.1f} s), PCG over {s['iters']} "
-                          f"iterations ({s['iter_s'] * 1e3:.2f} ms/it); extrapolated per cell and per nnz x "
-                          f"{repj['iterations']} Jacobi-PCG iterations (the oracle's solver, count measured on the B200 in this run) to the full workload")}
+               "sample": (f"oracle on the configs[{cfg_idx}] family at n={s['n']} ({s['nc']} cells): mesh+hybridise+"
+                          f"recover timed in full ({s['mesh_s'] + s['hyb_s'] + s['rec_s']:.1f} s), Jacobi PCG (the "
+                          f"oracle's solver) over {s['iters']} iterations ({s['iter_s'] * 1e3:.2f} ms/it); "
+                          f"extrapolated per cell and per nnz x {it_full} Jacobi-PCG iterations ({src}) to the "
+                          f"full workload")}
 
-    launches = rep["kernel_launches"] + 25     # mesh (sort/scan/geometry ~15), hybridise 1, recover 3, copies
-    launches += 12   # patch build (pairs, sort, scans, setup)
-    launches += (5 ** ndim) * ndim ** 2 * 8 + 200   # coarse E assembly (colour passes) + ND factorisation
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "ms_steps_rank0": ms, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args.n or cfg.n, world),
-            "pcg": {"method": METHOD, "matrix_free": MATRIX_FREE, "coarse_intervals": COARSE, "coarse": cinfo,
-                    "iterations": rep["iterations"],
-                    "rel_res_true": rep["rel_res_true"], "solve_s": rep["seconds"],
-                    "ms_per_iter": rep["seconds"] / max(rep["iterations"], 1) * 1e3,
-                    "iter_gbs": iter_gbs, "iter_bytes": iter_bytes, "precond": pinfo, "mf": minfo},
-            "pcg_patch_assembled_G": {"iterations": repa["iterations"], "rel_res_true": repa["rel_res_true"],
-                                "solve_s": repa["seconds"],
-                                "ms_per_iter": repa["seconds"] / max(repa["iterations"], 1) * 1e3},
-            "pcg_jacobi": {"iterations": repj["iterations"], "rel_res_true": repj["rel_res_true"],
-                           "solve_s": repj["seconds"],
-                           "ms_per_iter": repj["seconds"] / max(repj["iterations"], 1) * 1e3},
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "ms_steps_rank0": ms, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(cfg_idx, world),
+            "pcg": {**sol, "rtol": rtol, "coarse": cinfo, "precond": pinfo, "mf": minfo,
+                    "iterations": rep["iterations"], "rel_res_true": rep["rel_res_true"], "solve_s": rep["seconds"],
+                    "setup_s": rep["setup_seconds"], "ms_per_iter": iter_s / max(rep["iterations"], 1) * 1e3,
+                    "iter_gbs": iter_gbs, "bytes_moved": rep["bytes_moved"],
+                    "kappa_lanczos_est": rep["kappa_lanczos_est"], "kernel_shares_of_iteration": shares},
+            "pcg_jacobi": jac,
             "roofline": kernels[dominant],
             "roofline_kernels": kernels,
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
+            "gpu_launches_per_step": launches / args.steps,
+            "gpu_launches_note": "libcr kernels launched in the timed region (cr_kernel_launches: direct launches + "
+                                 "kernel nodes of every replayed solver graph; CUB / cuBLAS / cuSOLVER excluded)",
             "e2e": e2e,
-            "stages_configs1": stages,
+            "stages": stages,
             "other_configs": others,
             "time_stepping_configs1": tstep,
             "newton_cavity": newton,

@@ -241,6 +241,9 @@ typedef struct {
                                   the method's kernels x iterations)               */
     int32_t refine_rounds;     /* refine_dd: refinement rounds run                               */
     int32_t reserved;
+    double setup_seconds;      /* part of `seconds` spent building the preconditioner (patch blocks,
+                                  coarse space E = Z^t G Z and its factorisation) before the first
+                                  iteration; seconds - setup_seconds = the iterations             */
 } cr_solve_report;
 cr_status cr_solve(cr_hybrid h, const cr_solver_opts *opts, double *W_d, cr_stream_t s,
                    cr_solve_report *rep);

@@ -77,7 +77,7 @@ class SolveReport(ctypes.Structure):
                 ("kernel_launches", ctypes.c_int64), ("inner_iterations", ctypes.c_int64),
                 ("kappa_lanczos_est", ctypes.c_double), ("lambda_min_est", ctypes.c_double),
                 ("lambda_max_est", ctypes.c_double), ("bytes_moved", ctypes.c_double),
-                ("refine_rounds", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("refine_rounds", ctypes.c_int32), ("reserved", ctypes.c_int32), ("setup_seconds", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

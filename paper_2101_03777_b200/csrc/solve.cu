@@ -68,7 +68,7 @@ struct SolverWork {
     cudaGraphExec_t graph = nullptr;
     int graph_key = -1;
     int64_t graph_kernels = 0;  // kernel nodes of `graph` (launch accounting)
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr, es = nullptr;   // solve start / end, preconditioner setup done
     cudaStream_t cap = nullptr;   // private capture stream
     cudaStream_t side = nullptr;  // two-level: the coarse path runs here, concurrently with the patches
     cudaEvent_t fork = nullptr, join = nullptr;
@@ -81,6 +81,7 @@ struct SolverWork {
         if (hst) cudaFreeHost(hst);
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
+        if (es) cudaEventDestroy(es);
     }
 };
 
@@ -1058,6 +1059,7 @@ static void ensure_work(cr_hybrid_s *h, cudaStream_t s) {
     CR_CUDA(cudaMallocHost((void **)&w->hst, sizeof(KState)));
     CR_CUDA(cudaEventCreate(&w->e0));
     CR_CUDA(cudaEventCreate(&w->e1));
+    CR_CUDA(cudaEventCreate(&w->es));
     CR_CUDA(cudaStreamCreateWithFlags(&w->cap, cudaStreamNonBlocking));
     CR_CUDA(cudaStreamCreateWithFlags(&w->side, cudaStreamNonBlocking));
     CR_CUDA(cudaEventCreateWithFlags(&w->fork, cudaEventDisableTiming));
@@ -1356,6 +1358,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     CR_CUDA(cudaMemcpyAsync(w->b.get(), rhs ? rhs : h->S.get(), N * sizeof(double), cudaMemcpyDeviceToDevice, s));
     CR_CUDA(cudaMemsetAsync(w->st.get(), 0, sizeof(KState), s));
     CR_CUDA(cudaEventRecord(w->e0, s));
+    CR_CUDA(cudaEventRecord(w->es, s));   // re-recorded once a preconditioner / coarse space is built
     double *part = w->partials.get();
     KState *st = w->st.get();
     k_norm2<<<L.grid_vec, kT, 0, s>>>(w->b.get(), N, st, part, L.dist);
@@ -1423,6 +1426,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     } else if (method == CR_PCG_AFW) {
         constexpr int SLOTS = D == 2 ? 2 : 3;
         build_afw(h, AFW_SPD, s);
+        CR_CUDA(cudaEventRecord(w->es, s));
         if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
         double *zs = w->zs.get();
         auto init = [&]() {
@@ -1471,6 +1475,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     } else if (method == CR_PCG_AFW2) {
         constexpr int SLOTS = D == 2 ? 2 : 3;
         build_afw(h, AFW_SPD, s);
+        CR_CUDA(cudaEventRecord(w->es, s));
         trc.mark("patch preconditioner");
         const int H = o.coarse > 0 ? o.coarse : (D == 2 ? 64 : 16);
         // E = Z^t G Z needs G applied to colour sums of coarse columns; with the matrix-free G only
@@ -1513,6 +1518,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
             }
         }, s);
         trc.mark("coarse space (E, E^-1)");
+        CR_CUDA(cudaEventRecord(w->es, s));
         if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
         double *zs = w->zs.get();
         const CoarseView CV = h->coarse.view();
@@ -1590,6 +1596,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     } else if (method == CR_MINRES_AFW) {
         constexpr int SLOTS = D == 2 ? 2 : 3;
         build_afw(h, AFW_ABS, s);
+        CR_CUDA(cudaEventRecord(w->es, s));
         if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
         double *zs = w->zs.get();
         double *va = w->v.get(), *vb = w->v2.get(), *za = w->z.get(), *zb = w->z2.get();
@@ -1762,6 +1769,8 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     read_state(w, s);
     float ms = 0.f;
     CR_CUDA(cudaEventElapsedTime(&ms, w->e0, w->e1));
+    float ms_setup = 0.f;
+    CR_CUDA(cudaEventElapsedTime(&ms_setup, w->e0, w->es));
     const double bn = sqrt(w->hst->bb);
     const double tr = bn > 0 ? sqrt(w->hst->rr) / bn : 0.0;
     CR_CUDA(cudaMemcpyAsync(W, x, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -1781,6 +1790,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         rep->inner_iterations = 0;
         rep->kappa_lanczos_est = rep->lambda_min_est = rep->lambda_max_est = 0.0;
         rep->refine_rounds = 0;
+        rep->setup_seconds = ms_setup * 1e-3;
         rep->bytes_moved = iter_bytes(h, o) * (double)w->hst->iters;
         if (pcg_family && w->hst->iters > 1) lanczos_kappa(w, s, w->hst->iters, rep);
     }

@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 import torch
 
+import bench
 import cr_inputs as ci
 import oracle as O
 from oracle.scheme import _gidx, shift_E, local_blocks
@@ -132,9 +133,11 @@ def test_config1_full_size():
     eG, eS = sampled_rows(mo, prm, data, E, hg, 200)
     assert eG <= 1e-12 and eS <= 1e-12, (eG, eS)
     W = torch.zeros(hg.n_rows, dtype=torch.float64, device=DEV)
-    # the bench's solver: two-level PCG on the matrix-free factored G
-    rep = P.cr_solve(hg, W, "pcg_afw2", rtol=cfg.rtol, check_every=64, matrix_free=1, coarse=32)
-    assert rep["converged"] and rep["rel_res_true"] <= cfg.rtol
+    # the bench's solver (bench.SOLVERS[1]): two-level PCG on the matrix-free factored G
+    sol = dict(bench.SOLVERS[1])
+    rtol = sol.pop("rtol")
+    rep = P.cr_solve(hg, W, rtol=rtol, check_every=64, **sol)
+    assert rep["converged"] and rep["rel_res_true"] <= rtol
     U, Pp, diag = P.cr_recover(hg, W)
     eP, eU = sampled_recovery(mo, prm, data, E, W.cpu().numpy(), U.cpu().numpy(), Pp.cpu().numpy(), 400)
     assert eP <= 1e-11 and eU <= 1e-11, (eP, eU)
@@ -155,7 +158,9 @@ def test_well_balanced_full_size(dim, n):
     coords, cells = ci.square_mesh(n, 0.2, 2)
     f = np.array([0.7, -1.3])
     prob = P.Problem(mu=1.0, nu=1.0, fbar=tg(np.tile(f, (cells.shape[0], 1))))
-    out = P.hybrid_method(tg(coords), tg(cells), prob, "pcg_afw2", rtol=1e-10, matrix_free=1, coarse=32)
+    sol = dict(bench.SOLVERS[1])
+    rtol = sol.pop("rtol")
+    out = P.hybrid_method(tg(coords), tg(cells), prob, rtol=rtol, **sol)
     xK = out["mesh"].export()["xK"].cpu().numpy()
     Pex = (xK - xK[0]) @ f
     assert out["U"].abs().max().item() <= 1e-8
@@ -208,8 +213,10 @@ def test_config4_3d_full_size():
     eG, eS = sampled_rows(mo, prm, data, E, hg, 100)
     assert eG <= 1e-12 and eS <= 1e-12, (eG, eS)
     W = torch.zeros(hg.n_rows, dtype=torch.float64, device=DEV)
-    rep = P.cr_solve(hg, W, "pcg_afw2", rtol=cfg.rtol, check_every=64, matrix_free=1, coarse=16)   # ND coarse solve
-    assert rep["converged"] and rep["rel_res_true"] <= cfg.rtol
+    sol = dict(bench.SOLVERS[4])   # the bench's solver: two-level PCG, ND coarse solve, matrix-free G
+    rtol = sol.pop("rtol")
+    rep = P.cr_solve(hg, W, rtol=rtol, check_every=64, **sol)
+    assert rep["converged"] and rep["rel_res_true"] <= rtol
     U, Pp, diag = P.cr_recover(hg, W)
     eP, eU = sampled_recovery(mo, prm, data, E, W.cpu().numpy(), U.cpu().numpy(), Pp.cpu().numpy(), 200)
     assert eP <= 1e-11 and eU <= 1e-11, (eP, eU)

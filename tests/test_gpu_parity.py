@@ -57,11 +57,12 @@ def same_pattern(Ag, Ao):
 
 # ------------------------------------------------------------------ cases
 def make_case(dim, n, mu=1.0, nu=1.0, shift="none", jitter=0.2, seed=1, force="manufactured",
-              ns=False, dirichlet=False, k0=0):
+              ns=False, dirichlet=False, k0=0, flip=None):
+    """flip: seed of the unstructured variants (random diagonals in 2D, mirrored Kuhn splits in 3D)"""
     if dim == 2:
-        coords, cells = ci.square_mesh(n, jitter, seed)
+        coords, cells = ci.square_mesh(n, jitter, seed, flip_seed=flip)
     else:
-        coords, cells = ci.cube_mesh(n)
+        coords, cells = ci.cube_mesh(n, flip_seed=flip)
     nc = cells.shape[0]
     if force == "manufactured":
         _, _, f = (ci.manufactured_2d if dim == 2 else ci.manufactured_3d)(mu, nu)
@@ -140,6 +141,10 @@ HYB_CASES = {
     "2d-k0-interior": dict(dim=2, n=9, k0=77),
     "3d-transient-n3": dict(dim=3, n=3),
     "3d-steady-mis-n3": dict(dim=3, n=3, mu=0.0, shift="mis", force="gaussian"),
+    # unstructured topologies (vertex valences 4..8 in 2D, varying edge valences in 3D)
+    "2d-flip-transient-n14": dict(dim=2, n=14, flip=3),
+    "2d-flip-steady-mis-n12": dict(dim=2, n=12, mu=0.0, shift="mis", force="gaussian", flip=4),
+    "3d-flip-transient-n4": dict(dim=3, n=4, flip=5),
 }
 
 
@@ -178,7 +183,7 @@ def test_spmv_parity(name):
 
 
 @pytest.mark.parametrize("name", ["2d-config0", "2d-transient-jit-n17", "2d-dirichlet-n10", "2d-k0-interior",
-                                  "3d-transient-n3"])
+                                  "3d-transient-n3", "2d-flip-transient-n14", "3d-flip-transient-n4"])
 def test_matrix_free_spmv_parity(name):
     """y = sum_K H_K G_K H_K^t x from per-cell factors (Shat^{-1} split as 1/(mu|K|) 11^t + T,
     u = w/sqrt(B)) against the oracle's assembled G (entries rounded once from binary128)."""
@@ -239,6 +244,17 @@ MF_CASES = {   # the matrix-free factored operator (transient Stokes)
     "2d-dirichlet-n16-pcg-afw2-mf": (dict(dim=2, n=16, dirichlet=True), "pcg_afw2", 1e-12),
 }
 SOLVE_CASES["2d-jit-n24-pcg-afw2"] = (dict(dim=2, n=24), "pcg_afw2", 1e-12)
+# unstructured topologies: patch (KMAX 8 / 16 paths) and two-level solves, assembled and matrix-free
+SOLVE_CASES.update({
+    "2d-flip-n20-pcg-afw": (dict(dim=2, n=20, flip=3), "pcg_afw", 1e-12),
+    "3d-flip-n4-pcg-afw": (dict(dim=3, n=4, flip=5), "pcg_afw", 1e-12),
+    "2d-flip-steady-n12-minres-afw": (dict(dim=2, n=12, mu=0.0, shift="mis", force="gaussian", flip=4), "minres_afw",
+                                      1e-12),
+})
+MF_CASES.update({
+    "2d-flip-n20-pcg-afw2-mf": (dict(dim=2, n=20, flip=3), "pcg_afw2", 1e-12),
+    "3d-flip-n4-pcg-afw2-mf": (dict(dim=3, n=4, flip=5), "pcg_afw2", 1e-12),
+})
 # coupled defect correction (CR_DC_FGMRES): steady Stokes and NS steps, target residual 1e-11
 SOLVE_CASES.update({
     "2d-steady-n16-dc": (dict(dim=2, n=16, mu=0.0, shift="mis", force="gaussian"), "dc", 1e-11),
@@ -360,7 +376,10 @@ def _afw_numpy(G, pats, d, r, kind):
 
 @pytest.mark.parametrize("name,method,kind", [("2d-transient-jit-n17", "pcg_afw", "inv"),
                                               ("3d-transient-n3", "pcg_afw", "inv"),
-                                              ("2d-steady-mis-n16", "minres_afw", "abs")])
+                                              ("2d-steady-mis-n16", "minres_afw", "abs"),
+                                              ("2d-flip-transient-n14", "pcg_afw", "inv"),
+                                              ("2d-flip-steady-mis-n12", "minres_afw", "abs"),
+                                              ("3d-flip-transient-n4", "pcg_afw", "inv")])
 def test_patch_preconditioner_apply(name, method, kind):
     """z = sum_p R_p^t B_p^{-1} R_p r on the GPU vs numpy from the oracle's G."""
     coords, cells, prm, data, prob = make_case(**HYB_CASES[name])
@@ -374,6 +393,8 @@ def test_patch_preconditioner_apply(name, method, kind):
     info = hg.precond_info()
     assert info["npatch"] == len(pats) and info["nfallback"] == 0
     assert info["kmax"] == max(len(p) for p in pats)
+    if "flip" in name:
+        assert info["kmax"] == 8          # the KMAX = 8 kernels (structured meshes stop at 6)
     zo = _afw_numpy(ho["G"], pats, mo.dim, r, kind)
     assert relL2(z.cpu().numpy(), zo) <= 1e-9
 
