@@ -3,6 +3,7 @@
 // local.cuh), forms Shat_K^{-1} column by column, splits off the 1/(mu|K|) 1 1^t part for
 // cells with all faces interior (transient), scales w by 1/sqrt(B_K), and rounds once.
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "local.cuh"
 #include "mf.cuh"
@@ -139,9 +140,11 @@ __device__ __forceinline__ uint64_t spread3(uint64_t v) {   // 21 -> 63 bits, tw
     v = (v | (v << 2)) & 0x1249249249249249ull;
     return v;
 }
+// lex = 0: Morton (Z-order) key; lex = 1: lexicographic key (last coordinate most significant: the
+// order in which the face numbering sweeps the mesh)
 template <int D>
 __global__ void k_mf_morton(const double *xK, const int32_t *list, int64_t n, const double *lo, const double *hi,
-                            uint64_t *key) {
+                            uint64_t *key, int lex) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t K = list[t];
         uint64_t k = 0;
@@ -150,7 +153,8 @@ __global__ void k_mf_morton(const double *xK, const int32_t *list, int64_t n, co
             const double u = w > 0 ? (xK[K * D + i] - lo[i]) / w : 0.0;
             const double scale = D == 2 ? 2147483647.0 : 2097151.0;
             const uint64_t q = (uint64_t)fmin(fmax(u * scale, 0.0), scale);
-            k |= (D == 2 ? spread2(q) : spread3(q)) << i;
+            if (lex) k |= q << (i * (D == 2 ? 31 : 21));
+            else k |= (D == 2 ? spread2(q) : spread3(q)) << i;
         }
         key[t] = k;
     }
@@ -202,7 +206,9 @@ static void build_mf_t(cr_hybrid_s *h, cudaStream_t s) {
         DevBuf<uint64_t> key, key2;
         DevBuf<int32_t> list2;
         key.alloc(ncell, s); key2.alloc(ncell, s); list2.alloc(ncell, s);
-        k_mf_morton<D><<<grid_for(ncell, T), T, 0, s>>>(m->xK.get(), list.get(), ncell, lo.get(), hi.get(), key.get());
+        static const char *eo = std::getenv("CR_MF_ORDER");   // "lex": lexicographic cell order (A/B)
+        const int lex = (eo && eo[0] == 'l') ? 1 : 0;
+        k_mf_morton<D><<<grid_for(ncell, T), T, 0, s>>>(m->xK.get(), list.get(), ncell, lo.get(), hi.get(), key.get(), lex);
         CR_CHECK_LAUNCH();
         size_t ts = 0;
         CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, ts, key.get(), key2.get(), list.get(), list2.get(), (int)ncell, 0,

@@ -39,31 +39,16 @@ struct MfView {
 // in registers through shuffles and stored once by the lower cell; the others get one atomicAdd
 // from each side.  Either way exactly two contributions meet, and 0 + a + b rounds the same in
 // either order -> deterministic.  Returns this cell's share of p^t G p on rows < nown (owned).
+// (factors already loaded: id, sign mask, c, T, u, in-warp partner codes)
 template <int D>
-__device__ __forceinline__ double mf_cell(const MfView &M, int64_t t, const double *__restrict__ x,
-                                          double *__restrict__ q, int64_t nown) {
-    using LY = MfLayout<D>;
-    constexpr int NF = LY::NF, NT = LY::NT;
-    const int64_t slice = t >> 5;
-    const int lane = (int)(t & 31);
-    const int32_t *ip = M.ids + slice * (NF * 32) + lane;
-    const double *vp = M.v + slice * ((int64_t)LY::NE * 32) + lane;
-    int id[NF];
+__device__ __forceinline__ double mf_cell_core(const int (&id)[D + 1], unsigned sg, double c,
+                                               const double (&T)[MfLayout<D>::NT], const double (&u)[D][D + 1],
+                                               const unsigned (&nbc)[D + 1], int lane, const double *__restrict__ x,
+                                               double *__restrict__ q, int64_t nown) {
+    constexpr int NF = D + 1;
     double cs[NF];
-    const unsigned sg = M.sg[t];
 #pragma unroll
-    for (int l = 0; l < NF; ++l) {
-        id[l] = __ldcs(ip + l * 32);
-        cs[l] = ((sg >> l) & 1u) ? -1.0 : 1.0;
-    }
-    const double c = __ldcs(vp);
-    double T[NT], u[D][NF];
-#pragma unroll
-    for (int e = 0; e < NT; ++e) T[e] = __ldcs(vp + (1 + e) * 32);
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-        for (int l = 0; l < NF; ++l) u[i][l] = __ldcs(vp + (1 + NT + i * NF + l) * 32);
+    for (int l = 0; l < NF; ++l) cs[l] = ((sg >> l) & 1u) ? -1.0 : 1.0;
     double xs[D][NF];
 #pragma unroll
     for (int l = 0; l < NF; ++l) {
@@ -88,9 +73,6 @@ __device__ __forceinline__ double mf_cell(const MfView &M, int64_t t, const doub
 #pragma unroll
         for (int l = 0; l < NF; ++l) pu = fma(u[i][l], xs[i][l], pu);
     double quad = 0.0;
-    unsigned nbc[NF];
-#pragma unroll
-    for (int a = 0; a < NF; ++a) nbc[a] = M.nb[slice * (NF * 32) + a * 32 + lane];
 #pragma unroll
     for (int i = 0; i < D; ++i) {
         double sum = 0.0;
@@ -134,6 +116,112 @@ __device__ __forceinline__ double mf_cell(const MfView &M, int64_t t, const doub
         }
     }
     return quad;
+}
+
+// the same cell, factors streamed from HBM (coalesced warp rows)
+template <int D>
+__device__ __forceinline__ double mf_cell(const MfView &M, int64_t t, const double *__restrict__ x,
+                                          double *__restrict__ q, int64_t nown) {
+    using LY = MfLayout<D>;
+    constexpr int NF = LY::NF, NT = LY::NT;
+    const int64_t slice = t >> 5;
+    const int lane = (int)(t & 31);
+    const int32_t *ip = M.ids + slice * (NF * 32) + lane;
+    const double *vp = M.v + slice * ((int64_t)LY::NE * 32) + lane;
+    int id[NF];
+#pragma unroll
+    for (int l = 0; l < NF; ++l) id[l] = __ldcs(ip + l * 32);
+    const unsigned sg = M.sg[t];
+    const double c = __ldcs(vp);
+    double T[NT], u[D][NF];
+#pragma unroll
+    for (int e = 0; e < NT; ++e) T[e] = __ldcs(vp + (1 + e) * 32);
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int l = 0; l < NF; ++l) u[i][l] = __ldcs(vp + (1 + NT + i * NF + l) * 32);
+    unsigned nbc[NF];
+#pragma unroll
+    for (int a = 0; a < NF; ++a) nbc[a] = M.nb[slice * (NF * 32) + a * 32 + lane];
+    return mf_cell_core<D>(id, sg, c, T, u, nbc, lane, x, q, nown);
+}
+
+// ------------------------------------------------------------------ TMA-staged slices
+// One 32-cell slice as it lies in HBM, copied whole into shared memory by the bulk-copy engine
+// (cp.async.bulk: v, ids, nb, sg are contiguous per slice): v [NE][32] f64, ids [NF][32] i32,
+// nb [NF][32] u8, sg [32] u8.  All four sizes and offsets are multiples of 16 bytes.
+template <int D>
+struct MfSlice {
+    static constexpr int NF = D + 1, NE = MfLayout<D>::NE;
+    static constexpr int V = NE * 32 * 8, IDS = NF * 32 * 4, NB = NF * 32, SG = 32;
+    static constexpr int OFF_IDS = V, OFF_NB = V + IDS, OFF_SG = V + IDS + NB;
+    static constexpr int BYTES = V + IDS + NB + SG;
+    static_assert(V % 16 == 0 && IDS % 16 == 0 && NB % 16 == 0 && BYTES % 16 == 0, "bulk-copy granularity");
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// the elected lane arms the stage's barrier and issues the four bulk copies of slice `sl`
+template <int D>
+__device__ __forceinline__ void mf_issue_slice(const MfView &M, int64_t sl, unsigned char *stage, uint64_t *bar) {
+    using SL = MfSlice<D>;
+    mbar_expect_tx(bar, SL::BYTES);
+    bulk_g2s(stage, M.v + sl * (int64_t)(SL::NE * 32), SL::V, bar);
+    bulk_g2s(stage + SL::OFF_IDS, M.ids + sl * (int64_t)(SL::NF * 32), SL::IDS, bar);
+    bulk_g2s(stage + SL::OFF_NB, M.nb + sl * (int64_t)(SL::NF * 32), SL::NB, bar);
+    bulk_g2s(stage + SL::OFF_SG, M.sg + sl * 32, SL::SG, bar);
+}
+
+// the cell of `lane` in a staged slice
+template <int D>
+__device__ __forceinline__ double mf_cell_staged(const unsigned char *stage, int lane, const double *__restrict__ x,
+                                                 double *__restrict__ q, int64_t nown) {
+    using LY = MfLayout<D>;
+    using SL = MfSlice<D>;
+    constexpr int NF = LY::NF, NT = LY::NT;
+    const double *vp = reinterpret_cast<const double *>(stage) + lane;
+    const int32_t *ip = reinterpret_cast<const int32_t *>(stage + SL::OFF_IDS) + lane;
+    const uint8_t *np = stage + SL::OFF_NB + lane;
+    int id[NF];
+    unsigned nbc[NF];
+#pragma unroll
+    for (int l = 0; l < NF; ++l) {
+        id[l] = ip[l * 32];
+        nbc[l] = np[l * 32];
+    }
+    const unsigned sg = stage[SL::OFF_SG + lane];
+    const double c = vp[0];
+    double T[NT], u[D][NF];
+#pragma unroll
+    for (int e = 0; e < NT; ++e) T[e] = vp[(1 + e) * 32];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int l = 0; l < NF; ++l) u[i][l] = vp[(1 + NT + i * NF + l) * 32];
+    return mf_cell_core<D>(id, sg, c, T, u, nbc, lane, x, q, nown);
 }
 
 }  // namespace cr
