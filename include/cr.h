@@ -268,12 +268,19 @@ cr_status cr_recover(cr_hybrid h, const double *W_d, double *U_d, double *P_d, d
                      cr_stream_t s);
 
 /* ------------------------------------------------------------------ Newton update
- * U_d[i] += dU_d[i] (i < nU), P_d[k] += dP_d[k] (k < nP) on the device, and returns on the host
- * norms_h[0] = ||dU||_2, norms_h[1] = ||U + dU||_2 (fixed-order reductions: deterministic);
- * Newton's method stops when norms_h[0] <= tol * norms_h[1] (tol = 5e-7).
- * U_d / dU_d [nU], P_d / dP_d [nP] (dP_d may be NULL: P unchanged).  Synchronises `s`.       */
+ * U_d[i] += lam dU_d[i] (i < nU), P_d[k] += lam dP_d[k] (k < nP) on the device, and returns on the
+ * host norms_h[0] = ||lam dU||_2, norms_h[1] = ||U + lam dU||_2 (fixed-order reductions:
+ * deterministic); Newton's method stops when norms_h[0] <= tol * norms_h[1] (P:L783-799:
+ * tol = 5e-7).  lam = 1: the full step; lam < 1: a damped step (line search, see
+ * cr_coupled_rhs_norm).  U_d / dU_d [nU], P_d / dP_d [nP] (dP_d may be NULL: P unchanged).
+ * Synchronises `s`.                                                                          */
 cr_status cr_newton_update(int64_t nU, double *U_d, const double *dU_d, int64_t nP, double *P_d,
-                           const double *dP_d, double *norms_h, cr_stream_t s);
+                           const double *dP_d, double lam, double *norms_h, cr_stream_t s);
+/* ||[R; g]||_2 of the coupled system of (prm, data): for a Navier-Stokes Newton step
+ * (physics = CR_NS_NEWTON_STEP, u_iter / p_iter = the iterate) the increment-form right-hand side is
+ * minus the nonlinear residual F(U^k, P^k) of the discrete steady equations, so this is ||F||, the
+ * merit function of a damped Newton line search.  Returned on the host; synchronises `s`.     */
+cr_status cr_coupled_rhs_norm(cr_mesh m, const cr_params *prm, const cr_data *data, double *norm_h, cr_stream_t s);
 
 /* Per (cell, local face) values of a face field (the Newton iterate layout of cr_data.u_iter_d,
  * P:L302): out_d[K][l] = U_d[face_dof(sigma)] on interior faces, bnd_d[K][l] (wall / lid values;

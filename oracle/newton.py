@@ -28,10 +28,23 @@ def cell_face_values(m: Mesh, U: np.ndarray, wall: np.ndarray | None) -> np.ndar
     return out
 
 
+def residual_norm(m: Mesh, prm: Params, fbar: np.ndarray, wall: np.ndarray | None, U: np.ndarray,
+                  P: np.ndarray) -> float:
+    """||F(U, P)||_2: the right-hand side [R; g] of the increment-form Newton system at (U, P) is
+    minus the nonlinear residual of the discrete steady Navier-Stokes equations."""
+    _, rhs, _ = assemble_coupled(m, prm, Data(fbar=fbar, u_iter=cell_face_values(m, U, wall), p_iter=P))
+    return float(np.linalg.norm(rhs))
+
+
 def newton_ns(m: Mesh, prm: Params, fbar: np.ndarray, wall: np.ndarray | None, max_newton: int = 30,
-              tol: float = 5e-7):
+              tol: float = 5e-7, damped: bool = False, lam_min: float = 1.0 / 64):
     """Newton iterations from U^0 = 0 (interior), P^0 = 0.  Returns U [nf_int, d], P [nc] and the
-    list of ||dU|| / ||U^{k+1}||."""
+    list of ||lam dU|| / ||U^{k+1}||.
+
+    damped=True globalises the iteration (the paper's Re = 1000 cavity, diverges from
+    rest with full steps on some meshes): backtracking on the nonlinear residual, the step length
+    lam = 1, 1/2, 1/4, ... >= lam_min is the first with ||F(U + lam dU)|| < (1 - 1e-4 lam) ||F(U)||
+    (Armijo; lam_min is taken if none is)."""
     U = np.zeros((m.nf_int, m.dim))
     P = np.zeros(m.nc)
     hist = []
@@ -41,9 +54,16 @@ def newton_ns(m: Mesh, prm: Params, fbar: np.ndarray, wall: np.ndarray | None, m
         x = direct_refined(M, rhs)
         dU = x[:nU].reshape(m.nf_int, m.dim)
         dP = np.insert(x[nU:], prm.k0, 0.0)
-        U = U + dU
-        P = P + dP
-        rel = float(np.linalg.norm(dU) / max(np.linalg.norm(U), 1e-300))
+        lam = 1.0
+        if damped:
+            r0 = float(np.linalg.norm(rhs))
+            while lam > lam_min:
+                if residual_norm(m, prm, fbar, wall, U + lam * dU, P + lam * dP) < (1.0 - 1e-4 * lam) * r0:
+                    break
+                lam *= 0.5
+        U = U + lam * dU
+        P = P + lam * dP
+        rel = float(np.linalg.norm(lam * dU) / max(np.linalg.norm(U), 1e-300))
         hist.append(rel)
         if rel <= tol:
             break

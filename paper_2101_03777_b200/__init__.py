@@ -115,7 +115,8 @@ _sig = {
     "cr_coarse_nd_plan": [_i32, _i32, _i32, _P(_i64), _P(_i32), _P(_i64), _P(_i64), _vp, _vp, _vp, _vp, _vp, _vp],
     "cr_sparse_direct_solve": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _P(_i32)],
     "cr_hybrid_coarse_info": [_vp, _P(_i32), _P(_i64), _P(_i32), _P(_i64)],
-    "cr_newton_update": [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp],
+    "cr_newton_update": [_i64, _vp, _vp, _i64, _vp, _vp, ctypes.c_double, _vp, _vp],
+    "cr_coupled_rhs_norm": [_vp, _P(Params), _P(Data), _vp, _vp],
     "cr_hybrid_method_host": [_i32, _i64, _vp, _i64, _vp, _P(Params), _vp, _vp, _P(SolverOpts), _vp, _vp, _vp,
                               _P(MeshInfo), _P(SolveReport), _vp],
     "cr_pool_reserve": [_i64, _vp],
@@ -526,41 +527,66 @@ def cell_face_values(mesh: "Mesh", U: torch.Tensor, bnd: torch.Tensor | None = N
 
 def newton_ns(coords: torch.Tensor, cells: torch.Tensor, nu: float, fbar: torch.Tensor, wall: torch.Tensor | None,
               max_newton: int = 30, tol: float = 5e-7, mis_seed: int = 0, method: str = "dc", rtol: float = 1e-10,
-              stream=None, **solve_kw) -> dict:
+              damped: bool = False, lam_min: float = 1.0 / 64, stream=None, **solve_kw) -> dict:
     """Newton's method for steady Navier-Stokes from U^0 = 0, P^0 = 0: each
     step hybridises the linearised problem at (U^k, P^k) (MIS shift), solves it (default: coupled
     FGMRES preconditioned by the transient hybrid solve) and recovers the increments; stops when
-    ||dU|| <= tol ||U^{k+1}||."""
+    ||lam dU|| <= tol ||U^{k+1}||.  damped: Armijo backtracking lam = 1, 1/2, ... >= lam_min on the
+    nonlinear residual ||F|| (cr_coupled_rhs_norm), the rule of oracle.newton_ns(damped=True)."""
     mesh = cr_build_mesh(coords, cells, stream)
     dev = coords.device
     U = torch.zeros((mesh.nf_int, mesh.dim), dtype=torch.float64, device=dev)
     Pk = torch.zeros(mesh.nc, dtype=torch.float64, device=dev)
-    hist, reps = [], []
+    hist, reps, lams = [], [], []
+
+    def ns_problem(Uv, Pv):
+        return Problem(mu=0.0, nu=nu, fbar=fbar, physics=CR_NS_NEWTON_STEP, shift=CR_SHIFT_MIS, mis_seed=mis_seed,
+                       u_iter=cell_face_values(mesh, Uv, wall, stream), p_iter=Pv)
+
     for _ in range(max_newton):
-        uit = cell_face_values(mesh, U, wall, stream)
-        prob = Problem(mu=0.0, nu=nu, fbar=fbar, physics=CR_NS_NEWTON_STEP, shift=CR_SHIFT_MIS, mis_seed=mis_seed,
-                       u_iter=uit, p_iter=Pk)
+        prob = ns_problem(U, Pk)
         hyb = cr_hybridise(mesh, prob, stream)
         W = torch.zeros(hyb.n_rows, dtype=torch.float64, device=dev)
         reps.append(cr_solve(hyb, W, method, rtol, stream=stream, **solve_kw))
         dU, dP, _ = cr_recover(hyb, W, stream)
-        du, un = newton_update(U, dU, Pk, dP, stream)
+        del hyb
+        lam = 1.0
+        if damped:
+            r0 = coupled_rhs_norm(mesh, prob, stream)
+            while lam > lam_min:
+                Ut, Pt = U.clone(), Pk.clone()
+                newton_update(Ut, dU, Pt, dP, lam, stream)
+                if coupled_rhs_norm(mesh, ns_problem(Ut, Pt), stream) < (1.0 - 1e-4 * lam) * r0:
+                    break
+                lam *= 0.5
+        du, un = newton_update(U, dU, Pk, dP, lam, stream)
         rel = du / max(un, 1e-300)
         hist.append(rel)
-        del hyb
+        lams.append(lam)
         if rel <= tol:
             break
-    return dict(mesh=mesh, U=U, P=Pk, history=hist, reports=reps)
+    return dict(mesh=mesh, U=U, P=Pk, history=hist, step_lengths=lams, reports=reps)
 
 
 def newton_update(U: torch.Tensor, dU: torch.Tensor, P: torch.Tensor | None = None, dP: torch.Tensor | None = None,
-                  stream=None):
-    """U += dU, P += dP in place on the device (cr_newton_update); returns (||dU||, ||U_new||)."""
+                  lam: float = 1.0, stream=None):
+    """U += lam dU, P += lam dP in place on the device (cr_newton_update); returns
+    (||lam dU||, ||U_new||)."""
     norms = (ctypes.c_double * 2)()
     _check(_lib.cr_newton_update(U.numel(), _ptr(U, torch.float64), _ptr(dU, torch.float64),
                                  0 if P is None else P.numel(), _ptr(P, torch.float64), _ptr(dP, torch.float64),
-                                 ctypes.cast(norms, ctypes.c_void_p), _stream(stream)))
+                                 float(lam), ctypes.cast(norms, ctypes.c_void_p), _stream(stream)))
     return norms[0], norms[1]
+
+
+def coupled_rhs_norm(mesh: "Mesh", prob: Problem, stream=None) -> float:
+    """||[R; g]||_2 of the coupled system (cr_coupled_rhs_norm): for a Navier-Stokes step, the
+    nonlinear residual ||F(U^k, P^k)|| (the merit function of the damped Newton line search)."""
+    out = ctypes.c_double()
+    prm, data = prob.params(), prob.data()
+    _check(_lib.cr_coupled_rhs_norm(mesh._h, ctypes.byref(prm), ctypes.byref(data), ctypes.byref(out),
+                                    _stream(stream)))
+    return out.value
 
 
 def sparse_direct_solve(rp: torch.Tensor, ci: torch.Tensor, v: torch.Tensor, b: torch.Tensor, method: str = "chol",

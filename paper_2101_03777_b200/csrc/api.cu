@@ -392,10 +392,19 @@ cr_status cr_recover(cr_hybrid h, const double *W_d, double *U_d, double *P_d, d
 }
 
 cr_status cr_newton_update(int64_t nU, double *U_d, const double *dU_d, int64_t nP, double *P_d, const double *dP_d,
-                           double *norms_h, cr_stream_t s) {
+                           double lam, double *norms_h, cr_stream_t s) {
     CR_API_BEGIN
     CR_REQUIRE(nU >= 0 && nP >= 0 && U_d && dU_d && norms_h && (!dP_d || P_d), CR_ERR_INVALID_ARG, "bad arguments");
-    cr::newton_update(nU, U_d, dU_d, nP, P_d, dP_d, norms_h, (cudaStream_t)s);
+    cr::newton_update(nU, U_d, dU_d, nP, P_d, dP_d, lam, norms_h, (cudaStream_t)s);
+    CR_API_END
+}
+
+cr_status cr_coupled_rhs_norm(cr_mesh m, const cr_params *prm, const cr_data *data, double *norm_h, cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(m && prm && data && norm_h, CR_ERR_INVALID_ARG, "null argument");
+    cr_coupled_s c;
+    cr::assemble_coupled(&c, m, *prm, *data, (cudaStream_t)s);
+    *norm_h = cr::norm2(c.rhs.get(), c.n_rows, (cudaStream_t)s);
     CR_API_END
 }
 

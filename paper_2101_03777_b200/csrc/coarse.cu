@@ -455,6 +455,177 @@ __global__ void __launch_bounds__(256, 2) k_coarse_restrict3(CoarseView C, const
     }
 }
 
+// ------------------------------------------------------------------ batched setup (all D^2 (k, l) columns of a colour)
+// The D^2 columns of one colour, (k, l) -> column k D + l, stored as separate vectors of stride zs.
+template <int D>
+__global__ void __launch_bounds__(256) k_coarse_colour_chunks_all(CoarseView C, const int32_t *list, int colour, int clear,
+                                                                  double *z, int64_t zs, const int64_t *ends = nullptr) {
+    constexpr int NN = 1 << D;
+    const int64_t ch = list[blockIdx.x];
+    const int64_t end = ends ? ends[blockIdx.x] : C.chunk_start[ch + 1];
+    for (int64_t t = C.chunk_start[ch] + threadIdx.x; t < end; t += blockDim.x) {
+        const int64_t r = C.perm[t];
+        double s = 0.0;
+        if (!clear) {
+            int ic[D];
+            float xi[D];
+            coarse_locate<D>(C.g, C.fx + r * D, ic, xi);
+            double w[NN];
+            coarse_weights<D>(C.g, C.fx + r * D, w);
+            for (int n = 0; n < NN; ++n) {
+                int col = 0, mul = 1;
+                for (int i = 0; i < D; ++i) {
+                    col += ((ic[i] + ((n >> i) & 1)) % 5) * mul;
+                    mul *= 5;
+                }
+                if (col == colour) s += w[n];
+            }
+        }
+        for (int k = 0; k < D; ++k)
+            for (int l = 0; l < D; ++l) {
+                const double v = clear ? 0.0 : s * (double)C.fa[r * D + l];
+                double *zc = z + (int64_t)(k * D + l) * zs + r * D;
+                for (int i = 0; i < D; ++i) zc[i] = (i == k) ? v : 0.0;
+            }
+    }
+}
+
+// the D^2 columns of a colour on every local row (partitioned setup)
+template <int D>
+__global__ void k_coarse_colour_all(CoarseView C, int64_t nrows, int colour, double *z, int64_t zs) {
+    constexpr int NN = 1 << D;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+        int ic[D];
+        float xi[D];
+        coarse_locate<D>(C.g, C.fx + r * D, ic, xi);
+        double w[NN];
+        coarse_weights<D>(C.g, C.fx + r * D, w);
+        double sw = 0.0;
+        for (int n = 0; n < NN; ++n) {
+            int col = 0, mul = 1;
+            for (int i = 0; i < D; ++i) {
+                col += ((ic[i] + ((n >> i) & 1)) % 5) * mul;
+                mul *= 5;
+            }
+            if (col == colour) sw += w[n];
+        }
+        for (int k = 0; k < D; ++k)
+            for (int l = 0; l < D; ++l) {
+                const double v = sw * (double)C.fa[r * D + l];
+                double *zc = z + (int64_t)(k * D + l) * zs + r * D;
+                for (int i = 0; i < D; ++i) zc[i] = (i == k) ? v : 0.0;
+            }
+    }
+}
+
+// k_coarse_restrict3 for NC columns at once (column c at r + c * rs, partials at part + c * ps): the
+// row data (perm, centroid, area vector) is read once for all NC columns
+template <int NC>
+__global__ void __launch_bounds__(256, 2) k_coarse_restrict3m(CoarseView C, const double *r, int64_t rs, double *part,
+                                                           int64_t ps, const int32_t *list, const int64_t *ends) {
+    constexpr int D = 3, DD = 9, NV = 72, U = 2;
+    const int64_t ch = list ? (int64_t)list[blockIdx.x] : (int64_t)blockIdx.x;
+    const int64_t b = C.chunk_start[ch], e = ends ? ends[blockIdx.x] : C.chunk_start[ch + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int corner = lane & 7, rsub = lane >> 3;
+    double acc[NC][DD];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int v = 0; v < DD; ++v) acc[c][v] = 0.0;
+    for (int64_t t0 = b + warp * 32 + lane; t0 - lane < e; t0 += (int64_t)8 * 32 * U) {
+        float xi[U][D], av[U][D];
+        double rv[U][NC][D];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t t = t0 + (int64_t)u * 8 * 32;
+            const int64_t row = t < e ? (int64_t)C.perm[t] : -1;
+            float xv[D];
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                xv[i] = row >= 0 ? C.fx[row * D + i] : 0.f;
+                av[u][i] = row >= 0 ? C.fa[row * D + i] : 0.f;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) rv[u][c][i] = row >= 0 ? r[c * rs + row * D + i] : 0.0;
+            }
+            int ic[D];
+            coarse_locate<D>(C.g, xv, ic, xi[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int src = 4 * k + rsub;   // row of this batch handled now by this lane's corner
+                const float x0 = __shfl_sync(0xffffffffu, xi[u][0], src), x1 = __shfl_sync(0xffffffffu, xi[u][1], src),
+                            x2 = __shfl_sync(0xffffffffu, xi[u][2], src);
+                const float a0 = __shfl_sync(0xffffffffu, av[u][0], src), a1 = __shfl_sync(0xffffffffu, av[u][1], src),
+                            a2 = __shfl_sync(0xffffffffu, av[u][2], src);
+                const double wn = ((corner & 1) ? (double)x0 : 1.0 - (double)x0) *
+                                  ((corner & 2) ? (double)x1 : 1.0 - (double)x1) *
+                                  ((corner & 4) ? (double)x2 : 1.0 - (double)x2);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const double r0 = __shfl_sync(0xffffffffu, rv[u][c][0], src),
+                                 r1 = __shfl_sync(0xffffffffu, rv[u][c][1], src),
+                                 r2 = __shfl_sync(0xffffffffu, rv[u][c][2], src);
+                    const double ar[DD] = {(double)a0 * r0, (double)a1 * r0, (double)a2 * r0,
+                                           (double)a0 * r1, (double)a1 * r1, (double)a2 * r1,
+                                           (double)a0 * r2, (double)a1 * r2, (double)a2 * r2};
+#pragma unroll
+                    for (int v = 0; v < DD; ++v) acc[c][v] = fma(wn, ar[v], acc[c][v]);
+                }
+            }
+    }
+    __shared__ double sh[8][NV];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+#pragma unroll
+        for (int v = 0; v < DD; ++v) {
+            double x = acc[c][v];
+            x += __shfl_xor_sync(0xffffffffu, x, 16);
+            x += __shfl_xor_sync(0xffffffffu, x, 8);
+            if (lane < 8) sh[warp][lane * DD + v] = x;   // lane = corner
+        }
+        __syncthreads();
+        for (int v = threadIdx.x; v < NV; v += blockDim.x) {
+            double x = 0.0;
+            for (int w = 0; w < 8; ++w) x += sh[w][v];
+            part[c * ps + ch * NV + v] = x;
+        }
+        __syncthreads();
+    }
+}
+
+// k_coarse_gather for D^2 columns (partials at part + c * ps, result at out + c * nE)
+template <int D>
+__global__ void k_coarse_gather_all(CoarseView C, const double *part, int64_t ps, double *out) {
+    constexpr int NN = 1 << D, NV = NN * D * D, NCOL = D * D;
+    const int64_t nE = C.nE;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nE * NCOL; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t col = t / nE, q = t - col * nE;
+        const int64_t node = q / (D * D);
+        const int kl = (int)(q - node * D * D);
+        int nd[D];
+        int64_t tt = node;
+        for (int i = 0; i < D; ++i) { nd[i] = (int)(tt % (C.g.H + 1)); tt /= (C.g.H + 1); }
+        double sum = 0.0;
+        for (int n = 0; n < NN; ++n) {
+            int cc[D];
+            bool ok = true;
+            for (int i = 0; i < D; ++i) {
+                cc[i] = nd[i] - ((n >> i) & 1);
+                ok = ok && cc[i] >= 0 && cc[i] < C.g.H;
+            }
+            if (!ok) continue;
+            int64_t cell = 0;
+            for (int i = D - 1; i >= 0; --i) cell = cell * C.g.H + cc[i];
+            for (int64_t ch = C.cell_chunk[cell]; ch < C.cell_chunk[cell + 1]; ++ch)
+                sum += part[col * ps + ch * NV + n * D * D + kl];
+        }
+        out[col * nE + q] = sum;
+    }
+}
+
 // first sorted position with coarse cell >= c (c = 0..ncc)
 __global__ void k_cell_starts(const uint32_t *cc_sorted, int64_t n, int64_t ncc, int64_t *cstart, int mult = 1,
                               int add = 0) {
@@ -635,6 +806,32 @@ __global__ void k_coarse_scatterEs(int64_t nE, int H, int colour, int k, int l, 
         }
         if (!ok) continue;
         Es[((node * NBR + nbr) * M + (qp - node * M)) * M + k * D + l] = R[qp];
+    }
+}
+
+// k_coarse_scatterEs for the D^2 columns of a colour (R + (k D + l) nE)
+template <int D>
+__global__ void k_coarse_scatterEs_all(int64_t nE, int H, int colour, const double *R, double *Es) {
+    constexpr int M = D * D, NBR = D == 2 ? 25 : 125;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nE * M; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t col = t / nE, qp = t - col * nE;
+        const int64_t node = qp / M;
+        int64_t tt = node;
+        int cl = colour, nbr = 0, mul = 1;
+        bool ok = true;
+        for (int i = 0; i < D; ++i) {
+            const int ni = (int)(tt % (H + 1));
+            tt /= (H + 1);
+            const int ci = cl % 5;
+            cl /= 5;
+            int delta = ((ci - ni) % 5 + 5) % 5;
+            if (delta > 2) delta -= 5;
+            ok = ok && ni + delta >= 0 && ni + delta <= H;
+            nbr += (delta + 2) * mul;
+            mul *= 5;
+        }
+        if (!ok) continue;
+        Es[((node * NBR + nbr) * M + (qp - node * M)) * M + col] = R[t];
     }
 }
 
@@ -1472,8 +1669,7 @@ static bool lapack_potrf_batched(int n, int lda, int nb, double **A, int *info, 
 }
 
 template <int D>
-static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const double *, double *, int)> &applyG,
-                           cudaStream_t s) {
+static void build_coarse_t(cr_hybrid_s *h, int H, const ApplyG &applyG, cudaStream_t s) {
     constexpr int NN = 1 << D, NV = NN * D * D;
     const cr_mesh_s *m = h->mesh;
     CoarseOp &C = h->coarse;
@@ -1653,48 +1849,98 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
         upload(dend, lend, s);
         Y.zero(s);
     }
-    for (int colour = 0; colour < ncol; ++colour)
-        for (int k = 0; k < D; ++k)
-            for (int l = 0; l < D; ++l) {
-                const unsigned nsup = (unsigned)(osup[colour + 1] - osup[colour]);
-                const unsigned nact = (unsigned)(oact[colour + 1] - oact[colour]);
-                if (restricted) {
-                    if (nsup) k_coarse_colour_chunks<D><<<nsup, 256, 0, s>>>(V, dsup.get() + osup[colour], colour, k, l, 0, z.get());
+    if (restricted) {
+        // all D^2 (k, l) columns of a colour at once: one fill, one G application (D^2 right-hand
+        // sides, cell factors read once), NC-column restrictions reading the row data once, one
+        // gather and one scatter per colour (was one of each per column: 1,125 passes in 3D)
+        constexpr int NCOL = D * D;
+        const int64_t zs = Nalloc;
+        DevBuf<double> zall, Yall, pall, call;
+        zall.alloc((size_t)NCOL * zs, s);
+        Yall.alloc((size_t)NCOL * zs, s);
+        zall.zero(s);
+        Yall.zero(s);
+        const int64_t ps = C.nchunk * NV;
+        pall.alloc((size_t)NCOL * ps, s);
+        call.alloc((size_t)NCOL * C.nE, s);
+        for (int colour = 0; colour < ncol; ++colour) {
+            const unsigned nsup = (unsigned)(osup[colour + 1] - osup[colour]);
+            const unsigned nact = (unsigned)(oact[colour + 1] - oact[colour]);
+            if (nsup) k_coarse_colour_chunks_all<D><<<nsup, 256, 0, s>>>(V, dsup.get() + osup[colour], colour, 0, zall.get(), zs);
+            CR_CHECK_LAUNCH();
+            applyG(zall.get(), Yall.get(), colour, NCOL, zs);
+            pall.zero(s);
+            if (nact) {
+                if (D == 3) {
+                    for (int c0 = 0; c0 < NCOL; c0 += 3)
+                        k_coarse_restrict3m<3><<<nact, 256, 0, s>>>(V, Yall.get() + c0 * zs, zs, pall.get() + c0 * ps, ps,
+                                                                  dact.get() + oact[colour], dend.get() + oact[colour]);
                 } else {
-                    k_coarse_colour<D><<<grid_for(nrows, T), T, 0, s>>>(V, nrows, colour, k, l, z.get());
+                    for (int c = 0; c < NCOL; ++c)
+                        k_coarse_restrict<D><<<nact, 256, 0, s>>>(V, Yall.get() + c * zs, pall.get() + c * ps,
+                                                                  dact.get() + oact[colour], dend.get() + oact[colour]);
                 }
-                CR_CHECK_LAUNCH();
-                applyG(z.get(), Y.get(), restricted ? colour : -1 - colour);
-                if (restricted) {
-                    C.part.zero(s);
-                    if (nact) {
-                        if (D == 3)
-                            k_coarse_restrict3<<<nact, 256, 0, s>>>(V, Y.get(), C.part.get(), dact.get() + oact[colour],
-                                                                    dend.get() + oact[colour]);
-                        else
-                            k_coarse_restrict<D><<<nact, 256, 0, s>>>(V, Y.get(), C.part.get(), dact.get() + oact[colour],
-                                                                      dend.get() + oact[colour]);
-                    }
-                } else {
-                    if (D == 3) k_coarse_restrict3<<<(unsigned)C.nchunk, 256, 0, s>>>(V, Y.get(), C.part.get());
-                    else k_coarse_restrict<D><<<(unsigned)C.nchunk, 256, 0, s>>>(V, Y.get(), C.part.get());
-                }
-                k_coarse_gather<D><<<grid_for(C.nE, T), T, 0, s>>>(V, C.part.get(), C.c.get());
-                CR_CHECK_LAUNCH();
-                if (restricted) {
-                    if (nsup) k_coarse_colour_chunks<D><<<nsup, 256, 0, s>>>(V, dsup.get() + osup[colour], colour, k, l, 1, z.get());
-                    if (nact)
-                        k_coarse_colour_chunks<D><<<nact, 256, 0, s>>>(V, dact.get() + oact[colour], colour, k, l, 1, Y.get(),
-                                                                       dend.get() + oact[colour]);
-                    CR_CHECK_LAUNCH();
-                }
-                if (h->part.on) h->comm->impl->allreduce(C.c.get(), (int)C.nE, false, s);
-                if (dense)
-                    k_coarse_scatterE<D><<<grid_for(C.nE, T), T, 0, s>>>(C.nE, H, colour, k, l, C.c.get(), C.Einv.get());
-                else
-                    k_coarse_scatterEs<D><<<grid_for(C.nE, T), T, 0, s>>>(C.nE, H, colour, k, l, C.c.get(), Es.get());
                 CR_CHECK_LAUNCH();
             }
+            k_coarse_gather_all<D><<<grid_for(C.nE * NCOL, T), T, 0, s>>>(V, pall.get(), ps, call.get());
+            CR_CHECK_LAUNCH();
+            if (nsup) k_coarse_colour_chunks_all<D><<<nsup, 256, 0, s>>>(V, dsup.get() + osup[colour], colour, 1, zall.get(), zs);
+            if (nact)
+                k_coarse_colour_chunks_all<D><<<nact, 256, 0, s>>>(V, dact.get() + oact[colour], colour, 1, Yall.get(), zs,
+                                                                   dend.get() + oact[colour]);
+            CR_CHECK_LAUNCH();
+            if (dense) {
+                for (int k = 0; k < D; ++k)
+                    for (int l = 0; l < D; ++l)
+                        k_coarse_scatterE<D><<<grid_for(C.nE, T), T, 0, s>>>(C.nE, H, colour, k, l,
+                                                                             call.get() + (k * D + l) * C.nE, C.Einv.get());
+            } else {
+                k_coarse_scatterEs_all<D><<<grid_for(C.nE * NCOL, T), T, 0, s>>>(C.nE, H, colour, call.get(), Es.get());
+            }
+            CR_CHECK_LAUNCH();
+        }
+    } else {
+        // partitioned: every rank restricts its own rows (all chunks), the D^2 columns of a colour
+        // in one pass and one allreduce of the D^2 restricted vectors per colour
+        constexpr int NCOL = D * D;
+        const int64_t zs = Nalloc;
+        DevBuf<double> zall, Yall, pall, call;
+        zall.alloc((size_t)NCOL * zs, s);
+        Yall.alloc((size_t)NCOL * zs, s);
+        zall.zero(s);
+        Yall.zero(s);
+        const int64_t ps = C.nchunk * NV;
+        pall.alloc((size_t)NCOL * std::max<int64_t>(ps, 1), s);
+        call.alloc((size_t)NCOL * C.nE, s);
+        for (int colour = 0; colour < ncol; ++colour) {
+            k_coarse_colour_all<D><<<grid_for(nrows, T), T, 0, s>>>(V, nrows, colour, zall.get(), zs);
+            CR_CHECK_LAUNCH();
+            applyG(zall.get(), Yall.get(), -1 - colour, NCOL, zs);
+            if (C.nchunk > 0) {
+                if (D == 3) {
+                    for (int c0 = 0; c0 < NCOL; c0 += 3)
+                        k_coarse_restrict3m<3><<<(unsigned)C.nchunk, 256, 0, s>>>(V, Yall.get() + c0 * zs, zs,
+                                                                                pall.get() + c0 * ps, ps, nullptr, nullptr);
+                } else {
+                    for (int c = 0; c < NCOL; ++c)
+                        k_coarse_restrict<D><<<(unsigned)C.nchunk, 256, 0, s>>>(V, Yall.get() + c * zs, pall.get() + c * ps);
+                }
+                CR_CHECK_LAUNCH();
+            }
+            k_coarse_gather_all<D><<<grid_for(C.nE * NCOL, T), T, 0, s>>>(V, pall.get(), ps, call.get());
+            CR_CHECK_LAUNCH();
+            h->comm->impl->allreduce(call.get(), (int)(C.nE * NCOL), false, s);
+            if (dense) {
+                for (int k = 0; k < D; ++k)
+                    for (int l = 0; l < D; ++l)
+                        k_coarse_scatterE<D><<<grid_for(C.nE, T), T, 0, s>>>(C.nE, H, colour, k, l,
+                                                                             call.get() + (k * D + l) * C.nE, C.Einv.get());
+            } else {
+                k_coarse_scatterEs_all<D><<<grid_for(C.nE * NCOL, T), T, 0, s>>>(C.nE, H, colour, call.get(), Es.get());
+            }
+            CR_CHECK_LAUNCH();
+        }
+    }
     tr.mark("coarse: E = Z^t G Z");
     if (dense) {
         k_symmetrize<<<grid_for(C.nE * C.nE, T, 64), T, 0, s>>>(C.Einv.get(), C.nE);
@@ -1710,7 +1956,7 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const std::function<void(const
     C.built = H;
 }
 
-void build_coarse(cr_hybrid_s *h, int H, const std::function<void(const double *, double *, int)> &applyG,
+void build_coarse(cr_hybrid_s *h, int H, const ApplyG &applyG,
                   cudaStream_t s) {
     CR_REQUIRE(H >= 1 && H <= 256, CR_ERR_INVALID_ARG, "coarse grid intervals must be in [1, 256]");
     const int D = h->G.d;

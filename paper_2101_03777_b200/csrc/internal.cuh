@@ -330,8 +330,10 @@ void assemble_coupled(cr_coupled_s *c, const cr_mesh_s *m, const cr_params &prm,
 void spmv(const BlockEll &G, const double *x, double *y, cudaStream_t s);
 // recover.cu
 void recover(const cr_hybrid_s *h, const double *W, double *U, double *P, double *diag, cudaStream_t s);
-void newton_update(int64_t nU, double *U, const double *dU, int64_t nP, double *P, const double *dP, double *norms,
-                   cudaStream_t s);
+void newton_update(int64_t nU, double *U, const double *dU, int64_t nP, double *P, const double *dP, double lam,
+                   double *norms, cudaStream_t s);
+// refine.cu: ||a||_2 of a device vector (fixed-order block partials: deterministic), host result
+double norm2(const double *a, int64_t n, cudaStream_t s);
 // solve.cu
 void solve(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep);
 // one solve of G W = rhs (rhs NULL: S) with the fp64 solvers (solve.cu)
@@ -349,8 +351,10 @@ void build_afw(cr_hybrid_s *h, int mode, cudaStream_t s);
 // mf.cu
 void build_mf(cr_hybrid_s *h, cudaStream_t s);
 // coarse.cu
-// applyG(z, Y, colour): Y = G z, z a colour sum of coarse columns (colour < 0: any z)
-void build_coarse(cr_hybrid_s *h, int H, const std::function<void(const double *, double *, int)> &applyG,
+// applyG(z, Y, colour, ncol, stride): Y_c = G z_c for the ncol vectors z_c = z + c stride, each a
+// colour sum of coarse columns (colour < 0: any z; Y arrives zero on the rows G z can reach)
+using ApplyG = std::function<void(const double *, double *, int, int, int64_t)>;
+void build_coarse(cr_hybrid_s *h, int H, const ApplyG &applyG,
                   cudaStream_t s);
 void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double *partials, unsigned *ticket,
                            cudaStream_t s);

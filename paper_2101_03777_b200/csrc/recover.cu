@@ -199,18 +199,18 @@ void recover(const cr_hybrid_s *h, const double *W, double *U, double *P, double
 
 // Newton update: U += dU, P += dP, per-block partials of |dU|^2 and |U + dU|^2
 __global__ void __launch_bounds__(256) k_newton_update(int64_t nU, double *U, const double *dU, int64_t nP, double *P,
-                                                       const double *dP, double *part) {
+                                                       const double *dP, double lam, double *part) {
     __shared__ double s0[256], s1[256];
     double a = 0.0, b = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nU; i += (int64_t)gridDim.x * blockDim.x) {
-        const double d = dU[i], u = U[i] + d;
+        const double d = lam * dU[i], u = U[i] + d;
         U[i] = u;
         a = fma(d, d, a);
         b = fma(u, u, b);
     }
     if (dP)
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nP; i += (int64_t)gridDim.x * blockDim.x)
-            P[i] += dP[i];
+            P[i] += lam * dP[i];
     s0[threadIdx.x] = a;
     s1[threadIdx.x] = b;
     __syncthreads();
@@ -227,12 +227,12 @@ __global__ void __launch_bounds__(256) k_newton_update(int64_t nU, double *U, co
     }
 }
 
-void newton_update(int64_t nU, double *U, const double *dU, int64_t nP, double *P, const double *dP, double *norms,
-                   cudaStream_t s) {
+void newton_update(int64_t nU, double *U, const double *dU, int64_t nP, double *P, const double *dP, double lam,
+                   double *norms, cudaStream_t s) {
     const int G = num_sms() * 4;
     DevBuf<double> part;
     part.alloc(2 * G, s);
-    k_newton_update<<<G, 256, 0, s>>>(nU, U, dU, nP, P, dP, part.get());
+    k_newton_update<<<G, 256, 0, s>>>(nU, U, dU, nP, P, dP, lam, part.get());
     CR_CHECK_LAUNCH();
     std::vector<double> h(2 * G);
     CR_CUDA(cudaMemcpyAsync(h.data(), part.get(), 2 * G * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -128,7 +128,7 @@ __global__ void k_axpy1(int64_t n, double *y, const double *x) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) y[i] += x[i];
 }
 
-static double norm2_dev(const double *a, int64_t n, cudaStream_t s) {
+double norm2(const double *a, int64_t n, cudaStream_t s) {
     const int G = num_sms() * 4;
     DevBuf<double> part;
     part.alloc(G, s);
@@ -168,8 +168,8 @@ void residual_dd(cr_hybrid_s *h, bool mf, const double *W, double *r, double *rn
     if (h->G.d == 2) residual_dd_t<2>(h, mf, W, r, s);
     else residual_dd_t<3>(h, mf, W, r, s);
     const int64_t N = h->G.nrows * h->G.d;
-    *rnorm = norm2_dev(r, N, s);
-    *snorm = norm2_dev(h->S.get(), N, s);
+    *rnorm = norm2(r, N, s);
+    *snorm = norm2(h->S.get(), N, s);
 }
 
 // cr_solve: the fp64 solvers (solve.cu), plus the refinement of the parity mode

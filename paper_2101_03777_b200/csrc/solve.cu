@@ -324,6 +324,40 @@ __global__ void __launch_bounds__(kT, D == 2 ? 3 : 2) k_mf_spmv_slices(MfView M,
     }
 }
 
+// the same for ncol right-hand sides x + c xs -> q + c xs (coarse setup: the D^2 columns of a colour);
+// the cell's factors are loaded once for all of them
+template <int D>
+__global__ void __launch_bounds__(kT, D == 2 ? 3 : 2) k_mf_spmv_slices_all(MfView M, const int32_t *slices, const int64_t *nact,
+                                                           const double *x, double *q, int64_t xs, int ncol, int64_t nown) {
+    using LY = MfLayout<D>;
+    constexpr int NF = LY::NF, NT = LY::NT;
+    const int64_t n = *nact * 32;
+    GRID_STRIDE(t, n) {
+        const int64_t tt = (int64_t)slices[t >> 5] * 32 + (t & 31);
+        const int64_t slice = tt >> 5;
+        const int lane = (int)(tt & 31);
+        const int32_t *ip = M.ids + slice * (NF * 32) + lane;
+        const double *vp = M.v + slice * ((int64_t)LY::NE * 32) + lane;
+        int id[NF];
+        unsigned nbc[NF];
+#pragma unroll
+        for (int l = 0; l < NF; ++l) {
+            id[l] = ip[l * 32];
+            nbc[l] = M.nb[slice * (NF * 32) + l * 32 + lane];
+        }
+        const unsigned sg = M.sg[tt];
+        const double c = vp[0];
+        double T[NT], u[D][NF];
+#pragma unroll
+        for (int e = 0; e < NT; ++e) T[e] = vp[(1 + e) * 32];
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int l = 0; l < NF; ++l) u[i][l] = vp[(1 + NT + i * NF + l) * 32];
+        for (int col = 0; col < ncol; ++col) mf_cell_core<D>(id, sg, c, T, u, nbc, lane, x + col * xs, q + col * xs, nown);
+    }
+}
+
 // r = b - q, |r|^2 (FIN_RR)
 __global__ void __launch_bounds__(kT) k_resid_vec(int64_t N, const double *b, const double *q, double *r, KState *st,
                                                   double *partials, int dist) {
@@ -643,7 +677,7 @@ enum { AFW_PCG_INIT = 0, AFW_PCG = 1, AFW_MINRES_INIT = 2, AFW_MINRES = 3, AFW_P
 
 // zs (per face slot) = patch contributions of M^{-1} r
 template <int D, int SLOTS, int KMAX, bool SYM, int WHAT>
-__global__ void __launch_bounds__(kT, 4) k_afw_apply(AfwView A, const double *r, double *zs, double rtol, KState *st,
+__global__ void __launch_bounds__(kT, 5) k_afw_apply(AfwView A, const double *r, double *zs, double rtol, KState *st,
                                                   double *partials, int dist) {
     if (WHAT != AFW_PCG_INIT && WHAT != AFW_MINRES_INIT && WHAT != AFW_PCG2_INIT && st->flag != FLAG_RUN) return;
     double acc[1] = {0.0};
@@ -1553,8 +1587,8 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         DevBuf<int64_t> snum;
         DevBuf<uint8_t> stmp;
         int last_colour = -1;
-        build_coarse(h, H, [&](const double *z, double *Y, int colour) {
-            L.halo(s, const_cast<double *>(z));
+        build_coarse(h, H, [&](const double *z, double *Y, int colour, int ncol, int64_t stride) {
+            for (int c = 0; c < ncol; ++c) L.halo(s, const_cast<double *>(z) + c * stride);
             if (L.mf && colour >= 0 && !L.dist) {
                 const int64_t nsl = h->mf.ncells / 32;
                 if (colour != last_colour) {
@@ -1576,13 +1610,19 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                     last_colour = colour;
                 }
                 // Y arrives zero (build_coarse clears the rows it touched after each pass)
-                k_mf_spmv_slices<D><<<occ_grid(k_mf_spmv_slices<D>, kT, h->mf.ncells), kT, 0, s>>>(
-                    mf_view<D>(h), slist.get(), snum.get(), z, Y, L.nrows);
+                if (ncol == 1) {
+                    k_mf_spmv_slices<D><<<occ_grid(k_mf_spmv_slices<D>, kT, h->mf.ncells), kT, 0, s>>>(
+                        mf_view<D>(h), slist.get(), snum.get(), z, Y, L.nrows);
+                } else {
+                    k_mf_spmv_slices_all<D><<<occ_grid(k_mf_spmv_slices_all<D>, kT, h->mf.ncells), kT, 0, s>>>(
+                        mf_view<D>(h), slist.get(), snum.get(), z, Y, stride, ncol, L.nrows);
+                }
                 CR_CHECK_LAUNCH();
-            } else if (L.mf) {
-                mf_apply<D, false>(L, s, z, Y, 0.0);
             } else {
-                spmv(h->G, z, Y, s);
+                for (int c = 0; c < ncol; ++c) {
+                    if (L.mf) mf_apply<D, false>(L, s, z + c * stride, Y + c * stride, 0.0);
+                    else spmv(h->G, z + c * stride, Y + c * stride, s);
+                }
             }
         }, s);
         trc.mark("coarse space (E, E^-1)");
@@ -1904,7 +1944,9 @@ static void apply_precond_t(cr_hybrid_s *h, int method, const double *r, double 
             build_afw(h, AFW_SPD, s);
             // the coarse grid of the last two-level solve, else the default
             const int Hc = h->coarse.requested > 0 ? h->coarse.requested : (D == 2 ? 64 : 16);
-            build_coarse(h, Hc, [&](const double *zz, double *Y, int) { spmv(h->G, zz, Y, s); }, s);
+            build_coarse(h, Hc, [&](const double *zz, double *Y, int, int ncol, int64_t stride) {
+                for (int c = 0; c < ncol; ++c) spmv(h->G, zz + c * stride, Y + c * stride, s);
+            }, s);
             if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
             CR_CUDA(cudaMemsetAsync(w->st.get(), 0, sizeof(KState), s));
             coarse_restrict_solve(h, r, &w->st.get()->qc, w->partials.get(), &w->st.get()->tickets[4], s);

@@ -60,7 +60,10 @@ def test_invalid_arguments_fail_cleanly_without_gpu(lib):
 def test_new_entry_points_validate_arguments_without_gpu(lib):
     lib.cr_last_error.restype = ctypes.c_char_p
     lib.cr_newton_update.restype = ctypes.c_int
-    assert lib.cr_newton_update(ctypes.c_int64(-1), None, None, ctypes.c_int64(0), None, None, None, None) == -1
+    assert lib.cr_newton_update(ctypes.c_int64(-1), None, None, ctypes.c_int64(0), None, None, ctypes.c_double(1.0),
+                                None, None) == -1
+    lib.cr_coupled_rhs_norm.restype = ctypes.c_int
+    assert lib.cr_coupled_rhs_norm(None, None, None, None, None) == -1
     lib.cr_hybrid_method_host.restype = ctypes.c_int
     assert lib.cr_hybrid_method_host(ctypes.c_int32(2), ctypes.c_int64(3), None, ctypes.c_int64(1), None,
                                      None, None, None, None, None, None, None, None, None, None) == -1

@@ -608,3 +608,22 @@ def test_sparse_direct_hybrid_and_coupled(n):
     nU = 3 * mo.nf_int
     assert relL2(x[:nU].reshape(-1, 3), ho["U"]) <= 1e-8
     assert relL2(np.insert(x[nU:], 0, 0.0), ho["P"]) <= 1e-8
+
+
+def test_damped_newton_re1000_matches_oracle():
+    """The paper's steady lid-driven cavity at Re = 1000 (Table 7 right) by Armijo-damped
+    Newton from rest: the GPU iteration (cr_coupled_rhs_norm line search, cr_newton_update with the
+    step length, CR_DC_FGMRES linear solves) takes the oracle's steps and reaches its solution."""
+    n, nu = 16, 1e-3
+    coords, cells = ci.square_mesh(n, 0.0, 4)
+    mo = O.build_mesh(coords, cells)
+    wall = ci.lid_dirichlet_2d(coords, cells)
+    f = np.zeros((mo.nc, 2))
+    Uo, Po, ho = O.newton_ns(mo, O.Params(mu=0.0, nu=nu, physics="ns_step"), f, wall, tol=1e-10, damped=True,
+                             max_newton=40)
+    out = P.newton_ns(tg(coords), tg(cells), nu, tg(f), tg(wall), tol=1e-10, damped=True, max_newton=40, mis_seed=11,
+                      rtol=1e-12)
+    assert abs(len(out["history"]) - len(ho)) <= 1, (out["history"], ho)
+    assert out["history"][-1] <= 1e-10
+    assert relL2(out["U"].cpu().numpy(), Uo) <= 1e-8
+    assert relL2(out["P"].cpu().numpy(), Po) <= 1e-8

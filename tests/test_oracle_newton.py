@@ -43,3 +43,23 @@ def test_converged_velocity_is_divergence_free():
     Uc = O.cell_face_values(m, U, wall)
     div = np.einsum("kli,kli->k", m.a, Uc)
     assert np.abs(div).max() <= 1e-12 * np.abs(m.a).max()
+
+
+def test_damped_newton_reaches_the_re1000_cavity():
+    """P:L783-799 (Table 7 right: lid-driven cavity, Re = 1000, Newton tolerance 5e-7): full
+    Newton steps from rest do not converge on this mesh (n = 16), the Armijo-damped iteration does,
+    ends with full steps and quadratic decay, and its limit satisfies the discrete equations: the
+    nonlinear residual ||F|| at the limit is at rounding level and U is divergence-free per cell."""
+    m, wall, f = _cavity(16)
+    prm = O.Params(mu=0.0, nu=1e-3, physics="ns_step")
+    _, _, h_full = O.newton_ns(m, prm, f, wall, max_newton=25, tol=5e-7)
+    assert h_full[-1] > 1e-3                       # undamped: no convergence in 25 steps
+    U, P, h = O.newton_ns(m, prm, f, wall, max_newton=40, tol=5e-7, damped=True)
+    assert h[-1] <= 5e-7 and len(h) <= 25, h
+    assert h[-2] <= 1e-2 and h[-1] <= 10 * h[-2] ** 2, h  # final steps are full Newton steps
+    from oracle.newton import residual_norm
+    r = residual_norm(m, prm, f, wall, U, P)
+    r0 = residual_norm(m, prm, f, wall, 0 * U, 0 * P)
+    assert r <= 1e-9 * r0, (r, r0)
+    Uc = O.cell_face_values(m, U, wall)
+    assert np.abs(np.einsum("kli,kli->k", m.a, Uc)).max() <= 1e-12 * np.abs(m.a).max()
