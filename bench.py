@@ -310,9 +310,10 @@ def time_stepping(P, cfg, coords, cells, fbar, stream, nsteps=5):
             "note": "step 1 includes the preconditioner / coarse-space setup; later steps reuse them"}
 
 
-def newton_cavity(P, ci, dev, stream, n=256, nu=0.01, tol=5e-7):
+def newton_cavity(P, ci, dev, stream, n=256, nu=0.01, tol=5e-7, damped=False):
     """Steady lid-driven cavity (Re = 1/nu) by Newton's method (tolerance of P:L783-799
-    Table 7), each step through the hybrid path (NS step + CR_DC_FGMRES)."""
+    Table 7), each step through the hybrid path (NS step + CR_DC_FGMRES); damped: Armijo line search
+    on the nonlinear residual (Re = 1000 from rest, the paper's case)."""
     import torch
     coords, cells = ci.square_mesh(n, 0.0, 4)
     wall = ci.lid_dirichlet_2d(coords, cells)
@@ -321,11 +322,13 @@ def newton_cavity(P, ci, dev, stream, n=256, nu=0.01, tol=5e-7):
     torch.cuda.synchronize()
     a = _ev(torch, stream)
     out = P.newton_ns(tg(coords), tg(cells), nu, f, tg(wall), tol=tol, mis_seed=44, coarse=32, mu_inner=0.5,
-                      inner_rtol=1e-7)
+                      inner_rtol=1e-7, damped=damped, max_newton=40, restart=100, max_iter=2000)
     b = _ev(torch, stream)
     torch.cuda.synchronize()
-    return {"workload": f"2D lid-driven cavity n={n} Re={1 / nu:g}, Newton to ||dU|| <= {tol:g} ||U||",
-            "newton_steps": len(out["history"]), "history": out["history"], "total_s": a.elapsed_time(b) * 1e-3,
+    return {"workload": f"2D lid-driven cavity n={n} Re={1 / nu:g}, {'damped ' if damped else ''}Newton from rest "
+                        f"to ||dU|| <= {tol:g} ||U||",
+            "newton_steps": len(out["history"]), "converged": bool(out["history"][-1] <= tol),
+            "history": out["history"], "step_lengths": out["step_lengths"], "total_s": a.elapsed_time(b) * 1e-3,
             "outer_iterations": [r["iterations"] for r in out["reports"]],
             "inner_iterations": [r["inner_iterations"] for r in out["reports"]]}
 
@@ -622,7 +625,9 @@ def main():
         i1 = ci.make_inputs(c1)
         tg = lambda a: torch.from_numpy(a).to(dev)
         tstep = time_stepping(P, c1, tg(i1["coords"]), tg(i1["cells"]), tg(i1["fbar"]), stream)
-        newton = newton_cavity(P, ci, dev, stream)
+        newton = {"re100": newton_cavity(P, ci, dev, stream),
+                  # the paper's Table 7 case (Re = 1000) from rest, Armijo-damped
+                  "re1000": newton_cavity(P, ci, dev, stream, n=64, nu=1e-3, damped=True)}
         table4 = direct_table4(P, ci, dev, stream)
 
     cpu = None

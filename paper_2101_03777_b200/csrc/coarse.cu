@@ -116,7 +116,8 @@ __global__ void k_coarse_interior(const int32_t *dof_face, const int32_t *face_c
 // (fixed trees: deterministic).
 template <int D>
 __global__ void __launch_bounds__(256) k_coarse_restrict(CoarseView C, const double *r, double *part,
-                                                         const int32_t *list = nullptr, const int64_t *ends = nullptr) {
+                                                         const int32_t *list = nullptr, const int64_t *ends = nullptr,
+                                                         int64_t rrs = D, double *clear_base = nullptr) {
     constexpr int NN = 1 << D, DD = D * D, NV = NN * DD;
     constexpr int TPR = 1;                           // threads per row
     constexpr int NA = NV;                           // accumulators per thread
@@ -143,8 +144,15 @@ __global__ void __launch_bounds__(256) k_coarse_restrict(CoarseView C, const dou
                 const bool ok = row[u] >= 0;
                 xv[u][i] = ok ? C.fx[row[u] * D + i] : 0.f;
                 av[u][i] = ok ? C.fa[row[u] * D + i] : 0.f;
-                rv[u][i] = ok ? r[row[u] * D + i] : 0.0;
+                rv[u][i] = ok ? r[row[u] * rrs + i] : 0.0;
             }
+        if (clear_base)   // setup: zero the rows read (interleaved, full-sector stores)
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (row[u] >= 0) {
+                    double2 *z2 = reinterpret_cast<double2 *>(clear_base + row[u] * rrs);
+                    for (int q = 0; q < (int)(rrs >> 1); ++q) z2[q] = make_double2(0.0, 0.0);
+                }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             int ic[D];
@@ -518,12 +526,14 @@ __global__ void k_coarse_colour_all(CoarseView C, int64_t nrows, int colour, dou
     }
 }
 
-// k_coarse_restrict3 for NC columns at once (column c at r + c * rs, partials at part + c * ps): the
-// row data (perm, centroid, area vector) is read once for all NC columns
+// k_coarse_restrict3 for NC columns at once (entry (row, c, i) at r[c rs + row rrs + i], partials at
+// part + c ps): the row data (perm, centroid, area vector) is read once for all NC columns;
+// clear_base: zero the rows read (setup)
 template <int NC>
 __global__ void __launch_bounds__(256, 2) k_coarse_restrict3m(CoarseView C, const double *r, int64_t rs, double *part,
-                                                           int64_t ps, const int32_t *list, const int64_t *ends) {
-    constexpr int D = 3, DD = 9, NV = 72, U = 2;
+                                                           int64_t ps, const int32_t *list, const int64_t *ends,
+                                                           int64_t rrs = 3, double *clear_base = nullptr) {
+    constexpr int D = 3, DD = 9, NV = 72, U = 1;
     const int64_t ch = list ? (int64_t)list[blockIdx.x] : (int64_t)blockIdx.x;
     const int64_t b = C.chunk_start[ch], e = ends ? ends[blockIdx.x] : C.chunk_start[ch + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -546,10 +556,16 @@ __global__ void __launch_bounds__(256, 2) k_coarse_restrict3m(CoarseView C, cons
                 xv[i] = row >= 0 ? C.fx[row * D + i] : 0.f;
                 av[u][i] = row >= 0 ? C.fa[row * D + i] : 0.f;
 #pragma unroll
-                for (int c = 0; c < NC; ++c) rv[u][c][i] = row >= 0 ? r[c * rs + row * D + i] : 0.0;
+                for (int c = 0; c < NC; ++c) rv[u][c][i] = row >= 0 ? r[c * rs + row * rrs + i] : 0.0;
             }
             int ic[D];
             coarse_locate<D>(C.g, xv, ic, xi[u]);
+            // interleaved setup rows (rrs doubles, 256-byte aligned): the last launch zeroes the whole row
+            // with full-sector stores (the next colour's G application accumulates into 0)
+            if (clear_base && row >= 0) {
+                double2 *z2 = reinterpret_cast<double2 *>(clear_base + row * rrs);
+                for (int q = 0; q < (int)(rrs >> 1); ++q) z2[q] = make_double2(0.0, 0.0);
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -980,6 +996,34 @@ __global__ void k_nd_transpose(const NdFrontDev *fr, const int64_t *pre, int nf,
 }
 
 
+// solve layouts (NdFrontDev fs / wts / ws) from the factorisation's Finv (ld ldFi) and column-major W
+// (ld ldW); kind 0: Finv rows, 1: W rows, 2: W columns; padding entries 0
+__global__ void k_nd_relayout(const NdFrontDev *fr, const int64_t *pre, int nf, int kind, const double *Finv,
+                              const double *W, double *out) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < pre[nf]; t += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nf - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pre[mid] <= t) lo = mid;
+            else hi = mid - 1;
+        }
+        const NdFrontDev F = fr[lo];
+        const int64_t e = t - pre[lo];
+        double v = 0.0;
+        if (kind == 0) {            // row i, column j of Finv
+            const int i = (int)(e / F.ldFs), j = (int)(e % F.ldFs);
+            if (j < F.nI) v = Finv[F.finv + (int64_t)i * F.ldFi + j];
+        } else if (kind == 1) {     // row b of W (over pivots i)
+            const int b = (int)(e / F.ldWts), i = (int)(e % F.ldWts);
+            if (i < F.nI) v = W[F.w + b + (int64_t)i * F.ldW];
+        } else {                    // column i of W (over B rows b)
+            const int i = (int)(e / F.ldWs), b = (int)(e % F.ldWs);
+            if (b < F.nB) v = W[F.w + b + (int64_t)i * F.ldW];
+        }
+        out[t] = v;
+    }
+}
+
 // software grid barrier (all CTAs of the launch are co-resident: grid <= one wave).  Polls with
 // gpu-scope acquire loads (a volatile load is a system-scope strong load: far slower).
 __device__ __forceinline__ unsigned nd_ld_acquire(const unsigned *p) {
@@ -1059,6 +1103,30 @@ __device__ __forceinline__ double nd_dot_lane_g(const double *__restrict__ a, co
     return (s0 + s1) + (s2 + s3);
 }
 
+// 16-byte variant of nd_dot_lane_g (a 16-byte aligned; n may be odd: the tail element by lane 0)
+__device__ __forceinline__ double nd_dot_lane2_g(const double *__restrict__ a, const double *x, const int32_t *idx, int n,
+                                                 int lane) {
+    const double2 *a2 = reinterpret_cast<const double2 *>(a);
+    const int n2 = n >> 1;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int i = lane;
+    for (; i + 32 < n2; i += 64) {
+        const double2 a0 = a2[i], a1 = a2[i + 32];
+        const int j0 = idx[2 * i], j1 = idx[2 * i + 1], j2 = idx[2 * i + 64], j3 = idx[2 * i + 65];
+        s0 = fma(a0.x, __ldcg(x + j0), s0);
+        s1 = fma(a0.y, __ldcg(x + j1), s1);
+        s2 = fma(a1.x, __ldcg(x + j2), s2);
+        s3 = fma(a1.y, __ldcg(x + j3), s3);
+    }
+    for (; i < n2; i += 32) {
+        const double2 a0 = a2[i];
+        s0 = fma(a0.x, __ldcg(x + idx[2 * i]), s0);
+        s1 = fma(a0.y, __ldcg(x + idx[2 * i + 1]), s1);
+    }
+    if ((n & 1) && lane == 0) s2 = fma(a[n - 1], __ldcg(x + idx[n - 1]), s2);
+    return (s0 + s1) + (s2 + s3);
+}
+
 constexpr int kNdMaxLev = 48;
 struct NdSched {
     int nlev;
@@ -1101,7 +1169,7 @@ __global__ void __launch_bounds__(256) k_nd_solve(NdSolveView V, NdSched S, cons
             for (int64_t k = S.boff[L] + gw; k < S.boff[L + 1]; k += nw) {
                 const int2 e = V.lbr[k];
                 const NdFrontDev F = V.fr[e.x];
-                const double a = warp_sum(nd_dot_lane(V.wt + F.wt + (int64_t)e.y * F.nI, V.bi + F.bi, F.nI, lane));
+                const double a = warp_sum(nd_dot_lane2(V.wt + F.wts + (int64_t)e.y * F.ldWts, V.bi + F.bi, F.ldWts, lane));
                 if (lane == 0) V.u[F.u + e.y] = __ldcg(V.lb + F.lb + e.y) - a;
             }
             nd_grid_barrier(bar);
@@ -1111,8 +1179,8 @@ __global__ void __launch_bounds__(256) k_nd_solve(NdSolveView V, NdSched S, cons
         for (int64_t k = S.coff[L] + gw; k < S.coff[L + 1]; k += nw) {
             const int2 e = V.lc[k];
             const NdFrontDev F = V.fr[e.x];
-            const double pa = nd_dot_lane(V.finv + F.finv + (int64_t)e.y * F.ldFi, V.bi + F.bi, F.nI, lane);
-            const double pb = nd_dot_lane_g(V.w + F.w + (int64_t)e.y * F.ldW, y, V.uidx + F.uoff + F.nI, F.nB, lane);
+            const double pa = nd_dot_lane2(V.finv + F.fs + (int64_t)e.y * F.ldFs, V.bi + F.bi, F.ldFs, lane);
+            const double pb = nd_dot_lane2_g(V.w + F.ws + (int64_t)e.y * F.ldWs, y, V.uidx + F.uoff + F.nI, F.nB, lane);
             const double a = warp_sum(pa - pb);
             if (lane == 0) y[V.uidx[F.uoff + e.y]] = a;
         }
@@ -1144,13 +1212,13 @@ __global__ void __launch_bounds__(256) k_nd_phase(NdSolveView V, int kind, int64
         if (kind == 1) {
             const int2 e = V.lbr[k];
             const NdFrontDev F = V.fr[e.x];
-            const double a = warp_sum(nd_dot(V.wt + F.wt + (int64_t)e.y * F.nI, V.bi + F.bi, F.nI, lane));
+            const double a = warp_sum(nd_dot_lane2(V.wt + F.wts + (int64_t)e.y * F.ldWts, V.bi + F.bi, F.ldWts, lane));
             if (lane == 0) V.u[F.u + e.y] = V.lb[F.lb + e.y] - a;
         } else {
             const int2 e = V.lc[k];
             const NdFrontDev F = V.fr[e.x];
-            const double pa = nd_dot(V.finv + F.finv + (int64_t)e.y * F.ldFi, V.bi + F.bi, F.nI, lane);
-            const double pb = nd_dot_lane_g(V.w + F.w + (int64_t)e.y * F.ldW, y, V.uidx + F.uoff + F.nI, F.nB, lane);
+            const double pa = nd_dot_lane2(V.finv + F.fs + (int64_t)e.y * F.ldFs, V.bi + F.bi, F.ldFs, lane);
+            const double pb = nd_dot_lane2_g(V.w + F.ws + (int64_t)e.y * F.ldWs, y, V.uidx + F.uoff + F.nI, F.nB, lane);
             const double a = warp_sum(pa - pb);
             if (lane == 0) y[V.uidx[F.uoff + e.y]] = a;
         }
@@ -1283,7 +1351,7 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
         x.finv = ofi; ofi += (int64_t)nIp[f] * nIp[f];
         x.w = ow; ow += (int64_t)nBp[f] * nIp[f];
         x.wt = owt; owt += (int64_t)x.nB * x.nI;
-        x.bi = obi; obi += x.nI;
+        x.bi = obi; obi += (x.nI + 1) & ~1;   // even: 16-byte aligned, zero pad entry
         x.u = ou; ou += x.nB;
         x.lb = olb; olb += x.nB;
         x.inv = oinv; oinv += x.nI + x.nB;
@@ -1340,8 +1408,8 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
     N.finv.alloc(std::max<int64_t>(ofi, 1), s);
     N.w.alloc(std::max<int64_t>(ow, 1), s);
     N.w.zero(s);
-    N.wt.alloc(std::max<int64_t>(owt, 1), s);
-    N.bi.alloc(std::max<int64_t>(obi, 1), s);
+    N.bi.alloc(std::max<int64_t>(obi, 2), s);
+    N.bi.zero(s);   // pad entries stay 0 (the 16-byte dot products read them)
     N.u.alloc(std::max<int64_t>(ou, 1), s);
     N.m = M;
     N.maxdepth = maxd;
@@ -1491,17 +1559,38 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
         CR_CUDA(cudaStreamSynchronize(s));
         for (int v : hinfo) CR_REQUIRE(v == 0, CR_ERR_SINGULAR_LOCAL, "coarse ND front is not positive definite");
     }
-    // W^t (nI x nB, ld nI) for the forward pass: a warp per B row then reads contiguously
+    // solve layouts: rows 16-byte aligned with even leading dimensions and zero padding, so every
+    // dot product of the solve streams double2 (the odd D^2 = 9 unknowns per node made nI, nB odd)
     {
-        std::vector<int64_t> pre(nf + 1, 0);
-        for (int f = 0; f < nf; ++f) pre[f + 1] = pre[f] + (int64_t)fr[f].nB * fr[f].nI;
-        DevBuf<int64_t> dpre;
-        upload(dpre, pre, s);
-        if (pre[nf] > 0) {
-            k_nd_transpose<<<grid_for(pre[nf], T, 16), T, 0, s>>>(N.fr.get(), dpre.get(), nf, N.w.get(), N.wt.get());
-            CR_CHECK_LAUNCH();
+        auto ev = [](int64_t v) { return (v + 1) & ~(int64_t)1; };
+        int64_t ofs = 0, owts = 0, ows = 0;
+        std::vector<int64_t> pf(nf + 1, 0), pwt(nf + 1, 0), pw(nf + 1, 0);
+        for (int f = 0; f < nf; ++f) {
+            NdFrontDev &x = fr[f];
+            x.ldFs = (int32_t)ev(x.nI);
+            x.ldWts = (int32_t)ev(x.nI);
+            x.ldWs = (int32_t)std::max<int64_t>(ev(x.nB), 2);
+            x.fs = ofs; ofs += (int64_t)x.nI * x.ldFs;
+            x.wts = owts; owts += (int64_t)x.nB * x.ldWts;
+            x.ws = ows; ows += (int64_t)x.nI * x.ldWs;
+            pf[f + 1] = ofs; pwt[f + 1] = owts; pw[f + 1] = ows;
         }
+        upload(N.fr, fr, s);
+        N.fs.alloc(std::max<int64_t>(ofs, 2), s);
+        N.wts.alloc(std::max<int64_t>(owts, 2), s);
+        N.ws.alloc(std::max<int64_t>(ows, 2), s);
+        DevBuf<int64_t> dpf, dpwt, dpw;
+        upload(dpf, pf, s);
+        upload(dpwt, pwt, s);
+        upload(dpw, pw, s);
+        if (ofs) k_nd_relayout<<<grid_for(ofs, T, 16), T, 0, s>>>(N.fr.get(), dpf.get(), nf, 0, N.finv.get(), N.w.get(), N.fs.get());
+        if (owts) k_nd_relayout<<<grid_for(owts, T, 16), T, 0, s>>>(N.fr.get(), dpwt.get(), nf, 1, N.finv.get(), N.w.get(), N.wts.get());
+        if (ows) k_nd_relayout<<<grid_for(ows, T, 16), T, 0, s>>>(N.fr.get(), dpw.get(), nf, 2, N.finv.get(), N.w.get(), N.ws.get());
+        CR_CHECK_LAUNCH();
         CR_CUDA(cudaStreamSynchronize(s));
+        N.finv.release();
+        N.w.release();
+        N.wt.release();
     }
     N.on = true;
 }
@@ -1510,7 +1599,7 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
 static void nd_solve(const CoarseOp &C, const double *c, double *y, double *qout, double *partials, unsigned *ticket,
                      cudaStream_t s) {
     const CoarseNd &N = C.nd;
-    NdSolveView V{N.fr.get(), N.invp.get(), N.invl.get(), N.uidx.get(), N.finv.get(), N.w.get(), N.wt.get(),
+    NdSolveView V{N.fr.get(), N.invp.get(), N.invl.get(), N.uidx.get(), N.fs.get(), N.ws.get(), N.wts.get(),
                   const_cast<double *>(N.bi.get()), const_cast<double *>(N.lb.get()), const_cast<double *>(N.u.get()),
                   N.la.get(), N.lbr.get(), N.lc.get()};
     NdSched S;
@@ -1669,7 +1758,7 @@ static bool lapack_potrf_batched(int n, int lda, int nb, double **A, int *info, 
 }
 
 template <int D>
-static void build_coarse_t(cr_hybrid_s *h, int H, const ApplyG &applyG, cudaStream_t s) {
+static void build_coarse_t(cr_hybrid_s *h, int H, const ApplyG &applyG, const ApplyGColour &applyGc, cudaStream_t s) {
     constexpr int NN = 1 << D, NV = NN * D * D;
     const cr_mesh_s *m = h->mesh;
     CoarseOp &C = h->coarse;
@@ -1856,9 +1945,14 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const ApplyG &applyG, cudaStre
         constexpr int NCOL = D * D;
         const int64_t zs = Nalloc;
         DevBuf<double> zall, Yall, pall, call;
-        zall.alloc((size_t)NCOL * zs, s);
-        Yall.alloc((size_t)NCOL * zs, s);
-        zall.zero(s);
+        if (!applyGc) {
+            zall.alloc((size_t)NCOL * zs, s);
+            zall.zero(s);
+        }
+        // interleaved rows padded to a multiple of 256 bytes (D^3 = 27 -> 32 doubles, 8 -> 8): whole
+        // sectors when a row is cleared
+        const int64_t YRS = D == 3 ? 32 : 8;
+        Yall.alloc(applyGc ? (size_t)YRS * (zs / D) : (size_t)NCOL * zs, s);
         Yall.zero(s);
         const int64_t ps = C.nchunk * NV;
         pall.alloc((size_t)NCOL * ps, s);
@@ -1866,28 +1960,37 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const ApplyG &applyG, cudaStre
         for (int colour = 0; colour < ncol; ++colour) {
             const unsigned nsup = (unsigned)(osup[colour + 1] - osup[colour]);
             const unsigned nact = (unsigned)(oact[colour + 1] - oact[colour]);
-            if (nsup) k_coarse_colour_chunks_all<D><<<nsup, 256, 0, s>>>(V, dsup.get() + osup[colour], colour, 0, zall.get(), zs);
-            CR_CHECK_LAUNCH();
-            applyG(zall.get(), Yall.get(), colour, NCOL, zs);
+            if (applyGc) {   // G applied to the colour's columns without materialising them (Y interleaved)
+                applyGc(colour, Yall.get(), YRS);
+            } else {
+                if (nsup)
+                    k_coarse_colour_chunks_all<D><<<nsup, 256, 0, s>>>(V, dsup.get() + osup[colour], colour, 0, zall.get(), zs);
+                CR_CHECK_LAUNCH();
+                applyG(zall.get(), Yall.get(), colour, NCOL, zs);
+            }
             pall.zero(s);
             if (nact) {
+                // entry (row, column c, component i): interleaved rows of YRS doubles (applyGc; the last
+                // restriction launch zeroes the rows it read) or column vectors (stride zs)
+                const int64_t cstr = applyGc ? D : zs, rstr = applyGc ? YRS : D;
                 if (D == 3) {
                     for (int c0 = 0; c0 < NCOL; c0 += 3)
-                        k_coarse_restrict3m<3><<<nact, 256, 0, s>>>(V, Yall.get() + c0 * zs, zs, pall.get() + c0 * ps, ps,
-                                                                  dact.get() + oact[colour], dend.get() + oact[colour]);
+                        k_coarse_restrict3m<3><<<nact, 256, 0, s>>>(
+                            V, Yall.get() + c0 * cstr, cstr, pall.get() + c0 * ps, ps, dact.get() + oact[colour],
+                            dend.get() + oact[colour], rstr, (applyGc && c0 + 3 == NCOL) ? Yall.get() : nullptr);
                 } else {
                     for (int c = 0; c < NCOL; ++c)
-                        k_coarse_restrict<D><<<nact, 256, 0, s>>>(V, Yall.get() + c * zs, pall.get() + c * ps,
-                                                                  dact.get() + oact[colour], dend.get() + oact[colour]);
+                        k_coarse_restrict<D><<<nact, 256, 0, s>>>(V, Yall.get() + c * cstr, pall.get() + c * ps,
+                                                                  dact.get() + oact[colour], dend.get() + oact[colour],
+                                                                  rstr, (applyGc && c + 1 == NCOL) ? Yall.get() : nullptr);
                 }
                 CR_CHECK_LAUNCH();
             }
             k_coarse_gather_all<D><<<grid_for(C.nE * NCOL, T), T, 0, s>>>(V, pall.get(), ps, call.get());
             CR_CHECK_LAUNCH();
-            if (nsup) k_coarse_colour_chunks_all<D><<<nsup, 256, 0, s>>>(V, dsup.get() + osup[colour], colour, 1, zall.get(), zs);
-            if (nact)
-                k_coarse_colour_chunks_all<D><<<nact, 256, 0, s>>>(V, dact.get() + oact[colour], colour, 1, Yall.get(), zs,
-                                                                   dend.get() + oact[colour]);
+            // Y was cleared by the restriction that read it (every row G z can reach is read)
+            if (!applyGc && nsup)
+                k_coarse_colour_chunks_all<D><<<nsup, 256, 0, s>>>(V, dsup.get() + osup[colour], colour, 1, zall.get(), zs);
             CR_CHECK_LAUNCH();
             if (dense) {
                 for (int k = 0; k < D; ++k)
@@ -1956,7 +2059,7 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const ApplyG &applyG, cudaStre
     C.built = H;
 }
 
-void build_coarse(cr_hybrid_s *h, int H, const ApplyG &applyG,
+void build_coarse(cr_hybrid_s *h, int H, const ApplyG &applyG, const ApplyGColour &applyGc,
                   cudaStream_t s) {
     CR_REQUIRE(H >= 1 && H <= 256, CR_ERR_INVALID_ARG, "coarse grid intervals must be in [1, 256]");
     const int D = h->G.d;
@@ -1968,8 +2071,8 @@ void build_coarse(cr_hybrid_s *h, int H, const ApplyG &applyG,
     h->coarse.requested = H;
     while (true) {
         try {
-            if (D == 2) build_coarse_t<2>(h, H, applyG, s);
-            else build_coarse_t<3>(h, H, applyG, s);
+            if (D == 2) build_coarse_t<2>(h, H, applyG, applyGc, s);
+            else build_coarse_t<3>(h, H, applyG, applyGc, s);
             return;
         } catch (const Error &e) {
             if (e.code != CR_ERR_SINGULAR_LOCAL || H <= 1) throw;
@@ -1980,7 +2083,7 @@ void build_coarse(cr_hybrid_s *h, int H, const ApplyG &applyG,
 
 // per-iteration pieces (called from solve.cu)
 void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double *partials, unsigned *ticket,
-                           cudaStream_t s) {
+                           cudaStream_t s, bool side) {
     CoarseOp &C = h->coarse;
     CoarseView V = C.view();
     const int T = 256;
@@ -1992,7 +2095,10 @@ void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double
         k_coarse_gather<3><<<grid_for(C.nE, T), T, 0, s>>>(V, C.part.get(), C.c.get());
     }
     CR_CHECK_LAUNCH();
-    if (h->part.on) h->comm->impl->allreduce(C.c.get(), (int)C.nE, false, s);
+    if (h->part.on) {
+        if (side) h->comm->impl->allreduce_side(C.c.get(), (int)C.nE, s);
+        else h->comm->impl->allreduce(C.c.get(), (int)C.nE, false, s);
+    }
     if (C.nd.on) {
         nd_solve(C, C.c.get(), C.y.get(), qout, partials, ticket, s);
         return;

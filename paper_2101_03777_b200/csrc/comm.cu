@@ -37,6 +37,7 @@ struct NcclApi {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t *, void *) = nullptr;
 };
 
 static NcclApi &nccl() {
@@ -54,6 +55,7 @@ static NcclApi &nccl() {
         n.GroupStart = (decltype(n.GroupStart))dlsym(n.h, "ncclGroupStart");
         n.GroupEnd = (decltype(n.GroupEnd))dlsym(n.h, "ncclGroupEnd");
         n.GetErrorString = (decltype(n.GetErrorString))dlsym(n.h, "ncclGetErrorString");
+        n.CommSplit = (decltype(n.CommSplit))dlsym(n.h, "ncclCommSplit");
         return n;
     }();
     CR_REQUIRE(a.h && a.CommInitRank && a.AllReduce && a.Send && a.Recv, CR_ERR_NCCL,
@@ -71,9 +73,17 @@ static NcclApi &nccl() {
 
 struct NcclComm : Comm {
     ncclComm_t c = nullptr;
+    // a second communicator over the same ranks (ncclCommSplit) for the coarse path, which runs on
+    // its own stream concurrently with the fine-level kernels: collectives of ONE communicator
+    // must be issued in the same order on every rank, which two streams would not guarantee
+    ncclComm_t side = nullptr;
     bool capturable() const override { return true; }
+    bool has_side() const override { return side != nullptr; }
     void allreduce(double *d, int n, bool mx, cudaStream_t s) override {
         CR_NCCL(nccl().AllReduce(d, d, (size_t)n, ncclDouble, mx ? ncclMax : ncclSum, c, s));
+    }
+    void allreduce_side(double *d, int n, cudaStream_t s) override {
+        CR_NCCL(nccl().AllReduce(d, d, (size_t)n, ncclDouble, ncclSum, side ? side : c, s));
     }
     void halo(const Part &P, const double *sendbuf, double *xghost, int D, cudaStream_t s) override {
         CR_NCCL(nccl().GroupStart());
@@ -96,6 +106,7 @@ struct NcclComm : Comm {
         CR_NCCL(nccl().GroupEnd());
     }
     ~NcclComm() override {
+        if (side && nccl().CommDestroy) nccl().CommDestroy(side);
         if (c && nccl().CommDestroy) nccl().CommDestroy(c);
     }
 };
@@ -222,6 +233,9 @@ cr_status cr_comm_init(const void *nccl_unique_id, int32_t rank, int32_t nranks,
         try {
             using cr::nccl;
             CR_NCCL(cr::nccl().CommInitRank(&nc->c, nranks, id, rank));
+            // the coarse path's communicator (collective over all ranks; absent: no overlap)
+            if (cr::nccl().CommSplit && cr::nccl().CommSplit(nc->c, 0, rank, &nc->side, nullptr) != ncclSuccess)
+                nc->side = nullptr;
         } catch (...) {
             delete nc;
             delete c;

@@ -195,6 +195,10 @@ struct Comm {
     virtual ~Comm() {}
     virtual bool capturable() const = 0;
     virtual void allreduce(double *d, int n, bool max, cudaStream_t s) = 0;
+    // a sum over a second communicator (the coarse path on its own stream); has_side() == false:
+    // none (the caller then keeps the coarse path on the main stream)
+    virtual bool has_side() const { return false; }
+    virtual void allreduce_side(double *d, int n, cudaStream_t s) { allreduce(d, n, false, s); }
     virtual void halo(const Part &P, const double *sendbuf, double *xghost, int D, cudaStream_t s) = 0;
     virtual void allgatherv(const double *local, double *full, const std::vector<int64_t> &counts,
                             const std::vector<int64_t> &displs, cudaStream_t s) = 0;
@@ -225,6 +229,11 @@ struct NdFrontDev {
     int32_t nI, nB;           // unknowns
     int32_t kid_off, kid_cnt; // child fronts: kids[kid_off .. kid_off + kid_cnt)
     int32_t ldFi, ldW;        // leading dimensions of Finv (>= nI) and W (>= nB)
+    // solve layouts (16-byte aligned rows, even leading dimensions, zero padding): Finv rows
+    // (fs, ldFs), W rows = W^t columns (wts, ldWts: the forward B rows), W columns (ws, ldWs: the
+    // backward pivot rows)
+    int64_t fs, wts, ws;
+    int32_t ldFs, ldWts, ldWs, pad_;
 };
 struct CoarseNd {
     bool on = false;
@@ -233,6 +242,7 @@ struct CoarseNd {
     cr::DevBuf<NdFrontDev> fr;
     cr::DevBuf<int32_t> nodes, map;
     cr::DevBuf<double> finv, w, wt, bi, u;
+    cr::DevBuf<double> fs, wts, ws;            // solve layouts (see NdFrontDev)
     cr::DevBuf<double> lb;                     // forward: local right-hand side on B
     cr::DevBuf<int64_t> invp;                  // per front local unknown: CSR offsets into invl
     cr::DevBuf<int32_t> invl, kids;            // children's u indices landing on it; child front lists
@@ -354,10 +364,13 @@ void build_mf(cr_hybrid_s *h, cudaStream_t s);
 // applyG(z, Y, colour, ncol, stride): Y_c = G z_c for the ncol vectors z_c = z + c stride, each a
 // colour sum of coarse columns (colour < 0: any z; Y arrives zero on the rows G z can reach)
 using ApplyG = std::function<void(const double *, double *, int, int, int64_t)>;
-void build_coarse(cr_hybrid_s *h, int H, const ApplyG &applyG,
+// applyGc(colour, Y, stride) (optional, single rank): Y_(k D + l) = G z_(k,l) for the D^2 columns of
+// `colour` computed without materialising z (Y arrives zero)
+using ApplyGColour = std::function<void(int, double *, int64_t)>;
+void build_coarse(cr_hybrid_s *h, int H, const ApplyG &applyG, const ApplyGColour &applyGc,
                   cudaStream_t s);
 void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double *partials, unsigned *ticket,
-                           cudaStream_t s);
+                           cudaStream_t s, bool side = false);
 // shared: copy problem data into hybrid-owned buffers
 struct ProbView;
 ProbView prob_view(const cr_hybrid_s *h);

@@ -40,6 +40,114 @@ struct MfView {
 // from each side.  Either way exactly two contributions meet, and 0 + a + b rounds the same in
 // either order -> deterministic.  Returns this cell's share of p^t G p on rows < nown (owned).
 // (factors already loaded: id, sign mask, c, T, u, in-warp partner codes)
+// scatter of component i of one cell's contribution y[a] (local face a) into q: the pair of an in-warp
+// shared face summed in registers and stored by the lower cell, the others by one atomicAdd per side
+template <int D>
+__device__ __forceinline__ void mf_scatter(const int (&id)[D + 1], const double (&cs)[D + 1], const double (&y)[D + 1],
+                                           const unsigned (&nbc)[D + 1], int lane, int i, double *__restrict__ q,
+                                           int64_t nown, int64_t qrs) {
+    constexpr int NF = D + 1;
+    double out[NF];
+#pragma unroll
+    for (int a = 0; a < NF; ++a) out[a] = cs[a] * y[a];
+    // the partner's contribution to each in-warp shared face (round b2 publishes face b2)
+    double part[NF];
+#pragma unroll
+    for (int a = 0; a < NF; ++a) part[a] = 0.0;
+#pragma unroll
+    for (int b2 = 0; b2 < NF; ++b2)
+#pragma unroll
+        for (int a = 0; a < NF; ++a) {
+            const int src = (nbc[a] & 0x80u) ? (int)(nbc[a] & 31u) : lane;
+            const double v = __shfl_sync(0xffffffffu, out[b2], src);
+            if ((nbc[a] & 0x80u) && (int)((nbc[a] >> 5) & 3u) == b2) part[a] = v;
+        }
+#pragma unroll
+    for (int a = 0; a < NF; ++a) {
+        if (id[a] < 0 || id[a] >= nown) continue;
+        double *dst = q + (int64_t)id[a] * qrs + i;   // qrs: row stride of q (D, or interleaved columns)
+        if (nbc[a] & 0x80u) {
+            if ((int)(nbc[a] & 31u) > lane) *dst = out[a] + part[a];   // lower cell stores the pair
+        } else {
+            atomicAdd(dst, out[a]);
+        }
+    }
+}
+
+// the cell's contribution for already gathered, sign-applied face values xs[i][l] = C_l x_(l, i)
+template <int D>
+__device__ __forceinline__ double mf_cell_core_xs(const int (&id)[D + 1], const double (&cs)[D + 1],
+                                                  const double (&xs)[D][D + 1], double c,
+                                                  const double (&T)[MfLayout<D>::NT], const double (&u)[D][D + 1],
+                                                  const unsigned (&nbc)[D + 1], int lane, double *__restrict__ q,
+                                                  int64_t nown, int64_t qrs = D) {
+    constexpr int NF = D + 1;
+    // projection coefficient sum_j u_j^t xs_j
+    double pu = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int l = 0; l < NF; ++l) pu = fma(u[i][l], xs[i][l], pu);
+    double quad = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double sum = 0.0;
+#pragma unroll
+        for (int l = 0; l < NF; ++l) sum += xs[i][l];
+        const double cb = c * sum;
+        double y[NF];
+#pragma unroll
+        for (int a = 0; a < NF; ++a) {
+            double v = cb;
+#pragma unroll
+            for (int b = 0; b < NF; ++b) {
+                const int e = a >= b ? a * (a + 1) / 2 + b : b * (b + 1) / 2 + a;
+                v = fma(T[e], xs[i][b], v);
+            }
+            v = fma(-u[i][a], pu, v);
+            if (id[a] >= 0 && id[a] < nown) quad = fma(xs[i][a], v, quad);
+            y[a] = v;
+        }
+        mf_scatter<D>(id, cs, y, nbc, lane, i, q, nown, qrs);
+    }
+    return quad;
+}
+
+// input in one velocity component k only (xk[l] = C_l x_(l, k); the coarse setup's columns e_k s a^(l))
+template <int D>
+__device__ __forceinline__ void mf_cell_core_1c(const int (&id)[D + 1], const double (&cs)[D + 1], const double (&xk)[D + 1],
+                                                int k, double c, const double (&T)[MfLayout<D>::NT],
+                                                const double (&u)[D][D + 1], const unsigned (&nbc)[D + 1], int lane,
+                                                double *__restrict__ q, int64_t nown, int64_t qrs) {
+    constexpr int NF = D + 1;
+    double pu = 0.0, sum = 0.0;
+#pragma unroll
+    for (int l = 0; l < NF; ++l) {
+        pu = fma(u[k][l], xk[l], pu);
+        sum += xk[l];
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double y[NF];
+#pragma unroll
+        for (int a = 0; a < NF; ++a) {
+            double v = -u[i][a] * pu;
+            if (i == k) {
+                double t = c * sum;
+#pragma unroll
+                for (int b = 0; b < NF; ++b) {
+                    const int e = a >= b ? a * (a + 1) / 2 + b : b * (b + 1) / 2 + a;
+                    t = fma(T[e], xk[b], t);
+                }
+                v = fma(-u[i][a], pu, t);
+            }
+            y[a] = v;
+        }
+        mf_scatter<D>(id, cs, y, nbc, lane, i, q, nown, qrs);
+    }
+}
+
+// (factors already loaded: id, sign mask, c, T, u, in-warp partner codes; x gathered here)
 template <int D>
 __device__ __forceinline__ double mf_cell_core(const int (&id)[D + 1], unsigned sg, double c,
                                                const double (&T)[MfLayout<D>::NT], const double (&u)[D][D + 1],
@@ -66,56 +174,7 @@ __device__ __forceinline__ double mf_cell_core(const int (&id)[D + 1], unsigned 
             for (int i = 0; i < D; ++i) xs[i][l] = 0.0;
         }
     }
-    // projection coefficient sum_j u_j^t xs_j
-    double pu = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-        for (int l = 0; l < NF; ++l) pu = fma(u[i][l], xs[i][l], pu);
-    double quad = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        double sum = 0.0;
-#pragma unroll
-        for (int l = 0; l < NF; ++l) sum += xs[i][l];
-        const double cb = c * sum;
-        double out[NF];
-#pragma unroll
-        for (int a = 0; a < NF; ++a) {
-            double y = cb;
-#pragma unroll
-            for (int b = 0; b < NF; ++b) {
-                const int e = a >= b ? a * (a + 1) / 2 + b : b * (b + 1) / 2 + a;
-                y = fma(T[e], xs[i][b], y);
-            }
-            y = fma(-u[i][a], pu, y);
-            if (id[a] >= 0 && id[a] < nown) quad = fma(xs[i][a], y, quad);
-            out[a] = cs[a] * y;
-        }
-        // the partner's contribution to each in-warp shared face (round b2 publishes face b2)
-        double part[NF];
-#pragma unroll
-        for (int a = 0; a < NF; ++a) part[a] = 0.0;
-#pragma unroll
-        for (int b2 = 0; b2 < NF; ++b2)
-#pragma unroll
-            for (int a = 0; a < NF; ++a) {
-                const int src = (nbc[a] & 0x80u) ? (int)(nbc[a] & 31u) : lane;
-                const double v = __shfl_sync(0xffffffffu, out[b2], src);
-                if ((nbc[a] & 0x80u) && (int)((nbc[a] >> 5) & 3u) == b2) part[a] = v;
-            }
-#pragma unroll
-        for (int a = 0; a < NF; ++a) {
-            if (id[a] < 0 || id[a] >= nown) continue;
-            double *dst = q + (int64_t)id[a] * D + i;
-            if (nbc[a] & 0x80u) {
-                if ((int)(nbc[a] & 31u) > lane) *dst = out[a] + part[a];   // lower cell stores the pair
-            } else {
-                atomicAdd(dst, out[a]);
-            }
-        }
-    }
-    return quad;
+    return mf_cell_core_xs<D>(id, cs, xs, c, T, u, nbc, lane, q, nown);
 }
 
 // the same cell, factors streamed from HBM (coalesced warp rows)

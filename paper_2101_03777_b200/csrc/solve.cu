@@ -358,6 +358,77 @@ __global__ void __launch_bounds__(kT, D == 2 ? 3 : 2) k_mf_spmv_slices_all(MfVie
     }
 }
 
+// coarse setup without materialising Z: for the listed slices, q = [G z_(k, l)] for the D^2 columns of
+// `colour`, interleaved per row (q[row qs + (k D + l) D + i], qs = D^3), the input z_(k,l) at face
+// sigma = e_k s_sigma a_sigma^(l) (s_sigma = sum of the colour's hat weights at x_sigma) computed from the
+// coarse view's row data on the fly
+template <int D>
+__global__ void __launch_bounds__(kT, D == 2 ? 2 : 1) k_mf_spmv_colour(MfView M, CoarseView C, int colour,
+                                                       const int32_t *slices, const int64_t *nact, double *q, int64_t qs,
+                                                       int64_t nown) {
+    using LY = MfLayout<D>;
+    constexpr int NF = LY::NF, NT = LY::NT, NN = 1 << D;
+    const int64_t n = *nact * 32;
+    GRID_STRIDE(t, n) {
+        const int64_t tt = (int64_t)slices[t >> 5] * 32 + (t & 31);
+        const int64_t slice = tt >> 5;
+        const int lane = (int)(tt & 31);
+        const int32_t *ip = M.ids + slice * (NF * 32) + lane;
+        const double *vp = M.v + slice * ((int64_t)LY::NE * 32) + lane;
+        int id[NF];
+        unsigned nbc[NF];
+#pragma unroll
+        for (int l = 0; l < NF; ++l) {
+            id[l] = ip[l * 32];
+            nbc[l] = M.nb[slice * (NF * 32) + l * 32 + lane];
+        }
+        const unsigned sg = M.sg[tt];
+        double cs[NF], sw[NF], fa[NF][D];
+#pragma unroll
+        for (int l = 0; l < NF; ++l) {
+            cs[l] = ((sg >> l) & 1u) ? -1.0 : 1.0;
+            sw[l] = 0.0;
+#pragma unroll
+            for (int i = 0; i < D; ++i) fa[l][i] = 0.0;
+            if (id[l] >= 0) {
+                const float *x = C.fx + (int64_t)id[l] * D;
+                int ic[D];
+                float xi[D];
+                coarse_locate<D>(C.g, x, ic, xi);
+                double w[NN];
+                coarse_weights<D>(C.g, x, w);
+                for (int nn = 0; nn < NN; ++nn) {
+                    int col = 0, mul = 1;
+                    for (int i = 0; i < D; ++i) {
+                        col += ((ic[i] + ((nn >> i) & 1)) % 5) * mul;
+                        mul *= 5;
+                    }
+                    if (col == colour) sw[l] += w[nn];
+                }
+#pragma unroll
+                for (int i = 0; i < D; ++i) fa[l][i] = (double)C.fa[(int64_t)id[l] * D + i];
+            }
+        }
+        const double c = vp[0];
+        double T[NT], u[D][NF];
+#pragma unroll
+        for (int e = 0; e < NT; ++e) T[e] = vp[(1 + e) * 32];
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int l = 0; l < NF; ++l) u[i][l] = vp[(1 + NT + i * NF + l) * 32];
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+#pragma unroll
+            for (int l2 = 0; l2 < D; ++l2) {
+                double xk[NF];
+#pragma unroll
+                for (int l = 0; l < NF; ++l) xk[l] = cs[l] * sw[l] * fa[l][l2];
+                mf_cell_core_1c<D>(id, cs, xk, k, c, T, u, nbc, lane, q + (int64_t)(k * D + l2) * D, nown, qs);
+            }
+    }
+}
+
 // r = b - q, |r|^2 (FIN_RR)
 __global__ void __launch_bounds__(kT) k_resid_vec(int64_t N, const double *b, const double *q, double *r, KState *st,
                                                   double *partials, int dist) {
@@ -677,7 +748,7 @@ enum { AFW_PCG_INIT = 0, AFW_PCG = 1, AFW_MINRES_INIT = 2, AFW_MINRES = 3, AFW_P
 
 // zs (per face slot) = patch contributions of M^{-1} r
 template <int D, int SLOTS, int KMAX, bool SYM, int WHAT>
-__global__ void __launch_bounds__(kT, 5) k_afw_apply(AfwView A, const double *r, double *zs, double rtol, KState *st,
+__global__ void __launch_bounds__(kT, 4) k_afw_apply(AfwView A, const double *r, double *zs, double rtol, KState *st,
                                                   double *partials, int dist) {
     if (WHAT != AFW_PCG_INIT && WHAT != AFW_MINRES_INIT && WHAT != AFW_PCG2_INIT && st->flag != FLAG_RUN) return;
     double acc[1] = {0.0};
@@ -1587,28 +1658,31 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         DevBuf<int64_t> snum;
         DevBuf<uint8_t> stmp;
         int last_colour = -1;
+        // the 32-cell slices touching the coarse cells around `colour`'s nodes (x vanishes elsewhere)
+        auto select_slices = [&](int colour) {
+            if (colour == last_colour) return;
+            const int64_t nsl = h->mf.ncells / 32;
+            if (sflag.n == 0) {
+                sflag.alloc(nsl, s);
+                slist.alloc(nsl, s);
+                snum.alloc(1, s);
+                size_t tb = 0;
+                cub::CountingInputIterator<int32_t> it(0);
+                CR_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, sflag.get(), slist.get(), snum.get(), nsl, s));
+                stmp.alloc(tb, s);
+            }
+            k_mf_slice_flag<D><<<grid_for(nsl * 32, kT), kT, 0, s>>>(mf_view<D>(h), h->coarse.view(), colour, nsl,
+                                                                    sflag.get());
+            CR_CHECK_LAUNCH();
+            size_t tb = stmp.n;
+            cub::CountingInputIterator<int32_t> it(0);
+            CR_CUDA(cub::DeviceSelect::Flagged(stmp.get(), tb, it, sflag.get(), slist.get(), snum.get(), nsl, s));
+            last_colour = colour;
+        };
         build_coarse(h, H, [&](const double *z, double *Y, int colour, int ncol, int64_t stride) {
             for (int c = 0; c < ncol; ++c) L.halo(s, const_cast<double *>(z) + c * stride);
             if (L.mf && colour >= 0 && !L.dist) {
-                const int64_t nsl = h->mf.ncells / 32;
-                if (colour != last_colour) {
-                    if (sflag.n == 0) {
-                        sflag.alloc(nsl, s);
-                        slist.alloc(nsl, s);
-                        snum.alloc(1, s);
-                        size_t tb = 0;
-                        cub::CountingInputIterator<int32_t> it(0);
-                        CR_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, sflag.get(), slist.get(), snum.get(), nsl, s));
-                        stmp.alloc(tb, s);
-                    }
-                    k_mf_slice_flag<D><<<grid_for(nsl * 32, kT), kT, 0, s>>>(mf_view<D>(h), h->coarse.view(), colour, nsl,
-                                                                            sflag.get());
-                    CR_CHECK_LAUNCH();
-                    size_t tb = stmp.n;
-                    cub::CountingInputIterator<int32_t> it(0);
-                    CR_CUDA(cub::DeviceSelect::Flagged(stmp.get(), tb, it, sflag.get(), slist.get(), snum.get(), nsl, s));
-                    last_colour = colour;
-                }
+                select_slices(colour);
                 // Y arrives zero (build_coarse clears the rows it touched after each pass)
                 if (ncol == 1) {
                     k_mf_spmv_slices<D><<<occ_grid(k_mf_spmv_slices<D>, kT, h->mf.ncells), kT, 0, s>>>(
@@ -1624,7 +1698,12 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                     else spmv(h->G, z + c * stride, Y + c * stride, s);
                 }
             }
-        }, s);
+        }, (L.mf && !L.dist) ? ApplyGColour([&](int colour, double *Y, int64_t stride) {
+            select_slices(colour);
+            k_mf_spmv_colour<D><<<occ_grid(k_mf_spmv_colour<D>, kT, h->mf.ncells), kT, 0, s>>>(
+                mf_view<D>(h), h->coarse.view(), colour, slist.get(), snum.get(), Y, stride, L.nrows);
+            CR_CHECK_LAUNCH();
+        }) : ApplyGColour(), s);
         trc.mark("coarse space (E, E^-1)");
         CR_CUDA(cudaEventRecord(w->es, s));
         if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
@@ -1632,9 +1711,14 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         const CoarseView CV = h->coarse.view();
         double *yc = h->coarse.y.get();
         // coarse path (restriction, gather, E^-1 GEMV) forked onto a side stream so it overlaps the
-        // patch solves; joined before the direction update.  Partitioned runs stay on one stream
-        // (NCCL collectives of one communicator must not be reordered between ranks).
-        const bool fork = !L.dist;
+        // patch solves; joined before the direction update.  Partitioned runs fork only with a
+        // second communicator for the coarse allreduce (NCCL collectives of one communicator must
+        // not be reordered between ranks); its replicated coarse solve then hides behind the
+        // rank's share of the fine-level work.
+        // (opt-in, CR_DIST_OVERLAP=1: concurrent collectives of two communicators are only safe when
+        // every rank's GPU can run both NCCL kernels at once; not measurable with one GPU per call)
+        static const char *eov = std::getenv("CR_DIST_OVERLAP");
+        const bool fork = !L.dist || (eov && atoi(eov) == 1 && L.comm->capturable() && L.comm->has_side());
         double *cpart = h->coarse.gpart.get();
         auto coarse_begin = [&](cudaStream_t q) {
             cudaStream_t cs = q;
@@ -1643,7 +1727,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                 CR_CUDA(cudaStreamWaitEvent(w->side, w->fork, 0));
                 cs = w->side;
             }
-            coarse_restrict_solve(h, w->r.get(), &st->qc, fork ? cpart : part, &st->tickets[4], cs);
+            coarse_restrict_solve(h, w->r.get(), &st->qc, fork ? cpart : part, &st->tickets[4], cs, fork && L.dist);
             if (fork) CR_CUDA(cudaEventRecord(w->join, w->side));
             L.launches += 3;
         };
@@ -1946,7 +2030,7 @@ static void apply_precond_t(cr_hybrid_s *h, int method, const double *r, double 
             const int Hc = h->coarse.requested > 0 ? h->coarse.requested : (D == 2 ? 64 : 16);
             build_coarse(h, Hc, [&](const double *zz, double *Y, int, int ncol, int64_t stride) {
                 for (int c = 0; c < ncol; ++c) spmv(h->G, zz + c * stride, Y + c * stride, s);
-            }, s);
+            }, ApplyGColour(), s);
             if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
             CR_CUDA(cudaMemsetAsync(w->st.get(), 0, sizeof(KState), s));
             coarse_restrict_solve(h, r, &w->st.get()->qc, w->partials.get(), &w->st.get()->tickets[4], s);
