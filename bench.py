@@ -220,7 +220,8 @@ def workload_config(cfg_idx, world):
             "parallelism": (f"face rows partitioned over {world} GPUs (NCCL halo send/recv + allreduce)"
                             if world > 1 else "1 GPU"),
             "l2": "working set > L2 (G = %.2f GB assembled; per-iteration streams > 1 GB) and a 256 MB L2 flush "
-                  "before each step" % (8 * nnz / 1e9)}
+                  "before each step" % (8 * nnz / 1e9),
+            "memory": "libcr pool reserved up front (cr_pool_reserve, --pool-reserve-gb; DESIGN.md §1)"}
 
 
 def run_reference(args):
@@ -477,6 +478,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true")
+    ap.add_argument("--pool-reserve-gb", type=float, default=None,
+                    help="map this much into libcr's memory pool before the first step (cr_pool_reserve); default "
+                         "120 for configs[4], 24 for configs[1]: without it the pool maps new memory in the middle of "
+                         "some steps (3D: 3.5-6.1 s per step instead of 3.47 +- 0.01 s)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -509,6 +514,11 @@ def main():
     cfg_idx = args.config
     cfg = ci.CONFIGS[cfg_idx]
     sol, rtol = _solver(cfg_idx)
+    if args.pool_reserve_gb is None:
+        args.pool_reserve_gb = 120.0 if cfg.dim == 3 else 24.0
+    if args.pool_reserve_gb > 0:
+        free = torch.cuda.mem_get_info(dev)[0]
+        P.pool_reserve(int(min(args.pool_reserve_gb * 2 ** 30, 0.8 * free)))
     inp = ci.make_inputs(cfg, n=args.n)
     coords_h = torch.from_numpy(inp["coords"]).pin_memory()
     cells_h = torch.from_numpy(inp["cells"]).pin_memory()

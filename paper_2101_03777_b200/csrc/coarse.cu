@@ -1445,7 +1445,11 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
         CR_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
         // one co-resident wave (more resident warps: the phases are latency-bound); 0 = no
         // persistent kernel (per-phase launches)
-        N.grid = (coop && occ >= 1) ? num_sms() * std::min(occ, 8) : 0;
+        // CR_ND_GRID = CTAs per SM (tuning: a small grid can run beside the patch solves when they
+        // leave block slots free, CR_AFW_RSV)
+        static const char *eg = std::getenv("CR_ND_GRID");
+        const int per_sm = eg ? std::max(1, std::min(atoi(eg), occ)) : std::min(occ, 8);
+        N.grid = (coop && occ >= 1) ? num_sms() * per_sm : 0;
     }
     tr.mark("  nd: uploads + work lists");
     // numeric factorisation, deepest level first

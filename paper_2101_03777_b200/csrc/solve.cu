@@ -57,7 +57,7 @@ struct KState {
 constexpr size_t kStateHeader = offsetof(KState, H);
 
 struct SolverWork {
-    int64_t N = 0;
+    int64_t N = 0, Nalloc = 0;
     int D = 0;
     DevBuf<double> x, b, r, p, q, z, z2, v, v2, w, w2, y, t, rhat;
     DevBuf<double> V;           // GMRES basis (m+1) x N
@@ -1211,11 +1211,12 @@ static void ensure_work(cr_hybrid_s *h, cudaStream_t s) {
     h->work = w;
     w->N = N;
     w->D = D;
-    for (DevBuf<double> *b : {&w->x, &w->b, &w->r, &w->p, &w->q, &w->z, &w->z2, &w->v, &w->v2, &w->w, &w->w2, &w->y,
-                              &w->t, &w->rhat}) {
+    // the PCG methods' vectors; MINRES / BiCGStab / GMRES add theirs on first use (ensure_extra)
+    for (DevBuf<double> *b : {&w->x, &w->b, &w->r, &w->p, &w->q, &w->z, &w->t}) {
         b->alloc(Nalloc, s);
         b->zero(s);
     }
+    w->Nalloc = Nalloc;
     w->partials.alloc((size_t)num_sms() * 16 * (kMaxRestart + 1), s);
     w->st.alloc(1, s);
     w->st.zero(s);
@@ -1227,6 +1228,15 @@ static void ensure_work(cr_hybrid_s *h, cudaStream_t s) {
     CR_CUDA(cudaStreamCreateWithFlags(&w->side, cudaStreamNonBlocking));
     CR_CUDA(cudaEventCreateWithFlags(&w->fork, cudaEventDisableTiming));
     CR_CUDA(cudaEventCreateWithFlags(&w->join, cudaEventDisableTiming));
+}
+
+// vectors of the non-PCG methods (MINRES, BiCGStab, GMRES), allocated on first use
+static void ensure_extra(SolverWork *w, cudaStream_t s) {
+    if (w->v.n) return;
+    for (DevBuf<double> *b : {&w->z2, &w->v, &w->v2, &w->w, &w->w2, &w->y, &w->rhat}) {
+        b->alloc(w->Nalloc, s);
+        b->zero(s);
+    }
 }
 
 struct Launcher {
@@ -1786,6 +1796,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
             if (w->hst->iters >= max_iter) { status = CR_ERR_NOT_CONVERGED; break; }
         }
     } else if (method == CR_MINRES_AFW) {
+        ensure_extra(w, s);
         constexpr int SLOTS = D == 2 ? 2 : 3;
         build_afw(h, AFW_ABS, s);
         CR_CUDA(cudaEventRecord(w->es, s));
@@ -1831,6 +1842,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
             if (w->hst->iters >= max_iter) { status = CR_ERR_NOT_CONVERGED; break; }
         }
     } else if (method == CR_MINRES_ABSJACOBI) {
+        ensure_extra(w, s);
         const double *M = h->absdinv.get();
         double *va = w->v.get(), *vb = w->v2.get(), *za = w->z.get(), *zb = w->z2.get();
         double *wa = w->w.get(), *wb = w->w2.get();
@@ -1869,6 +1881,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
             if (w->hst->iters >= max_iter) { status = CR_ERR_NOT_CONVERGED; break; }
         }
     } else if (method == CR_BICGSTAB_JACOBI) {
+        ensure_extra(w, s);
         const double *M = h->dinv.get();
         true_residual<D>(L, x, w->r.get());
         k_bicg_init<D><<<L.grid_rows, kT, 0, s>>>(nrows, w->r.get(), w->rhat.get(), w->p.get(), w->v.get(), rtol, st, part);
@@ -1907,6 +1920,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
             if (w->hst->iters >= max_iter) { status = CR_ERR_NOT_CONVERGED; break; }
         }
     } else if (method == CR_GMRES_JACOBI) {
+        ensure_extra(w, s);
         const double *M = h->dinv.get();
         int m = o.restart > 0 ? o.restart : 50;
         CR_REQUIRE(m <= kMaxRestart, CR_ERR_INVALID_ARG, "GMRES restart must be <= 128");
