@@ -48,7 +48,7 @@ MAX_ITER = 20000     # a cap (the solves take ~500): a regression fails loudly i
 # Jacobi-PCG iterations to a true 1e-10 residual, measured on the B200 (the oracle's own solver;
 # used to extrapolate the CPU oracle's time): configs[1] by the r01 driver run (BENCH_r01.json
 # pcg_jacobi), configs[4] by `python bench.py --jacobi` (profiles/r02_jacobi_configs4.log).
-JACOBI_ITERS = {1: 161758, 4: None}
+JACOBI_ITERS = {1: 161758, 4: 48569}
 
 
 def measured_peaks():

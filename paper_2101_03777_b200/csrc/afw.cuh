@@ -32,6 +32,7 @@ struct AfwView {
     const double *vals;
     int64_t npatch;
     int64_t nrows;   // block rows (zs stride)
+    int shared = 0;  // 1: one block per patch for all D components (CR_AFW_SHARED, experiment)
 };
 
 // z-contributions of one patch for one velocity component: thread t of a launch covers slice
@@ -56,7 +57,7 @@ __device__ __forceinline__ double afw_patch_comp(const AfwView &A, int64_t t, co
         y[j] = 0.0;
     }
     const int T = SYM ? k * (k + 1) / 2 : k * k;
-    const double *vi = A.vals + A.voff[slice] + lane + (int64_t)i * T * 32;
+    const double *vi = A.vals + A.voff[slice] + lane + (int64_t)(A.shared ? 0 : i) * T * 32;
     if (SYM && k == KMAX) {
         // full-size slice (nearly all of them): every operator load is issued before the first
         // FMA needs one, instead of one row's worth per (data-dependent) branch

@@ -16,6 +16,10 @@
 // Per iteration: restriction c = Z^t r (chunk partials, fixed-order gather: deterministic),
 // y = E^{-1} c and c^t y (dense GEMV), prolongation fused into the direction update.
 #include <cub/cub.cuh>
+#include <tuple>
+#include <mutex>
+#include <memory>
+#include <map>
 #include <dlfcn.h>
 
 #include <algorithm>
@@ -142,8 +146,9 @@ __global__ void __launch_bounds__(256) k_coarse_restrict(CoarseView C, const dou
 #pragma unroll
             for (int i = 0; i < D; ++i) {
                 const bool ok = row[u] >= 0;
-                xv[u][i] = ok ? C.fx[row[u] * D + i] : 0.f;
-                av[u][i] = ok ? C.fa[row[u] * D + i] : 0.f;
+                const int64_t t = t0 + (int64_t)u * SL;   // sorted position: the row data is stored in this order
+                xv[u][i] = ok ? C.fxp[t * D + i] : 0.f;
+                av[u][i] = ok ? C.fap[t * D + i] : 0.f;
                 rv[u][i] = ok ? r[row[u] * rrs + i] : 0.0;
             }
         if (clear_base)   // setup: zero the rows read (interleaved, full-sector stores)
@@ -419,8 +424,8 @@ __global__ void __launch_bounds__(256, 2) k_coarse_restrict3(CoarseView C, const
             float xv[D];
 #pragma unroll
             for (int i = 0; i < D; ++i) {
-                xv[i] = row >= 0 ? C.fx[row * D + i] : 0.f;
-                av[u][i] = row >= 0 ? C.fa[row * D + i] : 0.f;
+                xv[i] = row >= 0 ? C.fxp[t * D + i] : 0.f;   // row data in sorted order: coalesced
+                av[u][i] = row >= 0 ? C.fap[t * D + i] : 0.f;
                 rv[u][i] = row >= 0 ? r[row * D + i] : 0.0;
             }
             int ic[D];
@@ -553,8 +558,8 @@ __global__ void __launch_bounds__(256, 2) k_coarse_restrict3m(CoarseView C, cons
             float xv[D];
 #pragma unroll
             for (int i = 0; i < D; ++i) {
-                xv[i] = row >= 0 ? C.fx[row * D + i] : 0.f;
-                av[u][i] = row >= 0 ? C.fa[row * D + i] : 0.f;
+                xv[i] = row >= 0 ? C.fxp[t * D + i] : 0.f;
+                av[u][i] = row >= 0 ? C.fap[t * D + i] : 0.f;
 #pragma unroll
                 for (int c = 0; c < NC; ++c) rv[u][c][i] = row >= 0 ? r[c * rs + row * rrs + i] : 0.0;
             }
@@ -639,6 +644,19 @@ __global__ void k_coarse_gather_all(CoarseView C, const double *part, int64_t ps
                 sum += part[col * ps + ch * NV + n * D * D + kl];
         }
         out[col * nE + q] = sum;
+    }
+}
+
+// row data in sorted (coarse-cell) order for the restrictions: fxp[t] = fx[perm[t]], fap likewise
+template <int D>
+__global__ void k_coarse_permute_rows(const int32_t *perm, int64_t n, const float *fx, const float *fa, float *fxp,
+                                      float *fap) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = perm[t];
+        for (int i = 0; i < D; ++i) {
+            fxp[t * D + i] = fx[r * D + i];
+            fap[t * D + i] = fa[r * D + i];
+        }
     }
 }
 
@@ -1296,104 +1314,166 @@ static bool nd_batched_cholesky_inverse(int n, int lda, int nb, double **dA, dou
     return true;
 }
 
+// host-side plan of nd_setup (depends only on H, D and the plan variant)
+struct NdHost {
+    std::vector<HostFront> F;
+    int nf = 0, maxd = 0;
+    std::vector<std::vector<int>> lev;
+    std::vector<int> parent, slot, nIp, nBp;
+    std::vector<char> batched;
+    std::vector<NdFrontDev> fr;
+    std::vector<int32_t> nodes, map, uidx, kidl;
+    std::vector<int64_t> fbase, invp;
+    std::vector<int32_t> invl;
+    int64_t ofi = 0, ow = 0, owt = 0, obi = 0, ou = 0, olb = 0, oinv = 0, fpool = 0, maxn = 0, bytes = 0;
+};
+
 template <int D>
 static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
     constexpr int M = D * D;
     CoarseNd &N = C.nd;
     Trace tr(s);
-    std::vector<HostFront> F;
-    // 2D: the flat two-level plan (boxes of 12 nodes per side under one separator front): 3 solve
-    // phases instead of 3 per bisection level, the whole separator set as one dense front
-    // (configs[1] H = 64: 470 iterations, 0.48 ms each against dense H = 32's 774 x 0.37 ms).
-    // 3D: recursive bisection.  CR_ND_BOX overrides (0 = bisection; tests / experiments).
+    // the host-side plan and index maps depend only on (H, D, box): built once per process and reused
+    // (the 3D bisection plan with its B sets and CSR maps took ~21 ms per solve)
     const char *eb = std::getenv("CR_ND_BOX");
-    nd_plan(H, D, F, eb ? std::max(0, atoi(eb)) : (D == 2 ? 12 : 0));
-    const int nf = (int)F.size();
-    int maxd = 0;
-    for (auto &f : F) maxd = std::max(maxd, f.depth);
-    std::vector<std::vector<int>> lev(maxd + 1);
-    for (int f = 0; f < nf; ++f) lev[F[f].depth].push_back(f);
-    std::vector<int> parent(nf, -1), slot(nf, 0);
-    for (int f = 0; f < nf; ++f)
-        for (int k : F[f].kids) parent[k] = f;
-    // padded sizes: levels with many small fronts are factorised by batched cuBLAS calls
-    std::vector<int> nIp(nf), nBp(nf);
-    std::vector<char> batched(maxd + 1, 0);
-    for (int d = 0; d <= maxd; ++d) {
-        int mi = 0, mb = 0;
-        for (int f : lev[d]) { mi = std::max(mi, (int)F[f].I.size() * M); mb = std::max(mb, (int)F[f].B.size() * M); }
-        batched[d] = lev[d].size() >= 4 && mi <= 640;
-        for (size_t k = 0; k < lev[d].size(); ++k) {
-            const int f = lev[d][k];
-            slot[f] = (int)k;
-            nIp[f] = batched[d] ? mi : (int)F[f].I.size() * M;
-            nBp[f] = batched[d] ? mb : (int)F[f].B.size() * M;
-        }
+    const int box = eb ? std::max(0, atoi(eb)) : (D == 2 ? 12 : 0);
+    static std::mutex plan_mu;
+    static std::map<std::tuple<int, int, int>, std::shared_ptr<NdHost>> plan_cache;
+    std::shared_ptr<NdHost> PH;
+    {
+        std::lock_guard<std::mutex> lk(plan_mu);
+        auto it = plan_cache.find(std::make_tuple(H, D, box));
+        if (it != plan_cache.end()) PH = it->second;
     }
-    std::vector<NdFrontDev> fr(nf);
-    std::vector<int32_t> nodes, map;
-    int64_t ofi = 0, ow = 0, owt = 0, obi = 0, ou = 0, olb = 0, oinv = 0, fpool = 0, maxn = 0, bytes = 0;
-    std::vector<int32_t> uidx, kidl;
-    std::vector<int64_t> fbase(nf);
-    for (int f = 0; f < nf; ++f) {
-        NdFrontDev &x = fr[f];
-        x.ioff = (int64_t)nodes.size();
-        nodes.insert(nodes.end(), F[f].I.begin(), F[f].I.end());
-        x.boff = (int64_t)nodes.size();
-        nodes.insert(nodes.end(), F[f].B.begin(), F[f].B.end());
-        x.nI = (int32_t)F[f].I.size() * M;
-        x.nB = (int32_t)F[f].B.size() * M;
-        x.kid_off = (int32_t)kidl.size();
-        x.kid_cnt = (int32_t)F[f].kids.size();
-        kidl.insert(kidl.end(), F[f].kids.begin(), F[f].kids.end());
-        x.ldFi = nIp[f];
-        x.ldW = std::max(nBp[f], 1);
-        x.finv = ofi; ofi += (int64_t)nIp[f] * nIp[f];
-        x.w = ow; ow += (int64_t)nBp[f] * nIp[f];
-        x.wt = owt; owt += (int64_t)x.nB * x.nI;
-        x.bi = obi; obi += (x.nI + 1) & ~1;   // even: 16-byte aligned, zero pad entry
-        x.u = ou; ou += x.nB;
-        x.lb = olb; olb += x.nB;
-        x.inv = oinv; oinv += x.nI + x.nB;
-        x.uoff = (int64_t)uidx.size();
-        for (int32_t v : F[f].I)
-            for (int cc = 0; cc < M; ++cc) uidx.push_back(v * M + cc);
-        for (int32_t v : F[f].B)
-            for (int cc = 0; cc < M; ++cc) uidx.push_back(v * M + cc);
-        fbase[f] = fpool;
-        fpool += (int64_t)(nIp[f] + nBp[f]) * (nIp[f] + nBp[f]);
-        maxn = std::max<int64_t>(maxn, x.nI + x.nB);
-        bytes += 8 * ((int64_t)x.nI * x.nI + 2 * (int64_t)x.nB * x.nI);
-        // this front's B unknowns -> local unknowns of the parent
-        x.map = (int64_t)map.size();
-        if (parent[f] >= 0) {
-            const HostFront &P = F[parent[f]];
-            for (int32_t v : F[f].B) {
-                int pos;
-                auto it = std::lower_bound(P.I.begin(), P.I.end(), v);
-                if (it != P.I.end() && *it == v) {
-                    pos = (int)(it - P.I.begin());
-                } else {
-                    auto jt = std::find(P.B.begin(), P.B.end(), v);
-                    CR_REQUIRE(jt != P.B.end(), CR_ERR_INVALID_ARG, "coarse ND plan: child boundary node missing in parent");
-                    pos = (int)P.I.size() + (int)(jt - P.B.begin());
-                }
-                for (int c = 0; c < M; ++c) map.push_back(pos * M + c);
+    if (!PH) {
+        PH = std::make_shared<NdHost>();
+        NdHost &Q = *PH;
+        auto &F = Q.F;
+        nd_plan(H, D, F, box);
+        const int nf = (int)F.size();
+        int maxd = 0;
+        for (auto &f : F) maxd = std::max(maxd, f.depth);
+        Q.nf = nf;
+        Q.maxd = maxd;
+        auto &lev = Q.lev;
+        lev.assign(maxd + 1, {});
+        for (int f = 0; f < nf; ++f) lev[F[f].depth].push_back(f);
+        auto &parent = Q.parent;
+        auto &slot = Q.slot;
+        parent.assign(nf, -1);
+        slot.assign(nf, 0);
+        for (int f = 0; f < nf; ++f)
+            for (int k : F[f].kids) parent[k] = f;
+        // padded sizes: levels with many small fronts are factorised by batched cuBLAS calls
+        auto &nIp = Q.nIp;
+        auto &nBp = Q.nBp;
+        auto &batched = Q.batched;
+        nIp.assign(nf, 0);
+        nBp.assign(nf, 0);
+        batched.assign(maxd + 1, 0);
+        for (int d = 0; d <= maxd; ++d) {
+            int mi = 0, mb = 0;
+            for (int f : lev[d]) { mi = std::max(mi, (int)F[f].I.size() * M); mb = std::max(mb, (int)F[f].B.size() * M); }
+            batched[d] = lev[d].size() >= 4 && mi <= 640;
+            for (size_t k = 0; k < lev[d].size(); ++k) {
+                const int f = lev[d][k];
+                slot[f] = (int)k;
+                nIp[f] = batched[d] ? mi : (int)F[f].I.size() * M;
+                nBp[f] = batched[d] ? mb : (int)F[f].B.size() * M;
             }
         }
+        auto &fr = Q.fr;
+        fr.assign(nf, NdFrontDev{});
+        auto &nodes = Q.nodes;
+        auto &map = Q.map;
+        int64_t ofi = 0, ow = 0, owt = 0, obi = 0, ou = 0, olb = 0, oinv = 0, fpool = 0, maxn = 0, bytes = 0;
+        auto &uidx = Q.uidx;
+        auto &kidl = Q.kidl;
+        auto &fbase = Q.fbase;
+        fbase.assign(nf, 0);
+        for (int f = 0; f < nf; ++f) {
+            NdFrontDev &x = fr[f];
+            x.ioff = (int64_t)nodes.size();
+            nodes.insert(nodes.end(), F[f].I.begin(), F[f].I.end());
+            x.boff = (int64_t)nodes.size();
+            nodes.insert(nodes.end(), F[f].B.begin(), F[f].B.end());
+            x.nI = (int32_t)F[f].I.size() * M;
+            x.nB = (int32_t)F[f].B.size() * M;
+            x.kid_off = (int32_t)kidl.size();
+            x.kid_cnt = (int32_t)F[f].kids.size();
+            kidl.insert(kidl.end(), F[f].kids.begin(), F[f].kids.end());
+            x.ldFi = nIp[f];
+            x.ldW = std::max(nBp[f], 1);
+            x.finv = ofi; ofi += (int64_t)nIp[f] * nIp[f];
+            x.w = ow; ow += (int64_t)nBp[f] * nIp[f];
+            x.wt = owt; owt += (int64_t)x.nB * x.nI;
+            x.bi = obi; obi += (x.nI + 1) & ~1;   // even: 16-byte aligned, zero pad entry
+            x.u = ou; ou += x.nB;
+            x.lb = olb; olb += x.nB;
+            x.inv = oinv; oinv += x.nI + x.nB;
+            x.uoff = (int64_t)uidx.size();
+            for (int32_t v : F[f].I)
+                for (int cc = 0; cc < M; ++cc) uidx.push_back(v * M + cc);
+            for (int32_t v : F[f].B)
+                for (int cc = 0; cc < M; ++cc) uidx.push_back(v * M + cc);
+            fbase[f] = fpool;
+            fpool += (int64_t)(nIp[f] + nBp[f]) * (nIp[f] + nBp[f]);
+            maxn = std::max<int64_t>(maxn, x.nI + x.nB);
+            bytes += 8 * ((int64_t)x.nI * x.nI + 2 * (int64_t)x.nB * x.nI);
+            // this front's B unknowns -> local unknowns of the parent
+            x.map = (int64_t)map.size();
+            if (parent[f] >= 0) {
+                const HostFront &P = F[parent[f]];
+                for (int32_t v : F[f].B) {
+                    int pos;
+                    auto it = std::lower_bound(P.I.begin(), P.I.end(), v);
+                    if (it != P.I.end() && *it == v) {
+                        pos = (int)(it - P.I.begin());
+                    } else {
+                        auto jt = std::find(P.B.begin(), P.B.end(), v);
+                        CR_REQUIRE(jt != P.B.end(), CR_ERR_INVALID_ARG, "coarse ND plan: child boundary node missing in parent");
+                        pos = (int)P.I.size() + (int)(jt - P.B.begin());
+                    }
+                    for (int c = 0; c < M; ++c) map.push_back(pos * M + c);
+                }
+            }
+        }
+        // children's u entries landing on each local unknown of their parent (absolute u indices, in
+        // child order: a fixed summation order), as CSR rows
+        std::vector<std::vector<int32_t>> invr(oinv);
+        for (int f = 0; f < nf; ++f)
+            for (int kid : F[f].kids)
+                for (int q = 0; q < fr[kid].nB; ++q) invr[fr[f].inv + map[fr[kid].map + q]].push_back((int32_t)(fr[kid].u + q));
+        std::vector<int64_t> invp(oinv + 1, 0);
+        std::vector<int32_t> invl;
+        for (int64_t g = 0; g < oinv; ++g) {
+            invl.insert(invl.end(), invr[g].begin(), invr[g].end());
+            invp[g + 1] = (int64_t)invl.size();
+        }
+        Q.ofi = ofi; Q.ow = ow; Q.owt = owt; Q.obi = obi; Q.ou = ou; Q.olb = olb; Q.oinv = oinv;
+        Q.fpool = fpool; Q.maxn = maxn; Q.bytes = bytes;
+        Q.invp = std::move(invp);
+        Q.invl = std::move(invl);
+        std::lock_guard<std::mutex> lk(plan_mu);
+        plan_cache[std::make_tuple(H, D, box)] = PH;
     }
-    // children's u entries landing on each local unknown of their parent (absolute u indices, in
-    // child order: a fixed summation order), as CSR rows
-    std::vector<std::vector<int32_t>> invr(oinv);
-    for (int f = 0; f < nf; ++f)
-        for (int kid : F[f].kids)
-            for (int q = 0; q < fr[kid].nB; ++q) invr[fr[f].inv + map[fr[kid].map + q]].push_back((int32_t)(fr[kid].u + q));
-    std::vector<int64_t> invp(oinv + 1, 0);
-    std::vector<int32_t> invl;
-    for (int64_t g = 0; g < oinv; ++g) {
-        invl.insert(invl.end(), invr[g].begin(), invr[g].end());
-        invp[g + 1] = (int64_t)invl.size();
-    }
+    const NdHost &Q = *PH;
+    const auto &F = Q.F;
+    const int nf = Q.nf, maxd = Q.maxd;
+    const auto &lev = Q.lev;
+    const auto &slot = Q.slot;
+    const auto &nIp = Q.nIp;
+    const auto &nBp = Q.nBp;
+    const auto &batched = Q.batched;
+    std::vector<NdFrontDev> fr = Q.fr;   // copied: the solve layouts are filled in below
+    const auto &nodes = Q.nodes;
+    const auto &map = Q.map;
+    const auto &uidx = Q.uidx;
+    std::vector<int32_t> kidl = Q.kidl;
+    const auto &fbase = Q.fbase;
+    const int64_t ofi = Q.ofi, ow = Q.ow, obi = Q.obi, ou = Q.ou, olb = Q.olb, fpool = Q.fpool, bytes = Q.bytes;
+    std::vector<int64_t> invp = Q.invp;
+    std::vector<int32_t> invl = Q.invl;
     tr.mark("  nd: plan + maps (host)");
     upload(N.fr, fr, s);
     upload(N.nodes, nodes, s);
@@ -1835,6 +1915,11 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const ApplyG &applyG, const Ap
         tmp.alloc(tb, s);
         CR_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, cc.get(), cc2.get(), idx.get(),
                                                 reinterpret_cast<uint32_t *>(C.perm.get()), (int)nrows, 0, bits, s));
+        C.fxp.alloc(nrows * D, s);
+        C.fap.alloc(nrows * D, s);
+        k_coarse_permute_rows<D><<<grid_for(nrows, T), T, 0, s>>>(C.perm.get(), nrows, C.fx.get(), C.fa.get(), C.fxp.get(),
+                                                                   C.fap.get());
+        CR_CHECK_LAUNCH();
         // rows of each coarse cell (device), chunks of <= kCH rows (host: a few thousand entries)
         DevBuf<int64_t> cs;
         cs.alloc(ncc + 1, s);

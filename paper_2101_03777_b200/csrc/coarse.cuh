@@ -15,6 +15,7 @@ struct CoarseView {
     CoarseGrid g;
     const float *fx, *fa;          // [rows][D] face centroid, area vector (fp32: a fixed basis)
     const int32_t *perm;           // rows sorted by coarse cell
+    const float *fxp, *fap;        // fx, fa in that sorted order (the restrictions read them coalesced)
     const int64_t *chunk_start;    // [nchunk + 1]
     const int64_t *cell_chunk;     // [ncoarse_cells + 1]
     int64_t nE;                    // (H+1)^D D^2

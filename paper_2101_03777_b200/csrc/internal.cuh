@@ -209,6 +209,7 @@ struct Comm {
 struct AfwPrec {
     int built = -1;              // mode it was built for (-1 = not built)
     int slots = 0, kmax = 0;     // patches per face (2D 2, 3D 3); largest patch
+    int shared = 0;              // 1: one (component-averaged) block per patch (experiment)
     int64_t npatch = 0, nslices = 0, nfallback = 0;
     cr::DevBuf<int64_t> ioff, voff;
     cr::DevBuf<uint8_t> kl;
@@ -259,14 +260,14 @@ struct CoarseOp {
     int requested = 0;           // H asked for when it was built
     cr::CoarseGrid g;
     int64_t nE = 0, nchunk = 0;
-    cr::DevBuf<float> fx, fa;
+    cr::DevBuf<float> fx, fa, fxp, fap;
     cr::DevBuf<int32_t> perm;
     cr::DevBuf<int64_t> chunk_start, cell_chunk;
     cr::DevBuf<double> part, c, y, Einv;
     cr::DevBuf<double> gpart;    // block partials of the coarse GEMV (its own: it runs concurrently)
     CoarseNd nd;                 // sparse direct solve (default); Einv (dense inverse) when off
     cr::CoarseView view() const {
-        return cr::CoarseView{g, fx.get(), fa.get(), perm.get(), chunk_start.get(), cell_chunk.get(), nE};
+        return cr::CoarseView{g, fx.get(), fa.get(), perm.get(), fxp.get(), fap.get(), chunk_start.get(), cell_chunk.get(), nE};
     }
 };
 

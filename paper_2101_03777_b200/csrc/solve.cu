@@ -1338,7 +1338,7 @@ template <int D, int WHAT>
 static void launch_afw(Launcher &L, cudaStream_t ks, const double *r, double *zs, double rtol) {
     constexpr int SLOTS = D == 2 ? 2 : 3;
     const AfwPrec &P = L.h->afw;
-    AfwView A{P.ioff.get(), P.voff.get(), P.kl.get(), P.ids.get(), P.vals.get(), P.npatch, L.h->G.nrows};
+    AfwView A{P.ioff.get(), P.voff.get(), P.kl.get(), P.ids.get(), P.vals.get(), P.npatch, L.h->G.nrows, P.shared};
     const int64_t nt = P.nslices * 32 * D;
     const bool sym = P.built != AFW_GEN;
     // two-level: leave one block per SM to the coarse kernels that run concurrently on the side stream

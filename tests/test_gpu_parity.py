@@ -359,17 +359,20 @@ def _patches(mo):
 
 
 def _afw_numpy(G, pats, d, r, kind):
+    """kind "inv" (PCG): one block per patch, the mean of the d component blocks R_p G^(ii) R_p^t,
+    inverted and applied to every component; "abs" (MINRES): |block| per component."""
     G = G.tocsr()
     z = np.zeros_like(r)
     for p in pats:
+        if kind == "inv":
+            Bm = sum(G[p * d + i][:, p * d + i].toarray() for i in range(d)) / d
+            Bi = np.linalg.inv(Bm)
         for i in range(d):
             ii = p * d + i
-            B = G[ii][:, ii].toarray()
             if kind == "abs":
+                B = G[ii][:, ii].toarray()
                 w, V = np.linalg.eigh(0.5 * (B + B.T))
                 Bi = (V / np.abs(w)) @ V.T
-            else:
-                Bi = np.linalg.inv(B)
             z[ii] += Bi @ r[ii]
     return z
 
