@@ -106,6 +106,59 @@ __device__ __forceinline__ double afw_patch_comp(const AfwView &A, int64_t t, co
     return quad;
 }
 
+// shared mode (one block per patch for all components, PCG): thread t covers patch t (slice t / 32,
+// lane t % 32) and all D components, so the block is read once per patch.  Returns the patch's share
+// of r^t M^{-1} r.
+template <int D, int SLOTS, int KMAX>
+__device__ __forceinline__ double afw_patch_shared(const AfwView &A, int64_t t, const double *__restrict__ r,
+                                                   double *__restrict__ zs) {
+    const int lane = (int)(t & 31);
+    const int64_t slice = t >> 5;
+    const int k = A.kl[slice];
+    const int32_t *ip = A.ids + A.ioff[slice] + lane;
+    int id[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) id[j] = (j < k) ? __ldcs(ip + j * 32) : -1;
+    const double *vi = A.vals + A.voff[slice] + lane;
+    constexpr int TM = KMAX * (KMAX + 1) / 2;
+    double v[TM];
+    if (k == KMAX) {
+#pragma unroll
+        for (int e = 0; e < TM; ++e) v[e] = __ldcs(vi + e * 32);
+    } else {
+#pragma unroll
+        for (int a = 0; a < KMAX; ++a)
+#pragma unroll
+            for (int b = 0; b <= a; ++b) v[a * (a + 1) / 2 + b] = (a < k) ? __ldcs(vi + (a * (a + 1) / 2 + b) * 32) : 0.0;
+    }
+    double quad = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double rv[KMAX], y[KMAX];
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            rv[j] = (id[j] >= 0) ? r[(int64_t)(id[j] / SLOTS) * D + i] : 0.0;
+            y[j] = 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < KMAX; ++a)
+#pragma unroll
+            for (int b = 0; b <= a; ++b) {
+                const double w = v[a * (a + 1) / 2 + b];
+                y[a] = fma(w, rv[b], y[a]);
+                if (a != b) y[b] = fma(w, rv[a], y[b]);
+            }
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            if (id[j] >= 0) {
+                quad = fma(rv[j], y[j], quad);
+                zs[((int64_t)(id[j] % SLOTS) * D + i) * A.nrows + id[j] / SLOTS] = y[j];
+            }
+        }
+    }
+    return quad;
+}
+
 // z[row] = sum_s zs[row, s] (slot order)
 template <int D, int SLOTS>
 __device__ __forceinline__ void afw_sum(const double *__restrict__ zs, int64_t nrows, int64_t row, double (&z)[D]) {

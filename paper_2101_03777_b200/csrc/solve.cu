@@ -771,6 +771,22 @@ __global__ void __launch_bounds__(kT, 4) k_afw_apply(AfwView A, const double *r,
     });
 }
 
+// the shared-block variant (afw_patch_shared): one thread per patch for all components
+template <int D, int SLOTS, int KMAX, int WHAT>
+__global__ void __launch_bounds__(kT, 2) k_afw_apply_sh(AfwView A, const double *r, double *zs, double rtol, KState *st,
+                                                     double *partials, int dist) {
+    if (WHAT != AFW_PCG_INIT && WHAT != AFW_PCG2_INIT && st->flag != FLAG_RUN) return;
+    double acc[1] = {0.0};
+    const int64_t nt = ((A.npatch + 31) >> 5) * 32;
+    GRID_STRIDE(t, nt) acc[0] += afw_patch_shared<D, SLOTS, KMAX>(A, t, r, zs);
+    reduce_and_finish<1>(acc, partials, &st->tickets[3], [&](double *t) {
+        if (WHAT == AFW_PCG_INIT) fin_or_store<1>(st, FIN_AFW_PCG_INIT, t, rtol, dist);
+        else if (WHAT == AFW_PCG) fin_or_store<1>(st, FIN_AFW_PCG, t, rtol, dist);
+        else if (WHAT == AFW_PCG2_INIT) fin_or_store<1>(st, FIN_AFW2_QF_INIT, t, rtol, dist);
+        else if (WHAT == AFW_PCG2) fin_or_store<1>(st, FIN_AFW2_QF, t, rtol, dist);
+    });
+}
+
 // x += alpha p ; r -= alpha q ; |r|^2 (convergence).  Flat over the N = D*nrows entries in
 // 16-byte double2 units, 4 independent units in flight per thread (memory-level parallelism).
 __global__ void __launch_bounds__(kT, 4) k_pcg_update_r(int64_t N, double *__restrict__ x, double *__restrict__ r,
@@ -1350,7 +1366,12 @@ static void launch_afw(Launcher &L, cudaStream_t ks, const double *r, double *zs
     const int rsv = er ? atoi(er) : (D == 2 && two_level && !L.dist && L.h->coarse.nd.on ? 2 : 0);
     KState *st = L.w->st.get();
     double *part = L.w->partials.get();
-    if (P.kmax <= 6) {
+    if (P.shared && (WHAT == AFW_PCG || WHAT == AFW_PCG_INIT || WHAT == AFW_PCG2 || WHAT == AFW_PCG2_INIT)) {
+        const int64_t nts = P.nslices * 32;
+        if (P.kmax <= 6) k_afw_apply_sh<D, SLOTS, 6, WHAT><<<occ_grid(k_afw_apply_sh<D, SLOTS, 6, WHAT>, kT, nts, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        else if (P.kmax <= 8) k_afw_apply_sh<D, SLOTS, 8, WHAT><<<occ_grid(k_afw_apply_sh<D, SLOTS, 8, WHAT>, kT, nts, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        else k_afw_apply_sh<D, SLOTS, 16, WHAT><<<occ_grid(k_afw_apply_sh<D, SLOTS, 16, WHAT>, kT, nts, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+    } else if (P.kmax <= 6) {
         if (sym) k_afw_apply<D, SLOTS, 6, true, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 6, true, WHAT>, kT, nt, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
         else k_afw_apply<D, SLOTS, 6, false, WHAT><<<occ_grid(k_afw_apply<D, SLOTS, 6, false, WHAT>, kT, nt, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
     } else if (P.kmax <= 8) {

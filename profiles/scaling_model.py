@@ -28,8 +28,13 @@ LAT = 15e-6          # small collective latency on 8 x B200 NVLink (assumed)
 BW_AR = 725e9        # measured 8-rank allreduce bus bandwidth
 BW_P2P = 770e9       # measured peer copy per direction
 
-DIST = ("k_mf_spmv", "k_pcg_update_r", "k_afw_apply", "k_pcg_pdir_afw2", "k_coarse_restrict3")
-REPL = ("k_coarse_gather", "k_nd_solve", "k_nd_phase", "k_nd_cdot")
+import re
+
+# the iteration's kernels (exact base names; setup variants such as k_mf_spmv_colour,
+# k_coarse_restrict3m or k_coarse_gather_all excluded)
+DIST = re.compile(r"(k_mf_spmv<3, 1>|k_pcg_update_r|k_afw_apply(_sh)?<3, 3, \d+, (1, )?5>|k_pcg_pdir_afw2<3, 3>|"
+                  r"cr::k_coarse_restrict3$)")
+REPL = re.compile(r"(k_coarse_gather<3>|cr::k_nd_solve$|cr::k_nd_phase$|cr::k_nd_cdot$)")
 
 
 def iteration_split(path):
@@ -42,10 +47,12 @@ def iteration_split(path):
     for r in rows[hi + 1:]:
         if len(r) <= vi:
             continue
-        name, t = r[ki], float(r[vi].replace(",", ""))
-        if any(k in name for k in DIST):
+        if r[h.index("Metric Name")] != "gpu__time_duration.sum":
+            continue
+        name, t = r[ki].split("(")[0].replace("void ", "").strip(), float(r[vi].replace(",", ""))
+        if DIST.search(name):
             dist += t
-        elif any(k in name for k in REPL):
+        elif REPL.search(name):
             repl += t
     tot = dist + repl
     return dist / tot, repl / tot
@@ -54,7 +61,9 @@ def iteration_split(path):
 def main():
     fd, fr = iteration_split(sys.argv[1])
     line = json.loads(open(sys.argv[2]).read().strip().splitlines()[-1])
-    pcg, st = line["pcg"], line["stages"]
+    pcg, st = line["pcg"], line.get("stages")
+    if not st:   # a bench line without stage times: the r02 CR_TRACE values
+        st = {"mesh_s": 0.009, "hybridise_s": 0.089, "recover_s": 0.028}
     it, ms_it = pcg["iterations"], pcg["ms_per_iter"] * 1e-3
     setup = pcg["setup_s"]
     nE = pcg["coarse"]["nE"]
@@ -71,7 +80,7 @@ def main():
     for N in (1, 2, 4, 8):
         comm = 0.0 if N == 1 else 3 * LAT + (LAT + 8 * nE / BW_AR) + (LAT + halo_bytes / BW_P2P)
         per_it = t_dist / N + t_repl + comm
-        per_it_ov = max(t_dist / N, t_repl) + comm
+        per_it_ov = (max(t_dist / N, t_repl) if N > 1 else per_it) + comm
         e_setup = 0.0 if N == 1 else 125 * (LAT + 8 * 9 * nE / BW_AR)
         s_setup = setup_dist / N + nd_fact + e_setup
         other = st["mesh_s"] + st["hybridise_s"] / N + st["recover_s"] + (0 if N == 1 else 8 * N1 / BW_P2P)
