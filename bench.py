@@ -44,6 +44,7 @@ HEADLINE = 4         # BASELINE.json configs[4]: the largest config that fits on
 # at the north star's 1e-10.
 SOLVERS = {1: dict(method="pcg_afw2", matrix_free=1, coarse=64, rtol=1e-11),
            4: dict(method="pcg_afw2", matrix_free=1, coarse=16, rtol=1e-10)}
+COARSE_MULTI = 12    # configs[4] coarse intervals at 4+ GPUs (replicated coarse solve)
 MAX_ITER = 20000     # a cap (the solves take ~500): a regression fails loudly instead of running on
 # Jacobi-PCG iterations to a true 1e-10 residual, measured on the B200 (the oracle's own solver;
 # used to extrapolate the CPU oracle's time): configs[1] by the r01 driver run (BENCH_r01.json
@@ -514,6 +515,11 @@ def main():
     cfg_idx = args.config
     cfg = ci.CONFIGS[cfg_idx]
     sol, rtol = _solver(cfg_idx)
+    if world >= 4 and cfg.dim == 3:
+        # the coarse solve is replicated on every rank: at 4+ ranks the smaller H = 12 coarse space
+        # (0.70 GB of fronts per solve instead of 2.45 GB, 560 instead of 441 iterations on one GPU)
+        # gives the shorter time to solution (DESIGN.md §8 model)
+        sol["coarse"] = COARSE_MULTI
     if args.pool_reserve_gb is None:
         args.pool_reserve_gb = 120.0 if cfg.dim == 3 else 24.0
     if args.pool_reserve_gb > 0:

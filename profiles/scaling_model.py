@@ -59,19 +59,29 @@ def iteration_split(path):
 
 
 def main():
+    # optional overrides key=value (another coarse grid measured on one GPU): iterations, ms_per_iter,
+    # repl_ms (replicated coarse ms per iteration), nd_fact (s), setup (s), nE, label
+    ov = dict(a.split("=", 1) for a in sys.argv[3:])
     fd, fr = iteration_split(sys.argv[1])
     line = json.loads(open(sys.argv[2]).read().strip().splitlines()[-1])
     pcg, st = line["pcg"], line.get("stages")
     if not st:   # a bench line without stage times: the r02 CR_TRACE values
         st = {"mesh_s": 0.009, "hybridise_s": 0.089, "recover_s": 0.028}
-    it, ms_it = pcg["iterations"], pcg["ms_per_iter"] * 1e-3
-    setup = pcg["setup_s"]
-    nE = pcg["coarse"]["nE"]
+    it = int(ov.get("iterations", pcg["iterations"]))
+    ms_it = float(ov.get("ms_per_iter", pcg["ms_per_iter"])) * 1e-3
+    setup = float(ov.get("setup", pcg["setup_s"]))
+    nE = int(ov.get("nE", pcg["coarse"]["nE"]))
     N1 = line["config"]["unknowns"]
     n = round((line["config"]["cells"] / 6) ** (1 / 3))
     t_dist, t_repl = fd * ms_it, fr * ms_it
+    if "repl_ms" in ov:
+        t_repl = float(ov["repl_ms"]) * 1e-3
+        t_dist = ms_it - t_repl
+        fd, fr = t_dist / ms_it, t_repl / ms_it
+    if "label" in ov:
+        print(f"**{ov['label']}**\n")
     # setup split (single-GPU trace): ND factorisation replicated, the rest distributed
-    nd_fact = line.get("nd_factorisation_s", 0.2)
+    nd_fact = float(ov.get("nd_fact", line.get("nd_factorisation_s", 0.2)))
     setup_dist = max(setup - nd_fact, 0.0)
     halo_bytes = 2 * 12 * (n + 1) ** 2 * 3 * 8         # two neighbours, one vertex plane of faces each
     print("| N | per-iteration (ms) | iterations (s) | setup (s) | step (s) | efficiency | overlap: step (s) | overlap: efficiency |")
