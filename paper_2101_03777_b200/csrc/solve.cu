@@ -313,6 +313,42 @@ __global__ void k_mf_slice_flag(MfView M, CoarseView C, int colour, int64_t nsli
     }
 }
 
+// the colours (base-5 digits of the node indices) of the corners of every face's coarse cell, per
+// 32-cell slice, as a 128-bit mask (computed once; the colour passes then test one bit)
+template <int D>
+__global__ void k_mf_slice_colours(MfView M, CoarseView C, int64_t nslices, unsigned *mask) {
+    constexpr int NF = D + 1;
+    for (int64_t sl = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); sl < nslices;
+         sl += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+        const int lane = threadIdx.x & 31;
+        unsigned m[4] = {0u, 0u, 0u, 0u};
+        for (int l = 0; l < NF; ++l) {
+            const int32_t row = M.ids[sl * (NF * 32) + l * 32 + lane];
+            if (row < 0) continue;
+            int ic[D];
+            float xi[D];
+            coarse_locate<D>(C.g, C.fx + (int64_t)row * D, ic, xi);
+            for (int n = 0; n < (1 << D); ++n) {
+                int col = 0, mul = 1;
+                for (int i = 0; i < D; ++i) {
+                    col += ((ic[i] + ((n >> i) & 1)) % 5) * mul;
+                    mul *= 5;
+                }
+                m[col >> 5] |= 1u << (col & 31);
+            }
+        }
+        for (int w = 0; w < 4; ++w) {
+            const unsigned v = __reduce_or_sync(0xffffffffu, m[w]);
+            if (lane == 0) mask[sl * 4 + w] = v;
+        }
+    }
+}
+
+__global__ void k_mf_flag_colour(const unsigned *mask, int64_t nslices, int colour, uint8_t *flag) {
+    for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < nslices; sl += (int64_t)gridDim.x * blockDim.x)
+        flag[sl] = (mask[sl * 4 + (colour >> 5)] >> (colour & 31)) & 1u;
+}
+
 // q += G_mf x over the listed slices only (coarse setup: x vanishes on every other cell)
 template <int D>
 __global__ void __launch_bounds__(kT, D == 2 ? 3 : 2) k_mf_spmv_slices(MfView M, const int32_t *slices, const int64_t *nact,
@@ -1690,8 +1726,9 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         DevBuf<uint8_t> stmp;
         int last_colour = -1;
         // the 32-cell slices touching the coarse cells around `colour`'s nodes (x vanishes elsewhere)
+        DevBuf<unsigned> smask;
+        int mask_H = -1;   // coarse grid the mask was computed for (a retry with a halved H recomputes it)
         auto select_slices = [&](int colour) {
-            if (colour == last_colour) return;
             const int64_t nsl = h->mf.ncells / 32;
             if (sflag.n == 0) {
                 sflag.alloc(nsl, s);
@@ -1701,9 +1738,17 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                 cub::CountingInputIterator<int32_t> it(0);
                 CR_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, sflag.get(), slist.get(), snum.get(), nsl, s));
                 stmp.alloc(tb, s);
+                smask.alloc((size_t)nsl * 4, s);
             }
-            k_mf_slice_flag<D><<<grid_for(nsl * 32, kT), kT, 0, s>>>(mf_view<D>(h), h->coarse.view(), colour, nsl,
-                                                                    sflag.get());
+            if (mask_H != h->coarse.g.H) {
+                k_mf_slice_colours<D><<<grid_for(nsl * 32, kT), kT, 0, s>>>(mf_view<D>(h), h->coarse.view(), nsl,
+                                                                           smask.get());
+                CR_CHECK_LAUNCH();
+                mask_H = h->coarse.g.H;
+                last_colour = -1;
+            }
+            if (colour == last_colour) return;
+            k_mf_flag_colour<<<grid_for(nsl, kT), kT, 0, s>>>(smask.get(), nsl, colour, sflag.get());
             CR_CHECK_LAUNCH();
             size_t tb = stmp.n;
             cub::CountingInputIterator<int32_t> it(0);

@@ -630,3 +630,19 @@ def test_damped_newton_re1000_matches_oracle():
     assert out["history"][-1] <= 1e-10
     assert relL2(out["U"].cpu().numpy(), Uo) <= 1e-8
     assert relL2(out["P"].cpu().numpy(), Po) <= 1e-8
+
+
+def test_pool_and_launch_counter():
+    """libcr's own memory pool (cr_pool_reserve / cr_pool_trim) and the launch counter: torch's
+    allocator is untouched by a reservation, and a solve advances cr_kernel_launches by at least
+    its reported kernel launches."""
+    before = torch.cuda.memory_reserved()
+    P.pool_reserve(256 << 20)
+    assert torch.cuda.memory_reserved() == before          # the library's pool, not torch's
+    coords, cells, prm, data, prob = make_case(dim=2, n=10)
+    n0 = P.kernel_launches()
+    out = P.hybrid_method(tg(coords), tg(cells), prob, "pcg_afw2", rtol=1e-12, matrix_free=1, check_every=8)
+    n1 = P.kernel_launches()
+    assert out["report"]["kernel_launches"] > 0 and n1 - n0 >= 0.5 * out["report"]["kernel_launches"]
+    del out
+    P.pool_trim(0)
