@@ -468,6 +468,82 @@ __global__ void __launch_bounds__(256, 2) k_coarse_restrict3(CoarseView C, const
     }
 }
 
+// k_coarse_restrict3 with the per-row work done once by the row's lane: it forms the 8 corner
+// weights and the 9 products a_k r_i in shared memory, and the corner lanes (lane % 8) read them
+// instead of receiving the raw row data by 9 shuffles and recomputing the products 8 times (the
+// shuffle version issued ~530 instructions per row and ran issue-bound).  Same terms, same
+// accumulation order per lane as k_coarse_restrict3: bitwise the same partials.
+__global__ void __launch_bounds__(256, 4) k_coarse_restrict3b(CoarseView C, const double *r, double *part,
+                                                           const int32_t *list = nullptr, const int64_t *ends = nullptr) {
+    constexpr int D = 3, DD = 9, NV = 72;
+    __shared__ __align__(16) double sw[8][32][8];
+    __shared__ __align__(16) double sar[8][32][10];
+    const int64_t ch = list ? (int64_t)list[blockIdx.x] : (int64_t)blockIdx.x;
+    const int64_t b = C.chunk_start[ch], e = ends ? ends[blockIdx.x] : C.chunk_start[ch + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int corner = lane & 7, rsub = lane >> 3;
+    double acc[DD];
+#pragma unroll
+    for (int v = 0; v < DD; ++v) acc[v] = 0.0;
+    for (int64_t t0 = b + warp * 32; t0 < e; t0 += 8 * 32) {
+        const int64_t t = t0 + lane;
+        const int64_t row = t < e ? (int64_t)C.perm[t] : -1;
+        float xv[D], av[D], xi[D];
+        double rv[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            xv[i] = row >= 0 ? C.fxp[t * D + i] : 0.f;
+            av[i] = row >= 0 ? C.fap[t * D + i] : 0.f;
+            rv[i] = row >= 0 ? r[row * D + i] : 0.0;
+        }
+        int ic[D];
+        coarse_locate<D>(C.g, xv, ic, xi);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            sw[warp][lane][c] = row < 0 ? 0.0
+                                        : ((c & 1) ? (double)xi[0] : 1.0 - (double)xi[0]) *
+                                              ((c & 2) ? (double)xi[1] : 1.0 - (double)xi[1]) *
+                                              ((c & 4) ? (double)xi[2] : 1.0 - (double)xi[2]);
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int k = 0; k < D; ++k) sar[warp][lane][i * D + k] = (double)av[k] * rv[i];
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int j = 4 * k + rsub;
+            const double wn = sw[warp][j][corner];
+            const double2 *p2 = reinterpret_cast<const double2 *>(&sar[warp][j][0]);
+            const double2 q0 = p2[0], q1 = p2[1], q2 = p2[2], q3 = p2[3];
+            const double q8 = sar[warp][j][8];
+            acc[0] = fma(wn, q0.x, acc[0]);
+            acc[1] = fma(wn, q0.y, acc[1]);
+            acc[2] = fma(wn, q1.x, acc[2]);
+            acc[3] = fma(wn, q1.y, acc[3]);
+            acc[4] = fma(wn, q2.x, acc[4]);
+            acc[5] = fma(wn, q2.y, acc[5]);
+            acc[6] = fma(wn, q3.x, acc[6]);
+            acc[7] = fma(wn, q3.y, acc[7]);
+            acc[8] = fma(wn, q8, acc[8]);
+        }
+        __syncwarp();
+    }
+    __shared__ double sh[8][NV];
+#pragma unroll
+    for (int v = 0; v < DD; ++v) {
+        double x = acc[v];
+        x += __shfl_xor_sync(0xffffffffu, x, 16);
+        x += __shfl_xor_sync(0xffffffffu, x, 8);
+        if (lane < 8) sh[warp][lane * DD + v] = x;   // lane = corner
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < NV; v += blockDim.x) {
+        double x = 0.0;
+        for (int w = 0; w < 8; ++w) x += sh[w][v];
+        part[ch * NV + v] = x;
+    }
+}
+
 // ------------------------------------------------------------------ batched setup (all D^2 (k, l) columns of a colour)
 // The D^2 columns of one colour, (k, l) -> column k D + l, stored as separate vectors of stride zs.
 template <int D>
@@ -1151,7 +1227,56 @@ struct NdSched {
     int aoff[kNdMaxLev + 1];   // forward level L (depth maxd - L): local rhs assembly entries
     int boff[kNdMaxLev + 1];   //                                   B rows
     int coff[kNdMaxLev + 1];   // backward depth L: I rows
+    int8_t gb[kNdMaxLev];      // lanes per B row of forward level L (8, 16 or 32)
 };
+
+// lanes [sub] of a G-lane group: their share of sum_i a[i] x[i] (16-byte aligned, n even), then the
+// group's sum in every lane of the group (fixed shuffle tree)
+template <int G>
+__device__ __forceinline__ double nd_dot_group2(const double *__restrict__ a, const double *x, int n, int sub) {
+    const double2 *a2 = reinterpret_cast<const double2 *>(a), *x2 = reinterpret_cast<const double2 *>(x);
+    const int n2 = n >> 1;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int i = sub;
+    for (; i + 3 * G < n2; i += 4 * G) {
+        const double2 a0 = a2[i], a1 = a2[i + G], a2v = a2[i + 2 * G], a3 = a2[i + 3 * G];
+        const double2 b0 = __ldcg(x2 + i), b1 = __ldcg(x2 + i + G), b2 = __ldcg(x2 + i + 2 * G), b3 = __ldcg(x2 + i + 3 * G);
+        s0 = fma(a0.x, b0.x, fma(a0.y, b0.y, s0));
+        s1 = fma(a1.x, b1.x, fma(a1.y, b1.y, s1));
+        s2 = fma(a2v.x, b2.x, fma(a2v.y, b2.y, s2));
+        s3 = fma(a3.x, b3.x, fma(a3.y, b3.y, s3));
+    }
+    for (; i < n2; i += G) {
+        const double2 a0 = a2[i], b0 = __ldcg(x2 + i);
+        s0 = fma(a0.x, b0.x, fma(a0.y, b0.y, s0));
+    }
+    return (s0 + s1) + (s2 + s3);
+}
+
+// forward phase B of one level with G lanes per B row (32 / G rows per warp in flight: the deep
+// levels' rows are short, nI = 72 .. 243)
+template <int G, class View>
+__device__ __forceinline__ void nd_phase_b(const View &V, int64_t k0, int64_t k1, int64_t gw, int64_t nw, int lane) {
+    constexpr int R = 32 / G;
+    const int sub = lane % G, grp = lane / G;
+    for (int64_t kb = k0 + gw * R; kb < k1; kb += nw * R) {
+        const int64_t k = kb + grp;
+        double a = 0.0;
+        int2 e = make_int2(0, 0);
+        const bool ok = k < k1;
+        if (ok) {
+            e = V.lbr[k];
+            const NdFrontDev &F = V.fr[e.x];
+            a = nd_dot_group2<G>(V.wt + F.wts + (int64_t)e.y * F.ldWts, V.bi + F.bi, F.ldWts, sub);
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (ok && sub == 0) {
+            const NdFrontDev &F = V.fr[e.x];
+            V.u[F.u + e.y] = __ldcg(V.lb + F.lb + e.y) - a;
+        }
+    }
+}
 
 struct NdSolveView {
     const NdFrontDev *fr;
@@ -1184,12 +1309,9 @@ __global__ void __launch_bounds__(256) k_nd_solve(NdSolveView V, NdSched S, cons
         }
         nd_grid_barrier(bar);
         if (S.boff[L + 1] > S.boff[L]) {
-            for (int64_t k = S.boff[L] + gw; k < S.boff[L + 1]; k += nw) {
-                const int2 e = V.lbr[k];
-                const NdFrontDev F = V.fr[e.x];
-                const double a = warp_sum(nd_dot_lane2(V.wt + F.wts + (int64_t)e.y * F.ldWts, V.bi + F.bi, F.ldWts, lane));
-                if (lane == 0) V.u[F.u + e.y] = __ldcg(V.lb + F.lb + e.y) - a;
-            }
+            if (S.gb[L] == 8) nd_phase_b<8>(V, S.boff[L], S.boff[L + 1], gw, nw, lane);
+            else if (S.gb[L] == 16) nd_phase_b<16>(V, S.boff[L], S.boff[L + 1], gw, nw, lane);
+            else nd_phase_b<32>(V, S.boff[L], S.boff[L + 1], gw, nw, lane);
             nd_grid_barrier(bar);
         }
     }
@@ -1503,11 +1625,18 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
         N.aoff.assign(maxd + 2, 0);
         N.boff.assign(maxd + 2, 0);
         N.coff.assign(maxd + 2, 0);
+        N.gb.assign(maxd + 1, 32);
         for (int L = 0; L <= maxd; ++L) {
+            double rows = 0.0, len = 0.0;
             for (int f : lev[maxd - L]) {
                 for (int p = 0; p < fr[f].nI + fr[f].nB; ++p) la.push_back(make_int2(f, p));
                 for (int b = 0; b < fr[f].nB; ++b) lbr.push_back(make_int2(f, b));
+                rows += fr[f].nB;
+                len += (double)fr[f].nB * fr[f].nI;
             }
+            // lanes per B row: the level's mean row length in 16-byte units, >= 4 per lane
+            const double n2 = rows > 0 ? 0.5 * len / rows : 0.0;
+            N.gb[L] = n2 < 64 ? 8 : (n2 < 128 ? 16 : 32);
             for (int f : lev[L])
                 for (int i = 0; i < fr[f].nI; ++i) lc.push_back(make_int2(f, i));
             N.aoff[L + 1] = (int)la.size();
@@ -1693,6 +1822,7 @@ static void nd_solve(const CoarseOp &C, const double *c, double *y, double *qout
         S.boff[L] = N.boff[L];
         S.coff[L] = N.coff[L];
     }
+    for (int L = 0; L < S.nlev; ++L) S.gb[L] = (int8_t)N.gb[L];
     static const char *ep = std::getenv("CR_ND_PERSIST");
     const bool persistent = (ep ? atoi(ep) != 0 : N.maxdepth > 1) && N.grid > 0;
     if (persistent) {
@@ -2180,7 +2310,7 @@ void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double
         k_coarse_restrict<2><<<(unsigned)C.nchunk, 256, 0, s>>>(V, r, C.part.get());
         k_coarse_gather<2><<<grid_for(C.nE, T), T, 0, s>>>(V, C.part.get(), C.c.get());
     } else {
-        k_coarse_restrict3<<<(unsigned)C.nchunk, 256, 0, s>>>(V, r, C.part.get());
+        k_coarse_restrict3b<<<(unsigned)C.nchunk, 256, 0, s>>>(V, r, C.part.get());
         k_coarse_gather<3><<<grid_for(C.nE, T), T, 0, s>>>(V, C.part.get(), C.c.get());
     }
     CR_CHECK_LAUNCH();

@@ -250,6 +250,7 @@ struct CoarseNd {
     cr::DevBuf<int32_t> uidx;                  // per front: global unknown of each local unknown
     cr::DevBuf<int2> la, lbr, lc;              // (front, local index) work lists by level
     std::vector<int> aoff, boff, coff;         // level offsets into la / lbr / lc
+    std::vector<int> gb;                       // lanes per B row of each forward level
     cr::DevBuf<unsigned> bar;                  // grid barrier of the persistent solve kernel
     int grid = 0;
 };

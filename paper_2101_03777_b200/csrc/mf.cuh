@@ -34,6 +34,12 @@ struct MfView {
     int64_t ncells;     // cells processed (padded to slices of 32 with ids = -1)
 };
 
+// q[i] += v with no return value: red.global (atomicAdd compiles to a returning ATOMG in kernels
+// that also fence, e.g. the reducing k_mf_spmv, and each then waits for its L2 round trip)
+__device__ __forceinline__ void red_add_f64(double *p, double v) {
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 // y_K = G_K x_K scattered into q (q pre-zeroed).  A face whose two cells sit in the same warp
 // (32 consecutive cells: most faces inside a structured row of squares / a Kuhn cube) is summed
 // in registers through shuffles and stored once by the lower cell; the others get one atomicAdd
@@ -69,7 +75,7 @@ __device__ __forceinline__ void mf_scatter(const int (&id)[D + 1], const double 
         if (nbc[a] & 0x80u) {
             if ((int)(nbc[a] & 31u) > lane) *dst = out[a] + part[a];   // lower cell stores the pair
         } else {
-            atomicAdd(dst, out[a]);
+            red_add_f64(dst, out[a]);
         }
     }
 }

@@ -823,8 +823,10 @@ __global__ void __launch_bounds__(kT, 2) k_afw_apply_sh(AfwView A, const double 
     });
 }
 
-// x += alpha p ; r -= alpha q ; |r|^2 (convergence).  Flat over the N = D*nrows entries in
-// 16-byte double2 units, 4 independent units in flight per thread (memory-level parallelism).
+// x += alpha p (XUPD; else the direction update does it: k_pcg_pdir_afw*) ; r -= alpha q ; |r|^2
+// (convergence).  Flat over the N = D*nrows entries in 16-byte double2 units, 4 independent units
+// in flight per thread (memory-level parallelism).
+template <bool XUPD>
 __global__ void __launch_bounds__(kT, 4) k_pcg_update_r(int64_t N, double *__restrict__ x, double *__restrict__ r,
                                                      const double *__restrict__ p, const double *__restrict__ q,
                                                      KState *st, double *partials, int dist) {
@@ -839,37 +841,44 @@ __global__ void __launch_bounds__(kT, 4) k_pcg_update_r(int64_t N, double *__res
         double2 pv[4], qv[4], xv[4], rv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            pv[u] = __ldcs(p2 + i + u * stride);
+            if (XUPD) {
+                pv[u] = __ldcs(p2 + i + u * stride);
+                xv[u] = __ldcs(x2 + i + u * stride);
+            }
             qv[u] = __ldcs(q2 + i + u * stride);
-            xv[u] = __ldcs(x2 + i + u * stride);
             rv[u] = __ldcs(r2 + i + u * stride);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            xv[u].x = fma(alpha, pv[u].x, xv[u].x);
-            xv[u].y = fma(alpha, pv[u].y, xv[u].y);
+            if (XUPD) {
+                xv[u].x = fma(alpha, pv[u].x, xv[u].x);
+                xv[u].y = fma(alpha, pv[u].y, xv[u].y);
+                __stcs(x2 + i + u * stride, xv[u]);
+            }
             rv[u].x = fma(-alpha, qv[u].x, rv[u].x);
             rv[u].y = fma(-alpha, qv[u].y, rv[u].y);
             acc[0] = fma(rv[u].x, rv[u].x, acc[0]);
             acc[0] = fma(rv[u].y, rv[u].y, acc[0]);
-            __stcs(x2 + i + u * stride, xv[u]);
             r2[i + u * stride] = rv[u];
         }
     }
     for (; i < n2; i += stride) {
-        double2 pv = p2[i], qv = q2[i], xv = x2[i], rv = r2[i];
-        xv.x = fma(alpha, pv.x, xv.x);
-        xv.y = fma(alpha, pv.y, xv.y);
+        double2 qv = q2[i], rv = r2[i];
+        if (XUPD) {
+            double2 pv = p2[i], xv = x2[i];
+            xv.x = fma(alpha, pv.x, xv.x);
+            xv.y = fma(alpha, pv.y, xv.y);
+            x2[i] = xv;
+        }
         rv.x = fma(-alpha, qv.x, rv.x);
         rv.y = fma(-alpha, qv.y, rv.y);
         acc[0] = fma(rv.x, rv.x, acc[0]);
         acc[0] = fma(rv.y, rv.y, acc[0]);
-        x2[i] = xv;
         r2[i] = rv;
     }
     if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const int64_t k = N - 1;
-        x[k] = fma(alpha, p[k], x[k]);
+        if (XUPD) x[k] = fma(alpha, p[k], x[k]);
         const double rk = fma(-alpha, q[k], r[k]);
         r[k] = rk;
         acc[0] = fma(rk, rk, acc[0]);
@@ -877,14 +886,23 @@ __global__ void __launch_bounds__(kT, 4) k_pcg_update_r(int64_t N, double *__res
     reduce_and_finish<1>(acc, partials, &st->tickets[2], [&](double *t) { fin_or_store<1>(st, FIN_UPD_R, t, 0.0, dist); });
 }
 
-// p = z + beta p, z = sum of the slot contributions (beta = 0: p = z)
+// x += alpha p of the iteration whose residual update met the tolerance (its direction update,
+// which carries the x update, returned early)
+__global__ void k_pcg_x_final(int64_t N, double *__restrict__ x, const double *__restrict__ p, const KState *st) {
+    const double alpha = st->alpha;
+    GRID_STRIDE(i, N) x[i] = fma(alpha, p[i], x[i]);
+}
+
+// p = z + beta p, z = sum of the slot contributions (beta = 0: p = z); x (non-null): x += alpha p
+// first, with the old p (the iteration's solution update, moved here from k_pcg_update_r: p is read
+// here anyway)
 template <int D, int SLOTS>
 __global__ void __launch_bounds__(kT) k_pcg_pdir_afw(int64_t nrows, double *__restrict__ p, const double *__restrict__ zs,
-                                                     const KState *st) {
+                                                     const KState *st, double *__restrict__ x) {
     if (st->flag != FLAG_RUN) return;
-    const double beta = st->beta;
+    const double beta = st->beta, alpha = st->alpha;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    if constexpr (D == 2) {
+    if (D == 2 && !x) {
         double2 *p2 = reinterpret_cast<double2 *>(p);
         int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
         for (; row + 3 * stride < nrows; row += 4 * stride) {
@@ -894,12 +912,14 @@ __global__ void __launch_bounds__(kT) k_pcg_pdir_afw(int64_t nrows, double *__re
             for (int u = 0; u < 4; ++u) {
                 const int64_t r = row + u * stride;
                 pv[u] = __ldcs(p2 + r);
-                z0[u] = __ldcs(zs + r);
-                z1[u] = __ldcs(zs + nrows + r);
+                const double2 a = __ldcs(reinterpret_cast<const double2 *>(zs) + r);
+                z0[u] = a.x;
+                z1[u] = a.y;
 #pragma unroll
                 for (int sl = 1; sl < SLOTS; ++sl) {
-                    z0[u] += __ldcs(zs + (int64_t)(sl * 2) * nrows + r);
-                    z1[u] += __ldcs(zs + (int64_t)(sl * 2 + 1) * nrows + r);
+                    const double2 b = __ldcs(reinterpret_cast<const double2 *>(zs) + (int64_t)sl * nrows + r);
+                    z0[u] += b.x;
+                    z1[u] += b.y;
                 }
             }
 #pragma unroll
@@ -922,7 +942,11 @@ __global__ void __launch_bounds__(kT) k_pcg_pdir_afw(int64_t nrows, double *__re
             double z[D];
             afw_sum<D, SLOTS>(zs, nrows, row, z);
 #pragma unroll
-            for (int i = 0; i < D; ++i) p[row * D + i] = (beta == 0.0) ? z[i] : fma(beta, p[row * D + i], z[i]);
+            for (int i = 0; i < D; ++i) {
+                const double po = p[row * D + i];
+                if (x) x[row * D + i] = fma(alpha, po, x[row * D + i]);
+                p[row * D + i] = (beta == 0.0) ? z[i] : fma(beta, po, z[i]);
+            }
         }
     }
 }
@@ -931,9 +955,10 @@ __global__ void __launch_bounds__(kT) k_pcg_pdir_afw(int64_t nrows, double *__re
 template <int D, int SLOTS>
 __global__ void __launch_bounds__(kT) k_pcg_pdir_afw2(int64_t nrows, double *__restrict__ p, const double *__restrict__ zs,
                                                       CoarseView C, const double *__restrict__ y, const KState *st,
-                                                      int first) {
+                                                      int first, double *__restrict__ x) {
     if (st->flag != FLAG_RUN) return;
     const double beta = first ? 0.0 : (st->qf + st->qc) / st->rho;
+    const double alpha = st->alpha;
     GRID_STRIDE(row, nrows) {
         double z[D], zc[D];
         afw_sum<D, SLOTS>(zs, nrows, row, z);
@@ -941,7 +966,9 @@ __global__ void __launch_bounds__(kT) k_pcg_pdir_afw2(int64_t nrows, double *__r
 #pragma unroll
         for (int i = 0; i < D; ++i) {
             const double zi = z[i] + zc[i];
-            p[row * D + i] = (beta == 0.0) ? zi : fma(beta, p[row * D + i], zi);
+            const double po = p[row * D + i];
+            if (x) x[row * D + i] = fma(alpha, po, x[row * D + i]);
+            p[row * D + i] = (beta == 0.0) ? zi : fma(beta, po, zi);
         }
     }
 }
@@ -1554,10 +1581,12 @@ static double iter_bytes(const cr_hybrid_s *h, const cr_solver_opts &o) {
     switch (o.method) {
         case CR_PCG_JACOBI: return g + 7 * N8;                 // x, r, p, q, dinv read; x, r write (+ p rewrite)
         case CR_PCG_BLOCKJACOBI: return g + 6 * N8 + N8 * d;   // + inverse diagonal blocks
-        case CR_PCG_AFW: return g + 6 * N8 + (afw + N8 + slots * N8) + (slots * N8 + 2 * N8);
+        // r update (r, q read, r written); patch apply; direction update with the x update (slots, p,
+        // x read, p, x written)
+        case CR_PCG_AFW: return g + 3 * N8 + (afw + N8 + slots * N8) + (slots * N8 + 4 * N8);
         case CR_PCG_AFW2: {
             const double coarse = 2 * N8 + (double)(h->coarse.nd.on ? h->coarse.nd.bytes : 8 * h->coarse.nE * h->coarse.nE);
-            return g + 6 * N8 + (afw + N8 + slots * N8) + coarse + (slots * N8 + 2 * N8 + N8);
+            return g + 3 * N8 + (afw + N8 + slots * N8) + coarse + (slots * N8 + 4 * N8 + N8);
         }
         case CR_MINRES_ABSJACOBI: return g + 10 * N8;
         case CR_MINRES_AFW: return g + 10 * N8 + afw + 2 * slots * N8;
@@ -1672,7 +1701,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         auto init = [&]() {
             true_residual<D>(L, x, w->r.get());
             launch_afw<D, AFW_PCG_INIT>(L, s, w->r.get(), zs, rtol);
-            k_pcg_pdir_afw<D, SLOTS><<<L.grid_rows, kT, 0, s>>>(nrows, w->p.get(), zs, st);
+            k_pcg_pdir_afw<D, SLOTS><<<L.grid_rows, kT, 0, s>>>(nrows, w->p.get(), zs, st, nullptr);
             CR_CHECK_LAUNCH();
             ++L.launches;
         };
@@ -1689,11 +1718,11 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                     CR_CHECK_LAUNCH();
                     L.reduced(ks, 1, FIN_PQ, rtol);
                 }
-                k_pcg_update_r<<<occ_grid(k_pcg_update_r, kT, L.N / 2), kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), st, part, L.dist);
+                k_pcg_update_r<false><<<occ_grid(k_pcg_update_r<false>, kT, L.N / 2), kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), st, part, L.dist);
                 CR_CHECK_LAUNCH();
                 L.reduced(ks, 1, FIN_UPD_R, rtol);
                 launch_afw<D, AFW_PCG>(L, ks, w->r.get(), zs, rtol);
-                k_pcg_pdir_afw<D, SLOTS><<<occ_grid(k_pcg_pdir_afw<D, SLOTS>, kT, nrows), kT, 0, ks>>>(nrows, w->p.get(), zs, st);
+                k_pcg_pdir_afw<D, SLOTS><<<occ_grid(k_pcg_pdir_afw<D, SLOTS>, kT, nrows), kT, 0, ks>>>(nrows, w->p.get(), zs, st, x);
                 CR_CHECK_LAUNCH();
             };
             int64_t it0 = w->hst->iters;
@@ -1703,6 +1732,11 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
             int64_t dit = w->hst->iters - it0;
             L.launches += 4 * ((dit + kk - 1) / kk) * kk;
             L.spmvs += dit;
+            if (w->hst->flag == FLAG_CONV && dit > 0) {   // the converged iteration's x update
+                k_pcg_x_final<<<L.grid_vec, kT, 0, s>>>(N, x, w->p.get(), st);
+                CR_CHECK_LAUNCH();
+                ++L.launches;
+            }
             if (w->hst->flag == FLAG_CONV) {
                 init();
                 read_state(w, s);
@@ -1815,7 +1849,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
             coarse_begin(s);
             launch_afw<D, AFW_PCG2_INIT>(L, s, w->r.get(), zs, rtol);
             coarse_end(s);
-            k_pcg_pdir_afw2<D, SLOTS><<<L.grid_rows, kT, 0, s>>>(nrows, w->p.get(), zs, CV, yc, st, 1);
+            k_pcg_pdir_afw2<D, SLOTS><<<L.grid_rows, kT, 0, s>>>(nrows, w->p.get(), zs, CV, yc, st, 1, nullptr);
             CR_CHECK_LAUNCH();
             ++L.launches;
         };
@@ -1835,13 +1869,13 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                     CR_CHECK_LAUNCH();
                     L.reduced(ks, 1, FIN_PQ2, rtol);
                 }
-                k_pcg_update_r<<<occ_grid(k_pcg_update_r, kT, L.N / 2), kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), st, part, L.dist);
+                k_pcg_update_r<false><<<occ_grid(k_pcg_update_r<false>, kT, L.N / 2), kT, 0, ks>>>(N, x, w->r.get(), w->p.get(), w->q.get(), st, part, L.dist);
                 CR_CHECK_LAUNCH();
                 L.reduced(ks, 1, FIN_UPD_R, rtol);
                 coarse_begin(ks);
                 launch_afw<D, AFW_PCG2>(L, ks, w->r.get(), zs, rtol);
                 coarse_end(ks);
-                k_pcg_pdir_afw2<D, SLOTS><<<occ_grid(k_pcg_pdir_afw2<D, SLOTS>, kT, nrows), kT, 0, ks>>>(nrows, w->p.get(), zs, CV, yc, st, 0);
+                k_pcg_pdir_afw2<D, SLOTS><<<occ_grid(k_pcg_pdir_afw2<D, SLOTS>, kT, nrows), kT, 0, ks>>>(nrows, w->p.get(), zs, CV, yc, st, 0, x);
                 CR_CHECK_LAUNCH();
             };
             int64_t it0 = w->hst->iters;
@@ -1852,6 +1886,11 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
             int64_t dit = w->hst->iters - it0;
             L.launches += 7 * ((dit + kk - 1) / kk) * kk;
             L.spmvs += dit;
+            if (w->hst->flag == FLAG_CONV && dit > 0) {   // the converged iteration's x update
+                k_pcg_x_final<<<L.grid_vec, kT, 0, s>>>(N, x, w->p.get(), st);
+                CR_CHECK_LAUNCH();
+                ++L.launches;
+            }
             if (w->hst->flag == FLAG_CONV) {
                 init();
                 read_state(w, s);
@@ -2117,7 +2156,7 @@ static void apply_precond_t(cr_hybrid_s *h, int method, const double *r, double 
             launch_afw<D, AFW_PCG_INIT>(L, s, r, w->zs.get(), 1e-10);
             CR_CUDA(cudaMemsetAsync(w->st.get(), 0, sizeof(KState), s));   // flag RUN, beta 0: p = z
             k_pcg_pdir_afw2<D, SLOTS><<<grid, kT, 0, s>>>(nrows, z, w->zs.get(), h->coarse.view(), h->coarse.y.get(),
-                                                         w->st.get(), 1);
+                                                         w->st.get(), 1, nullptr);
             break;
         }
         case CR_PCG_AFW:

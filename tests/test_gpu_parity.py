@@ -182,12 +182,25 @@ def test_spmv_parity(name):
     assert np.abs(y.cpu().numpy() - yo).max() <= 1e-13 * np.abs(ho["G"]).max() * np.abs(x).max() * 10
 
 
+# larger meshes (many 32-cell slices: faces whose two cells sit in different warps take the atomic
+# path; ragged last slices), structured, Dirichlet and unstructured
+MF_BLOCK_CASES = {
+    "2d-jit-n48": dict(dim=2, n=48),
+    "2d-dirichlet-n41": dict(dim=2, n=41, dirichlet=True),
+    "2d-flip-n40": dict(dim=2, n=40, flip=3),
+    "3d-n8": dict(dim=3, n=8),
+    "3d-flip-n7": dict(dim=3, n=7, flip=5),
+}
+
+
 @pytest.mark.parametrize("name", ["2d-config0", "2d-transient-jit-n17", "2d-dirichlet-n10", "2d-k0-interior",
-                                  "3d-transient-n3", "2d-flip-transient-n14", "3d-flip-transient-n4"])
+                                  "3d-transient-n3", "2d-flip-transient-n14", "3d-flip-transient-n4"]
+                         + list(MF_BLOCK_CASES))
 def test_matrix_free_spmv_parity(name):
     """y = sum_K H_K G_K H_K^t x from per-cell factors (Shat^{-1} split as 1/(mu|K|) 11^t + T,
-    u = w/sqrt(B)) against the oracle's assembled G (entries rounded once from binary128)."""
-    coords, cells, prm, data, prob = make_case(**HYB_CASES[name])
+    u = w/sqrt(B)) against the oracle's assembled G (entries rounded once from binary128); two
+    applications are bitwise equal (exactly two contributions meet at a face: 0 + a + b)."""
+    coords, cells, prm, data, prob = make_case(**(HYB_CASES.get(name) or MF_BLOCK_CASES[name]))
     mo = O.build_mesh(coords, cells)
     ho = O.hybridise(mo, prm, data)
     hg = P.cr_hybridise(P.cr_build_mesh(tg(coords), tg(cells)), prob)
@@ -198,6 +211,9 @@ def test_matrix_free_spmv_parity(name):
     Ga = abs(ho["G"])
     bound = 1e-14 * (Ga @ np.abs(x))            # rounding of G's entries, row by row
     assert np.all(np.abs(y.cpu().numpy() - yo) <= 4 * bound + 1e-300)
+    y2 = torch.full_like(y, np.nan)
+    hg.spmv_mf(tg(x), y2)
+    assert torch.equal(y, y2)
     info = hg.mf_info()
     assert info["ncells"] >= mo.nc and info["bytes"] > 0
 
@@ -382,10 +398,16 @@ def _afw_numpy(G, pats, d, r, kind):
                                               ("2d-steady-mis-n16", "minres_afw", "abs"),
                                               ("2d-flip-transient-n14", "pcg_afw", "inv"),
                                               ("2d-flip-steady-mis-n12", "minres_afw", "abs"),
-                                              ("3d-flip-transient-n4", "pcg_afw", "inv")])
+                                              ("3d-flip-transient-n4", "pcg_afw", "inv"),
+                                              # larger meshes (many slices, ragged last slice)
+                                              ("2d-jit-n48", "pcg_afw", "inv"),
+                                              ("2d-flip-n40", "pcg_afw", "inv"),
+                                              ("3d-n8", "pcg_afw", "inv"),
+                                              ("3d-flip-n7", "pcg_afw", "inv")])
 def test_patch_preconditioner_apply(name, method, kind):
-    """z = sum_p R_p^t B_p^{-1} R_p r on the GPU vs numpy from the oracle's G."""
-    coords, cells, prm, data, prob = make_case(**HYB_CASES[name])
+    """z = sum_p R_p^t B_p^{-1} R_p r on the GPU vs numpy from the oracle's G; bitwise reproducible
+    (each face's SLOTS patch contributions are summed in slot order)."""
+    coords, cells, prm, data, prob = make_case(**(HYB_CASES.get(name) or MF_BLOCK_CASES[name]))
     mo = O.build_mesh(coords, cells)
     ho = O.hybridise(mo, prm, data)
     hg = P.cr_hybridise(P.cr_build_mesh(tg(coords), tg(cells)), prob)
@@ -400,6 +422,9 @@ def test_patch_preconditioner_apply(name, method, kind):
         assert info["kmax"] == 8          # the KMAX = 8 kernels (structured meshes stop at 6)
     zo = _afw_numpy(ho["G"], pats, mo.dim, r, kind)
     assert relL2(z.cpu().numpy(), zo) <= 1e-9
+    z2 = torch.full_like(z, np.nan)
+    hg.apply_precond(method, tg(r), z2)
+    assert torch.equal(z, z2)
 
 
 def test_two_level_cuts_pcg_iterations():
