@@ -912,14 +912,12 @@ __global__ void __launch_bounds__(kT) k_pcg_pdir_afw(int64_t nrows, double *__re
             for (int u = 0; u < 4; ++u) {
                 const int64_t r = row + u * stride;
                 pv[u] = __ldcs(p2 + r);
-                const double2 a = __ldcs(reinterpret_cast<const double2 *>(zs) + r);
-                z0[u] = a.x;
-                z1[u] = a.y;
+                z0[u] = __ldcs(zs + r);
+                z1[u] = __ldcs(zs + nrows + r);
 #pragma unroll
                 for (int sl = 1; sl < SLOTS; ++sl) {
-                    const double2 b = __ldcs(reinterpret_cast<const double2 *>(zs) + (int64_t)sl * nrows + r);
-                    z0[u] += b.x;
-                    z1[u] += b.y;
+                    z0[u] += __ldcs(zs + (int64_t)(sl * 2) * nrows + r);
+                    z1[u] += __ldcs(zs + (int64_t)(sl * 2 + 1) * nrows + r);
                 }
             }
 #pragma unroll
