@@ -1228,6 +1228,7 @@ struct NdSched {
     int boff[kNdMaxLev + 1];   //                                   B rows
     int coff[kNdMaxLev + 1];   // backward depth L: I rows
     int8_t gb[kNdMaxLev];      // lanes per B row of forward level L (8, 16 or 32)
+    int goff[kNdMaxLev + 1];   // backward depth L: y_B gather entries
 };
 
 // lanes [sub] of a G-lane group: their share of sum_i a[i] x[i] (16-byte aligned, n even), then the
@@ -1286,6 +1287,8 @@ struct NdSolveView {
     const double *finv, *w, *wt;
     double *bi, *lb, *u;
     const int2 *la, *lbr, *lc;
+    double *yb;
+    const int2 *lg;
 };
 
 // The whole solve E y = c in one persistent launch.  Per forward level: (A) every local
@@ -1316,11 +1319,21 @@ __global__ void __launch_bounds__(256) k_nd_solve(NdSolveView V, NdSched S, cons
         }
     }
     for (int L = 0; L < S.nlev; ++L) {
+        // (G) the level's y_B gathered once into a contiguous, zero-padded copy per front, so the
+        // pivot rows below stream it instead of an index -> y gather per element of W
+        if (S.goff[L + 1] > S.goff[L]) {
+            for (int64_t k = S.goff[L] + gt; k < S.goff[L + 1]; k += gs) {
+                const int2 e = V.lg[k];
+                const NdFrontDev &F = V.fr[e.x];
+                V.yb[F.yb + e.y] = e.y < F.nB ? __ldcg(y + V.uidx[F.uoff + F.nI + e.y]) : 0.0;
+            }
+            nd_grid_barrier(bar);
+        }
         for (int64_t k = S.coff[L] + gw; k < S.coff[L + 1]; k += nw) {
             const int2 e = V.lc[k];
             const NdFrontDev F = V.fr[e.x];
             const double pa = nd_dot_lane2(V.finv + F.fs + (int64_t)e.y * F.ldFs, V.bi + F.bi, F.ldFs, lane);
-            const double pb = nd_dot_lane2_g(V.w + F.ws + (int64_t)e.y * F.ldWs, y, V.uidx + F.uoff + F.nI, F.nB, lane);
+            const double pb = nd_dot_lane2(V.w + F.ws + (int64_t)e.y * F.ldWs, V.yb + F.yb, F.ldWs, lane);
             const double a = warp_sum(pa - pb);
             if (lane == 0) y[V.uidx[F.uoff + e.y]] = a;
         }
@@ -1636,7 +1649,8 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
             }
             // lanes per B row: the level's mean row length in 16-byte units, >= 4 per lane
             const double n2 = rows > 0 ? 0.5 * len / rows : 0.0;
-            N.gb[L] = n2 < 64 ? 8 : (n2 < 128 ? 16 : 32);
+            static const char *eg = std::getenv("CR_ND_GROUPS");   // 0: a warp per B row everywhere
+            N.gb[L] = (eg && atoi(eg) == 0) ? 32 : (n2 < 64 ? 8 : (n2 < 128 ? 16 : 32));
             for (int f : lev[L])
                 for (int i = 0; i < fr[f].nI; ++i) lc.push_back(make_int2(f, i));
             N.aoff[L + 1] = (int)la.size();
@@ -1776,7 +1790,7 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
     // dot product of the solve streams double2 (the odd D^2 = 9 unknowns per node made nI, nB odd)
     {
         auto ev = [](int64_t v) { return (v + 1) & ~(int64_t)1; };
-        int64_t ofs = 0, owts = 0, ows = 0;
+        int64_t ofs = 0, owts = 0, ows = 0, oyb = 0;
         std::vector<int64_t> pf(nf + 1, 0), pwt(nf + 1, 0), pw(nf + 1, 0);
         for (int f = 0; f < nf; ++f) {
             NdFrontDev &x = fr[f];
@@ -1786,9 +1800,21 @@ static void nd_setup(CoarseOp &C, const double *Es, int H, cudaStream_t s) {
             x.fs = ofs; ofs += (int64_t)x.nI * x.ldFs;
             x.wts = owts; owts += (int64_t)x.nB * x.ldWts;
             x.ws = ows; ows += (int64_t)x.nI * x.ldWs;
+            x.yb = oyb; oyb += x.ldWs;
             pf[f + 1] = ofs; pwt[f + 1] = owts; pw[f + 1] = ows;
         }
         upload(N.fr, fr, s);
+        N.yb.alloc(std::max<int64_t>(oyb, 2), s);
+        {   // backward y_B gathers by depth (root first, like the pivot rows)
+            std::vector<int2> lg;
+            N.goff.assign(maxd + 2, 0);
+            for (int L = 0; L <= maxd; ++L) {
+                for (int f : lev[L])
+                    for (int b = 0; b < fr[f].ldWs; ++b) lg.push_back(make_int2(f, b));
+                N.goff[L + 1] = (int)lg.size();
+            }
+            upload(N.lg, lg, s);
+        }
         N.fs.alloc(std::max<int64_t>(ofs, 2), s);
         N.wts.alloc(std::max<int64_t>(owts, 2), s);
         N.ws.alloc(std::max<int64_t>(ows, 2), s);
@@ -1814,7 +1840,7 @@ static void nd_solve(const CoarseOp &C, const double *c, double *y, double *qout
     const CoarseNd &N = C.nd;
     NdSolveView V{N.fr.get(), N.invp.get(), N.invl.get(), N.uidx.get(), N.fs.get(), N.ws.get(), N.wts.get(),
                   const_cast<double *>(N.bi.get()), const_cast<double *>(N.lb.get()), const_cast<double *>(N.u.get()),
-                  N.la.get(), N.lbr.get(), N.lc.get()};
+                  N.la.get(), N.lbr.get(), N.lc.get(), const_cast<double *>(N.yb.get()), N.lg.get()};
     NdSched S;
     S.nlev = N.maxdepth + 1;
     for (int L = 0; L <= S.nlev; ++L) {
@@ -1823,6 +1849,7 @@ static void nd_solve(const CoarseOp &C, const double *c, double *y, double *qout
         S.coff[L] = N.coff[L];
     }
     for (int L = 0; L < S.nlev; ++L) S.gb[L] = (int8_t)N.gb[L];
+    for (int L = 0; L <= S.nlev; ++L) S.goff[L] = N.goff[L];
     static const char *ep = std::getenv("CR_ND_PERSIST");
     const bool persistent = (ep ? atoi(ep) != 0 : N.maxdepth > 1) && N.grid > 0;
     if (persistent) {

@@ -235,6 +235,7 @@ struct NdFrontDev {
     // backward pivot rows)
     int64_t fs, wts, ws;
     int32_t ldFs, ldWts, ldWs, pad_;
+    int64_t yb;               // backward: this front's y_B gathered contiguously (ldWs entries, zero pad)
 };
 struct CoarseNd {
     bool on = false;
@@ -251,6 +252,9 @@ struct CoarseNd {
     cr::DevBuf<int2> la, lbr, lc;              // (front, local index) work lists by level
     std::vector<int> aoff, boff, coff;         // level offsets into la / lbr / lc
     std::vector<int> gb;                       // lanes per B row of each forward level
+    cr::DevBuf<int2> lg;                       // backward: (front, b) entries of the y_B gathers by depth
+    std::vector<int> goff;                     // depth offsets into lg
+    cr::DevBuf<double> yb;                     // gathered y_B of every front
     cr::DevBuf<unsigned> bar;                  // grid barrier of the persistent solve kernel
     int grid = 0;
 };

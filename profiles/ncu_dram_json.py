@@ -1,0 +1,60 @@
+"""DRAM traffic per launch of the bench's roofline kernels, from an ncu `--page raw --csv` export of
+`profiles/prof_kernels.py --only mf,afw,spmv` (standalone launches), into the files bench.py reads
+for the `traffic` field of its roofline entries:
+
+    python profiles/ncu_dram_json.py RAW.csv --config 4 --source "..."
+
+  r02_dram_bytes_c{config}_mf.json    k_mf_spmv (non-reducing: cr_spmv_mf)
+  r02_dram_bytes_c{config}_afw.json   k_afw_apply_sh + k_afw_zsum (cr_apply_precond, one-level patch)
+  r02_dram_bytes_c{config}_spmv.json  k_spmv (assembled G)
+
+The last launch of each kernel in the capture is taken (the standalone ones come after the solve).
+"""
+import argparse
+import csv
+import json
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GROUPS = {"mf": ["k_mf_spmv"], "afw": ["k_afw_apply_sh", "k_afw_zsum"], "spmv": ["k_spmv"]}
+UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("csv")
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--source", default="")
+    a = ap.parse_args()
+    rows = list(csv.reader(open(a.csv)))
+    h, units = rows[0], rows[1]
+    ix = {n: i for i, n in enumerate(h)}
+    last = {}
+    for r in rows[2:]:
+        base = r[ix["Kernel Name"]].split("<")[0].split("(")[0].replace("void ", "").strip()
+        last[base] = r
+
+    def val(r, m):
+        return float(r[ix[m]].replace(",", "")) * UNIT.get(units[ix[m]], 1.0)
+
+    for tag, names in GROUPS.items():
+        rs = [last[n] for n in names if n in last]
+        if len(rs) != len(names):
+            print("missing", tag, [n for n in names if n not in last])
+            continue
+        rd = sum(val(r, "dram__bytes_read.sum") for r in rs)
+        wr = sum(val(r, "dram__bytes_write.sum") for r in rs)
+        out = {"kernel": " + ".join(r[ix["Kernel Name"]].split("(")[0] for r in rs) + f" (configs[{a.config}])",
+               "dram_bytes_read": int(rd), "dram_bytes_write": int(wr), "dram_bytes_per_launch": int(rd + wr),
+               "duration_us_ncu": sum(val(r, "gpu__time_duration.sum") for r in rs) *
+               (1e-3 if units[ix["gpu__time_duration.sum"]] == "nsecond" else
+                1e3 if units[ix["gpu__time_duration.sum"]] == "msecond" else 1.0),
+               "source": a.source or os.path.basename(a.csv)}
+        p = os.path.join(HERE, f"r02_dram_bytes_c{a.config}_{tag}.json")
+        with open(p, "w") as f:
+            json.dump(out, f, indent=1)
+        print(p, out["dram_bytes_per_launch"])
+
+
+if __name__ == "__main__":
+    main()
