@@ -47,8 +47,7 @@ def main():
         out = {"kernel": " + ".join(r[ix["Kernel Name"]].split("(")[0] for r in rs) + f" (configs[{a.config}])",
                "dram_bytes_read": int(rd), "dram_bytes_write": int(wr), "dram_bytes_per_launch": int(rd + wr),
                "duration_us_ncu": sum(val(r, "gpu__time_duration.sum") for r in rs) *
-               (1e-3 if units[ix["gpu__time_duration.sum"]] == "nsecond" else
-                1e3 if units[ix["gpu__time_duration.sum"]] == "msecond" else 1.0),
+               {"ns": 1e-3, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3}.get(units[ix["gpu__time_duration.sum"]], 1.0),
                "source": a.source or os.path.basename(a.csv)}
         p = os.path.join(HERE, f"r02_dram_bytes_c{a.config}_{tag}.json")
         with open(p, "w") as f:
