@@ -405,41 +405,45 @@ def other_config(P, ci, idx, dev, stream):
 
 
 def kernel_rooflines(P, torch, hyb, mesh, rep, stream, dev, peak, peak_src, cfg_idx):
-    """Per-kernel algorithmic GB/s of the iteration's kernels, each re-launched standalone on the
-    bench's stream and timed with CUDA events (the in-solve launches replay inside CUDA graphs).
-    The dominant kernel is the one with the largest share of the iteration (every kernel below
-    launches once per iteration, so share = its time / the sum)."""
+    """Per-kernel algorithmic GB/s of the solve's iteration.  Each kernel group is launched by
+    cr_solve_profile on the handle's own solver buffers exactly as the solve launches it (same row
+    order, grids) and timed alone with CUDA events on the bench's stream; share = its time / the
+    solve's ms per iteration (the coarse path overlaps the patch solves on a side stream in the solve,
+    so the shares can add up to slightly more than 1).  The dominant kernel is the one with the
+    largest share.  The assembled SpMV (not used by the solve) is timed through cr_spmv for
+    reference."""
     N, nnz, nb = hyb.n_rows, hyb.nnz, hyb.nblocks
     N8 = 8 * N
     pinfo, minfo, cinfo = hyb.precond_info(), hyb.mf_info(), hyb.coarse_info()
     slots = 2 if mesh.dim == 2 else 3
-
-    def time_launch(fn, nrep=20):
-        for _ in range(3):
-            fn()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(nrep):
-            fn()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / nrep * 1e-3
+    D = mesh.dim
+    sol = SOLVERS[cfg_idx]
+    prof = P.cr_solve_profile(hyb, sol["method"], nrep=20, matrix_free=sol["matrix_free"], coarse=sol["coarse"],
+                              stream=stream)
+    s_ = {k: v * 1e-3 for k, v in prof.items()}
 
     x = torch.randn(N, dtype=torch.float64, device=dev)
     y = torch.empty_like(x)
-    mf_s = time_launch(lambda: hyb.spmv_mf(x, y))
-    mf_bytes = minfo["bytes"] + N8 + N8                   # per-cell factors + x once + q once
-    prec_s = time_launch(lambda: hyb.apply_precond("pcg_afw", x, y))
-    # patch operator + r read + slot contributions written, then read back and z written
-    prec_bytes = pinfo["bytes"] + N8 + slots * N8 + slots * N8 + N8
-    prec2_s = time_launch(lambda: hyb.apply_precond(SOLVERS[cfg_idx]["method"], x, y))
-    coarse_bytes = N8 + 8 * N + cinfo["solve_bytes"] + 8 * N   # r, (x, a) fp32, E^-1 or ND fronts, (x, a) again
-    prec2_bytes = prec_bytes + coarse_bytes
-    spmv_s = time_launch(lambda: hyb.spmv(x, y))
-    spmv_bytes = 8 * nnz + 4 * nb + N8 + N8               # SURVEY §8(d): values + block cols + x once + y
+    for _ in range(3):
+        hyb.spmv(x, y)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(20):
+        hyb.spmv(x, y)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    spmv_s = e0.elapsed_time(e1) / 20 * 1e-3
+
+    # algorithmic bytes per launch (DESIGN.md §5 table)
+    b_mf = minfo["bytes"] + N8 + N8                                        # cell factors + p once + q once
+    b_upd = 3 * N8                                                         # r, q read; r written
+    b_coarse = N8 + 8 * N + 4 * (N // D) + cinfo["solve_bytes"]            # r, fp32 basis, perm, E^-1 / ND fronts
+    b_patch = pinfo["bytes"] + N8 + slots * N8                             # operator + r + slot contributions
+    b_pdir = slots * N8 + 2 * N8 + 2 * N8 + 8 * N                          # slots, p and x read + written, basis
+    b_spmv = 8 * nnz + 4 * nb + N8 + N8                                    # SURVEY §8(d): values + block cols + x + y
 
     def traffic(tag):
-        f = os.path.join(ROOT, "profiles", f"r02_dram_bytes_{tag}.json")
+        f = os.path.join(ROOT, "profiles", f"r02_dram_bytes_c{cfg_idx}_{tag}.json")
         try:
             return json.load(open(f)).get("dram_bytes_per_launch")
         except Exception:
@@ -448,22 +452,28 @@ def kernel_rooflines(P, torch, hyb, mesh, rep, stream, dev, peak, peak_src, cfg_
     def roof(kernel, bytes_, sec, tr=None):
         return {"kernel": kernel, "bound": "hbm", "achieved": bytes_ / sec / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": bytes_ / sec / 1e9 / peak, "traffic": tr, "peak_source": peak_src,
-                "algorithmic_bytes": bytes_, "launch_s": sec}
+                "algorithmic_bytes": bytes_, "launch_s": sec, "timing": "in-solve launch (cr_solve_profile)"}
 
-    tag = f"c{cfg_idx}"
     kernels = {
-        "mf": roof("k_mf_spmv (matrix-free factored G x, per-cell factors: the in-solve G apply)", mf_bytes, mf_s,
-                   traffic(tag + "_mf")),
-        "precond": roof("k_afw_apply + k_afw_zsum (patch additive Schwarz z = M^-1 r)", prec_bytes, prec_s,
-                        traffic(tag + "_afw")),
-        "precond_two_level": roof("coarse restrict + gather + E^-1 (nested dissection) + patch apply + combine "
-                                  "(z = M2^-1 r)", prec2_bytes, prec2_s),
-        "spmv_assembled": roof("k_spmv (assembled sliced block-ELL G x; not used by the bench's solve)", spmv_bytes,
-                               spmv_s, traffic(tag + "_spmv")),
+        "mf": roof(f"k_mf_spmv<{D},1> + memset(q) (matrix-free factored G p with p.q: the in-solve G apply)", b_mf,
+                   s_["mf"], traffic("mf")),
+        "update_r": roof("k_pcg_update_r<false> (r -= alpha q, r.r)", b_upd, s_["update_r"]),
+        "coarse": roof("k_coarse_restrict3b / k_coarse_restrict + k_coarse_gather + nested-dissection / dense E^-1 "
+                       "(y = E^-1 Z^t r)", b_coarse, s_["coarse"]) if s_["coarse"] > 0 else None,
+        "precond": roof("k_afw_apply_sh (patch additive Schwarz solves, slot contributions)", b_patch, s_["patch"],
+                        traffic("afw_apply")),
+        "pdir": roof("k_pcg_pdir_afw2 (p = z + Z y + beta p, x += alpha p)", b_pdir, s_["pdir"]),
     }
+    kernels["precond_two_level"] = roof("coarse path + patch solves (z = M2^-1 r)", b_coarse + b_patch,
+                                        s_["coarse"] + s_["patch"])
+    kernels["spmv_assembled"] = roof("k_spmv (assembled sliced block-ELL G x; not used by the bench's solve; "
+                                     "timed through cr_spmv)", b_spmv, spmv_s, traffic("spmv"))
+    kernels["spmv_assembled"]["timing"] = "standalone cr_spmv launches"
+    kernels = {k: v for k, v in kernels.items() if v is not None}
     it_s = (rep["seconds"] - rep["setup_seconds"]) / max(rep["iterations"], 1)
-    shares = {"mf": mf_s / it_s, "precond_two_level": prec2_s / it_s}
-    dominant = "precond" if prec_s >= mf_s else "mf"
+    shares = {k: s_[k] / it_s for k in ("mf", "update_r", "coarse", "patch", "pdir")}
+    groups = {"mf": "mf", "update_r": "update_r", "coarse": "coarse", "patch": "precond", "pdir": "pdir"}
+    dominant = groups[max(shares, key=shares.get)]
     return kernels, dominant, shares
 
 

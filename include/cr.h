@@ -202,7 +202,12 @@ enum { CR_PCG_JACOBI = 0, CR_PCG_BLOCKJACOBI = 1, CR_MINRES_ABSJACOBI = 2,
         * the target's true ||S - G W|| / ||S|| <= rtol (assembled G).  iterations = outer
         * iterations; inner_iterations = total inner PCG iterations; max_iter caps the outer
         * ones (default 500); the initial W is ignored (x0 = 0).  Single rank.  DESIGN.md §7.1. */
-       CR_DC_FGMRES = 8 };
+       CR_DC_FGMRES = 8,
+       /* MINRES preconditioned by |patch| + a coarse |E|^{-1} (E = Z^t G Z of the shifted, indefinite
+        * G; |E|^{-1} = V |Lambda|^{-1} V^t by a dense symmetric eigendecomposition, so the coarse grid
+        * is capped at ~8,000 coarse unknowns: H <= 43 in 2D, 8 in 3D): the SPD two-level
+        * preconditioner MINRES needs for steady Stokes (round-2 measurement). */
+       CR_MINRES_AFW2 = 9 };
 typedef struct {
     int32_t method;       /* CR_* above                                                        */
     int32_t restart;      /* GMRES m (default 50)                                              */
@@ -247,6 +252,17 @@ typedef struct {
 } cr_solve_report;
 cr_status cr_solve(cr_hybrid h, const cr_solver_opts *opts, double *W_d, cr_stream_t s,
                    cr_solve_report *rep);
+
+/* Device time of each kernel group of the patch-preconditioned PCG iteration (opts->method =
+ * CR_PCG_AFW2 or CR_PCG_AFW, matrix_free = 1, one GPU), launched on the handle's own solver buffers
+ * exactly as cr_solve launches them (same row order, grids and streams' kernels), each group timed
+ * alone with CUDA events on s over nrep launches (the solver state is reset before each launch, the
+ * numbers computed are discarded).  Requires a preceding cr_solve of `h` with the same options (its
+ * preconditioner, coarse space and work vectors are reused; a later cr_solve is unaffected).
+ * ms[5] (host, caller-owned): mean ms per launch of 0 G p with p.q (k_mf_spmv), 1 r update,
+ * 2 coarse restriction + gather + coarse solve (0 for CR_PCG_AFW), 3 patch solves,
+ * 4 direction + solution update.  Synchronises s.  (bench.py's rooflines.)          */
+cr_status cr_solve_profile(cr_hybrid h, const cr_solver_opts *opts, int32_t nrep, double *ms, cr_stream_t s);
 
 /* z_d = M^{-1} r_d for the preconditioner that `method` (CR_* above) uses: diag(G)^{-1},
  * |diag(G)|^{-1}, inverse diagonal blocks, or the patch additive Schwarz operator (built on

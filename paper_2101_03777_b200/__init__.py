@@ -34,10 +34,10 @@ STATUS = {0: "CR_OK", -1: "CR_ERR_INVALID_ARG", -2: "CR_ERR_CUDA", -3: "CR_ERR_O
 CR_STOKES, CR_NS_NEWTON_STEP = 0, 1
 CR_SHIFT_NONE, CR_SHIFT_MIS = 0, 1
 (CR_PCG_JACOBI, CR_PCG_BLOCKJACOBI, CR_MINRES_ABSJACOBI, CR_BICGSTAB_JACOBI, CR_GMRES_JACOBI,
- CR_PCG_AFW, CR_MINRES_AFW, CR_PCG_AFW2, CR_DC_FGMRES) = range(9)
+ CR_PCG_AFW, CR_MINRES_AFW, CR_PCG_AFW2, CR_DC_FGMRES, CR_MINRES_AFW2) = range(10)
 METHODS = {"pcg": CR_PCG_JACOBI, "pcg_block": CR_PCG_BLOCKJACOBI, "minres": CR_MINRES_ABSJACOBI,
            "bicgstab": CR_BICGSTAB_JACOBI, "gmres": CR_GMRES_JACOBI, "pcg_afw": CR_PCG_AFW,
-           "minres_afw": CR_MINRES_AFW, "pcg_afw2": CR_PCG_AFW2, "dc": CR_DC_FGMRES}
+           "minres_afw": CR_MINRES_AFW, "pcg_afw2": CR_PCG_AFW2, "dc": CR_DC_FGMRES, "minres_afw2": CR_MINRES_AFW2}
 
 
 class CrError(RuntimeError):
@@ -109,6 +109,7 @@ _sig = {
     "cr_partition_plan": [_i32, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp],
     "cr_apply_precond": [_vp, _i32, _vp, _vp, _vp],
     "cr_hybrid_precond_info": [_vp, _P(_i64), _P(_i32), _P(_i64), _P(_i64)],
+    "cr_solve_profile": [_vp, _P(SolverOpts), _i32, _vp, _vp],
     "cr_transient_rhs": [_vp, _vp, _vp, _vp, _vp],
     "cr_hybrid_set_cell_rhs": [_vp, _vp, _vp, _vp],
     "cr_cell_face_values": [_vp, _vp, _vp, _vp, _vp],
@@ -433,6 +434,21 @@ def cr_solve(hyb: Hybrid, W: torch.Tensor, method: str | int = "pcg", rtol: floa
         _check(st, out)
     out["status_name"] = STATUS.get(st, st)
     return out
+
+
+SOLVE_PROFILE_KERNELS = ("mf", "update_r", "coarse", "patch", "pdir")
+
+
+def cr_solve_profile(hyb: Hybrid, method: str | int = "pcg_afw2", nrep: int = 20, matrix_free: int = 1,
+                     coarse: int = 0, stream=None) -> dict:
+    """Mean device ms per launch of each kernel group of the patch-preconditioned PCG iteration,
+    launched on the handle's solver buffers as cr_solve launches them (after a cr_solve with the
+    same options): G p + p.q, r update, coarse path, patch solves, direction + solution update."""
+    opts = _opts(method, 1e-10, 1, 64, 50, matrix_free, coarse, 0.0, 0.0, 0)
+    ms = (ctypes.c_double * 5)()
+    _check(_lib.cr_solve_profile(hyb._h, ctypes.byref(opts), int(nrep), ctypes.cast(ms, ctypes.c_void_p),
+                                 _stream(stream)))
+    return dict(zip(SOLVE_PROFILE_KERNELS, list(ms)))
 
 
 def cr_recover(hyb: Hybrid, W: torch.Tensor, stream=None):

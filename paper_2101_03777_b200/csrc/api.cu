@@ -357,6 +357,14 @@ cr_status cr_solve(cr_hybrid h, const cr_solver_opts *opts, double *W_d, cr_stre
     CR_API_END
 }
 
+cr_status cr_solve_profile(cr_hybrid h, const cr_solver_opts *opts, int32_t nrep, double *ms, cr_stream_t s) {
+    CR_API_BEGIN
+    CR_REQUIRE(h && opts && ms && nrep > 0, CR_ERR_INVALID_ARG, "bad arguments");
+    for (int k = 0; k < 5; ++k) ms[k] = 0.0;
+    cr::solve_profile(h, *opts, nrep, ms, (cudaStream_t)s);
+    CR_API_END
+}
+
 cr_status cr_apply_precond(cr_hybrid h, int32_t method, const double *r_d, double *z_d, cr_stream_t s) {
     CR_API_BEGIN
     CR_REQUIRE(h && r_d && z_d && r_d != z_d, CR_ERR_INVALID_ARG, "bad arguments");

@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(256, 2) k_coarse_restrict3(CoarseView C, const
 __global__ void __launch_bounds__(256, 4) k_coarse_restrict3b(CoarseView C, const double *r, double *part,
                                                            const int32_t *list = nullptr, const int64_t *ends = nullptr) {
     constexpr int D = 3, DD = 9, NV = 72;
-    __shared__ __align__(16) double sw[8][32][8];
+    __shared__ __align__(16) double sw[8][32][9];   // odd row stride: the 8 weight stores are 2-way, not 16-way, bank-conflicted
     __shared__ __align__(16) double sar[8][32][10];
     const int64_t ch = list ? (int64_t)list[blockIdx.x] : (int64_t)blockIdx.x;
     const int64_t b = C.chunk_start[ch], e = ends ? ends[blockIdx.x] : C.chunk_start[ch + 1];
@@ -1928,6 +1928,8 @@ struct Lapack {
     int (*Potrf)(void *, int, int, double *, int, double *, int, int *) = nullptr;
     int (*PotriBS)(void *, int, int, double *, int, int *) = nullptr;
     int (*Potri)(void *, int, int, double *, int, double *, int, int *) = nullptr;
+    int (*SyevdBS)(void *, int, int, int, const double *, int, const double *, int *) = nullptr;
+    int (*Syevd)(void *, int, int, int, double *, int, double *, double *, int, int *) = nullptr;
     int (*PotrfB)(void *, int, int, double *[], int, int *, int) = nullptr;
 };
 static Lapack &lapack() {
@@ -1941,6 +1943,8 @@ static Lapack &lapack() {
         x.Potrf = (decltype(x.Potrf))dlsym(x.h, "cusolverDnDpotrf");
         x.PotriBS = (decltype(x.PotriBS))dlsym(x.h, "cusolverDnDpotri_bufferSize");
         x.Potri = (decltype(x.Potri))dlsym(x.h, "cusolverDnDpotri");
+        x.SyevdBS = (decltype(x.SyevdBS))dlsym(x.h, "cusolverDnDsyevd_bufferSize");
+        x.Syevd = (decltype(x.Syevd))dlsym(x.h, "cusolverDnDsyevd");
         x.PotrfB = (decltype(x.PotrfB))dlsym(x.h, "cusolverDnDpotrfBatched");
         if (!(x.Create && x.SetStream && x.PotrfBS && x.Potrf && x.PotriBS && x.Potri) || x.Create(&x.handle) != 0)
             x.handle = nullptr;
@@ -1988,6 +1992,56 @@ static void spd_invert(double *A, int64_t n64, cudaStream_t s, int *info_d) {
     CR_CUDA(cudaMemcpyAsync(hi, inf, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     CR_CUDA(cudaStreamSynchronize(s));
     CR_REQUIRE(hi[0] == 0 && hi[1] == 0, CR_ERR_SINGULAR_LOCAL, "coarse matrix is not positive definite (potrf/potri)");
+}
+
+// |A|^{-1} = V |Lambda|^{-1} V^t in place for a symmetric (indefinite) A: cuSOLVER syevd (plain
+// library eigendecomposition), columns of V scaled by 1 / max(|lambda|, 1e-13 max|lambda|), one DGEMM
+__global__ void k_scale_cols_absinv(const double *V, const double *w, int64_t n, double wmax, double *B) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / n;   // column-major: column j
+        B[t] = V[t] / fmax(fabs(w[j]), 1e-13 * wmax);
+    }
+}
+
+static void abs_invert(double *A, int64_t n64, cudaStream_t s) {
+    Lapack &L = lapack();
+    Blas &bl = blas();
+    CR_REQUIRE(L.handle && L.SyevdBS && L.Syevd && bl.handle && bl.Dgemm, CR_ERR_CUDA,
+               "cuSOLVER syevd / cuBLAS DGEMM unavailable for the coarse |E|^{-1}");
+    const int n = (int)n64;
+    L.SetStream(L.handle, s);
+    DevBuf<double> w, B;
+    w.alloc(n, s);
+    B.alloc((size_t)n * n, s);
+    int lw = 0;
+    CR_REQUIRE(L.SyevdBS(L.handle, 1, 0, n, A, n, w.get(), &lw) == 0, CR_ERR_CUDA, "cusolverDnDsyevd_bufferSize failed");
+    DevBuf<double> work;
+    work.alloc(std::max(lw, 1), s);
+    DevBuf<int> info;
+    info.alloc(1, s);
+    CR_REQUIRE(L.Syevd(L.handle, 1, 0, n, A, n, w.get(), work.get(), lw, info.get()) == 0, CR_ERR_CUDA,
+               "cusolverDnDsyevd failed");
+    std::vector<double> hw(n);
+    int hi = 0;
+    CR_CUDA(cudaMemcpyAsync(hw.data(), w.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CR_CUDA(cudaMemcpyAsync(&hi, info.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    CR_CUDA(cudaStreamSynchronize(s));
+    CR_REQUIRE(hi == 0, CR_ERR_CUDA, "cusolverDnDsyevd did not converge");
+    double wmax = 0.0;
+    for (double v : hw) wmax = std::max(wmax, std::fabs(v));
+    CR_REQUIRE(wmax > 0.0, CR_ERR_SINGULAR_LOCAL, "coarse matrix is zero");
+    k_scale_cols_absinv<<<grid_for(n64 * n64, 256, 16), 256, 0, s>>>(A, w.get(), n64, wmax, B.get());
+    CR_CHECK_LAUNCH();
+    // A <- B V^t (column-major, symmetric up to rounding; symmetrised below)
+    DevBuf<double> V;
+    V.alloc((size_t)n * n, s);
+    CR_CUDA(cudaMemcpyAsync(V.get(), A, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    bl.SetStream(bl.handle, s);
+    const double one = 1.0, zero = 0.0;
+    CR_REQUIRE(bl.Dgemm(bl.handle, 0, 1, n, n, n, &one, B.get(), n, V.get(), n, &zero, A, n) == 0, CR_ERR_CUDA,
+               "cublasDgemm failed");
+    k_symmetrize<<<grid_for(n64 * n64, 256, 64), 256, 0, s>>>(A, n64);
+    CR_CHECK_LAUNCH();
 }
 
 static bool lapack_potrf_batched(int n, int lda, int nb, double **A, int *info, cudaStream_t s) {
@@ -2043,6 +2097,9 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const ApplyG &applyG, const Ap
     DevBuf<uint32_t> cc, cc2, idx;
     cc.alloc(nrows, s); cc2.alloc(nrows, s); idx.alloc(nrows, s);
     C.perm.alloc(nrows, s);
+    C.perm_so.release();   // solve-order copies follow the new rows (coarse_so)
+    C.fx_so.release();
+    C.fa_so.release();
     k_coarse_faces<D><<<grid_for(nrows, T), T, 0, s>>>(m->dof_face.get(), row0, nrows, m->face_cells.get(),
                                                        m->cell_faces.get(), m->a.get(), m->xs.get(), C.g, C.fx.get(),
                                                        C.fa.get(), cc.get());
@@ -2115,7 +2172,8 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const ApplyG &applyG, const Ap
     // dense E^{-1} (one bandwidth-bound GEMV per iteration) while it is at most 8000^2 doubles,
     // the ND sparse direct solve beyond (its ~2 log2(H) dependent levels cost latency, its bytes
     // grow only like nE log nE).  CR_COARSE_DENSE=1 / CR_COARSE_ND=1 force one (tests).
-    const bool dense = std::getenv("CR_COARSE_DENSE") ? true : std::getenv("CR_COARSE_ND") ? false : C.nE <= 8000;
+    const bool dense = C.absmode || (std::getenv("CR_COARSE_DENSE") ? true : std::getenv("CR_COARSE_ND") ? false
+                                                                                                   : C.nE <= 8000);
     C.nd = CoarseNd();
     constexpr int NBR = D == 2 ? 25 : 125;
     DevBuf<double> Es;
@@ -2294,8 +2352,13 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const ApplyG &applyG, const Ap
     if (dense) {
         k_symmetrize<<<grid_for(C.nE * C.nE, T, 64), T, 0, s>>>(C.Einv.get(), C.nE);
         CR_CHECK_LAUNCH();
-        spd_invert(C.Einv.get(), C.nE, s);
-        tr.mark("coarse: E^-1 (Cholesky potrf + potri)");
+        if (C.absmode) {
+            abs_invert(C.Einv.get(), C.nE, s);
+            tr.mark("coarse: |E|^-1 (syevd)");
+        } else {
+            spd_invert(C.Einv.get(), C.nE, s);
+            tr.mark("coarse: E^-1 (Cholesky potrf + potri)");
+        }
     } else {
         k_es_symmetrize<D><<<grid_for((int64_t)nnode * NBR * D * D * D * D, T, 16), T, 0, s>>>(nnode, H, Es.get());
         CR_CHECK_LAUNCH();
@@ -2306,9 +2369,15 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const ApplyG &applyG, const Ap
 }
 
 void build_coarse(cr_hybrid_s *h, int H, const ApplyG &applyG, const ApplyGColour &applyGc,
-                  cudaStream_t s) {
+                  cudaStream_t s, bool absmode) {
     CR_REQUIRE(H >= 1 && H <= 256, CR_ERR_INVALID_ARG, "coarse grid intervals must be in [1, 256]");
     const int D = h->G.d;
+    if (absmode) H = std::min(H, D == 2 ? 43 : 8);   // dense eigendecomposition: <= ~8,000 coarse unknowns
+    if ((h->coarse.absmode != 0) != absmode) {       // the other inverse: rebuild
+        h->coarse.built = 0;
+        h->coarse.requested = 0;
+    }
+    h->coarse.absmode = absmode ? 1 : 0;
     // at least ~4 faces per coarse unknown: a coarse grid finer than the mesh makes Z rank-deficient
     const double nglob = (double)(h->part.on ? h->part.nglobal : h->G.nrows);
     const int hmax = std::max(1, (int)std::floor(std::pow(nglob / (4.0 * D * D), 1.0 / D)));
@@ -2328,10 +2397,35 @@ void build_coarse(cr_hybrid_s *h, int H, const ApplyG &applyG, const ApplyGColou
 }
 
 // per-iteration pieces (called from solve.cu)
-void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double *partials, unsigned *ticket,
-                           cudaStream_t s, bool side) {
+__global__ void k_coarse_rows_so(const int32_t *perm, int64_t n, const int32_t *iperm, const float *fx, const float *fa,
+                                 int D, int32_t *perm_so, float *fx_so, float *fa_so) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        perm_so[t] = iperm[perm[t]];
+        const int64_t nr = iperm[t];   // row t in the solve order
+        for (int i = 0; i < D; ++i) {
+            fx_so[nr * D + i] = fx[t * D + i];
+            fa_so[nr * D + i] = fa[t * D + i];
+        }
+    }
+}
+
+void coarse_so(cr_hybrid_s *h, cudaStream_t s) {
     CoarseOp &C = h->coarse;
-    CoarseView V = C.view();
+    if (!h->so.built || !C.built || C.perm_so.n == C.perm.n) return;
+    const int64_t n = (int64_t)C.perm.n;
+    const int D = h->G.d;
+    C.perm_so.alloc(n, s);
+    C.fx_so.alloc((size_t)n * D, s);
+    C.fa_so.alloc((size_t)n * D, s);
+    k_coarse_rows_so<<<grid_for(n, 256), 256, 0, s>>>(C.perm.get(), n, h->so.iperm.get(), C.fx.get(), C.fa.get(), D,
+                                                      C.perm_so.get(), C.fx_so.get(), C.fa_so.get());
+    CR_CHECK_LAUNCH();
+}
+
+void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double *partials, unsigned *ticket,
+                           cudaStream_t s, bool side, bool so) {
+    CoarseOp &C = h->coarse;
+    CoarseView V = so ? C.view_so() : C.view();
     const int T = 256;
     if (h->G.d == 2) {
         k_coarse_restrict<2><<<(unsigned)C.nchunk, 256, 0, s>>>(V, r, C.part.get());

@@ -214,6 +214,7 @@ struct AfwPrec {
     cr::DevBuf<int64_t> ioff, voff;
     cr::DevBuf<uint8_t> kl;
     cr::DevBuf<int32_t> ids;
+    cr::DevBuf<int32_t> ids_so;  // ids with solve-order rows (cr_hybrid_s::so)
     cr::DevBuf<double> vals;
 };
 enum { AFW_SPD = 0, AFW_ABS = 1, AFW_GEN = 2 };
@@ -262,6 +263,7 @@ struct CoarseNd {
 // two-level coarse correction (coarse.cu)
 struct CoarseOp {
     int built = 0;               // H it was built for (0 = not built)
+    int absmode = 0;             // 1: Einv = |E|^{-1} (eigendecomposition; MINRES on the indefinite G)
     int requested = 0;           // H asked for when it was built
     cr::CoarseGrid g;
     int64_t nE = 0, nchunk = 0;
@@ -271,8 +273,15 @@ struct CoarseOp {
     cr::DevBuf<double> part, c, y, Einv;
     cr::DevBuf<double> gpart;    // block partials of the coarse GEMV (its own: it runs concurrently)
     CoarseNd nd;                 // sparse direct solve (default); Einv (dense inverse) when off
+    // the solve order (cr_hybrid_s::so): sorted position -> solve-order row, per-row data by solve-order row
+    cr::DevBuf<int32_t> perm_so;
+    cr::DevBuf<float> fx_so, fa_so;
     cr::CoarseView view() const {
         return cr::CoarseView{g, fx.get(), fa.get(), perm.get(), fxp.get(), fap.get(), chunk_start.get(), cell_chunk.get(), nE};
+    }
+    cr::CoarseView view_so() const {
+        return cr::CoarseView{g, fx_so.get(), fa_so.get(), perm_so.get(), fxp.get(), fap.get(), chunk_start.get(),
+                              cell_chunk.get(), nE};
     }
 };
 
@@ -281,6 +290,7 @@ struct MfOp {
     bool built = false;
     int64_t ncells = 0;          // padded to a multiple of 32
     cr::DevBuf<int32_t> ids;
+    cr::DevBuf<int32_t> ids_so;  // ids in the solve order (cr_hybrid_s::so)
     cr::DevBuf<uint8_t> sg;
     cr::DevBuf<double> v;
     cr::DevBuf<uint8_t> nb;      // in-warp face partners (mf.cuh)
@@ -306,6 +316,15 @@ struct cr_hybrid_s {
     AfwPrec afw;
     MfOp mf;
     CoarseOp coarse;
+    // Solve order: the face rows renumbered in the order the matrix-free cells visit them (a row's
+    // position = the first (cell, local face) slot touching it), so that the gathers of the
+    // iteration's kernels (p at a cell's faces, r at a patch's faces) read nearby rows.  Built for
+    // the matrix-free patch-preconditioned PCG on one GPU; the solve permutes S, W in and W out,
+    // every other entry point keeps the mesh's face order.
+    struct {
+        bool built = false;
+        cr::DevBuf<int32_t> perm, iperm;   // solve-order row -> row, row -> solve-order row
+    } so;
     cr::Part part;               // row partition (multi-GPU); part.on == false on one GPU
     cr_comm_s *comm = nullptr;   // borrowed
     cr::SolverWork *work = nullptr;
@@ -352,6 +371,7 @@ void newton_update(int64_t nU, double *U, const double *dU, int64_t nP, double *
 double norm2(const double *a, int64_t n, cudaStream_t s);
 // solve.cu
 void solve(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep);
+void solve_profile(cr_hybrid_s *h, const cr_solver_opts &o, int nrep, double *ms, cudaStream_t s);
 // one solve of G W = rhs (rhs NULL: S) with the fp64 solvers (solve.cu)
 void solve_rhs(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep,
                const double *rhs);
@@ -366,6 +386,10 @@ void spmv_mf(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s);
 void build_afw(cr_hybrid_s *h, int mode, cudaStream_t s);
 // mf.cu
 void build_mf(cr_hybrid_s *h, cudaStream_t s);
+// the solve order h->so from the matrix-free cell order, and mf.ids_so (mf.cu)
+void build_so(cr_hybrid_s *h, cudaStream_t s);
+// afw.ids_so from afw.ids (precond.cu)
+void afw_so(cr_hybrid_s *h, cudaStream_t s);
 // coarse.cu
 // applyG(z, Y, colour, ncol, stride): Y_c = G z_c for the ncol vectors z_c = z + c stride, each a
 // colour sum of coarse columns (colour < 0: any z; Y arrives zero on the rows G z can reach)
@@ -374,9 +398,11 @@ using ApplyG = std::function<void(const double *, double *, int, int, int64_t)>;
 // `colour` computed without materialising z (Y arrives zero)
 using ApplyGColour = std::function<void(int, double *, int64_t)>;
 void build_coarse(cr_hybrid_s *h, int H, const ApplyG &applyG, const ApplyGColour &applyGc,
-                  cudaStream_t s);
+                  cudaStream_t s, bool absmode = false);
 void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double *partials, unsigned *ticket,
-                           cudaStream_t s, bool side = false);
+                           cudaStream_t s, bool side = false, bool so = false);
+// the coarse space's solve-order copies (perm_so, fx_so, fa_so) once h->so is built
+void coarse_so(cr_hybrid_s *h, cudaStream_t s);
 // shared: copy problem data into hybrid-owned buffers
 struct ProbView;
 ProbView prob_view(const cr_hybrid_s *h);

@@ -265,6 +265,72 @@ static void build_mf_t(cr_hybrid_s *h, cudaStream_t s) {
     M.built = true;
 }
 
+// ------------------------------------------------------------------ solve order
+// key of a row = the first stored (cell slot, local face) position touching it
+template <int D>
+__global__ void k_so_key(const int32_t *ids, int64_t npos, uint32_t *key) {
+    constexpr int NF = D + 1;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npos; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = p / NF;
+        const int l = (int)(p - t * NF);
+        const int32_t id = ids[(t >> 5) * (NF * 32) + l * 32 + (t & 31)];
+        if (id >= 0) atomicMin(key + id, (uint32_t)p);
+    }
+}
+__global__ void k_so_inverse(const int32_t *perm, int64_t n, int32_t *iperm) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        iperm[perm[i]] = (int32_t)i;
+}
+__global__ void k_so_map(const int32_t *in, int64_t n, const int32_t *iperm, int32_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = in[i];
+        out[i] = v >= 0 ? iperm[v] : -1;
+    }
+}
+__global__ void k_iota_i32(int32_t *a, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = (int32_t)i;
+}
+
+template <int D>
+static void build_so_t(cr_hybrid_s *h, cudaStream_t s) {
+    constexpr int NF = D + 1;
+    MfOp &M = h->mf;
+    const int64_t nrows = h->G.nrows, npos = M.ncells * NF;
+    CR_REQUIRE(npos < ((int64_t)1 << 32), CR_ERR_INVALID_ARG, "mesh too large for the solve order");
+    const int T = 256;
+    DevBuf<uint32_t> key, key2;
+    DevBuf<int32_t> idx;
+    key.alloc(nrows, s); key2.alloc(nrows, s); idx.alloc(nrows, s);
+    key.fill_bytes(0xFF, s);
+    k_so_key<D><<<grid_for(npos, T), T, 0, s>>>(M.ids.get(), npos, key.get());
+    CR_CHECK_LAUNCH();
+    k_iota_i32<<<grid_for(nrows, T), T, 0, s>>>(idx.get(), nrows);
+    CR_CHECK_LAUNCH();
+    h->so.perm.alloc(nrows, s);
+    h->so.iperm.alloc(nrows, s);
+    size_t tb = 0;
+    CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.get(), key2.get(), idx.get(), h->so.perm.get(), (int)nrows, 0,
+                                            32, s));
+    DevBuf<uint8_t> tmp;
+    tmp.alloc(tb, s);
+    CR_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, key.get(), key2.get(), idx.get(), h->so.perm.get(), (int)nrows,
+                                            0, 32, s));
+    k_so_inverse<<<grid_for(nrows, T), T, 0, s>>>(h->so.perm.get(), nrows, h->so.iperm.get());
+    CR_CHECK_LAUNCH();
+    M.ids_so.alloc(M.ids.n, s);
+    k_so_map<<<grid_for((int64_t)M.ids.n, T), T, 0, s>>>(M.ids.get(), (int64_t)M.ids.n, h->so.iperm.get(), M.ids_so.get());
+    CR_CHECK_LAUNCH();
+    h->so.built = true;
+}
+
+void build_so(cr_hybrid_s *h, cudaStream_t s) {
+    if (h->so.built) return;
+    CR_REQUIRE(h->mf.built && !h->part.on, CR_ERR_INVALID_ARG, "the solve order needs the matrix-free operator, one GPU");
+    if (h->mesh->dim == 2) build_so_t<2>(h, s);
+    else build_so_t<3>(h, s);
+}
+
 void build_mf(cr_hybrid_s *h, cudaStream_t s) {
     if (h->mf.built) return;
     CR_REQUIRE(!h->is_ns && h->prm.shift == CR_SHIFT_NONE && h->prm.mu > 0.0, CR_ERR_INVALID_ARG,

@@ -40,6 +40,18 @@ __global__ void k_patch_pairs(const int32_t *faces, const int32_t *dof_face, int
     }
 }
 
+// key of patch p (run p of the sorted pairs): its first face in the solve order
+template <int SLOTS>
+__global__ void k_patch_so_key(const int64_t *start, const uint32_t *sorted, int64_t npatch, const int32_t *iperm,
+                               uint32_t *key, int32_t *idx) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npatch; p += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t k = 0xFFFFFFFFu;
+        for (int64_t e = start[p]; e < start[p + 1]; ++e) k = min(k, (uint32_t)iperm[sorted[e] / SLOTS]);
+        key[p] = k;
+        idx[p] = (int32_t)p;
+    }
+}
+
 __global__ void k_patch_heads(const uint64_t *keys, int64_t n, int32_t *head) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         head[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
@@ -52,11 +64,15 @@ __global__ void k_patch_starts(const int32_t *head, const int32_t *pid, int64_t 
     }
 }
 
-__global__ void k_slice_sizes(const int64_t *start, int64_t npatch, int64_t nslices, int D, int sym, uint8_t *kl,
-                              int64_t *isz, int64_t *vsz, int *kmax) {
+// perm (may be null): patch p of the layout is run perm[p] of the sorted pairs
+__global__ void k_slice_sizes(const int64_t *start, const int32_t *perm, int64_t npatch, int64_t nslices, int D, int sym,
+                              uint8_t *kl, int64_t *isz, int64_t *vsz, int *kmax) {
     for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < nslices; sl += (int64_t)gridDim.x * blockDim.x) {
         int k = 0;
-        for (int64_t p = sl * 32; p < npatch && p < sl * 32 + 32; ++p) k = max(k, (int)(start[p + 1] - start[p]));
+        for (int64_t p = sl * 32; p < npatch && p < sl * 32 + 32; ++p) {
+            const int64_t o = perm ? perm[p] : p;
+            k = max(k, (int)(start[o + 1] - start[o]));
+        }
         kl[sl] = (uint8_t)min(k, 255);
         isz[sl] = (int64_t)k * 32;
         const int64_t T = sym ? (int64_t)k * (k + 1) / 2 : (int64_t)k * k;
@@ -200,7 +216,7 @@ __device__ bool inv_gen(double (&B)[KMAX][KMAX], int k) {
 
 template <int D, int KMAX, int MODE>
 __global__ void __launch_bounds__(64) k_patch_setup(EllView<D> G, const uint8_t *rowlen, const int64_t *start,
-                                                    const uint32_t *sorted, int64_t npatch, AfwView A,
+                                                    const int32_t *perm, const uint32_t *sorted, int64_t npatch, AfwView A,
                                                     int32_t *ids, double *vals, unsigned long long *nfallback) {
     constexpr int SLOTS = D == 2 ? 2 : 3;
     constexpr bool SYM = MODE != AFW_GEN;
@@ -209,12 +225,13 @@ __global__ void __launch_bounds__(64) k_patch_setup(EllView<D> G, const uint8_t 
         const int64_t slice = p >> 5;
         const int lane = (int)(p & 31);
         const int ks = A.kl[slice];
-        const int k = p < npatch ? (int)(start[p + 1] - start[p]) : 0;
+        const int64_t o = (p < npatch && perm) ? perm[p] : p;
+        const int k = p < npatch ? (int)(start[o + 1] - start[o]) : 0;
         int32_t *ip = ids + A.ioff[slice] + lane;
         int64_t dof[KMAX];
         for (int j = 0; j < ks; ++j) {
             if (j < k) {
-                const uint32_t v = sorted[start[p] + j];
+                const uint32_t v = sorted[start[o] + j];
                 ip[j * 32] = (int32_t)v;
                 dof[j] = v / SLOTS;
             } else {
@@ -314,8 +331,23 @@ static void build_afw_t(cr_hybrid_s *h, int mode, cudaStream_t s) {
     // CR_AFW_SHARED=0 restores one block per component; MINRES's |block| keeps them.
     static const char *esh = std::getenv("CR_AFW_SHARED");
     P.shared = (!(esh && atoi(esh) == 0) && mode == AFW_SPD) ? 1 : 0;
-    k_slice_sizes<<<grid_for(nsl, T), T, 0, s>>>(start.get(), npatch, nsl, P.shared ? 1 : D, mode != AFW_GEN, P.kl.get(),
-                                                 isz.get(), vsz.get(), kmax.get());
+    // with the solve order built: patches ordered by their first solve-order row, so a warp's 32
+    // patches gather r from nearby rows (the layout's ids stay mesh rows; ids_so maps them)
+    DevBuf<int32_t> perm;
+    if (h->so.built) {
+        DevBuf<uint32_t> pk, pk2;
+        DevBuf<int32_t> pi;
+        pk.alloc(npatch, s); pk2.alloc(npatch, s); pi.alloc(npatch, s); perm.alloc(npatch, s);
+        k_patch_so_key<SLOTS><<<grid_for(npatch, T), T, 0, s>>>(start.get(), v1.get(), npatch, h->so.iperm.get(),
+                                                               pk.get(), pi.get());
+        CR_CHECK_LAUNCH();
+        size_t ts = 0;
+        CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, ts, pk.get(), pk2.get(), pi.get(), perm.get(), (int)npatch, 0, 32, s));
+        if (ts > tb) { tmp.alloc(ts, s); tb = ts; }
+        CR_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), ts, pk.get(), pk2.get(), pi.get(), perm.get(), (int)npatch, 0, 32, s));
+    }
+    k_slice_sizes<<<grid_for(nsl, T), T, 0, s>>>(start.get(), perm.get(), npatch, nsl, P.shared ? 1 : D, mode != AFW_GEN,
+                                                 P.kl.get(), isz.get(), vsz.get(), kmax.get());
     CR_CHECK_LAUNCH();
     size_t tb3 = 0;
     CR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb3, isz.get(), P.ioff.get(), (int)nsl, s));
@@ -341,7 +373,7 @@ static void build_afw_t(cr_hybrid_s *h, int mode, cudaStream_t s) {
     AfwView A{P.ioff.get(), P.voff.get(), P.kl.get(), P.ids.get(), P.vals.get(), npatch, nrows, P.shared};
     const int grid = grid_for(nsl * 32, 64, 16);
 #define CR_SETUP(KM, MD) \
-    k_patch_setup<D, KM, MD><<<grid, 64, 0, s>>>(Gv, h->rowlen.get(), start.get(), v1.get(), npatch, A, P.ids.get(), P.vals.get(), nfb.get())
+    k_patch_setup<D, KM, MD><<<grid, 64, 0, s>>>(Gv, h->rowlen.get(), start.get(), perm.get(), v1.get(), npatch, A, P.ids.get(), P.vals.get(), nfb.get())
     if (hk <= 8) {
         if (mode == AFW_SPD) CR_SETUP(8, AFW_SPD);
         else if (mode == AFW_ABS) CR_SETUP(8, AFW_ABS);
@@ -357,7 +389,26 @@ static void build_afw_t(cr_hybrid_s *h, int mode, cudaStream_t s) {
     CR_CUDA(cudaMemcpyAsync(&hf, nfb.get(), sizeof(hf), cudaMemcpyDeviceToHost, s));
     CR_CUDA(cudaStreamSynchronize(s));
     P.nfallback = (int64_t)hf;
+    P.ids_so.release();
     P.built = mode;
+    if (h->so.built) afw_so(h, s);
+}
+
+__global__ void k_afw_ids_so(const int32_t *ids, int64_t n, int slots, const int32_t *iperm, int32_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = ids[i];
+        out[i] = v >= 0 ? iperm[v / slots] * slots + v % slots : -1;
+    }
+}
+
+void afw_so(cr_hybrid_s *h, cudaStream_t s) {
+    AfwPrec &P = h->afw;
+    if (P.built < 0 || P.ids_so.n == P.ids.n || !h->so.built) return;
+    P.ids_so.alloc(P.ids.n, s);
+    const int T = 256;
+    k_afw_ids_so<<<grid_for((int64_t)P.ids.n, T), T, 0, s>>>(P.ids.get(), (int64_t)P.ids.n, P.slots, h->so.iperm.get(),
+                                                            P.ids_so.get());
+    CR_CHECK_LAUNCH();
 }
 
 void build_afw(cr_hybrid_s *h, int mode, cudaStream_t s) {

@@ -780,13 +780,16 @@ __global__ void __launch_bounds__(kT) k_minres_wx(int64_t nrows, const double *z
 
 // ------------------------------------------------------------------ patch (AFW) preconditioner
 // What the last block does with q = sum_p r_p^t B_p^{-1} r_p  (= r^t M^{-1} r)
-enum { AFW_PCG_INIT = 0, AFW_PCG = 1, AFW_MINRES_INIT = 2, AFW_MINRES = 3, AFW_PCG2_INIT = 4, AFW_PCG2 = 5 };
+enum { AFW_PCG_INIT = 0, AFW_PCG = 1, AFW_MINRES_INIT = 2, AFW_MINRES = 3, AFW_PCG2_INIT = 4, AFW_PCG2 = 5,
+       AFW_MINRES2_INIT = 6, AFW_MINRES2 = 7 };
 
 // zs (per face slot) = patch contributions of M^{-1} r
 template <int D, int SLOTS, int KMAX, bool SYM, int WHAT>
 __global__ void __launch_bounds__(kT, 4) k_afw_apply(AfwView A, const double *r, double *zs, double rtol, KState *st,
                                                   double *partials, int dist) {
-    if (WHAT != AFW_PCG_INIT && WHAT != AFW_MINRES_INIT && WHAT != AFW_PCG2_INIT && st->flag != FLAG_RUN) return;
+    if (WHAT != AFW_PCG_INIT && WHAT != AFW_MINRES_INIT && WHAT != AFW_PCG2_INIT && WHAT != AFW_MINRES2_INIT &&
+        st->flag != FLAG_RUN)
+        return;
     double acc[1] = {0.0};
     const int64_t nt = ((A.npatch + 31) >> 5) * 32 * D;     // one thread per (patch, component)
     GRID_STRIDE(t, nt) acc[0] += afw_patch_comp<D, SLOTS, KMAX, SYM>(A, t, r, zs);
@@ -801,6 +804,10 @@ __global__ void __launch_bounds__(kT, 4) k_afw_apply(AfwView A, const double *r,
             fin_or_store<1>(st, FIN_AFW2_QF, t, rtol, dist);
         } else if (WHAT == AFW_MINRES_INIT) {
             minres_start(st, t[0]);
+        } else if (WHAT == AFW_MINRES2_INIT) {   // v^t M v = patch part + coarse part c^t |E|^-1 c
+            minres_start(st, t[0] + st->qc);
+        } else if (WHAT == AFW_MINRES2) {
+            minres_givens(st, t[0] + st->qc);
         } else {
             minres_givens(st, t[0]);
         }
@@ -980,6 +987,20 @@ __global__ void __launch_bounds__(kT) k_afw_zsum(int64_t nrows, double *z, const
         afw_sum<D, SLOTS>(zs, nrows, row, zv);
 #pragma unroll
         for (int i = 0; i < D; ++i) z[row * D + i] = zv[i];
+    }
+}
+
+// z = sum of the slot contributions + Z y (MINRES with the coarse |E|^-1 part); `guard` as k_afw_zsum
+template <int D, int SLOTS>
+__global__ void __launch_bounds__(kT) k_afw_zsum2(int64_t nrows, double *z, const double *zs, CoarseView C,
+                                                  const double *__restrict__ y, const KState *st, int guard) {
+    if (guard && st->flag != FLAG_RUN) return;
+    GRID_STRIDE(row, nrows) {
+        double zv[D], zc[D];
+        afw_sum<D, SLOTS>(zs, nrows, row, zv);
+        coarse_prolong<D>(C, row, y, zc);
+#pragma unroll
+        for (int i = 0; i < D; ++i) z[row * D + i] = zv[i] + zc[i];
     }
 }
 
@@ -1328,6 +1349,7 @@ struct Launcher {
     int dist = 0;           // partitioned over several ranks
     Comm *comm = nullptr;
     int mf = 0;             // matrix-free factored G
+    int so = 0;             // vectors in the solve order (h->so): mf / patch / coarse views in that order
 
     // after a reducing kernel: allreduce this rank's values and apply the recurrence
     void reduced(cudaStream_t ks, int nv, int kind, double rtol) {
@@ -1359,9 +1381,27 @@ static void read_state(SolverWork *w, cudaStream_t s) {
     CR_CUDA(cudaStreamSynchronize(s));
 }
 
+// out[i] = in[perm[i]] / out[perm[i]] = in[i] by block rows of D (the solve order's permutation)
 template <int D>
-static MfView mf_view(const cr_hybrid_s *h) {
-    return MfView{h->mf.ids.get(), h->mf.sg.get(), h->mf.v.get(), h->mf.nb.get(), h->mf.ncells};
+__global__ void k_so_gather(int64_t nrows, const int32_t *perm, const double *in, double *out) {
+    GRID_STRIDE(i, nrows) {
+        const int64_t r = perm[i];
+#pragma unroll
+        for (int k = 0; k < D; ++k) out[i * D + k] = in[r * D + k];
+    }
+}
+template <int D>
+__global__ void k_so_scatter(int64_t nrows, const int32_t *perm, const double *in, double *out) {
+    GRID_STRIDE(i, nrows) {
+        const int64_t r = perm[i];
+#pragma unroll
+        for (int k = 0; k < D; ++k) out[r * D + k] = in[i * D + k];
+    }
+}
+
+template <int D>
+static MfView mf_view(const cr_hybrid_s *h, int so = 0) {
+    return MfView{so ? h->mf.ids_so.get() : h->mf.ids.get(), h->mf.sg.get(), h->mf.v.get(), h->mf.nb.get(), h->mf.ncells};
 }
 
 // q = G_mf x (q zeroed first); REDUCE also reduces x.q -> alpha
@@ -1373,12 +1413,12 @@ static void mf_apply(Launcher &L, cudaStream_t ks, const double *x, double *q, d
     static const char *et = std::getenv("CR_MF_TMA");
     if (!et || atoi(et) == 0) {
         k_mf_spmv<D, REDUCE><<<occ_grid(k_mf_spmv<D, REDUCE>, kT, L.h->mf.ncells), kT, 0, ks>>>(
-            mf_view<D>(L.h), x, q, L.nrows, L.w->st.get(), L.w->partials.get(), L.dist, pqkind);
+            mf_view<D>(L.h, L.so), x, q, L.nrows, L.w->st.get(), L.w->partials.get(), L.dist, pqkind);
     } else {
         const int64_t nsl = L.h->mf.ncells / 32;
         const int grid = (int)std::min<int64_t>(mf_tma_grid<D, REDUCE>(), (nsl + kMfTmaWarps - 1) / kMfTmaWarps);
         k_mf_spmv_tma<D, REDUCE><<<std::max(grid, 1), kMfTmaWarps * 32, mf_tma_smem<D>(), ks>>>(
-            mf_view<D>(L.h), x, q, L.nrows, L.w->st.get(), L.w->partials.get(), L.dist, pqkind);
+            mf_view<D>(L.h, L.so), x, q, L.nrows, L.w->st.get(), L.w->partials.get(), L.dist, pqkind);
     }
     CR_CHECK_LAUNCH();
     ++L.launches;
@@ -1415,7 +1455,8 @@ template <int D, int WHAT>
 static void launch_afw(Launcher &L, cudaStream_t ks, const double *r, double *zs, double rtol) {
     constexpr int SLOTS = D == 2 ? 2 : 3;
     const AfwPrec &P = L.h->afw;
-    AfwView A{P.ioff.get(), P.voff.get(), P.kl.get(), P.ids.get(), P.vals.get(), P.npatch, L.h->G.nrows, P.shared};
+    AfwView A{P.ioff.get(), P.voff.get(), P.kl.get(), L.so ? P.ids_so.get() : P.ids.get(), P.vals.get(), P.npatch,
+              L.h->G.nrows, P.shared};
     const int64_t nt = P.nslices * 32 * D;
     const bool sym = P.built != AFW_GEN;
     // two-level: leave one block per SM to the coarse kernels that run concurrently on the side stream
@@ -1588,6 +1629,8 @@ static double iter_bytes(const cr_hybrid_s *h, const cr_solver_opts &o) {
         }
         case CR_MINRES_ABSJACOBI: return g + 10 * N8;
         case CR_MINRES_AFW: return g + 10 * N8 + afw + 2 * slots * N8;
+        case CR_MINRES_AFW2:
+            return g + 10 * N8 + afw + 2 * slots * N8 + 3 * N8 + (double)(8 * h->coarse.nE * h->coarse.nE);
         case CR_BICGSTAB_JACOBI: return 2 * g + 12 * N8;
         default: return 0.0;
     }
@@ -1621,8 +1664,20 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     int kk = o.check_every > 0 ? o.check_every : 64;
     kk = (kk + 1) & ~1;   // even: MINRES buffer rotation has period 2
     double *x = w->x.get();
-    CR_CUDA(cudaMemcpyAsync(x, W, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    CR_CUDA(cudaMemcpyAsync(w->b.get(), rhs ? rhs : h->S.get(), N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    // solve order (h->so): the matrix-free patch-preconditioned PCG on one GPU runs on
+    // S, W permuted into it (CR_SOLVE_ORDER=0: the mesh's face order)
+    const char *eso = std::getenv("CR_SOLVE_ORDER");   // read per solve (tests compare both orders)
+    const bool so_on = L.mf && !L.dist && (o.method == CR_PCG_AFW || o.method == CR_PCG_AFW2) && !(eso && atoi(eso) == 0);
+    if (so_on) {
+        build_so(h, s);
+        k_so_gather<D><<<L.grid_rows, kT, 0, s>>>(nrows, h->so.perm.get(), W, x);
+        CR_CHECK_LAUNCH();
+        k_so_gather<D><<<L.grid_rows, kT, 0, s>>>(nrows, h->so.perm.get(), rhs ? rhs : h->S.get(), w->b.get());
+        CR_CHECK_LAUNCH();
+    } else {
+        CR_CUDA(cudaMemcpyAsync(x, W, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        CR_CUDA(cudaMemcpyAsync(w->b.get(), rhs ? rhs : h->S.get(), N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
     CR_CUDA(cudaMemsetAsync(w->st.get(), 0, sizeof(KState), s));
     CR_CUDA(cudaEventRecord(w->e0, s));
     CR_CUDA(cudaEventRecord(w->es, s));   // re-recorded once a preconditioner / coarse space is built
@@ -1693,6 +1748,8 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     } else if (method == CR_PCG_AFW) {
         constexpr int SLOTS = D == 2 ? 2 : 3;
         build_afw(h, AFW_SPD, s);
+        L.so = so_on ? 1 : 0;
+        if (L.so) afw_so(h, s);
         CR_CUDA(cudaEventRecord(w->es, s));
         if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
         double *zs = w->zs.get();
@@ -1816,7 +1873,12 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
         CR_CUDA(cudaEventRecord(w->es, s));
         if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
         double *zs = w->zs.get();
-        const CoarseView CV = h->coarse.view();
+        L.so = so_on ? 1 : 0;
+        if (L.so) {
+            afw_so(h, s);
+            coarse_so(h, s);
+        }
+        const CoarseView CV = L.so ? h->coarse.view_so() : h->coarse.view();
         double *yc = h->coarse.y.get();
         // coarse path (restriction, gather, E^-1 GEMV) forked onto a side stream so it overlaps the
         // patch solves; joined before the direction update.  Partitioned runs fork only with a
@@ -1835,7 +1897,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
                 CR_CUDA(cudaStreamWaitEvent(w->side, w->fork, 0));
                 cs = w->side;
             }
-            coarse_restrict_solve(h, w->r.get(), &st->qc, fork ? cpart : part, &st->tickets[4], cs, fork && L.dist);
+            coarse_restrict_solve(h, w->r.get(), &st->qc, fork ? cpart : part, &st->tickets[4], cs, fork && L.dist, L.so);
             if (fork) CR_CUDA(cudaEventRecord(w->join, w->side));
             L.launches += 3;
         };
@@ -1898,21 +1960,44 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
             if (w->hst->flag == FLAG_BREAK) { status = CR_ERR_BREAKDOWN; break; }
             if (w->hst->iters >= max_iter) { status = CR_ERR_NOT_CONVERGED; break; }
         }
-    } else if (method == CR_MINRES_AFW) {
+    } else if (method == CR_MINRES_AFW || method == CR_MINRES_AFW2) {
         ensure_extra(w, s);
         constexpr int SLOTS = D == 2 ? 2 : 3;
+        const bool two = method == CR_MINRES_AFW2;
         build_afw(h, AFW_ABS, s);
+        if (two) {
+            // coarse |E|^{-1}: E = Z^t G Z of the shifted G by the assembled G, dense eigendecomposition
+            const int H = o.coarse > 0 ? o.coarse : (D == 2 ? 32 : 8);
+            build_coarse(h, H, [&](const double *z, double *Y, int, int ncol, int64_t stride) {
+                for (int c = 0; c < ncol; ++c) spmv(h->G, z + c * stride, Y + c * stride, s);
+            }, ApplyGColour(), s, true);
+        }
         CR_CUDA(cudaEventRecord(w->es, s));
         if (w->zs.n < (size_t)SLOTS * N) w->zs.alloc((size_t)SLOTS * N, s);
         double *zs = w->zs.get();
         double *va = w->v.get(), *vb = w->v2.get(), *za = w->z.get(), *zb = w->z2.get();
         double *wa = w->w.get(), *wb = w->w2.get();
+        const CoarseView CV = h->coarse.view();
+        double *yc = h->coarse.y.get();
+        // z = M v: the |patch| part, plus Z |E|^{-1} Z^t v (its c^t y lands in st->qc before the patch
+        // kernel's last block forms v^t M v)
+        auto precond = [&](cudaStream_t q, const double *v, double *zout, bool init) {
+            if (two) coarse_restrict_solve(h, v, &st->qc, part, &st->tickets[4], q);
+            if (init) {
+                if (two) launch_afw<D, AFW_MINRES2_INIT>(L, q, v, zs, rtol);
+                else launch_afw<D, AFW_MINRES_INIT>(L, q, v, zs, rtol);
+            } else {
+                if (two) launch_afw<D, AFW_MINRES2>(L, q, v, zs, rtol);
+                else launch_afw<D, AFW_MINRES>(L, q, v, zs, rtol);
+            }
+            if (two) k_afw_zsum2<D, SLOTS><<<L.grid_rows, kT, 0, q>>>(nrows, zout, zs, CV, yc, st, init ? 0 : 1);
+            else k_afw_zsum<D, SLOTS><<<L.grid_rows, kT, 0, q>>>(nrows, zout, zs, st, init ? 0 : 1);
+            CR_CHECK_LAUNCH();
+        };
         true_residual<D>(L, x, va);
         k_zero3<<<L.grid_vec, kT, 0, s>>>(N, wa, wb, vb);
         CR_CHECK_LAUNCH();
-        launch_afw<D, AFW_MINRES_INIT>(L, s, va, zs, rtol);
-        k_afw_zsum<D, SLOTS><<<L.grid_rows, kT, 0, s>>>(nrows, za, zs, st, 0);
-        CR_CHECK_LAUNCH();
+        precond(s, va, za, true);
         L.launches += 2;
         read_state(w, s);
         const double bnorm = sqrt(w->hst->bb);
@@ -1923,8 +2008,7 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
             k_minres_spmv<D><<<L.grid_rows, kT, 0, ks>>>(ell<D>(h), z, w->q.get(), st, part);
             k_minres_lanczos_v<D><<<L.grid_rows, kT, 0, ks>>>(nrows, w->q.get(), v, vold, st);
             CR_CHECK_LAUNCH();
-            launch_afw<D, AFW_MINRES>(L, ks, vold, zs, rtol);
-            k_afw_zsum<D, SLOTS><<<L.grid_rows, kT, 0, ks>>>(nrows, zn, zs, st, 1);
+            precond(ks, vold, zn, false);
             k_minres_wx<D><<<L.grid_rows, kT, 0, ks>>>(nrows, z, ww, wold, x, st);
             CR_CHECK_LAUNCH();
         };
@@ -2082,13 +2166,18 @@ static void solve_t(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStre
     CR_CUDA(cudaEventElapsedTime(&ms_setup, w->e0, w->es));
     const double bn = sqrt(w->hst->bb);
     const double tr = bn > 0 ? sqrt(w->hst->rr) / bn : 0.0;
-    CR_CUDA(cudaMemcpyAsync(W, x, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (L.so) {
+        k_so_scatter<D><<<L.grid_rows, kT, 0, s>>>(nrows, h->so.perm.get(), x, W);
+        CR_CHECK_LAUNCH();
+    } else {
+        CR_CUDA(cudaMemcpyAsync(W, x, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
     CR_CUDA(cudaStreamSynchronize(s));
     if (status == CR_OK && !(tr <= rtol)) status = CR_ERR_NOT_CONVERGED;
     if (rep) {
         rep->iterations = w->hst->iters;
         rep->rel_res_true = tr;
-        rep->rel_res_recursive = (method == CR_MINRES_ABSJACOBI || method == CR_MINRES_AFW)
+        rep->rel_res_recursive = (method == CR_MINRES_ABSJACOBI || method == CR_MINRES_AFW || method == CR_MINRES_AFW2)
                                      ? fabs(w->hst->eta) / (w->hst->eta0 > 0 ? w->hst->eta0 : 1.0)
                                      : tr;
         rep->converged = status == CR_OK;
@@ -2223,6 +2312,87 @@ void spmv_mf(cr_hybrid_s *h, const double *x, double *y, cudaStream_t s) {
 void apply_precond(cr_hybrid_s *h, int method, const double *r, double *z, cudaStream_t s) {
     if (h->G.d == 2) apply_precond_t<2>(h, method, r, z, s);
     else apply_precond_t<3>(h, method, r, z, s);
+}
+
+// Per-kernel device times of the patch-preconditioned PCG iteration (cr_solve_profile): the kernels
+// of one iteration launched on the handle's own buffers exactly as the solve launches them (same
+// row order, same grids), each timed alone with CUDA events on s.  The solver state is zeroed
+// before every launch (flag RUN), so every launch does its full work; the numbers it computes are
+// discarded.
+template <int D>
+static void profile_t(cr_hybrid_s *h, const cr_solver_opts &o, int nrep, double *ms, cudaStream_t s) {
+    constexpr int SLOTS = D == 2 ? 2 : 3;
+    SolverWork *w = h->work;
+    CR_REQUIRE(w && w->zs.n >= (size_t)SLOTS * w->N && h->afw.built == AFW_SPD && o.matrix_free && h->mf.built &&
+                   !h->part.on && (o.method == CR_PCG_AFW2 ? h->coarse.built > 0 : o.method == CR_PCG_AFW),
+               CR_ERR_INVALID_ARG, "cr_solve_profile: run cr_solve with the same (matrix-free, patch PCG) options first");
+    Launcher L{h, w, s};
+    L.D = D;
+    L.nrows = h->G.nrows;
+    L.N = w->N;
+    L.grid_rows = grid_for(L.nrows, kT);
+    L.grid_vec = grid_for(L.N, kT);
+    L.mf = 1;
+    const char *eso = std::getenv("CR_SOLVE_ORDER");
+    L.so = (h->so.built && !(eso && atoi(eso) == 0)) ? 1 : 0;
+    if (L.so) {
+        afw_so(h, s);
+        coarse_so(h, s);
+    }
+    const int64_t N = w->N, nrows = L.nrows;
+    KState *st = w->st.get();
+    double *part = w->partials.get(), *x = w->x.get(), *zs = w->zs.get();
+    const CoarseView CV = L.so ? h->coarse.view_so() : h->coarse.view();
+    double *yc = h->coarse.y.get();
+    const bool two = o.method == CR_PCG_AFW2;
+    const double rtol = 1e-30;
+    cudaEvent_t a, b;
+    CR_CUDA(cudaEventCreate(&a));
+    CR_CUDA(cudaEventCreate(&b));
+    auto timed = [&](auto launch) {
+        double tot = 0.0;
+        for (int k = 0; k < nrep; ++k) {
+            CR_CUDA(cudaMemsetAsync(st, 0, kStateHeader, s));
+            CR_CUDA(cudaEventRecord(a, s));
+            launch();
+            CR_CUDA(cudaEventRecord(b, s));
+            CR_CUDA(cudaEventSynchronize(b));
+            float t = 0.f;
+            CR_CUDA(cudaEventElapsedTime(&t, a, b));
+            tot += t;
+        }
+        return tot / nrep;
+    };
+    ms[0] = timed([&] { mf_apply<D, true>(L, s, w->p.get(), w->q.get(), rtol, two ? FIN_PQ2 : FIN_PQ); });
+    ms[1] = timed([&] {
+        k_pcg_update_r<false><<<occ_grid(k_pcg_update_r<false>, kT, L.N / 2), kT, 0, s>>>(N, x, w->r.get(), w->p.get(),
+                                                                                         w->q.get(), st, part, 0);
+        CR_CHECK_LAUNCH();
+    });
+    ms[2] = two ? timed([&] { coarse_restrict_solve(h, w->r.get(), &st->qc, part, &st->tickets[4], s, false, L.so); })
+                : 0.0;
+    if (two) ms[3] = timed([&] { launch_afw<D, AFW_PCG2>(L, s, w->r.get(), zs, rtol); });
+    else ms[3] = timed([&] { launch_afw<D, AFW_PCG>(L, s, w->r.get(), zs, rtol); });
+    if (two)
+        ms[4] = timed([&] {
+            k_pcg_pdir_afw2<D, SLOTS><<<occ_grid(k_pcg_pdir_afw2<D, SLOTS>, kT, nrows), kT, 0, s>>>(nrows, w->p.get(), zs, CV,
+                                                                                                 yc, st, 0, x);
+            CR_CHECK_LAUNCH();
+        });
+    else
+        ms[4] = timed([&] {
+            k_pcg_pdir_afw<D, SLOTS><<<occ_grid(k_pcg_pdir_afw<D, SLOTS>, kT, nrows), kT, 0, s>>>(nrows, w->p.get(), zs, st, x);
+            CR_CHECK_LAUNCH();
+        });
+    CR_CUDA(cudaEventDestroy(a));
+    CR_CUDA(cudaEventDestroy(b));
+    CR_CUDA(cudaMemsetAsync(st, 0, sizeof(KState), s));
+    CR_CUDA(cudaStreamSynchronize(s));
+}
+
+void solve_profile(cr_hybrid_s *h, const cr_solver_opts &o, int nrep, double *ms, cudaStream_t s) {
+    if (h->G.d == 2) profile_t<2>(h, o, nrep, ms, s);
+    else profile_t<3>(h, o, nrep, ms, s);
 }
 
 void solve_rhs(cr_hybrid_s *h, const cr_solver_opts &o, double *W, cudaStream_t s, cr_solve_report *rep,

@@ -17,6 +17,8 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 GROUPS = {"mf": ["k_mf_spmv"], "afw": ["k_afw_apply_sh", "k_afw_zsum"], "spmv": ["k_spmv"]}
+# --groups "mf=k_mf_spmv afw_apply=k_afw_apply_sh": other tags / kernel sets (e.g. from a capture of the
+# solve's own launches: profiles/prof_kernels.py --solve-iters 8 --only spmv)
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
@@ -25,7 +27,11 @@ def main():
     ap.add_argument("csv")
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--source", default="")
+    ap.add_argument("--groups", default=None)
     a = ap.parse_args()
+    groups = GROUPS
+    if a.groups:
+        groups = {g.split("=")[0]: g.split("=")[1].split("+") for g in a.groups.split()}
     rows = list(csv.reader(open(a.csv)))
     h, units = rows[0], rows[1]
     ix = {n: i for i, n in enumerate(h)}
@@ -37,7 +43,7 @@ def main():
     def val(r, m):
         return float(r[ix[m]].replace(",", "")) * UNIT.get(units[ix[m]], 1.0)
 
-    for tag, names in GROUPS.items():
+    for tag, names in groups.items():
         rs = [last[n] for n in names if n in last]
         if len(rs) != len(names):
             print("missing", tag, [n for n in names if n not in last])

@@ -74,6 +74,8 @@ def main():
            "ms_per_iter": (rep["seconds"] - rep["setup_seconds"]) / max(rep["iterations"], 1) * 1e3,
            "iter_gbs": rep["bytes_moved"] / max(rep["seconds"] - rep["setup_seconds"], 1e-9) / 1e9,
            "precond": pinfo, "mf": minfo, "coarse": cinfo}
+    out["in_solve_ms"] = P.cr_solve_profile(hyb, sol["method"], nrep=10, matrix_free=sol["matrix_free"],
+                                            coarse=sol["coarse"])
     for name in args.only.split(","):
         fn, nbytes = cases[name]
         fn()

@@ -266,6 +266,11 @@ SOLVE_CASES.update({
     "3d-flip-n4-pcg-afw": (dict(dim=3, n=4, flip=5), "pcg_afw", 1e-12),
     "2d-flip-steady-n12-minres-afw": (dict(dim=2, n=12, mu=0.0, shift="mis", force="gaussian", flip=4), "minres_afw",
                                       1e-12),
+    # MINRES with |patch| + the coarse |E|^-1 (SPD two-level preconditioner of the indefinite G)
+    "2d-steady-n16-minres-afw2": (dict(dim=2, n=16, mu=0.0, shift="mis", force="gaussian"), "minres_afw2", 1e-12),
+    "2d-flip-steady-n12-minres-afw2": (dict(dim=2, n=12, mu=0.0, shift="mis", force="gaussian", flip=4),
+                                       "minres_afw2", 1e-12),
+    "3d-steady-n3-minres-afw2": (dict(dim=3, n=3, mu=0.0, shift="mis", force="gaussian"), "minres_afw2", 1e-12),
 })
 MF_CASES.update({
     "2d-flip-n20-pcg-afw2-mf": (dict(dim=2, n=20, flip=3), "pcg_afw2", 1e-12),
@@ -425,6 +430,44 @@ def test_patch_preconditioner_apply(name, method, kind):
     z2 = torch.full_like(z, np.nan)
     hg.apply_precond(method, tg(r), z2)
     assert torch.equal(z, z2)
+
+
+@pytest.mark.parametrize("dim,n,method", [(2, 40, "pcg_afw2"), (3, 8, "pcg_afw2"), (3, 6, "pcg_afw"),
+                                          (2, 33, "pcg_afw")])
+def test_solve_order_matches_mesh_order(dim, n, method, monkeypatch):
+    """The matrix-free patch-preconditioned PCG runs on the rows renumbered in the cells' visiting
+    order (h->so): same operator, same preconditioner, only the reductions' order
+    differs — W agrees with the mesh-order solve (CR_SOLVE_ORDER=0) and the counts match."""
+    coords, cells, prm, data, prob = make_case(dim=dim, n=n, seed=3)
+    mesh = P.cr_build_mesh(tg(coords), tg(cells))
+    out = {}
+    for so in ("1", "0"):
+        monkeypatch.setenv("CR_SOLVE_ORDER", so)
+        hg = P.cr_hybridise(mesh, prob)
+        W = torch.zeros(hg.n_rows, dtype=torch.float64, device=DEV)
+        rep = P.cr_solve(hg, W, method, rtol=1e-11, matrix_free=1)
+        assert rep["converged"] and rep["rel_res_true"] <= 1e-11
+        out[so] = (W.cpu().numpy(), rep["iterations"])
+    assert abs(out["1"][1] - out["0"][1]) <= 2, (out["1"][1], out["0"][1])
+    assert relL2(out["1"][0], out["0"][0]) <= 1e-9
+
+
+def test_solve_profile_times_the_iteration_and_leaves_the_solve_unchanged():
+    """cr_solve_profile launches the iteration's kernel groups on the handle's buffers (after a solve)
+    and times them; a later solve from the same W reproduces the first one bit for bit."""
+    coords, cells, prm, data, prob = make_case(dim=3, n=6, seed=5)
+    hg = P.cr_hybridise(P.cr_build_mesh(tg(coords), tg(cells)), prob)
+    sols = []
+    for k in range(2):
+        W = torch.zeros(hg.n_rows, dtype=torch.float64, device=DEV)
+        rep = P.cr_solve(hg, W, "pcg_afw2", rtol=1e-11, matrix_free=1, coarse=2)
+        sols.append((W.cpu().numpy(), rep["iterations"]))
+        if k == 0:
+            ms = P.cr_solve_profile(hg, "pcg_afw2", nrep=3, coarse=2)
+            assert set(ms) == set(P.SOLVE_PROFILE_KERNELS) and all(v > 0 for v in ms.values()), ms
+    assert sols[0][1] == sols[1][1] and np.array_equal(sols[0][0], sols[1][0])
+    with pytest.raises(P.CrError):
+        P.cr_solve_profile(P.cr_hybridise(P.cr_build_mesh(tg(coords), tg(cells)), prob), "pcg_afw2")
 
 
 def test_two_level_cuts_pcg_iterations():
