@@ -159,6 +159,50 @@ __device__ __forceinline__ double afw_patch_shared(const AfwView &A, int64_t t, 
     return quad;
 }
 
+// shared mode split over components (CR_AFW_SPLIT=1): warp (slice, component i) of a thread block
+// whose D warps share the slice; ids and the packed block are read through the read-only path so
+// the slice's other component warps find them in L1.  The component's products are the same FMAs
+// in the same order as afw_patch_shared: identical slot values.
+template <int D, int SLOTS, int KMAX>
+__device__ __forceinline__ double afw_patch_split(const AfwView &A, int64_t slice, int i, int lane,
+                                                  const double *__restrict__ r, double *__restrict__ zs) {
+    const int k = A.kl[slice];
+    const int32_t *ip = A.ids + A.ioff[slice] + lane;
+    int id[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) id[j] = (j < k) ? __ldg(ip + j * 32) : -1;
+    const double *vi = A.vals + A.voff[slice] + lane;
+    constexpr int TM = KMAX * (KMAX + 1) / 2;
+    double v[TM];
+#pragma unroll
+    for (int a = 0; a < KMAX; ++a)
+#pragma unroll
+        for (int b = 0; b <= a; ++b) v[a * (a + 1) / 2 + b] = (a < k) ? __ldg(vi + (a * (a + 1) / 2 + b) * 32) : 0.0;
+    double rv[KMAX], y[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        rv[j] = (id[j] >= 0) ? r[(int64_t)(id[j] / SLOTS) * D + i] : 0.0;
+        y[j] = 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < KMAX; ++a)
+#pragma unroll
+        for (int b = 0; b <= a; ++b) {
+            const double w = v[a * (a + 1) / 2 + b];
+            y[a] = fma(w, rv[b], y[a]);
+            if (a != b) y[b] = fma(w, rv[a], y[b]);
+        }
+    double quad = 0.0;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        if (id[j] >= 0) {
+            quad = fma(rv[j], y[j], quad);
+            zs[((int64_t)(id[j] % SLOTS) * D + i) * A.nrows + id[j] / SLOTS] = y[j];
+        }
+    }
+    return quad;
+}
+
 // z[row] = sum_s zs[row, s] (slot order)
 template <int D, int SLOTS>
 __device__ __forceinline__ void afw_sum(const double *__restrict__ zs, int64_t nrows, int64_t row, double (&z)[D]) {

@@ -16,6 +16,7 @@
 // Per iteration: restriction c = Z^t r (chunk partials, fixed-order gather: deterministic),
 // y = E^{-1} c and c^t y (dense GEMV), prolongation fused into the direction update.
 #include <cub/cub.cuh>
+#include <string>
 #include <tuple>
 #include <mutex>
 #include <memory>
@@ -535,6 +536,82 @@ __global__ void __launch_bounds__(256, 4) k_coarse_restrict3b(CoarseView C, cons
         x += __shfl_xor_sync(0xffffffffu, x, 16);
         x += __shfl_xor_sync(0xffffffffu, x, 8);
         if (lane < 8) sh[warp][lane * DD + v] = x;   // lane = corner
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < NV; v += blockDim.x) {
+        double x = 0.0;
+        for (int w = 0; w < 8; ++w) x += sh[w][v];
+        part[ch * NV + v] = x;
+    }
+}
+
+// k_coarse_restrict3b was bound by shared-memory wavefronts (ncu: L1/shared throughput 95 %): each
+// lane served one corner and re-read a row's 9 products once per corner.  Here a lane serves the
+// corner pair (c, c + 4) that differs in z only, so every product it reads from shared memory feeds
+// two accumulators, and it forms the two hat weights from the row's (xi, eta, zeta) itself (the same
+// double products in the same order as 3b).  Lanes 4 apart (8 rows at a time) share a pair; the sum
+// over them is a fixed xor-shuffle tree: deterministic, not bitwise 3b's order.
+__global__ void __launch_bounds__(256, 3) k_coarse_restrict3c(CoarseView C, const double *r, double *part) {
+    constexpr int D = 3, DD = 9, NV = 72;
+    __shared__ __align__(16) float4 sxi[8][32];
+    __shared__ __align__(16) double sar[8][32][10];
+    const int64_t ch = blockIdx.x;
+    const int64_t b = C.chunk_start[ch], e = C.chunk_start[ch + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cp = lane & 3, rsub = lane >> 2;
+    double acc0[DD], acc1[DD];
+#pragma unroll
+    for (int v = 0; v < DD; ++v) acc0[v] = acc1[v] = 0.0;
+    for (int64_t t0 = b + warp * 32; t0 < e; t0 += 8 * 32) {
+        const int64_t t = t0 + lane;
+        const int64_t row = t < e ? (int64_t)C.perm[t] : -1;
+        float xv[D], av[D], xi[D];
+        double rv[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            xv[i] = row >= 0 ? C.fxp[t * D + i] : 0.f;
+            av[i] = row >= 0 ? C.fap[t * D + i] : 0.f;   // a padding row's products are 0
+            rv[i] = row >= 0 ? r[row * D + i] : 0.0;
+        }
+        int ic[D];
+        coarse_locate<D>(C.g, xv, ic, xi);
+        sxi[warp][lane] = make_float4(xi[0], xi[1], xi[2], 0.f);
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int k = 0; k < D; ++k) sar[warp][lane][i * D + k] = (double)av[k] * rv[i];
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int j = 8 * k + rsub;
+            const float4 xq = sxi[warp][j];
+            const double wxy = ((cp & 1) ? (double)xq.x : 1.0 - (double)xq.x) * ((cp & 2) ? (double)xq.y : 1.0 - (double)xq.y);
+            const double w0 = wxy * (1.0 - (double)xq.z), w1 = wxy * (double)xq.z;
+            const double2 *p2 = reinterpret_cast<const double2 *>(&sar[warp][j][0]);
+            const double2 q0 = p2[0], q1 = p2[1], q2 = p2[2], q3 = p2[3];
+            const double q[DD] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y, sar[warp][j][8]};
+#pragma unroll
+            for (int v = 0; v < DD; ++v) {
+                acc0[v] = fma(w0, q[v], acc0[v]);
+                acc1[v] = fma(w1, q[v], acc1[v]);
+            }
+        }
+        __syncwarp();
+    }
+    __shared__ double sh[8][NV];
+#pragma unroll
+    for (int v = 0; v < DD; ++v) {
+        double x0 = acc0[v], x1 = acc1[v];
+        x0 += __shfl_xor_sync(0xffffffffu, x0, 4);
+        x1 += __shfl_xor_sync(0xffffffffu, x1, 4);
+        x0 += __shfl_xor_sync(0xffffffffu, x0, 8);
+        x1 += __shfl_xor_sync(0xffffffffu, x1, 8);
+        x0 += __shfl_xor_sync(0xffffffffu, x0, 16);
+        x1 += __shfl_xor_sync(0xffffffffu, x1, 16);
+        if (lane < 4) {
+            sh[warp][lane * DD + v] = x0;         // corner cp
+            sh[warp][(lane + 4) * DD + v] = x1;   // corner cp + 4
+        }
     }
     __syncthreads();
     for (int v = threadIdx.x; v < NV; v += blockDim.x) {
@@ -2431,7 +2508,10 @@ void coarse_restrict_solve(cr_hybrid_s *h, const double *r, double *qout, double
         k_coarse_restrict<2><<<(unsigned)C.nchunk, 256, 0, s>>>(V, r, C.part.get());
         k_coarse_gather<2><<<grid_for(C.nE, T), T, 0, s>>>(V, C.part.get(), C.c.get());
     } else {
-        k_coarse_restrict3b<<<(unsigned)C.nchunk, 256, 0, s>>>(V, r, C.part.get());
+        // CR_RESTRICT=3b: the one-corner-per-lane restriction (measured 0.07 ms slower on configs[4])
+        static const char *ep = std::getenv("CR_RESTRICT");
+        if (!(ep && std::string(ep) == "3b")) k_coarse_restrict3c<<<(unsigned)C.nchunk, 256, 0, s>>>(V, r, C.part.get());
+        else k_coarse_restrict3b<<<(unsigned)C.nchunk, 256, 0, s>>>(V, r, C.part.get());
         k_coarse_gather<3><<<grid_for(C.nE, T), T, 0, s>>>(V, C.part.get(), C.c.get());
     }
     CR_CHECK_LAUNCH();

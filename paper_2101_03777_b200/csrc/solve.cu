@@ -830,6 +830,27 @@ __global__ void __launch_bounds__(kT, 2) k_afw_apply_sh(AfwView A, const double 
     });
 }
 
+// the shared-block variant split over components (afw_patch_split): blocks of 4 slices x D warps
+constexpr int kAfwSpb = 4;
+template <int D, int SLOTS, int KMAX, int WHAT>
+__global__ void __launch_bounds__(32 * D * kAfwSpb, D == 3 ? 2 : 3) k_afw_apply_sc(AfwView A, const double *r, double *zs,
+                                                                                 double rtol, KState *st, double *partials,
+                                                                                 int dist) {
+    if (WHAT != AFW_PCG_INIT && WHAT != AFW_PCG2_INIT && st->flag != FLAG_RUN) return;
+    double acc[1] = {0.0};
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = warp % D;
+    const int64_t nslices = (A.npatch + 31) >> 5;
+    for (int64_t slice = (int64_t)blockIdx.x * kAfwSpb + warp / D; slice < nslices; slice += (int64_t)gridDim.x * kAfwSpb)
+        acc[0] += afw_patch_split<D, SLOTS, KMAX>(A, slice, i, lane, r, zs);
+    reduce_and_finish<1>(acc, partials, &st->tickets[3], [&](double *t) {
+        if (WHAT == AFW_PCG_INIT) fin_or_store<1>(st, FIN_AFW_PCG_INIT, t, rtol, dist);
+        else if (WHAT == AFW_PCG) fin_or_store<1>(st, FIN_AFW_PCG, t, rtol, dist);
+        else if (WHAT == AFW_PCG2_INIT) fin_or_store<1>(st, FIN_AFW2_QF_INIT, t, rtol, dist);
+        else if (WHAT == AFW_PCG2) fin_or_store<1>(st, FIN_AFW2_QF, t, rtol, dist);
+    });
+}
+
 // x += alpha p (XUPD; else the direction update does it: k_pcg_pdir_afw*) ; r -= alpha q ; |r|^2
 // (convergence).  Flat over the N = D*nrows entries in 16-byte double2 units, 4 independent units
 // in flight per thread (memory-level parallelism).
@@ -1470,7 +1491,14 @@ static void launch_afw(Launcher &L, cudaStream_t ks, const double *r, double *zs
     double *part = L.w->partials.get();
     if (P.shared && (WHAT == AFW_PCG || WHAT == AFW_PCG_INIT || WHAT == AFW_PCG2 || WHAT == AFW_PCG2_INIT)) {
         const int64_t nts = P.nslices * 32;
-        if (P.kmax <= 6) k_afw_apply_sh<D, SLOTS, 6, WHAT><<<occ_grid(k_afw_apply_sh<D, SLOTS, 6, WHAT>, kT, nts, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
+        // default: one warp per (slice, component) (k_afw_apply_sc, 1.39 vs 1.54 ms on configs[4]);
+        // CR_AFW_SPLIT=0: one thread per patch for all components (k_afw_apply_sh)
+        static const char *es = std::getenv("CR_AFW_SPLIT");
+        if (!(es && atoi(es) == 0) && P.kmax <= 6) {
+            constexpr int NT = 32 * D * kAfwSpb;
+            k_afw_apply_sc<D, SLOTS, 6, WHAT><<<occ_grid(k_afw_apply_sc<D, SLOTS, 6, WHAT>, NT, nts * D, rsv), NT, 0, ks>>>(
+                A, r, zs, rtol, st, part, L.dist);
+        } else if (P.kmax <= 6) k_afw_apply_sh<D, SLOTS, 6, WHAT><<<occ_grid(k_afw_apply_sh<D, SLOTS, 6, WHAT>, kT, nts, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
         else if (P.kmax <= 8) k_afw_apply_sh<D, SLOTS, 8, WHAT><<<occ_grid(k_afw_apply_sh<D, SLOTS, 8, WHAT>, kT, nts, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
         else k_afw_apply_sh<D, SLOTS, 16, WHAT><<<occ_grid(k_afw_apply_sh<D, SLOTS, 16, WHAT>, kT, nts, rsv), kT, 0, ks>>>(A, r, zs, rtol, st, part, L.dist);
     } else if (P.kmax <= 6) {
