@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <mutex>
+#include <nvtx3/nvToolsExt.h>
 
 namespace cr {
 static thread_local std::string g_last_error;
@@ -26,7 +27,10 @@ Trace::Trace(cudaStream_t st) : s(st) {
         t0 = now_s();
     }
 }
+Range::Range(const char *name) { nvtxRangePushA(name); }
+Range::~Range() { nvtxRangePop(); }
 void Trace::mark(const char *what) {
+    nvtxMarkA(what);
     if (!on) return;
     cudaStreamSynchronize(s);
     const double t = now_s();
@@ -133,6 +137,7 @@ cr_status cr_pool_trim(int64_t keep_bytes) {
 
 cr_status cr_build_mesh(int32_t dim, int64_t nv, const double *coords_d, int64_t nc, const int32_t *cells_d,
                         cr_stream_t s, cr_mesh *out) {
+    cr::Range nvtx_range("cr_build_mesh");
     CR_API_BEGIN
     CR_REQUIRE(out, CR_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
@@ -186,6 +191,7 @@ void cr_destroy_mesh(cr_mesh m) {
 }
 
 cr_status cr_assemble_coupled(cr_mesh m, const cr_params *prm, const cr_data *data, cr_stream_t s, cr_coupled *out) {
+    cr::Range nvtx_range("cr_assemble_coupled");
     CR_API_BEGIN
     CR_REQUIRE(m && prm && data && out, CR_ERR_INVALID_ARG, "null argument");
     *out = nullptr;
@@ -227,6 +233,7 @@ void cr_destroy_coupled(cr_coupled c) {
 
 cr_status cr_hybridise(cr_mesh m, const cr_params *prm, const cr_data *data, cr_comm comm, cr_stream_t s,
                        cr_hybrid *out) {
+    cr::Range nvtx_range("cr_hybridise");
     CR_API_BEGIN
     CR_REQUIRE(m && prm && data && out, CR_ERR_INVALID_ARG, "null argument");
     *out = nullptr;
@@ -280,6 +287,7 @@ cr_status cr_hybrid_export_shift(cr_hybrid h, uint8_t *inM1_d, double *E_d, cr_s
 }
 
 cr_status cr_spmv(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s) {
+    cr::Range nvtx_range("cr_spmv");
     CR_API_BEGIN
     CR_REQUIRE(h && x_d && y_d && x_d != y_d, CR_ERR_INVALID_ARG, "bad arguments");
     if (h->part.on) cr::spmv_part(h, x_d, y_d, (cudaStream_t)s);
@@ -288,6 +296,7 @@ cr_status cr_spmv(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s) {
 }
 
 cr_status cr_spmv_mf(cr_hybrid h, const double *x_d, double *y_d, cr_stream_t s) {
+    cr::Range nvtx_range("cr_spmv_mf");
     CR_API_BEGIN
     CR_REQUIRE(h && x_d && y_d && x_d != y_d, CR_ERR_INVALID_ARG, "bad arguments");
     cr::spmv_mf(h, x_d, y_d, (cudaStream_t)s);
@@ -315,6 +324,7 @@ cr_status cr_hybrid_set_cell_rhs(cr_hybrid h, const double *R_d, const double *g
 }
 
 cr_status cr_transient_rhs(cr_hybrid h, const double *U_prev_d, double *R_d, double *g_d, cr_stream_t s) {
+    cr::Range nvtx_range("cr_transient_rhs");
     CR_API_BEGIN
     CR_REQUIRE(h && U_prev_d && R_d && g_d, CR_ERR_INVALID_ARG, "null argument");
     cr::transient_rhs(h, U_prev_d, R_d, g_d, (cudaStream_t)s);
@@ -349,6 +359,7 @@ void cr_destroy_hybrid(cr_hybrid h) {
 }
 
 cr_status cr_solve(cr_hybrid h, const cr_solver_opts *opts, double *W_d, cr_stream_t s, cr_solve_report *rep) {
+    cr::Range nvtx_range("cr_solve");
     CR_API_BEGIN
     CR_REQUIRE(h && opts && W_d, CR_ERR_INVALID_ARG, "null argument");
     if (rep) std::memset(rep, 0, sizeof(*rep));
@@ -358,6 +369,7 @@ cr_status cr_solve(cr_hybrid h, const cr_solver_opts *opts, double *W_d, cr_stre
 }
 
 cr_status cr_solve_profile(cr_hybrid h, const cr_solver_opts *opts, int32_t nrep, double *ms, cr_stream_t s) {
+    cr::Range nvtx_range("cr_solve_profile");
     CR_API_BEGIN
     CR_REQUIRE(h && opts && ms && nrep > 0, CR_ERR_INVALID_ARG, "bad arguments");
     for (int k = 0; k < 5; ++k) ms[k] = 0.0;
@@ -366,6 +378,7 @@ cr_status cr_solve_profile(cr_hybrid h, const cr_solver_opts *opts, int32_t nrep
 }
 
 cr_status cr_apply_precond(cr_hybrid h, int32_t method, const double *r_d, double *z_d, cr_stream_t s) {
+    cr::Range nvtx_range("cr_apply_precond");
     CR_API_BEGIN
     CR_REQUIRE(h && r_d && z_d && r_d != z_d, CR_ERR_INVALID_ARG, "bad arguments");
     cr::apply_precond(h, method, r_d, z_d, (cudaStream_t)s);
@@ -393,6 +406,7 @@ cr_status cr_cell_face_values(cr_mesh m, const double *U_d, const double *bnd_d,
 }
 
 cr_status cr_recover(cr_hybrid h, const double *W_d, double *U_d, double *P_d, double *diag_d, cr_stream_t s) {
+    cr::Range nvtx_range("cr_recover");
     CR_API_BEGIN
     CR_REQUIRE(h && W_d && U_d && P_d, CR_ERR_INVALID_ARG, "null argument");
     cr::recover(h, W_d, U_d, P_d, diag_d, (cudaStream_t)s);
@@ -401,6 +415,7 @@ cr_status cr_recover(cr_hybrid h, const double *W_d, double *U_d, double *P_d, d
 
 cr_status cr_newton_update(int64_t nU, double *U_d, const double *dU_d, int64_t nP, double *P_d, const double *dP_d,
                            double lam, double *norms_h, cr_stream_t s) {
+    cr::Range nvtx_range("cr_newton_update");
     CR_API_BEGIN
     CR_REQUIRE(nU >= 0 && nP >= 0 && U_d && dU_d && norms_h && (!dP_d || P_d), CR_ERR_INVALID_ARG, "bad arguments");
     cr::newton_update(nU, U_d, dU_d, nP, P_d, dP_d, lam, norms_h, (cudaStream_t)s);
@@ -408,6 +423,7 @@ cr_status cr_newton_update(int64_t nU, double *U_d, const double *dU_d, int64_t 
 }
 
 cr_status cr_coupled_rhs_norm(cr_mesh m, const cr_params *prm, const cr_data *data, double *norm_h, cr_stream_t s) {
+    cr::Range nvtx_range("cr_coupled_rhs_norm");
     CR_API_BEGIN
     CR_REQUIRE(m && prm && data && norm_h, CR_ERR_INVALID_ARG, "null argument");
     cr_coupled_s c;
@@ -420,6 +436,7 @@ cr_status cr_hybrid_method_host(int32_t dim, int64_t nv, const double *coords_h,
                                 const cr_params *prm, const double *fbar_h, const double *dirichlet_h,
                                 const cr_solver_opts *opts, double *U_h, double *P_h, const int64_t *sizes_h,
                                 cr_mesh_info_t *mesh_info, cr_solve_report *rep, cr_stream_t s) {
+    cr::Range nvtx_range("cr_hybrid_method_host");
     CR_API_BEGIN
     CR_REQUIRE(coords_h && cells_h && prm && fbar_h && opts && U_h && P_h && sizes_h, CR_ERR_INVALID_ARG,
                "null argument");

@@ -2129,6 +2129,10 @@ static bool lapack_potrf_batched(int n, int lda, int nb, double **A, int *info, 
     return true;
 }
 
+__global__ void k_coarse_scale(double *a, int64_t n, double f) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) a[i] *= f;
+}
+
 template <int D>
 static void build_coarse_t(cr_hybrid_s *h, int H, const ApplyG &applyG, const ApplyGColour &applyGc, cudaStream_t s) {
     constexpr int NN = 1 << D, NV = NN * D * D;
@@ -2426,6 +2430,13 @@ static void build_coarse_t(cr_hybrid_s *h, int H, const ApplyG &applyG, const Ap
         }
     }
     tr.mark("coarse: E = Z^t G Z");
+    // relative weight theta of the coarse term in M^-1 = sum_p R_p^t B_p^-1 R_p + theta Z E^-1 Z^t
+    // (E is scaled by 1/theta before it is factorised)
+    if (C.weight != 1.0) {
+        const int64_t ne = dense ? C.nE * C.nE : (int64_t)nnode * NBR * D * D * D * D;
+        k_coarse_scale<<<grid_for(ne, T, 16), T, 0, s>>>(dense ? C.Einv.get() : Es.get(), ne, 1.0 / C.weight);
+        CR_CHECK_LAUNCH();
+    }
     if (dense) {
         k_symmetrize<<<grid_for(C.nE * C.nE, T, 64), T, 0, s>>>(C.Einv.get(), C.nE);
         CR_CHECK_LAUNCH();
@@ -2455,6 +2466,10 @@ void build_coarse(cr_hybrid_s *h, int H, const ApplyG &applyG, const ApplyGColou
         h->coarse.requested = 0;
     }
     h->coarse.absmode = absmode ? 1 : 0;
+    if (const char *ew = std::getenv("CR_COARSE_WEIGHT")) {
+        const double w = std::atof(ew);
+        if (w > 0.0) h->coarse.weight = w;
+    }
     // at least ~4 faces per coarse unknown: a coarse grid finer than the mesh makes Z rank-deficient
     const double nglob = (double)(h->part.on ? h->part.nglobal : h->G.nrows);
     const int hmax = std::max(1, (int)std::floor(std::pow(nglob / (4.0 * D * D), 1.0 / D)));

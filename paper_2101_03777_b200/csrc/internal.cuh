@@ -131,7 +131,17 @@ inline int grid_for(int64_t work, int threads, int max_blocks_per_sm = 8) {
     return (int)b;
 }
 
-// CR_TRACE=1: host wall time of setup phases on stderr (synchronises the stream at each mark)
+// NVTX range around an ABI call (domain-less push/pop; a no-op unless a profiler injects NVTX):
+// nsys / ncu --nvtx show the stages of the path by name.
+struct Range {
+    explicit Range(const char *name);
+    ~Range();
+    Range(const Range &) = delete;
+    Range &operator=(const Range &) = delete;
+};
+
+// CR_TRACE=1: host wall time of setup phases on stderr (synchronises the stream at each mark);
+// every mark is also an NVTX marker.
 struct Trace {
     bool on = false;
     double t0 = 0.0;
@@ -263,6 +273,7 @@ struct CoarseNd {
 // two-level coarse correction (coarse.cu)
 struct CoarseOp {
     int built = 0;               // H it was built for (0 = not built)
+    double weight = 1.0;         // theta: relative weight of the coarse term in the additive preconditioner
     int absmode = 0;             // 1: Einv = |E|^{-1} (eigendecomposition; MINRES on the indefinite G)
     int requested = 0;           // H asked for when it was built
     cr::CoarseGrid g;
