@@ -458,9 +458,9 @@ def kernel_rooflines(P, torch, hyb, mesh, rep, stream, dev, peak, peak_src, cfg_
         "mf": roof(f"k_mf_spmv<{D},1> + memset(q) (matrix-free factored G p with p.q: the in-solve G apply)", b_mf,
                    s_["mf"], traffic("mf")),
         "update_r": roof("k_pcg_update_r<false> (r -= alpha q, r.r)", b_upd, s_["update_r"]),
-        "coarse": roof("k_coarse_restrict3b / k_coarse_restrict + k_coarse_gather + nested-dissection / dense E^-1 "
+        "coarse": roof("k_coarse_restrict3c / k_coarse_restrict + k_coarse_gather + k_nd_solve (nested dissection) / dense E^-1 "
                        "(y = E^-1 Z^t r)", b_coarse, s_["coarse"]) if s_["coarse"] > 0 else None,
-        "precond": roof("k_afw_apply_sh (patch additive Schwarz solves, slot contributions)", b_patch, s_["patch"],
+        "precond": roof("k_afw_apply_sc (patch additive Schwarz solves, one warp per (slice, component), slot contributions)", b_patch, s_["patch"],
                         traffic("afw_apply")),
         "pdir": roof("k_pcg_pdir_afw2 (p = z + Z y + beta p, x += alpha p)", b_pdir, s_["pdir"]),
     }
