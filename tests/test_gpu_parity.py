@@ -507,6 +507,35 @@ def test_coarse_nd_matches_dense_inverse(dim, n, H, monkeypatch):
     assert abs(out["CR_COARSE_ND"][1] - out["CR_COARSE_DENSE"][1]) <= 1
 
 
+@pytest.mark.parametrize("dim,n,H,mode", [(2, 48, 8, "CR_COARSE_DENSE"), (2, 64, 8, "CR_COARSE_ND"),
+                                          (3, 8, 4, "CR_COARSE_ND")])
+def test_coarse_weight_is_linear_in_the_coarse_term(dim, n, H, mode, monkeypatch):
+    """CR_COARSE_WEIGHT = theta scales E by 1/theta before it is inverted / factorised:
+    M2(theta)^-1 r = M_patch^-1 r + theta Z E^-1 Z^t r, so z(2) = 2 z(1) - z_patch, and the weighted
+    two-level PCG still reaches the same solution."""
+    coords, cells, prm, data, prob = make_case(dim=dim, n=n, seed=6)
+    mesh = P.cr_build_mesh(tg(coords), tg(cells))
+    r = tg(np.random.default_rng(11).normal(size=dim * int(mesh.nf_int)))
+    monkeypatch.setenv(mode, "1")
+    z, Ws = {}, {}
+    for th in ("1", "2"):
+        monkeypatch.setenv("CR_COARSE_WEIGHT", th)
+        hg = P.cr_hybridise(mesh, prob)
+        W = torch.zeros(hg.n_rows, dtype=torch.float64, device=DEV)
+        rep = P.cr_solve(hg, W, "pcg_afw2", rtol=1e-11, matrix_free=1, coarse=H)
+        assert rep["converged"]
+        zz = torch.empty_like(r)
+        hg.apply_precond("pcg_afw2", r, zz)
+        z[th], Ws[th] = zz.cpu().numpy(), W.cpu().numpy()
+        if th == "1":
+            zp = torch.empty_like(r)
+            hg.apply_precond("pcg_afw", r, zp)
+            zp = zp.cpu().numpy()
+    assert relL2(z["2"], 2.0 * z["1"] - zp) <= 1e-9
+    assert np.linalg.norm(z["1"] - zp) > 1e-3 * np.linalg.norm(zp)   # the coarse term is not negligible
+    assert relL2(Ws["2"], Ws["1"]) <= 1e-8
+
+
 def test_patch_preconditioner_cuts_pcg_iterations():
     """The patch preconditioner resolves the two scales of G: >= 4x fewer PCG iterations than
     Jacobi at n = 32 (numpy experiment: 3186 vs 429)."""
