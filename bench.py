@@ -489,12 +489,19 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true")
+    ap.add_argument("--profile-run", action="store_true",
+                    help="profiler runs only (ncu launch list): keep --warmup as given (< 3 allowed) and skip the "
+                         "Jacobi-PCG sample; the printed numbers are not bench values")
+    ap.add_argument("--force-comm", action="store_true",
+                    help="debug: run the partitioned (--gpus N > 1) code path on one GPU through a one-rank NCCL "
+                         "communicator (not a bench value)")
     ap.add_argument("--pool-reserve-gb", type=float, default=None,
                     help="map this much into libcr's memory pool before the first step (cr_pool_reserve); default "
                          "120 for configs[4], 24 for configs[1]: without it the pool maps new memory in the middle of "
                          "some steps (3D: 3.5-6.1 s per step instead of 3.47 +- 0.01 s)")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
+    if not args.profile_run:
+        args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -517,6 +524,9 @@ def main():
         uid = [P.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = P.Comm.nccl(uid[0], rank, world)
+    elif args.force_comm:
+        comm = P.Comm.nccl(P.nccl_unique_id(), 0, 1)
+    multi = comm is not None   # the partitioned path: no single-GPU extras
 
     def barrier():
         if world > 1:
@@ -591,7 +601,7 @@ def main():
     # the north star's baseline solver (Jacobi PCG) on the same G: to solution with --jacobi, else
     # a sample of 2,000 iterations for its time per iteration
     jac = None
-    if world == 1:
+    if not multi and not args.profile_run:
         Wj = torch.zeros(nrows, dtype=torch.float64, device=dev)
         if args.jacobi:
             rj = P.cr_solve(hyb, Wj, "pcg", rtol=rtol, check_every=256, raise_on_fail=False)
@@ -611,7 +621,7 @@ def main():
     nf_int = mesh.nf_int
     del out, hyb, mesh
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not multi:
         Uh = torch.empty(nf_int * ndim, dtype=torch.float64, pin_memory=True)
         Ph = torch.empty(nc_full, dtype=torch.float64, pin_memory=True)
 
@@ -637,7 +647,7 @@ def main():
 
     # ---- stage times of one step and time-to-solution of the other configs (single GPU only)
     stages, others, tstep, newton, table4 = None, None, None, None, None
-    if world == 1 and not args.no_other_configs:
+    if not multi and not args.no_other_configs:
         stages = stage_times(P, cfg_idx, coords, cells, fbar, stream)
         del coords, cells, fbar
         torch.cuda.empty_cache()
@@ -657,7 +667,7 @@ def main():
         table4 = direct_table4(P, ci, dev, stream)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not multi and not args.no_cpu_baseline:
         s = oracle_sample(cfg_idx)
         it_full, src = jacobi_iters(cfg_idx)
         v = oracle_extrapolate(s, nc_full, nnz, it_full)

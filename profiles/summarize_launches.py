@@ -13,7 +13,8 @@ import os
 
 
 def load(path):
-    rows = list(csv.reader(open(path)))
+    import gzip
+    rows = list(csv.reader(gzip.open(path, 'rt') if path.endswith('.gz') else open(path)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]
     ki, ni, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
