@@ -593,10 +593,21 @@ def main():
     nnz, nb, nrows = hyb.nnz, hyb.nblocks, hyb.n_rows
 
     peak, peak_src = measured_peaks()
-    kernels, dominant, shares = kernel_rooflines(P, torch, hyb, mesh, rep, stream, dev, peak, peak_src, cfg_idx)
     cinfo, pinfo, minfo = hyb.coarse_info(), hyb.precond_info(), hyb.mf_info()
     iter_s = rep["seconds"] - rep["setup_seconds"]
     iter_gbs = rep["bytes_moved"] / iter_s / 1e9 if iter_s > 0 else None
+    if not multi:
+        kernels, dominant, shares = kernel_rooflines(P, torch, hyb, mesh, rep, stream, dev, peak, peak_src, cfg_idx)
+    else:
+        # partitioned runs: cr_solve_profile times single-GPU handles only; report this rank's whole
+        # iteration (its algorithmic bytes / its iteration time) against the same peak
+        dominant, shares = "iteration", None
+        kernels = {"iteration": {
+            "kernel": "two-level PCG iteration, all kernels of rank 0's partition (per-kernel profile: single GPU only)",
+            "bound": "hbm", "achieved": iter_gbs, "peak": peak, "unit": "GB/s",
+            "frac": iter_gbs / peak if iter_gbs else None, "traffic": None, "peak_source": peak_src,
+            "algorithmic_bytes": rep["bytes_moved"] / max(rep["iterations"], 1),
+            "launch_s": iter_s / max(rep["iterations"], 1), "timing": "solve report (CUDA events around the iterations)"}}
 
     # the north star's baseline solver (Jacobi PCG) on the same G: to solution with --jacobi, else
     # a sample of 2,000 iterations for its time per iteration

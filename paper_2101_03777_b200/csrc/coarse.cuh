@@ -92,43 +92,11 @@ __device__ __forceinline__ void coarse_prolong(const CoarseView &C, int64_t row,
 #pragma unroll
     for (int n = 0; n < (1 << D); ++n) {
         const double *yn = y + coarse_node<D>(C.g, ic, n) * D * D;
-        double yv[D * D];
-        if (D == 3) {
-            // 9 doubles per node: 4 aligned double2 + 1 scalar, the scalar first on odd nodes
-            // (5 loads instead of 9; same values, same arithmetic order)
-            if ((reinterpret_cast<uintptr_t>(yn) & 15) == 0) {
-                const double2 *y2 = reinterpret_cast<const double2 *>(yn);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const double2 t = y2[q];
-                    yv[2 * q] = t.x;
-                    yv[2 * q + 1] = t.y;
-                }
-                yv[8] = yn[8];
-            } else {
-                yv[0] = yn[0];
-                const double2 *y2 = reinterpret_cast<const double2 *>(yn + 1);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const double2 t = y2[q];
-                    yv[2 * q + 1] = t.x;
-                    yv[2 * q + 2] = t.y;
-                }
-            }
-        } else {
-            const double2 *y2 = reinterpret_cast<const double2 *>(yn);   // 4 doubles per node: 32-byte aligned
-#pragma unroll
-            for (int q = 0; q < D * D / 2; ++q) {
-                const double2 t = y2[q];
-                yv[2 * q] = t.x;
-                yv[2 * q + 1] = t.y;
-            }
-        }
 #pragma unroll
         for (int k = 0; k < D; ++k) {
             double s = 0.0;
 #pragma unroll
-            for (int l = 0; l < D; ++l) s = fma(av[l], yv[k * D + l], s);
+            for (int l = 0; l < D; ++l) s = fma(av[l], yn[k * D + l], s);
             z[k] = fma(w[n], s, z[k]);
         }
     }
